@@ -1,0 +1,213 @@
+/*
+ * wgpf.h -- C-ABI of the B200-native KPerfIR trace post-processor (P2) and the
+ * host helpers of the device instrumentation runtime (P1).
+ *
+ * This is the drop-in boundary.  The reference (arXiv 2505.21661,
+ * /root/reference/proj) exposes its hot path as inline C++ functions in
+ * namespace wgprof; each entry point below states the reference function it
+ * replaces (file:line, relative to proj/include/).  include/wgprof_b200.hpp
+ * wraps this ABI back into those exact C++ signatures (value semantics,
+ * wgprof::Error exceptions), and paper_2505_21661_b200/trace.py mirrors them in
+ * Python.  INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - No exceptions cross the ABI; every call returns a wgpf_status.  Status
+ *    1..9 are the reference's ErrorKind values + 1 (wgprof/error.hpp:8-18), so
+ *    a shim rethrows wgprof::Error((ErrorKind)(status - 1), wgpf_last_error()).
+ *  - Caller-allocated outputs with capacity / count out-parameters.  When a
+ *    capacity is too small the call returns WGPF_E_BUFFER and writes the
+ *    needed count.
+ *  - All device work is stream-ordered on the context's CUDA stream.  Calls
+ *    that return host values synchronise that stream.
+ *  - One context per host thread; contexts are independent (the reference
+ *    functions are pure).
+ *  - There is no CPU fallback: without a usable CUDA device wgpf_create fails
+ *    with WGPF_E_CUDA.
+ */
+#ifndef WGPF_H
+#define WGPF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "wgpf_format.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WGPF_ABI_VERSION 1
+
+typedef enum wgpf_status {
+  WGPF_OK = 0,
+  WGPF_E_PARSE = 1,      /* ErrorKind::Parse      "parse-error"         */
+  WGPF_E_VALIDATE = 2,   /* ErrorKind::Validate   "validate-error"      */
+  WGPF_E_INSTRUMENT = 3, /* ErrorKind::Instrument "instrument-error"    */
+  WGPF_E_LOWER = 4,      /* ErrorKind::Lower      "lower-error"         */
+  WGPF_E_CAPACITY = 5,   /* ErrorKind::Capacity   "capacity-error"      */
+  WGPF_E_DEADLOCK = 6,   /* ErrorKind::Deadlock   "simulation-deadlock" */
+  WGPF_E_TRACE = 7,      /* ErrorKind::Trace      "trace-error"         */
+  WGPF_E_CONFIG = 8,     /* ErrorKind::Config     "config-error"        */
+  WGPF_E_IO = 9,         /* ErrorKind::Io         "io-error"            */
+  WGPF_E_CUDA = 10,      /* CUDA runtime failure / no device           */
+  WGPF_E_ARG = 11,       /* invalid argument                            */
+  WGPF_E_BUFFER = 12     /* caller buffer too small (count written)     */
+} wgpf_status;
+
+typedef struct wgpf_ctx wgpf_ctx;
+
+typedef struct wgpf_warnings { /* TraceReplay counters, pipeline.hpp:58-64 */
+  uint32_t dropped_heads;
+  uint32_t truncated_tails;
+  uint32_t flagged_preconditions;
+  uint32_t malformed_groups;
+} wgpf_warnings;
+
+typedef struct wgpf_decoded_stream { /* DecodedStream, trace.hpp:215-220 */
+  uint32_t block_index;
+  uint32_t warp_group;
+  uint32_t dropped_records;
+  uint32_t pad;
+  uint64_t offset; /* first record in the flat record output */
+  uint64_t count;
+} wgpf_decoded_stream;
+
+typedef struct wgpf_interval { /* RawInterval, trace.hpp:278-286 (label -> id) */
+  uint32_t region_id;
+  uint32_t iteration;
+  uint64_t start;
+  uint64_t end;
+  uint64_t start_pos;
+  uint64_t end_pos;
+} wgpf_interval;
+
+typedef struct wgpf_region_stat { /* RegionStats, pipeline.hpp:105-112 + ext */
+  const char* label;    /* owned by the context, valid until the next call */
+  uint32_t warp_group;  /* of the first event with this label */
+  uint32_t kind;        /* 0 exec, 1 wait (first event)        */
+  uint64_t count;
+  uint64_t min;
+  uint64_t max;
+  uint64_t sum;         /* exact integer sum of durations      */
+  double mean;          /* see WGPF_F_EXACT_MEAN               */
+  uint64_t first_event; /* global event index of the first event */
+  uint64_t hist[WGPF_HIST_BINS]; /* wgpf_hist_bin() bins          */
+} wgpf_region_stat;
+
+/* replay flags */
+#define WGPF_F_STATS_ONLY 0x1u  /* do not materialise events (stats only) */
+#define WGPF_F_EXACT_MEAN 0x2u  /* mean by the reference's order-dependent
+                                   double recurrence (pipeline.hpp:129),
+                                   bit-exact; needs materialised events.
+                                   Default: mean = (double)sum / count.   */
+#define WGPF_F_FORCE_GENERAL 0x4u /* route every stream through the general
+                                     (thread-per-stream) kernels            */
+#define WGPF_F_NO_STATS 0x8u    /* skip region statistics                  */
+
+/* ----------------------------------------------------------------------- */
+/* Lifecycle                                                                 */
+/* ----------------------------------------------------------------------- */
+
+int wgpf_abi_version(void);
+/* device: CUDA ordinal; stream: cudaStream_t (NULL = legacy default). */
+int wgpf_create(int device, void* stream, wgpf_ctx** out);
+void wgpf_destroy(wgpf_ctx* ctx);
+int wgpf_set_stream(wgpf_ctx* ctx, void* stream);
+const char* wgpf_last_error(const wgpf_ctx* ctx);
+/* Error::category() for a status (error.hpp:29-51). */
+const char* wgpf_error_category(int status);
+
+/* BufferPlan (lower.hpp:57-73): slots per stream, strategy, region table. */
+int wgpf_set_plan(wgpf_ctx* ctx, uint64_t slots_per_warp_group,
+                  uint32_t strategy, const char* const* region_labels,
+                  uint32_t n_labels);
+
+/* ----------------------------------------------------------------------- */
+/* P2: the trace post-processor                                              */
+/* ----------------------------------------------------------------------- */
+
+/*
+ * replay_image (pipeline.hpp:66-81) = decode_image (trace.hpp:222) +
+ * pair_records (trace.hpp:294) + replay (trace.hpp:398) per stream, events
+ * concatenated in image order, warnings summed; plus region_stats
+ * (pipeline.hpp:114) and duration histograms over the produced events.
+ *
+ * Device variant: d_body is a KPFT body (per stream: 16-byte header + slots)
+ * already resident in HBM, n_streams streams of uniform stride
+ * 16 + 8 * plan.slots.  stream_base is the global index of the first stream
+ * (multi-GPU shards; 0 otherwise).  d_events (device) may be NULL with
+ * WGPF_F_STATS_ONLY.  Synchronises the context stream before returning.
+ */
+int wgpf_replay_device(wgpf_ctx* ctx, const void* d_body, uint64_t body_bytes,
+                       uint64_t n_streams, uint64_t stream_base,
+                       uint64_t record_cost, wgpf_event* d_events,
+                       uint64_t events_cap, uint32_t flags,
+                       uint64_t* n_events, wgpf_warnings* warnings);
+
+/*
+ * Host variant (the reference-facing call): a complete KPFT v1 or v2 image in
+ * host memory -> events in host memory.  Includes the host->device copy of
+ * the image and the device->host copy of the events.  deserialize_image
+ * errors (trace.hpp:181-209) are reproduced exactly.
+ */
+int wgpf_replay_image(wgpf_ctx* ctx, const uint8_t* kpft, uint64_t n_bytes,
+                      uint64_t record_cost, wgpf_event* h_events,
+                      uint64_t events_cap, uint32_t flags, uint64_t* n_events,
+                      wgpf_warnings* warnings);
+
+/* decode_image (trace.hpp:222-251) on a host KPFT image. */
+int wgpf_decode_image(wgpf_ctx* ctx, const uint8_t* kpft, uint64_t n_bytes,
+                      wgpf_record* h_records, uint64_t records_cap,
+                      uint64_t* n_records, wgpf_decoded_stream* h_streams,
+                      uint64_t streams_cap, uint64_t* n_streams);
+
+/* unwrap_clock (trace.hpp:257-272). */
+int wgpf_unwrap_clock(wgpf_ctx* ctx, const uint32_t* h_values, uint64_t n,
+                      uint64_t* h_out);
+
+/* pair_records (trace.hpp:294-346) on one chronological stream. */
+int wgpf_pair_records(wgpf_ctx* ctx, const wgpf_record* h_records, uint64_t n,
+                      wgpf_interval* h_out, uint64_t cap, uint64_t* n_out,
+                      uint32_t* dropped_heads, uint32_t* truncated_tails);
+
+/* replay (trace.hpp:398-487) on one stream's intervals. */
+int wgpf_replay_intervals(wgpf_ctx* ctx, const wgpf_interval* h_iv, uint64_t n,
+                          uint32_t block_index, uint32_t warp_group,
+                          uint64_t record_cost, wgpf_event* h_out,
+                          uint64_t cap, uint64_t* n_out,
+                          wgpf_warnings* warnings);
+
+/* Region statistics of the last replay (sorted by label bytes, as the
+ * reference's std::map).  *n receives the number of labels. */
+int wgpf_stats_get(wgpf_ctx* ctx, wgpf_region_stat* out, uint32_t cap,
+                   uint32_t* n);
+
+/* region_stats (pipeline.hpp:114-133) over an arbitrary event array
+ * (device pointer when on_device != 0, else host). */
+int wgpf_region_stats(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n,
+                      int on_device, uint32_t flags, wgpf_region_stat* out,
+                      uint32_t cap, uint32_t* n_out);
+
+/* Multi-GPU: export this rank's packed statistics (device buffer of
+ * wgpf_stats_packed_bytes() bytes), and merge n_ranks gathered exports (one
+ * after the other in d_gathered) into this context's statistics.  The caller
+ * moves the bytes (e.g. one NCCL all-gather over NVLink). */
+uint64_t wgpf_stats_packed_bytes(const wgpf_ctx* ctx);
+int wgpf_stats_export(wgpf_ctx* ctx, void* d_dst);
+int wgpf_stats_merge(wgpf_ctx* ctx, const void* d_gathered, uint32_t n_ranks);
+
+/* ----------------------------------------------------------------------- */
+/* Synthetic trace generator (bench / tests)    */
+/* ----------------------------------------------------------------------- */
+
+#define WGPF_SYNTH_MIXED 0u  /* config 4: producers/consumers, flush, cap 256 */
+#define WGPF_SYNTH_NESTED 1u /* config 5: 64 nested scopes, circular 1000 w */
+
+int wgpf_synth_body(wgpf_ctx* ctx, void* d_body, uint32_t shape,
+                    uint64_t stream0, uint64_t n_streams, uint64_t n_long);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WGPF_H */

@@ -1,0 +1,478 @@
+// wgprof_b200.hpp -- drop-in C++ shim: the reference's namespace wgprof trace
+// API (value semantics, wgprof::Error exceptions) implemented over the C-ABI
+// of libwgpf.so (include/wgpf.h), i.e. over the sm_100a kernels.
+//
+// Replaces, signature for signature (paths relative to
+// /root/reference/proj/include/):
+//   wgprof/error.hpp:8-55       ErrorKind, Error, category()
+//   wgprof/trace.hpp:58-99      ProfileRecord, encode_record, decode_record
+//   wgprof/trace.hpp:105-209    TraceStream, GlobalTraceImage,
+//                               serialize_image, deserialize_image
+//   wgprof/lower.hpp:42,57-73   BufferStrategy, BufferPlan
+//   wgprof/trace.hpp:215-251    DecodedStream, decode_image        (GPU)
+//   wgprof/trace.hpp:257-272    unwrap_clock                       (GPU)
+//   wgprof/trace.hpp:278-346    RawInterval, PairResult, pair_records (GPU)
+//   wgprof/trace.hpp:352-487    EventKind, TimelineEvent, ReplayResult,
+//                               replay                             (GPU)
+//   wgprof/pipeline.hpp:58-81   TraceReplay, replay_image          (GPU)
+//   wgprof/pipeline.hpp:105-133 RegionStats, region_stats          (GPU)
+//
+// A program built against the reference's headers switches by including this
+// header instead and linking libwgpf.so.  Do not include it
+// together with the reference headers (same namespace).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "wgpf.h"
+
+namespace wgprof {
+
+enum class ErrorKind { Parse, Validate, Instrument, Lower, Capacity, Deadlock,
+                       Trace, Config, Io };
+
+class Error : public std::runtime_error {
+ public:
+  Error(ErrorKind kind, const std::string& message)
+      : std::runtime_error(message), kind_(kind) {}
+  ErrorKind kind() const { return kind_; }
+  const char* category() const {
+    return wgpf_error_category(1 + static_cast<int>(kind_));
+  }
+
+ private:
+  ErrorKind kind_;
+};
+
+inline constexpr std::uint32_t kStartFlag = WGPF_START_FLAG;
+inline constexpr std::uint32_t kSignatureMask = WGPF_SIGNATURE_MASK;
+inline constexpr std::uint32_t kRegionIdBits = WGPF_REGION_BITS;
+inline constexpr std::uint32_t kMaxRegions = WGPF_MAX_REGIONS;
+inline constexpr std::uint64_t kRecordBytes = WGPF_RECORD_BYTES;
+inline constexpr std::uint16_t kTraceVersion = 1;
+inline const char* kWaitSuffix = ".wait";
+
+struct ProfileRecord {
+  std::uint32_t tag = 0;
+  std::uint32_t payload = 0;
+  bool is_start() const { return (tag & kStartFlag) != 0; }
+  std::uint32_t region_id() const { return (tag >> 12) & (kMaxRegions - 1); }
+  std::uint16_t signature() const {
+    return static_cast<std::uint16_t>(tag & kSignatureMask);
+  }
+  static ProfileRecord make(bool is_start, std::uint32_t region,
+                            std::uint16_t signature, std::uint32_t clock) {
+    if (region >= kMaxRegions)
+      throw Error(ErrorKind::Trace, "region id " + std::to_string(region) +
+                                        " overflows the 19-bit tag field");
+    return ProfileRecord{(is_start ? kStartFlag : 0u) | (region << 12) |
+                             (signature & kSignatureMask),
+                         clock};
+  }
+  bool operator==(const ProfileRecord&) const = default;
+};
+
+inline std::array<std::uint8_t, 8> encode_record(const ProfileRecord& r) {
+  std::array<std::uint8_t, 8> out{};
+  for (int i = 0; i < 4; ++i) out[i] = (r.tag >> (8 * i)) & 0xFF;
+  for (int i = 0; i < 4; ++i) out[4 + i] = (r.payload >> (8 * i)) & 0xFF;
+  return out;
+}
+
+inline ProfileRecord decode_record(const std::uint8_t* b) {
+  ProfileRecord r;
+  for (int i = 0; i < 4; ++i) r.tag |= static_cast<std::uint32_t>(b[i]) << (8 * i);
+  for (int i = 0; i < 4; ++i)
+    r.payload |= static_cast<std::uint32_t>(b[4 + i]) << (8 * i);
+  return r;
+}
+
+struct TraceStream {
+  std::uint32_t block_index = 0;
+  std::uint32_t warp_group = 0;
+  std::uint32_t record_count = 0;
+  std::uint32_t slot_capacity = 0;
+  std::vector<ProfileRecord> slots;
+  bool operator==(const TraceStream&) const = default;
+};
+
+struct GlobalTraceImage {
+  std::vector<TraceStream> streams;
+  bool operator==(const GlobalTraceImage&) const = default;
+};
+
+enum class BufferStrategy { Circular, Flush };
+
+struct BufferPlan {
+  std::uint64_t slots_per_warp_group = 0;
+  BufferStrategy strategy = BufferStrategy::Circular;
+  std::vector<std::string> region_labels;
+  std::uint64_t base_offset(std::uint32_t wg) const {
+    return wg * slots_per_warp_group * kRecordBytes;
+  }
+  bool operator==(const BufferPlan&) const = default;
+};
+
+struct DecodedStream {
+  std::uint32_t block_index = 0;
+  std::uint32_t warp_group = 0;
+  std::uint32_t dropped_records = 0;
+  std::vector<ProfileRecord> records;
+};
+
+struct RawInterval {
+  std::uint32_t region_id = 0;
+  std::string label;
+  std::uint32_t iteration = 0;
+  std::uint64_t start = 0;
+  std::uint64_t end = 0;
+  std::size_t start_pos = 0;
+  std::size_t end_pos = 0;
+};
+
+struct PairResult {
+  std::vector<RawInterval> intervals;
+  std::uint32_t dropped_heads = 0;
+  std::uint32_t truncated_tails = 0;
+};
+
+enum class EventKind { Exec, Wait };
+
+struct TimelineEvent {
+  std::string region;
+  std::uint32_t block_index = 0;
+  std::uint32_t warp_group = 0;
+  std::uint32_t iteration = 0;
+  std::uint64_t start = 0;
+  std::uint64_t end = 0;
+  EventKind kind = EventKind::Exec;
+  bool corrected = false;
+  std::uint64_t duration() const { return end - start; }
+  bool operator==(const TimelineEvent&) const = default;
+};
+
+struct ReplayResult {
+  std::vector<TimelineEvent> events;
+  std::uint32_t flagged_preconditions = 0;
+  std::uint32_t malformed_groups = 0;
+};
+
+struct TraceReplay {
+  std::vector<TimelineEvent> events;
+  std::uint32_t dropped_heads = 0;
+  std::uint32_t truncated_tails = 0;
+  std::uint32_t flagged_preconditions = 0;
+  std::uint32_t malformed_groups = 0;
+};
+
+struct RegionStats {
+  std::uint32_t warp_group = 0;
+  EventKind kind = EventKind::Exec;
+  std::uint32_t count = 0;
+  std::uint64_t min = 0;
+  std::uint64_t max = 0;
+  double mean = 0.0;
+};
+
+// ---------------------------------------------------------------------------
+// implementation details
+// ---------------------------------------------------------------------------
+namespace b200 {
+
+struct Ctx {
+  wgpf_ctx* h = nullptr;
+  Ctx() {
+    int rc = wgpf_create(0, nullptr, &h);
+    if (rc != WGPF_OK)
+      throw std::runtime_error(
+          "wgprof_b200: no usable CUDA device (this implementation has no "
+          "CPU fallback)");
+  }
+  ~Ctx() {
+    if (h) wgpf_destroy(h);
+  }
+};
+
+inline wgpf_ctx* ctx() {
+  thread_local std::unique_ptr<Ctx> c;
+  if (!c) c = std::make_unique<Ctx>();
+  return c->h;
+}
+
+inline void check(int rc) {
+  if (rc == WGPF_OK) return;
+  const std::string msg = wgpf_last_error(ctx());
+  if (rc >= 1 && rc <= 9) throw Error(static_cast<ErrorKind>(rc - 1), msg);
+  throw std::runtime_error(std::string("wgpf: ") + wgpf_error_category(rc) +
+                           ": " + msg);
+}
+
+inline void set_plan(std::uint64_t slots, BufferStrategy st,
+                     const std::vector<std::string>& labels) {
+  std::vector<const char*> p;
+  p.reserve(labels.size());
+  for (const auto& s : labels) p.push_back(s.c_str());
+  check(wgpf_set_plan(ctx(), slots, static_cast<std::uint32_t>(st), p.data(),
+                      static_cast<std::uint32_t>(p.size())));
+}
+
+inline std::string label_of(const std::vector<std::string>& t, std::uint32_t id) {
+  return id < t.size() ? t[id] : "region#" + std::to_string(id);
+}
+
+inline TimelineEvent to_event(const wgpf_event& e,
+                              const std::vector<std::string>& labels) {
+  TimelineEvent t;
+  t.region = label_of(labels, e.region & WGPF_EV_REGION_MASK);
+  t.block_index = e.block_index;
+  t.warp_group = e.warp_group;
+  t.iteration = e.iteration;
+  t.start = e.start;
+  t.end = e.end;
+  t.kind = (e.region & WGPF_EV_WAIT) ? EventKind::Wait : EventKind::Exec;
+  t.corrected = (e.region & WGPF_EV_CORRECTED) != 0;
+  return t;
+}
+
+inline void put_u32(std::vector<std::uint8_t>& o, std::uint32_t v) {
+  for (int i = 0; i < 4; ++i) o.push_back((v >> (8 * i)) & 0xFF);
+}
+
+}  // namespace b200
+
+// ---------------------------------------------------------------------------
+// image format (host)
+// ---------------------------------------------------------------------------
+
+inline std::vector<std::uint8_t> serialize_image(const GlobalTraceImage& img) {
+  std::vector<std::uint8_t> out = {'K', 'P', 'F', 'T', 1, 0};
+  if (img.streams.size() > 0xFFFF)
+    throw Error(ErrorKind::Trace, "too many streams for the image header");
+  out.push_back(img.streams.size() & 0xFF);
+  out.push_back((img.streams.size() >> 8) & 0xFF);
+  for (const auto& s : img.streams) {
+    if (s.slots.size() != s.slot_capacity)
+      throw Error(ErrorKind::Trace,
+                  "stream slot count does not match its declared capacity");
+    b200::put_u32(out, s.block_index);
+    b200::put_u32(out, s.warp_group);
+    b200::put_u32(out, s.record_count);
+    b200::put_u32(out, s.slot_capacity);
+    for (const auto& r : s.slots) {
+      auto b = encode_record(r);
+      out.insert(out.end(), b.begin(), b.end());
+    }
+  }
+  return out;
+}
+
+inline GlobalTraceImage deserialize_image(const std::vector<std::uint8_t>& bytes) {
+  auto need = [&](std::size_t pos, std::size_t n) {
+    if (pos + n > bytes.size()) throw Error(ErrorKind::Trace, "truncated trace image");
+  };
+  auto u32 = [&](std::size_t pos) {
+    return static_cast<std::uint32_t>(bytes[pos]) |
+           (static_cast<std::uint32_t>(bytes[pos + 1]) << 8) |
+           (static_cast<std::uint32_t>(bytes[pos + 2]) << 16) |
+           (static_cast<std::uint32_t>(bytes[pos + 3]) << 24);
+  };
+  need(0, 4);
+  if (std::memcmp(bytes.data(), "KPFT", 4) != 0)
+    throw Error(ErrorKind::Trace, "bad magic: not a trace image");
+  need(4, 2);
+  const std::uint16_t version = bytes[4] | (bytes[5] << 8);
+  if (version != kTraceVersion)
+    throw Error(ErrorKind::Trace,
+                "unsupported trace version " + std::to_string(version));
+  need(6, 2);
+  const std::uint16_t count = bytes[6] | (bytes[7] << 8);
+  std::size_t pos = 8;
+  GlobalTraceImage img;
+  img.streams.resize(count);
+  for (auto& s : img.streams) {
+    need(pos, 16);
+    s.block_index = u32(pos);
+    s.warp_group = u32(pos + 4);
+    s.record_count = u32(pos + 8);
+    s.slot_capacity = u32(pos + 12);
+    pos += 16;
+    need(pos, static_cast<std::size_t>(s.slot_capacity) * 8);
+    s.slots.resize(s.slot_capacity);
+    for (auto& r : s.slots) {
+      r = decode_record(&bytes[pos]);
+      pos += 8;
+    }
+  }
+  if (pos != bytes.size())
+    throw Error(ErrorKind::Trace, "trailing bytes after trace image");
+  return img;
+}
+
+// ---------------------------------------------------------------------------
+// GPU-backed post-processing
+// ---------------------------------------------------------------------------
+
+inline std::vector<DecodedStream> decode_image(const GlobalTraceImage& img,
+                                               const BufferPlan& plan) {
+  b200::set_plan(plan.slots_per_warp_group, plan.strategy, plan.region_labels);
+  const auto bytes = serialize_image(img);
+  std::size_t total = 0;
+  for (const auto& s : img.streams) total += s.slot_capacity;
+  std::vector<wgpf_record> recs(total + 1);
+  std::vector<wgpf_decoded_stream> ds(img.streams.size() + 1);
+  std::uint64_t nr = 0, ns = 0;
+  b200::check(wgpf_decode_image(b200::ctx(), bytes.data(), bytes.size(),
+                                recs.data(), recs.size(), &nr, ds.data(),
+                                ds.size(), &ns));
+  std::vector<DecodedStream> out(ns);
+  for (std::uint64_t s = 0; s < ns; ++s) {
+    out[s].block_index = ds[s].block_index;
+    out[s].warp_group = ds[s].warp_group;
+    out[s].dropped_records = ds[s].dropped_records;
+    for (std::uint64_t k = 0; k < ds[s].count; ++k)
+      out[s].records.push_back(ProfileRecord{recs[ds[s].offset + k].tag,
+                                             recs[ds[s].offset + k].payload});
+  }
+  return out;
+}
+
+inline std::vector<std::uint64_t> unwrap_clock(const std::vector<std::uint32_t>& v) {
+  std::vector<std::uint64_t> out(v.size());
+  if (!v.empty())
+    b200::check(wgpf_unwrap_clock(b200::ctx(), v.data(), v.size(), out.data()));
+  return out;
+}
+
+inline PairResult pair_records(const std::vector<ProfileRecord>& stream,
+                               const std::vector<std::string>& region_table) {
+  b200::set_plan(0, BufferStrategy::Flush, region_table);
+  std::vector<wgpf_record> r(stream.size() + 1);
+  for (std::size_t i = 0; i < stream.size(); ++i)
+    r[i] = wgpf_record{stream[i].tag, stream[i].payload};
+  std::vector<wgpf_interval> iv(stream.size() / 2 + 1);
+  std::uint64_t n = 0;
+  PairResult out;
+  b200::check(wgpf_pair_records(b200::ctx(), r.data(), stream.size(), iv.data(),
+                                iv.size(), &n, &out.dropped_heads,
+                                &out.truncated_tails));
+  for (std::uint64_t i = 0; i < n; ++i) {
+    RawInterval x;
+    x.region_id = iv[i].region_id;
+    x.label = b200::label_of(region_table, iv[i].region_id);
+    x.iteration = iv[i].iteration;
+    x.start = iv[i].start;
+    x.end = iv[i].end;
+    x.start_pos = iv[i].start_pos;
+    x.end_pos = iv[i].end_pos;
+    out.intervals.push_back(std::move(x));
+  }
+  return out;
+}
+
+inline ReplayResult replay(const PairResult& pairs, std::uint32_t block_index,
+                           std::uint32_t warp_group, std::uint64_t record_cost) {
+  // Labels travel as ids: one table entry per distinct label string.
+  std::vector<std::string> table;
+  std::unordered_map<std::string, std::uint32_t> ids;
+  std::vector<wgpf_interval> iv(pairs.intervals.size() + 1);
+  for (std::size_t i = 0; i < pairs.intervals.size(); ++i) {
+    const auto& a = pairs.intervals[i];
+    auto it = ids.find(a.label);
+    std::uint32_t id;
+    if (it == ids.end()) {
+      id = static_cast<std::uint32_t>(table.size());
+      ids.emplace(a.label, id);
+      table.push_back(a.label);
+    } else {
+      id = it->second;
+    }
+    iv[i] = wgpf_interval{id, a.iteration, a.start, a.end, a.start_pos, a.end_pos};
+  }
+  b200::set_plan(0, BufferStrategy::Flush, table);
+  std::vector<wgpf_event> ev(pairs.intervals.size() + 1);
+  std::uint64_t n = 0;
+  wgpf_warnings w{};
+  b200::check(wgpf_replay_intervals(b200::ctx(), iv.data(), pairs.intervals.size(),
+                                    block_index, warp_group, record_cost,
+                                    ev.data(), ev.size(), &n, &w));
+  ReplayResult out;
+  for (std::uint64_t i = 0; i < n; ++i) out.events.push_back(b200::to_event(ev[i], table));
+  out.flagged_preconditions = w.flagged_preconditions;
+  out.malformed_groups = w.malformed_groups;
+  return out;
+}
+
+inline TraceReplay replay_image(const GlobalTraceImage& image,
+                                const BufferPlan& plan,
+                                std::uint64_t record_cost) {
+  b200::set_plan(plan.slots_per_warp_group, plan.strategy, plan.region_labels);
+  const auto bytes = serialize_image(image);
+  std::size_t cap = 1;
+  for (const auto& s : image.streams) cap += s.slot_capacity / 2 + 1;
+  std::vector<wgpf_event> ev(cap);
+  std::uint64_t n = 0;
+  wgpf_warnings w{};
+  int rc = wgpf_replay_image(b200::ctx(), bytes.data(), bytes.size(), record_cost,
+                             ev.data(), ev.size(), 0, &n, &w);
+  b200::check(rc);
+  TraceReplay out;
+  out.events.reserve(n);
+  for (std::uint64_t i = 0; i < n; ++i)
+    out.events.push_back(b200::to_event(ev[i], plan.region_labels));
+  out.dropped_heads = w.dropped_heads;
+  out.truncated_tails = w.truncated_tails;
+  out.flagged_preconditions = w.flagged_preconditions;
+  out.malformed_groups = w.malformed_groups;
+  return out;
+}
+
+inline std::map<std::string, RegionStats> region_stats(
+    const std::vector<TimelineEvent>& events) {
+  std::vector<std::string> table;
+  std::unordered_map<std::string, std::uint32_t> ids;
+  std::vector<wgpf_event> ev(events.size() + 1);
+  for (std::size_t i = 0; i < events.size(); ++i) {
+    const auto& e = events[i];
+    auto it = ids.find(e.region);
+    std::uint32_t id;
+    if (it == ids.end()) {
+      id = static_cast<std::uint32_t>(table.size());
+      ids.emplace(e.region, id);
+      table.push_back(e.region);
+    } else {
+      id = it->second;
+    }
+    ev[i] = wgpf_event{e.start, e.end,
+                       id | (e.kind == EventKind::Wait ? WGPF_EV_WAIT : 0u) |
+                           (e.corrected ? WGPF_EV_CORRECTED : 0u),
+                       e.iteration, e.block_index, e.warp_group};
+  }
+  b200::set_plan(0, BufferStrategy::Flush, table);
+  std::vector<wgpf_region_stat> st(table.size() + 1);
+  std::uint32_t n = 0;
+  b200::check(wgpf_region_stats(b200::ctx(), ev.data(), events.size(), 0,
+                                WGPF_F_EXACT_MEAN, st.data(),
+                                static_cast<std::uint32_t>(st.size()), &n));
+  std::map<std::string, RegionStats> out;
+  for (std::uint32_t i = 0; i < n; ++i) {
+    RegionStats r;
+    r.warp_group = st[i].warp_group;
+    r.kind = st[i].kind ? EventKind::Wait : EventKind::Exec;
+    r.count = static_cast<std::uint32_t>(st[i].count);
+    r.min = st[i].min;
+    r.max = st[i].max;
+    r.mean = st[i].mean;
+    out.emplace(st[i].label, r);
+  }
+  return out;
+}
+
+}  // namespace wgprof

@@ -1,0 +1,116 @@
+"""ctypes binding of the C-ABI in include/wgpf.h (libwgpf.so, sm_100a).
+
+Loading fails loudly when the library cannot be built or loaded, and context
+creation fails when no CUDA device is present: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _build
+
+HIST_BINS = 64
+
+EVENT_DTYPE = np.dtype(
+    [("start", "<u8"), ("end", "<u8"), ("region", "<u4"), ("iteration", "<u4"),
+     ("block_index", "<u4"), ("warp_group", "<u4")])
+RECORD_DTYPE = np.dtype([("tag", "<u4"), ("payload", "<u4")])
+INTERVAL_DTYPE = np.dtype([("region_id", "<u4"), ("iteration", "<u4"),
+                           ("start", "<u8"), ("end", "<u8"),
+                           ("start_pos", "<u8"), ("end_pos", "<u8")])
+DECODED_DTYPE = np.dtype([("block_index", "<u4"), ("warp_group", "<u4"),
+                          ("dropped_records", "<u4"), ("pad", "<u4"),
+                          ("offset", "<u8"), ("count", "<u8")])
+
+EV_WAIT = 0x80000000
+EV_CORRECTED = 0x40000000
+EV_REGION_MASK = 0x7FFFF
+
+F_STATS_ONLY = 0x1
+F_EXACT_MEAN = 0x2
+F_FORCE_GENERAL = 0x4
+F_NO_STATS = 0x8
+
+OK, E_BUFFER = 0, 12
+
+
+class Warnings(C.Structure):
+    _fields_ = [("dropped_heads", C.c_uint32), ("truncated_tails", C.c_uint32),
+                ("flagged_preconditions", C.c_uint32),
+                ("malformed_groups", C.c_uint32)]
+
+
+class RegionStat(C.Structure):
+    _fields_ = [("label", C.c_char_p), ("warp_group", C.c_uint32),
+                ("kind", C.c_uint32), ("count", C.c_uint64), ("min", C.c_uint64),
+                ("max", C.c_uint64), ("sum", C.c_uint64), ("mean", C.c_double),
+                ("first_event", C.c_uint64), ("hist", C.c_uint64 * HIST_BINS)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads (building if needed) libwgpf.so."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = _build.build()
+        L = C.CDLL(path)
+        vp, u64, u32, i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
+        sig = {
+            "wgpf_abi_version": ([], i32),
+            "wgpf_create": ([i32, vp, C.POINTER(vp)], i32),
+            "wgpf_destroy": ([vp], None),
+            "wgpf_set_stream": ([vp, vp], i32),
+            "wgpf_last_error": ([vp], C.c_char_p),
+            "wgpf_error_category": ([i32], C.c_char_p),
+            "wgpf_set_plan": ([vp, u64, u32, C.POINTER(C.c_char_p), u32], i32),
+            "wgpf_replay_device": ([vp, vp, u64, u64, u64, u64, vp, u64, u32,
+                                    C.POINTER(u64), C.POINTER(Warnings)], i32),
+            "wgpf_replay_image": ([vp, vp, u64, u64, vp, u64, u32, C.POINTER(u64),
+                                   C.POINTER(Warnings)], i32),
+            "wgpf_decode_image": ([vp, vp, u64, vp, u64, C.POINTER(u64), vp, u64,
+                                   C.POINTER(u64)], i32),
+            "wgpf_unwrap_clock": ([vp, vp, u64, vp], i32),
+            "wgpf_pair_records": ([vp, vp, u64, vp, u64, C.POINTER(u64),
+                                   C.POINTER(u32), C.POINTER(u32)], i32),
+            "wgpf_replay_intervals": ([vp, vp, u64, u32, u32, u64, vp, u64,
+                                       C.POINTER(u64), C.POINTER(Warnings)], i32),
+            "wgpf_stats_get": ([vp, C.POINTER(RegionStat), u32, C.POINTER(u32)], i32),
+            "wgpf_region_stats": ([vp, vp, u64, i32, u32, C.POINTER(RegionStat), u32,
+                                   C.POINTER(u32)], i32),
+            "wgpf_stats_packed_bytes": ([vp], u64),
+            "wgpf_stats_export": ([vp, vp], i32),
+            "wgpf_stats_merge": ([vp, vp, u32], i32),
+            "wgpf_synth_body": ([vp, vp, u32, u64, u64, u64], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+def loaded_path() -> str:
+    return _build.LIB
+
+
+def ptr(a) -> int:
+    """Address of a numpy array / torch tensor / int."""
+    if a is None:
+        return 0
+    if isinstance(a, int):
+        return a
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    raise TypeError(f"cannot take the address of {type(a)}")

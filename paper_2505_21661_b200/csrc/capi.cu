@@ -1,0 +1,1300 @@
+// capi.cu -- host side of the C-ABI (include/wgpf.h): context, plan tables,
+// buffer management and the replay orchestration.  Single translation unit:
+// the kernels live in the k_*.cuh headers included below.
+//
+// replay orchestration (one call of wgpf_replay_device):
+//   k_count_fast      pass 1, warp/stream: decode checks, counts, routing
+//   cub ExclusiveSum  counts -> event offsets
+//   k_fast_emit       pass 2, warp/stream: pair + replay + stats (fast path)
+//   k_general_emit    thread/stream, exact: streams routed off the fast path
+//   (rare) exact recount of single-stack-invalid streams + re-emit
+//   k_resolve_first   first-event warp_group per label
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
+
+#include "wgpf.h"
+#include "wgpf_dev.cuh"
+#include "k_count.cuh"
+#include "k_fast.cuh"
+#include "k_general.cuh"
+#include "k_misc.cuh"
+#include "k_stats.cuh"
+#include "k_synth.cuh"
+
+using namespace wgpf;
+
+namespace {
+
+struct ToU64 {
+  __host__ __device__ uint64_t operator()(uint32_t x) const { return x; }
+};
+
+constexpr uint32_t kSynthHash = 1024;  // out-of-table label classes per call
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  bool ensure(size_t bytes) {
+    if (bytes <= n) return true;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    if (cudaMalloc(&p, want) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    n = want;
+    return true;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct wgpf_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  // plan
+  bool has_plan = false;
+  uint64_t slots = 0;
+  uint32_t strategy = 0;
+  std::vector<std::string> labels;
+  std::vector<std::string> class_label;  // dense classes
+  std::unordered_map<std::string, uint32_t> class_by_label;
+  uint32_t K = 0;
+  DevBuf d_class_of, d_wait_class, d_is_marker, d_swait_id, d_swait_cls;
+  uint32_t n_synth_wait = 0;
+
+  // stats
+  DevBuf d_count, d_sum, d_min, d_max, d_first, d_hist, d_hkey, d_first_wg,
+      d_mean;
+  bool stats_valid = false;
+  bool mean_exact_valid = false;
+  std::vector<wgpf_region_stat> stats_out;
+  std::vector<std::string> stats_names;
+
+  // per call
+  DevBuf d_status, d_counts, d_zpos, d_sflag, d_offsets, d_scan_tmp, d_glist,
+      d_glen, d_orphans, d_gscratch, d_image, d_events, d_aux0, d_aux1, d_aux2,
+      d_aux3;
+  DevStatus* h_status = nullptr;  // pinned
+  uint64_t last_stream_base = 0, last_n_streams = 0;
+  const uint8_t* last_body = nullptr;
+  uint64_t last_stride = 0;
+
+  ~wgpf_ctx() {
+    if (h_status) cudaFreeHost(h_status);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+
+static int set_err(wgpf_ctx* c, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  c->err = buf;
+  return code;
+}
+
+#define CUDA_OK(ctx, expr)                                                    \
+  do {                                                                        \
+    cudaError_t e_ = (expr);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      cudaGetLastError();                                                     \
+      return set_err(ctx, WGPF_E_CUDA, "%s: %s (%s:%d)", #expr,               \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);             \
+    }                                                                         \
+  } while (0)
+
+#define ALLOC_OK(ctx, buf, bytes)                                             \
+  do {                                                                        \
+    if (!(buf).ensure(bytes))                                                 \
+      return set_err(ctx, WGPF_E_CUDA, "cudaMalloc of %zu bytes failed",      \
+                     (size_t)(bytes));                                        \
+  } while (0)
+
+static std::string label_of(const wgpf_ctx* c, uint32_t rid) {
+  if (rid < c->labels.size()) return c->labels[rid];
+  return "region#" + std::to_string(rid);
+}
+
+static std::string class_name(const wgpf_ctx* c, uint32_t cls) {
+  if (cls < c->K) return c->class_label[cls];
+  return "region#" + std::to_string(cls - c->K);
+}
+
+static DevPlan dev_plan(const wgpf_ctx* c) {
+  DevPlan p;
+  p.slots = c->slots;
+  p.strategy = c->strategy;
+  p.T = (uint32_t)c->labels.size();
+  p.K = c->K;
+  p.n_synth_wait = c->n_synth_wait;
+  p.class_of = c->d_class_of.as<uint32_t>();
+  p.wait_class = c->d_wait_class.as<uint32_t>();
+  p.is_marker = c->d_is_marker.as<uint8_t>();
+  p.synth_wait_id = c->d_swait_id.as<uint32_t>();
+  p.synth_wait_cls = c->d_swait_cls.as<uint32_t>();
+  return p;
+}
+
+static uint32_t n_slots(const wgpf_ctx* c) { return c->K + kSynthHash; }
+
+static DevStats dev_stats(const wgpf_ctx* c) {
+  DevStats s;
+  s.count = c->d_count.as<unsigned long long>();
+  s.sum = c->d_sum.as<unsigned long long>();
+  s.min = c->d_min.as<unsigned long long>();
+  s.max = c->d_max.as<unsigned long long>();
+  s.first = c->d_first.as<unsigned long long>();
+  s.hist = c->d_hist.as<unsigned long long>();
+  s.hkey = c->d_hkey.as<uint32_t>();
+  s.K = c->K;
+  s.H = kSynthHash;
+  return s;
+}
+
+static int stats_reset(wgpf_ctx* c) {
+  const size_t ns = n_slots(c);
+  CUDA_OK(c, cudaMemsetAsync(c->d_count.p, 0, 8 * ns, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_sum.p, 0, 8 * ns, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_min.p, 0xFF, 8 * ns, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_max.p, 0, 8 * ns, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_first.p, 0xFF, 8 * ns, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_first_wg.p, 0, 8 * ns, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_hist.p, 0, 8 * ns * WGPF_HIST_BINS, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_hkey.p, 0xFF, 4 * kSynthHash, c->stream));
+  c->stats_valid = false;
+  c->mean_exact_valid = false;
+  return WGPF_OK;
+}
+
+static int status_reset(wgpf_ctx* c) {
+  DevStatus s;
+  memset(&s, 0, sizeof s);
+  s.decode_err = kNoErr;
+  s.pair_err = kNoErr;
+  *c->h_status = s;
+  CUDA_OK(c, cudaMemcpyAsync(c->d_status.p, c->h_status, sizeof(DevStatus),
+                             cudaMemcpyHostToDevice, c->stream));
+  return WGPF_OK;
+}
+
+static int status_read(wgpf_ctx* c) {
+  CUDA_OK(c, cudaMemcpyAsync(c->h_status, c->d_status.p, sizeof(DevStatus),
+                             cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  return WGPF_OK;
+}
+
+static uint32_t grid_for(wgpf_ctx* c, const void* kernel, int threads,
+                         size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads,
+                                                    smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  return (uint32_t)(c->sms * per_sm);
+}
+
+// ---------------------------------------------------------------------------
+// lifecycle
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+int wgpf_abi_version(void) { return WGPF_ABI_VERSION; }
+
+const char* wgpf_error_category(int status) {
+  switch (status) {
+    case WGPF_OK: return "ok";
+    case WGPF_E_PARSE: return "parse-error";
+    case WGPF_E_VALIDATE: return "validate-error";
+    case WGPF_E_INSTRUMENT: return "instrument-error";
+    case WGPF_E_LOWER: return "lower-error";
+    case WGPF_E_CAPACITY: return "capacity-error";
+    case WGPF_E_DEADLOCK: return "simulation-deadlock";
+    case WGPF_E_TRACE: return "trace-error";
+    case WGPF_E_CONFIG: return "config-error";
+    case WGPF_E_IO: return "io-error";
+    case WGPF_E_CUDA: return "cuda-error";
+    case WGPF_E_ARG: return "argument-error";
+    case WGPF_E_BUFFER: return "buffer-too-small";
+    default: return "error";
+  }
+}
+
+int wgpf_create(int device, void* stream, wgpf_ctx** out) {
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return WGPF_E_CUDA;
+  }
+  if (device < 0 || device >= n) return WGPF_E_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return WGPF_E_CUDA;
+  wgpf_ctx* c = new wgpf_ctx();
+  c->device = device;
+  c->stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMallocHost(&c->h_status, sizeof(DevStatus)) != cudaSuccess ||
+      !c->d_status.ensure(sizeof(DevStatus)) || !c->d_glen.ensure(64)) {
+    delete c;
+    return WGPF_E_CUDA;
+  }
+  cudaFuncSetAttribute(k_fast_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(FastSmem));
+  *out = c;
+  return WGPF_OK;
+}
+
+void wgpf_destroy(wgpf_ctx* ctx) { delete ctx; }
+
+int wgpf_set_stream(wgpf_ctx* ctx, void* stream) {
+  ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+  return WGPF_OK;
+}
+
+const char* wgpf_last_error(const wgpf_ctx* ctx) { return ctx->err.c_str(); }
+
+// BufferPlan (lower.hpp:57-73).  Label classes: one per distinct label
+// string (duplicates in the table share statistics and wait matching, as
+// the reference keys both by label string, pipeline.hpp:116, trace.hpp:442).
+int wgpf_set_plan(wgpf_ctx* c, uint64_t slots, uint32_t strategy,
+                  const char* const* labels, uint32_t n_labels) {
+  if (strategy > 1) return set_err(c, WGPF_E_ARG, "strategy must be 0 or 1");
+  if (n_labels > WGPF_MAX_REGIONS)
+    return set_err(c, WGPF_E_ARG, "more than 2^19 region labels");
+  c->slots = slots;
+  c->strategy = strategy;
+  c->labels.assign(labels, labels + n_labels);
+  c->class_label.clear();
+  c->class_by_label.clear();
+  std::vector<uint32_t> cls_of_table(n_labels);
+  for (uint32_t i = 0; i < n_labels; ++i) {
+    auto it = c->class_by_label.find(c->labels[i]);
+    if (it == c->class_by_label.end()) {
+      uint32_t k = (uint32_t)c->class_label.size();
+      c->class_by_label.emplace(c->labels[i], k);
+      c->class_label.push_back(c->labels[i]);
+      cls_of_table[i] = k;
+    } else {
+      cls_of_table[i] = it->second;
+    }
+  }
+  c->K = (uint32_t)c->class_label.size();
+  std::vector<uint32_t> class_of(WGPF_MAX_REGIONS);
+  for (uint32_t r = 0; r < WGPF_MAX_REGIONS; ++r)
+    class_of[r] = r < n_labels ? cls_of_table[r] : c->K + r;
+  std::vector<uint32_t> wait_class(c->K + 1, kNone);
+  std::vector<uint8_t> is_marker(c->K + 1, 0);
+  std::vector<std::pair<uint32_t, uint32_t>> swait;
+  for (uint32_t k = 0; k < c->K; ++k) {
+    const std::string& L = c->class_label[k];
+    is_marker[k] = L.size() > 5 && L.compare(L.size() - 5, 5, ".wait") == 0;
+    auto it = c->class_by_label.find(L + ".wait");
+    if (it != c->class_by_label.end()) wait_class[k] = it->second;
+    // out-of-table ids whose synthesized label is a table label
+    if (L.rfind("region#", 0) == 0) {
+      const std::string d = L.substr(7);
+      if (!d.empty() && d.size() <= 7 &&
+          d.find_first_not_of("0123456789") == std::string::npos) {
+        const unsigned long id = std::stoul(d);
+        if (id >= n_labels && id < WGPF_MAX_REGIONS &&
+            std::to_string(id) == d)
+          class_of[id] = k;
+      }
+    }
+    if (is_marker[k]) {
+      const std::string b = L.substr(0, L.size() - 5);
+      if (b.rfind("region#", 0) == 0) {
+        const std::string d = b.substr(7);
+        if (!d.empty() && d.size() <= 7 &&
+            d.find_first_not_of("0123456789") == std::string::npos) {
+          const unsigned long id = std::stoul(d);
+          if (id >= n_labels && id < WGPF_MAX_REGIONS &&
+              std::to_string(id) == d)
+            swait.emplace_back((uint32_t)id, k);
+        }
+      }
+    }
+  }
+  std::sort(swait.begin(), swait.end());
+  c->n_synth_wait = (uint32_t)swait.size();
+  std::vector<uint32_t> sw_id, sw_cls;
+  for (auto& p : swait) {
+    sw_id.push_back(p.first);
+    sw_cls.push_back(p.second);
+  }
+  ALLOC_OK(c, c->d_class_of, 4ull * WGPF_MAX_REGIONS);
+  ALLOC_OK(c, c->d_wait_class, 4ull * (c->K + 1));
+  ALLOC_OK(c, c->d_is_marker, c->K + 1);
+  ALLOC_OK(c, c->d_swait_id, 4ull * (sw_id.size() + 1));
+  ALLOC_OK(c, c->d_swait_cls, 4ull * (sw_id.size() + 1));
+  CUDA_OK(c, cudaMemcpyAsync(c->d_class_of.p, class_of.data(),
+                             4ull * WGPF_MAX_REGIONS, cudaMemcpyHostToDevice,
+                             c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(c->d_wait_class.p, wait_class.data(),
+                             4ull * (c->K + 1), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(c->d_is_marker.p, is_marker.data(), c->K + 1,
+                             cudaMemcpyHostToDevice, c->stream));
+  if (!sw_id.empty()) {
+    CUDA_OK(c, cudaMemcpyAsync(c->d_swait_id.p, sw_id.data(), 4 * sw_id.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(c, cudaMemcpyAsync(c->d_swait_cls.p, sw_cls.data(), 4 * sw_id.size(),
+                               cudaMemcpyHostToDevice, c->stream));
+  }
+  const size_t ns = n_slots(c);
+  ALLOC_OK(c, c->d_count, 8 * ns);
+  ALLOC_OK(c, c->d_sum, 8 * ns);
+  ALLOC_OK(c, c->d_min, 8 * ns);
+  ALLOC_OK(c, c->d_max, 8 * ns);
+  ALLOC_OK(c, c->d_first, 8 * ns);
+  ALLOC_OK(c, c->d_first_wg, 8 * ns);
+  ALLOC_OK(c, c->d_mean, 8 * ns);
+  ALLOC_OK(c, c->d_hist, 8 * ns * WGPF_HIST_BINS);
+  ALLOC_OK(c, c->d_hkey, 4 * kSynthHash);
+  int rc = stats_reset(c);
+  if (rc) return rc;
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->has_plan = true;
+  return WGPF_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// replay orchestration
+// ---------------------------------------------------------------------------
+
+static int run_general(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                       uint64_t n_streams, uint64_t stream_base,
+                       uint64_t record_cost, wgpf_event* events,
+                       uint64_t events_cap, bool no_stats, bool use_list,
+                       uint64_t n_work) {
+  if (n_work == 0) return WGPF_OK;
+  const uint32_t cap = (uint32_t)c->slots;
+  uint32_t hm = 16;
+  while (hm < 2u * cap + 2u) hm <<= 1;
+  const uint64_t per = gen_scratch_bytes(cap, hm);
+  uint64_t batch = std::max<uint64_t>(1, (256ull << 20) / per);
+  batch = std::min<uint64_t>(batch, n_work);
+  batch = (batch + 127) / 128 * 128;
+  ALLOC_OK(c, c->d_gscratch, per * batch);
+  GenArgs a;
+  a.body = body;
+  a.stride = stride;
+  a.n_streams = n_streams;
+  a.stream_base = stream_base;
+  a.plan = dev_plan(c);
+  a.stats = dev_stats(c);
+  a.status = c->d_status.as<DevStatus>();
+  a.counts = c->d_counts.as<uint32_t>();
+  a.sflag = c->d_sflag.as<uint32_t>();
+  a.offsets = c->d_offsets.as<uint64_t>();
+  a.events = events;
+  a.events_cap = events_cap;
+  a.record_cost = record_cost;
+  a.list = use_list ? c->d_glist.as<uint64_t>() : nullptr;
+  a.list_len = c->d_glen.as<unsigned long long>();
+  a.batch = batch;
+  a.scratch = c->d_gscratch.as<uint8_t>();
+  a.scratch_stride = per;
+  a.cap = cap;
+  a.hm_size = hm;
+  a.no_stats = no_stats ? 1u : 0u;
+  for (uint64_t first = 0; first < n_work; first += batch) {
+    a.first = first;
+    k_general_emit<<<(uint32_t)(batch / 128), 128, 0, c->stream>>>(a);
+    CUDA_OK(c, cudaGetLastError());
+  }
+  return WGPF_OK;
+}
+
+static int run_general_count(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                             uint64_t n_streams, uint64_t stream_base,
+                             uint64_t n_work) {
+  if (n_work == 0) return WGPF_OK;
+  const uint32_t cap = (uint32_t)c->slots;
+  uint32_t hm = 16;
+  while (hm < 2u * cap + 2u) hm <<= 1;
+  const uint64_t per = gen_scratch_bytes(cap, hm);
+  uint64_t batch = std::max<uint64_t>(1, (256ull << 20) / per);
+  batch = std::min<uint64_t>(batch, n_work);
+  batch = (batch + 127) / 128 * 128;
+  ALLOC_OK(c, c->d_gscratch, per * batch);
+  GenArgs a;
+  memset(&a, 0, sizeof a);
+  a.body = body;
+  a.stride = stride;
+  a.n_streams = n_streams;
+  a.stream_base = stream_base;
+  a.plan = dev_plan(c);
+  a.status = c->d_status.as<DevStatus>();
+  a.counts = c->d_counts.as<uint32_t>();
+  a.sflag = c->d_sflag.as<uint32_t>();
+  a.list = c->d_glist.as<uint64_t>();
+  a.list_len = c->d_glen.as<unsigned long long>();
+  a.batch = batch;
+  a.scratch = c->d_gscratch.as<uint8_t>();
+  a.scratch_stride = per;
+  a.cap = cap;
+  a.hm_size = hm;
+  for (uint64_t first = 0; first < n_work; first += batch) {
+    a.first = first;
+    k_general_count<<<(uint32_t)(batch / 128), 128, 0, c->stream>>>(a);
+    CUDA_OK(c, cudaGetLastError());
+  }
+  return WGPF_OK;
+}
+
+__global__ void k_total(const uint32_t* counts, const uint64_t* off, uint64_t n,
+                        DevStatus* st) {
+  st->total_events = n ? off[n - 1] + counts[n - 1] : 0;
+}
+
+// streams flagged SF_INVALID -> general list (and SF_GENERAL for the re-emit)
+__global__ void k_collect_invalid(uint32_t* sflag, uint64_t n,
+                                  unsigned long long* list,
+                                  unsigned long long* len) {
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (uint64_t)gridDim.x * blockDim.x)
+    if (sflag[s] & SF_INVALID) {
+      sflag[s] = (sflag[s] & ~SF_INVALID) | SF_GENERAL;
+      list[atomicAdd(len, 1ull)] = s;
+    }
+}
+
+static int scan_counts(wgpf_ctx* c, uint64_t n) {
+  size_t tmp = 0;
+  const uint32_t* in = c->d_counts.as<uint32_t>();
+  uint64_t* out = c->d_offsets.as<uint64_t>();
+  // widen to 64-bit accumulation
+  auto it = thrust::make_transform_iterator(in, ToU64());
+  CUDA_OK(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, it, out, (int64_t)n,
+                                           c->stream));
+  ALLOC_OK(c, c->d_scan_tmp, tmp);
+  CUDA_OK(c, cub::DeviceScan::ExclusiveSum(c->d_scan_tmp.p, tmp, it, out,
+                                           (int64_t)n, c->stream));
+  k_total<<<1, 1, 0, c->stream>>>(in, out, n, c->d_status.as<DevStatus>());
+  CUDA_OK(c, cudaGetLastError());
+  return WGPF_OK;
+}
+
+static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                     uint64_t n_streams, uint64_t stream_base,
+                     uint64_t record_cost, wgpf_event* events,
+                     uint64_t events_cap, bool no_stats, bool force_general) {
+  CUDA_OK(c, cudaMemsetAsync(c->d_glen.p, 0, 8, c->stream));
+  if (force_general) {
+    int rc = run_general(c, body, stride, n_streams, stream_base, record_cost,
+                         events, events_cap, no_stats, false, n_streams);
+    return rc;
+  }
+  FastArgs f;
+  f.body = body;
+  f.stride = stride;
+  f.n_streams = n_streams;
+  f.stream_base = stream_base;
+  f.plan = dev_plan(c);
+  f.stats = dev_stats(c);
+  f.status = c->d_status.as<DevStatus>();
+  f.counts = c->d_counts.as<uint32_t>();
+  f.zpos = c->d_zpos.as<int32_t>();
+  f.sflag = c->d_sflag.as<uint32_t>();
+  f.offsets = c->d_offsets.as<uint64_t>();
+  f.events = events;
+  f.events_cap = events_cap;
+  f.record_cost = record_cost;
+  f.cap = (uint32_t)c->slots;
+  f.fast_regions = std::min<uint32_t>((uint32_t)c->labels.size(), kFastRegions);
+  f.no_stats = no_stats ? 1u : 0u;
+  f.general_list = c->d_glist.as<unsigned long long>();
+  f.general_len = c->d_glen.as<unsigned long long>();
+  const uint32_t grid =
+      grid_for(c, (const void*)k_fast_emit, kFastWarps * 32, sizeof(FastSmem));
+  ALLOC_OK(c, c->d_orphans,
+           sizeof(wgpf_event) * (uint64_t)grid * kFastWarps * (c->slots / 2 + 1));
+  f.orphan_scratch = c->d_orphans.as<wgpf_event>();
+  k_fast_emit<<<grid, kFastWarps * 32, sizeof(FastSmem), c->stream>>>(f);
+  CUDA_OK(c, cudaGetLastError());
+  // streams the fast path routed away
+  unsigned long long glen = 0;
+  CUDA_OK(c, cudaMemcpyAsync(&glen, c->d_glen.p, 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  return run_general(c, body, stride, n_streams, stream_base, record_cost,
+                     events, events_cap, no_stats, true, glen);
+}
+
+static int report_errors(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                         uint64_t stream_base) {
+  const DevStatus& st = *c->h_status;
+  if (st.decode_err != kNoErr) {
+    const uint64_t s = st.decode_err >> 2;
+    const uint32_t code = (uint32_t)(st.decode_err & 3u);
+    if (code == DEC_CAP) {
+      wgpf_stream_hdr h;
+      CUDA_OK(c, cudaMemcpy(&h, body + s * stride, 16, cudaMemcpyDeviceToHost));
+      return set_err(c, WGPF_E_TRACE,
+                     "stream capacity %u does not match the buffer plan (%llu)",
+                     h.slot_capacity, (unsigned long long)c->slots);
+    }
+    if (code == DEC_FLUSH)
+      return set_err(c, WGPF_E_TRACE,
+                     "flush stream claims more records than slots");
+    return set_err(c, WGPF_E_TRACE, "circular stream has zero slot capacity");
+  }
+  if (st.pair_err != kNoErr) {
+    const uint64_t gs = st.pair_err >> 32;
+    const uint32_t pos = (uint32_t)(st.pair_err & 0xFFFFFFFFu);
+    const uint64_t s = gs - stream_base;
+    wgpf_stream_hdr h;
+    CUDA_OK(c, cudaMemcpy(&h, body + s * stride, 16, cudaMemcpyDeviceToHost));
+    const uint32_t start =
+        h.record_count <= h.slot_capacity ? 0u : h.record_count % h.slot_capacity;
+    uint32_t slot = start + pos;
+    if (slot >= h.slot_capacity) slot -= h.slot_capacity;
+    wgpf_record r;
+    CUDA_OK(c, cudaMemcpy(&r, body + s * stride + 16 + 8ull * slot, 8,
+                          cudaMemcpyDeviceToHost));
+    const uint32_t rid = (r.tag >> 12) & (WGPF_MAX_REGIONS - 1u);
+    return set_err(c, WGPF_E_TRACE,
+                   "interval \"%s\" exceeds 2^32 cycles; the 32-bit clock "
+                   "cannot represent it",
+                   label_of(c, rid).c_str());
+  }
+  return WGPF_OK;
+}
+
+static int finalize_stats(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                          uint64_t stream_base, uint64_t n_streams,
+                          const wgpf_event* events, uint64_t n_events,
+                          bool exact) {
+  const uint32_t ns = n_slots(c);
+  k_resolve_first<<<(ns + 127) / 128, 128, 0, c->stream>>>(
+      dev_stats(c), ns, body, stride, stream_base, n_streams,
+      c->d_first_wg.as<unsigned long long>());
+  CUDA_OK(c, cudaGetLastError());
+  c->mean_exact_valid = false;
+  if (exact && events && n_events) {
+    // stable class sort of durations, then the recurrence per class
+    ALLOC_OK(c, c->d_aux0, 4 * n_events);
+    ALLOC_OK(c, c->d_aux1, 8 * n_events);
+    ALLOC_OK(c, c->d_aux2, 4 * n_events);
+    ALLOC_OK(c, c->d_aux3, 8 * n_events);
+    k_event_class_dur<<<c->sms * 8, 256, 0, c->stream>>>(
+        events, n_events, dev_plan(c), c->d_aux0.as<uint32_t>(),
+        c->d_aux1.as<unsigned long long>());
+    CUDA_OK(c, cudaGetLastError());
+    size_t tmp = 0;
+    CUDA_OK(c, cub::DeviceRadixSort::SortPairs(
+                   nullptr, tmp, c->d_aux0.as<uint32_t>(), c->d_aux2.as<uint32_t>(),
+                   c->d_aux1.as<unsigned long long>(),
+                   c->d_aux3.as<unsigned long long>(), (int64_t)n_events, 0, 32,
+                   c->stream));
+    ALLOC_OK(c, c->d_scan_tmp, tmp);
+    CUDA_OK(c, cub::DeviceRadixSort::SortPairs(
+                   c->d_scan_tmp.p, tmp, c->d_aux0.as<uint32_t>(),
+                   c->d_aux2.as<uint32_t>(), c->d_aux1.as<unsigned long long>(),
+                   c->d_aux3.as<unsigned long long>(), (int64_t)n_events, 0, 32,
+                   c->stream));
+    k_exact_mean<<<(ns + 127) / 128, 128, 0, c->stream>>>(
+        c->d_aux2.as<uint32_t>(), c->d_aux3.as<unsigned long long>(), n_events,
+        dev_stats(c), ns, c->d_mean.as<double>(), nullptr);
+    CUDA_OK(c, cudaGetLastError());
+    c->mean_exact_valid = true;
+  }
+  c->stats_valid = true;
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
+                                  uint64_t body_bytes, uint64_t n_streams,
+                                  uint64_t stream_base, uint64_t record_cost,
+                                  wgpf_event* d_events, uint64_t events_cap,
+                                  uint32_t flags, uint64_t* n_events,
+                                  wgpf_warnings* warnings) {
+  if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
+  if (n_events) *n_events = 0;
+  if (warnings) memset(warnings, 0, sizeof *warnings);
+  const uint64_t stride = 16ull + 8ull * c->slots;
+  if (body_bytes < n_streams * stride)
+    return set_err(c, WGPF_E_ARG, "body of %llu bytes < %llu streams x %llu",
+                   (unsigned long long)body_bytes,
+                   (unsigned long long)n_streams, (unsigned long long)stride);
+  if (c->slots >= (1ull << 31))
+    return set_err(c, WGPF_E_ARG, "slot capacity too large");
+  if ((reinterpret_cast<uintptr_t>(d_body) & 15u) || (stride & 15u)) {
+    // the kernels read 16-byte headers with vector loads
+    return set_err(c, WGPF_E_ARG,
+                   "KPFT body must be 16-byte aligned with an even capacity");
+  }
+  const bool stats_only = flags & WGPF_F_STATS_ONLY;
+  const bool no_stats = flags & WGPF_F_NO_STATS;
+  const bool force_general = flags & WGPF_F_FORCE_GENERAL;
+  wgpf_event* events = stats_only ? nullptr : d_events;
+  const uint8_t* body = static_cast<const uint8_t*>(d_body);
+  int rc = status_reset(c);
+  if (rc) return rc;
+  rc = stats_reset(c);
+  if (rc) return rc;
+  c->last_body = body;
+  c->last_stride = stride;
+  c->last_stream_base = stream_base;
+  c->last_n_streams = n_streams;
+  if (n_streams == 0) {
+    c->stats_valid = true;
+    return WGPF_OK;
+  }
+  ALLOC_OK(c, c->d_counts, 4 * n_streams);
+  ALLOC_OK(c, c->d_zpos, 4 * n_streams);
+  ALLOC_OK(c, c->d_sflag, 4 * n_streams);
+  ALLOC_OK(c, c->d_offsets, 8 * n_streams);
+  ALLOC_OK(c, c->d_glist, 8 * n_streams);
+
+  CountArgs ca;
+  ca.body = body;
+  ca.stride = stride;
+  ca.n_streams = n_streams;
+  ca.plan = dev_plan(c);
+  ca.counts = c->d_counts.as<uint32_t>();
+  ca.zpos = c->d_zpos.as<int32_t>();
+  ca.sflag = c->d_sflag.as<uint32_t>();
+  ca.status = c->d_status.as<DevStatus>();
+  ca.fast_regions = std::min<uint32_t>((uint32_t)c->labels.size(), kFastRegions);
+  ca.max_depth = kMaxDepth;
+  ca.force_general = force_general ? 1u : 0u;
+  k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
+                 c->stream>>>(ca);
+  CUDA_OK(c, cudaGetLastError());
+  rc = scan_counts(c, n_streams);
+  if (rc) return rc;
+  rc = emit_pass(c, body, stride, n_streams, stream_base, record_cost, events,
+                 events_cap, no_stats, force_general);
+  if (rc) return rc;
+  rc = status_read(c);
+  if (rc) return rc;
+  if (c->h_status->invalid && c->h_status->decode_err == kNoErr) {
+    // exact recount of the streams that broke the single-stack assumption,
+    // then re-emit everything at the corrected offsets
+    CUDA_OK(c, cudaMemsetAsync(c->d_glen.p, 0, 8, c->stream));
+    k_collect_invalid<<<c->sms * 4, 256, 0, c->stream>>>(
+        c->d_sflag.as<uint32_t>(), n_streams,
+        c->d_glist.as<unsigned long long>(), c->d_glen.as<unsigned long long>());
+    unsigned long long n_inv = 0;
+    CUDA_OK(c, cudaMemcpyAsync(&n_inv, c->d_glen.p, 8, cudaMemcpyDeviceToHost,
+                               c->stream));
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    rc = run_general_count(c, body, stride, n_streams, stream_base, n_inv);
+    if (rc) return rc;
+    const unsigned long long pair_err = c->h_status->pair_err;
+    rc = status_reset(c);
+    if (rc) return rc;
+    rc = stats_reset(c);
+    if (rc) return rc;
+    rc = scan_counts(c, n_streams);
+    if (rc) return rc;
+    rc = emit_pass(c, body, stride, n_streams, stream_base, record_cost,
+                   events, events_cap, no_stats, force_general);
+    if (rc) return rc;
+    rc = status_read(c);
+    if (rc) return rc;
+    if (pair_err < c->h_status->pair_err) c->h_status->pair_err = pair_err;
+  }
+  rc = report_errors(c, body, stride, stream_base);
+  if (rc) return rc;
+  const DevStatus& st = *c->h_status;
+  if (n_events) *n_events = st.total_events;
+  if (warnings) {
+    warnings->dropped_heads = (uint32_t)st.warn[0];
+    warnings->truncated_tails = (uint32_t)st.warn[1];
+    warnings->flagged_preconditions = (uint32_t)st.warn[2];
+    warnings->malformed_groups = (uint32_t)st.warn[3];
+  }
+  if (st.synth_overflow)
+    return set_err(c, WGPF_E_CAPACITY,
+                   "more than %u distinct out-of-table region labels",
+                   kSynthHash);
+  if (events && st.total_events > events_cap)
+    return set_err(c, WGPF_E_BUFFER, "event buffer holds %llu of %llu events",
+                   (unsigned long long)events_cap,
+                   (unsigned long long)st.total_events);
+  if (!no_stats) {
+    rc = finalize_stats(c, body, stride, stream_base, n_streams, events,
+                        st.total_events, (flags & WGPF_F_EXACT_MEAN) != 0);
+    if (rc) return rc;
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  }
+  return WGPF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-image entry points
+// ---------------------------------------------------------------------------
+
+static uint32_t rd32(const uint8_t* p) {
+  return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) |
+         ((uint32_t)p[3] << 24);
+}
+
+// deserialize_image framing (trace.hpp:181-209) followed by the first
+// decode_image error (trace.hpp:222-251), walking the host headers.  Only
+// used when the image is not a uniform body of the plan's capacity.
+static int host_walk(wgpf_ctx* c, const uint8_t* b, uint64_t n, uint64_t pos,
+                     uint64_t count) {
+  std::vector<wgpf_stream_hdr> hdr;
+  for (uint64_t s = 0; s < count; ++s) {
+    if (pos + 16 > n) return set_err(c, WGPF_E_TRACE, "truncated trace image");
+    wgpf_stream_hdr h{rd32(b + pos), rd32(b + pos + 4), rd32(b + pos + 8),
+                      rd32(b + pos + 12)};
+    pos += 16;
+    const uint64_t need = 8ull * h.slot_capacity;
+    if (pos + need > n) return set_err(c, WGPF_E_TRACE, "truncated trace image");
+    pos += need;
+    hdr.push_back(h);
+  }
+  if (pos != n)
+    return set_err(c, WGPF_E_TRACE, "trailing bytes after trace image");
+  for (const auto& h : hdr) {
+    if ((uint64_t)h.slot_capacity != c->slots)
+      return set_err(c, WGPF_E_TRACE,
+                     "stream capacity %u does not match the buffer plan (%llu)",
+                     h.slot_capacity, (unsigned long long)c->slots);
+    if (h.record_count > h.slot_capacity) {
+      if (c->strategy == WGPF_STRATEGY_FLUSH)
+        return set_err(c, WGPF_E_TRACE,
+                       "flush stream claims more records than slots");
+      if (h.slot_capacity == 0)
+        return set_err(c, WGPF_E_TRACE, "circular stream has zero slot capacity");
+    }
+  }
+  return set_err(c, WGPF_E_TRACE, "internal: image walk found no error");
+}
+
+// Parses the KPFT file header; on success *body_off / *count are set.
+static int parse_header(wgpf_ctx* c, const uint8_t* b, uint64_t n,
+                        uint64_t* body_off, uint64_t* count) {
+  if (n < 4) return set_err(c, WGPF_E_TRACE, "truncated trace image");
+  if (memcmp(b, "KPFT", 4) != 0)
+    return set_err(c, WGPF_E_TRACE, "bad magic: not a trace image");
+  if (n < 6) return set_err(c, WGPF_E_TRACE, "truncated trace image");
+  const uint16_t version = (uint16_t)(b[4] | (b[5] << 8));
+  if (version == 1) {
+    if (n < 8) return set_err(c, WGPF_E_TRACE, "truncated trace image");
+    *count = (uint16_t)(b[6] | (b[7] << 8));
+    *body_off = 8;
+  } else if (version == 2) {
+    if (n < 16) return set_err(c, WGPF_E_TRACE, "truncated trace image");
+    *count = (uint64_t)rd32(b + 8) | ((uint64_t)rd32(b + 12) << 32);
+    *body_off = 16;
+  } else {
+    return set_err(c, WGPF_E_TRACE, "unsupported trace version %u",
+                   (unsigned)version);
+  }
+  return WGPF_OK;
+}
+
+// Stages the image body on the device; returns the device body pointer.
+static int stage_image(wgpf_ctx* c, const uint8_t* kpft, uint64_t n,
+                       const uint8_t** d_body, uint64_t* n_streams) {
+  uint64_t off = 0, count = 0;
+  int rc = parse_header(c, kpft, n, &off, &count);
+  if (rc) return rc;
+  const uint64_t stride = 16ull + 8ull * c->slots;
+  const uint64_t body = n - off;
+  if (count == 0 || body / stride != count || body % stride != 0 ||
+      (stride & 15u)) {
+    // not a uniform body of the plan capacity: the reference would fail in
+    // deserialize or decode (or it is empty)
+    if (count == 0 && body == 0) {
+      *n_streams = 0;
+      *d_body = nullptr;
+      return WGPF_OK;
+    }
+    if (body / stride == count && body % stride == 0 && (stride & 15u)) {
+      return set_err(c, WGPF_E_ARG,
+                     "odd slot capacities are not supported by the device path");
+    }
+    return host_walk(c, kpft, n, off, count);
+  }
+  ALLOC_OK(c, c->d_image, body);
+  CUDA_OK(c, cudaMemcpyAsync(c->d_image.p, kpft + off, body,
+                             cudaMemcpyHostToDevice, c->stream));
+  *d_body = c->d_image.as<uint8_t>();
+  *n_streams = count;
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_replay_image(wgpf_ctx* c, const uint8_t* kpft,
+                                 uint64_t n_bytes, uint64_t record_cost,
+                                 wgpf_event* h_events, uint64_t events_cap,
+                                 uint32_t flags, uint64_t* n_events,
+                                 wgpf_warnings* warnings) {
+  if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
+  if (n_events) *n_events = 0;
+  if (warnings) memset(warnings, 0, sizeof *warnings);
+  const uint8_t* d_body = nullptr;
+  uint64_t ns = 0;
+  int rc = stage_image(c, kpft, n_bytes, &d_body, &ns);
+  if (rc) {
+    // a capacity mismatch found on the device must still be checked
+    // against deserialize framing; stage_image already walked it.
+    return rc;
+  }
+  const uint64_t stride = 16ull + 8ull * c->slots;
+  const bool want_events = !(flags & WGPF_F_STATS_ONLY) && h_events;
+  // device event buffer sized by the caller's capacity
+  wgpf_event* d_ev = nullptr;
+  if (want_events) {
+    ALLOC_OK(c, c->d_events, sizeof(wgpf_event) * std::max<uint64_t>(events_cap, 1));
+    d_ev = c->d_events.as<wgpf_event>();
+  }
+  uint64_t ne = 0;
+  rc = wgpf_replay_device(c, d_body, ns * stride, ns, 0, record_cost, d_ev,
+                          want_events ? events_cap : 0,
+                          want_events ? flags : (flags | WGPF_F_STATS_ONLY),
+                          &ne, warnings);
+  if (rc == WGPF_E_TRACE && c->h_status->decode_err != kNoErr &&
+      c->h_status->cap_mismatch) {
+    // uniform size but a stream's capacity differs: the reference's
+    // deserialize walk decides between framing and decode errors
+    uint64_t off = 0, count = 0;
+    parse_header(c, kpft, n_bytes, &off, &count);
+    return host_walk(c, kpft, n_bytes, off, count);
+  }
+  if (n_events) *n_events = ne;
+  if (rc) return rc;
+  if (want_events && ne) {
+    CUDA_OK(c, cudaMemcpyAsync(h_events, d_ev, sizeof(wgpf_event) * ne,
+                               cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  }
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
+                                 uint64_t n_bytes, wgpf_record* h_records,
+                                 uint64_t records_cap, uint64_t* n_records,
+                                 wgpf_decoded_stream* h_streams,
+                                 uint64_t streams_cap, uint64_t* n_streams) {
+  if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
+  *n_records = 0;
+  *n_streams = 0;
+  const uint8_t* d_body = nullptr;
+  uint64_t ns = 0;
+  int rc = stage_image(c, kpft, n_bytes, &d_body, &ns);
+  if (rc) return rc;
+  if (ns == 0) return WGPF_OK;
+  const uint64_t stride = 16ull + 8ull * c->slots;
+  // decode checks via pass 1
+  int r2 = status_reset(c);
+  if (r2) return r2;
+  ALLOC_OK(c, c->d_counts, 4 * ns);
+  ALLOC_OK(c, c->d_zpos, 4 * ns);
+  ALLOC_OK(c, c->d_sflag, 4 * ns);
+  CountArgs ca;
+  ca.body = d_body;
+  ca.stride = stride;
+  ca.n_streams = ns;
+  ca.plan = dev_plan(c);
+  ca.counts = c->d_counts.as<uint32_t>();
+  ca.zpos = c->d_zpos.as<int32_t>();
+  ca.sflag = c->d_sflag.as<uint32_t>();
+  ca.status = c->d_status.as<DevStatus>();
+  ca.fast_regions = 0;
+  ca.max_depth = kMaxDepth;
+  ca.force_general = 1;
+  k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
+                 c->stream>>>(ca);
+  CUDA_OK(c, cudaGetLastError());
+  r2 = status_read(c);
+  if (r2) return r2;
+  if (c->h_status->decode_err != kNoErr) {
+    if (c->h_status->cap_mismatch) {
+      uint64_t off = 0, count = 0;
+      parse_header(c, kpft, n_bytes, &off, &count);
+      return host_walk(c, kpft, n_bytes, off, count);
+    }
+    return report_errors(c, d_body, stride, 0);
+  }
+  ALLOC_OK(c, c->d_aux1, 8 * ns);
+  ALLOC_OK(c, c->d_aux3, 8 * ns);
+  ALLOC_OK(c, c->d_aux2, sizeof(wgpf_decoded_stream) * ns);
+  k_decode_counts<<<c->sms * 4, 256, 0, c->stream>>>(
+      d_body, stride, ns, c->d_aux1.as<uint64_t>(),
+      c->d_aux2.as<wgpf_decoded_stream>());
+  size_t tmp = 0;
+  CUDA_OK(c, cub::DeviceScan::ExclusiveSum(nullptr, tmp, c->d_aux1.as<uint64_t>(),
+                                           c->d_aux3.as<uint64_t>(), (int64_t)ns,
+                                           c->stream));
+  ALLOC_OK(c, c->d_scan_tmp, tmp);
+  CUDA_OK(c, cub::DeviceScan::ExclusiveSum(c->d_scan_tmp.p, tmp,
+                                           c->d_aux1.as<uint64_t>(),
+                                           c->d_aux3.as<uint64_t>(), (int64_t)ns,
+                                           c->stream));
+  std::vector<uint64_t> cnt(ns), off(ns);
+  CUDA_OK(c, cudaMemcpyAsync(cnt.data(), c->d_aux1.p, 8 * ns,
+                             cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(off.data(), c->d_aux3.p, 8 * ns,
+                             cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  const uint64_t total = off[ns - 1] + cnt[ns - 1];
+  *n_records = total;
+  *n_streams = ns;
+  if (total > records_cap || ns > streams_cap)
+    return set_err(c, WGPF_E_BUFFER, "decode needs %llu records / %llu streams",
+                   (unsigned long long)total, (unsigned long long)ns);
+  ALLOC_OK(c, c->d_aux0, sizeof(wgpf_record) * std::max<uint64_t>(total, 1));
+  k_decode_records<<<c->sms * 4, 256, 0, c->stream>>>(
+      d_body, stride, ns, c->d_aux3.as<uint64_t>(), c->d_aux0.as<wgpf_record>());
+  CUDA_OK(c, cudaGetLastError());
+  std::vector<wgpf_decoded_stream> ds(ns);
+  CUDA_OK(c, cudaMemcpyAsync(ds.data(), c->d_aux2.p,
+                             sizeof(wgpf_decoded_stream) * ns,
+                             cudaMemcpyDeviceToHost, c->stream));
+  if (total)
+    CUDA_OK(c, cudaMemcpyAsync(h_records, c->d_aux0.p, sizeof(wgpf_record) * total,
+                               cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  for (uint64_t s = 0; s < ns; ++s) {
+    ds[s].offset = off[s];
+    h_streams[s] = ds[s];
+  }
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_unwrap_clock(wgpf_ctx* c, const uint32_t* h_values,
+                                 uint64_t n, uint64_t* h_out) {
+  if (n == 0) return WGPF_OK;
+  ALLOC_OK(c, c->d_aux0, 4 * n);
+  ALLOC_OK(c, c->d_aux2, 4 * n);
+  ALLOC_OK(c, c->d_aux1, 8 * n);
+  ALLOC_OK(c, c->d_aux3, 8 * n);
+  CUDA_OK(c, cudaMemcpyAsync(c->d_aux0.p, h_values, 4 * n,
+                             cudaMemcpyHostToDevice, c->stream));
+  k_unwrap_flags<<<c->sms * 4, 256, 0, c->stream>>>(c->d_aux0.as<uint32_t>(), n,
+                                                   c->d_aux2.as<uint32_t>());
+  auto it = thrust::make_transform_iterator(c->d_aux2.as<uint32_t>(), ToU64());
+  size_t tmp = 0;
+  CUDA_OK(c, cub::DeviceScan::InclusiveSum(nullptr, tmp, it,
+                                           c->d_aux1.as<uint64_t>(), (int64_t)n,
+                                           c->stream));
+  ALLOC_OK(c, c->d_scan_tmp, tmp);
+  CUDA_OK(c, cub::DeviceScan::InclusiveSum(c->d_scan_tmp.p, tmp, it,
+                                           c->d_aux1.as<uint64_t>(), (int64_t)n,
+                                           c->stream));
+  k_unwrap_combine<<<c->sms * 4, 256, 0, c->stream>>>(
+      c->d_aux0.as<uint32_t>(), c->d_aux1.as<uint64_t>(), n,
+      c->d_aux3.as<uint64_t>());
+  CUDA_OK(c, cudaGetLastError());
+  CUDA_OK(c, cudaMemcpyAsync(h_out, c->d_aux3.p, 8 * n, cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_pair_records(wgpf_ctx* c, const wgpf_record* h_records,
+                                 uint64_t n, wgpf_interval* h_out, uint64_t cap,
+                                 uint64_t* n_out, uint32_t* dropped_heads,
+                                 uint32_t* truncated_tails) {
+  if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
+  *n_out = 0;
+  if (n >= (1ull << 31)) return set_err(c, WGPF_E_ARG, "stream too long");
+  const uint64_t stride = 16 + 8 * n;
+  ALLOC_OK(c, c->d_image, stride);
+  wgpf_stream_hdr h{0, 0, (uint32_t)n, (uint32_t)n};
+  CUDA_OK(c, cudaMemcpyAsync(c->d_image.p, &h, 16, cudaMemcpyHostToDevice,
+                             c->stream));
+  if (n)
+    CUDA_OK(c, cudaMemcpyAsync(c->d_image.as<uint8_t>() + 16, h_records, 8 * n,
+                               cudaMemcpyHostToDevice, c->stream));
+  int rc = status_reset(c);
+  if (rc) return rc;
+  uint32_t hm = 16;
+  while (hm < 2u * (uint32_t)n + 2u) hm <<= 1;
+  const uint64_t per = gen_scratch_bytes((uint32_t)std::max<uint64_t>(n, 1), hm);
+  ALLOC_OK(c, c->d_gscratch, per);
+  ALLOC_OK(c, c->d_aux1, sizeof(wgpf_interval) * (n / 2 + 1));
+  ALLOC_OK(c, c->d_aux0, 16);
+  GenArgs a;
+  memset(&a, 0, sizeof a);
+  a.body = c->d_image.as<uint8_t>();
+  a.stride = stride;
+  a.n_streams = 1;
+  a.plan = dev_plan(c);
+  a.status = c->d_status.as<DevStatus>();
+  a.scratch = c->d_gscratch.as<uint8_t>();
+  a.scratch_stride = per;
+  a.cap = (uint32_t)std::max<uint64_t>(n, 1);
+  a.hm_size = hm;
+  k_pair_one<<<1, 1, 0, c->stream>>>(a, c->d_aux1.as<wgpf_interval>(),
+                                      c->d_aux0.as<uint32_t>());
+  CUDA_OK(c, cudaGetLastError());
+  uint32_t info[3];
+  CUDA_OK(c, cudaMemcpyAsync(info, c->d_aux0.p, 12, cudaMemcpyDeviceToHost,
+                             c->stream));
+  rc = status_read(c);
+  if (rc) return rc;
+  if (c->h_status->pair_err != kNoErr) {
+    const uint32_t pos = (uint32_t)(c->h_status->pair_err & 0xFFFFFFFFu);
+    const uint32_t rid = (h_records[pos].tag >> 12) & (WGPF_MAX_REGIONS - 1u);
+    return set_err(c, WGPF_E_TRACE,
+                   "interval \"%s\" exceeds 2^32 cycles; the 32-bit clock "
+                   "cannot represent it",
+                   label_of(c, rid).c_str());
+  }
+  *n_out = info[0];
+  if (dropped_heads) *dropped_heads = info[1];
+  if (truncated_tails) *truncated_tails = info[2];
+  if (info[0] > cap)
+    return set_err(c, WGPF_E_BUFFER, "pair_records needs %u intervals", info[0]);
+  if (info[0])
+    CUDA_OK(c, cudaMemcpy(h_out, c->d_aux1.p, sizeof(wgpf_interval) * info[0],
+                          cudaMemcpyDeviceToHost));
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_replay_intervals(wgpf_ctx* c, const wgpf_interval* h_iv,
+                                     uint64_t n, uint32_t block_index,
+                                     uint32_t warp_group, uint64_t record_cost,
+                                     wgpf_event* h_out, uint64_t cap,
+                                     uint64_t* n_out, wgpf_warnings* w) {
+  if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
+  *n_out = 0;
+  if (w) memset(w, 0, sizeof *w);
+  ALLOC_OK(c, c->d_aux0, sizeof(wgpf_interval) * (n + 1));
+  ALLOC_OK(c, c->d_aux1, sizeof(wgpf_event) * (n + 1));
+  ALLOC_OK(c, c->d_aux2, n + 1);
+  ALLOC_OK(c, c->d_aux3, 32);
+  if (n)
+    CUDA_OK(c, cudaMemcpyAsync(c->d_aux0.p, h_iv, sizeof(wgpf_interval) * n,
+                               cudaMemcpyHostToDevice, c->stream));
+  k_replay_one<<<1, 1, 0, c->stream>>>(
+      c->d_aux0.as<wgpf_interval>(), n, dev_plan(c), block_index, warp_group,
+      record_cost, c->d_aux2.as<uint8_t>(), c->d_aux1.as<wgpf_event>(),
+      c->d_aux3.as<unsigned long long>());
+  CUDA_OK(c, cudaGetLastError());
+  unsigned long long info[3];
+  CUDA_OK(c, cudaMemcpyAsync(info, c->d_aux3.p, 24, cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  *n_out = info[0];
+  if (w) {
+    w->flagged_preconditions = (uint32_t)info[1];
+    w->malformed_groups = (uint32_t)info[2];
+  }
+  if (info[0] > cap)
+    return set_err(c, WGPF_E_BUFFER, "replay needs %llu events", info[0]);
+  if (info[0])
+    CUDA_OK(c, cudaMemcpy(h_out, c->d_aux1.p, sizeof(wgpf_event) * info[0],
+                          cudaMemcpyDeviceToHost));
+  return WGPF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// statistics read-out
+// ---------------------------------------------------------------------------
+
+static int read_stats(wgpf_ctx* c, bool event_keys) {
+  const uint32_t ns = n_slots(c);
+  std::vector<unsigned long long> cnt(ns), sum(ns), mn(ns), mx(ns), first(ns),
+      fwg(ns), hist((size_t)ns * WGPF_HIST_BINS);
+  std::vector<double> mean(ns);
+  std::vector<uint32_t> hkey(kSynthHash);
+  CUDA_OK(c, cudaMemcpyAsync(cnt.data(), c->d_count.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(sum.data(), c->d_sum.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(mn.data(), c->d_min.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(mx.data(), c->d_max.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(first.data(), c->d_first.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(fwg.data(), c->d_first_wg.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(hist.data(), c->d_hist.p, 8ull * ns * WGPF_HIST_BINS, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaMemcpyAsync(hkey.data(), c->d_hkey.p, 4 * kSynthHash, cudaMemcpyDeviceToHost, c->stream));
+  if (c->mean_exact_valid)
+    CUDA_OK(c, cudaMemcpyAsync(mean.data(), c->d_mean.p, 8 * ns, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  std::vector<std::pair<std::string, uint32_t>> order;
+  for (uint32_t i = 0; i < ns; ++i) {
+    if (!cnt[i]) continue;
+    const uint32_t cls = i < c->K ? i : hkey[i - c->K];
+    order.emplace_back(class_name(c, cls), i);
+  }
+  std::sort(order.begin(), order.end());
+  c->stats_out.clear();
+  c->stats_names.clear();
+  c->stats_names.reserve(order.size());
+  for (auto& [name, i] : order) {
+    c->stats_names.push_back(name);
+    wgpf_region_stat r;
+    memset(&r, 0, sizeof r);
+    r.warp_group = (uint32_t)fwg[i];
+    r.kind = (uint32_t)(first[i] & 1u);
+    r.count = cnt[i];
+    r.min = mn[i];
+    r.max = mx[i];
+    r.sum = sum[i];
+    r.mean = c->mean_exact_valid ? mean[i] : (double)sum[i] / (double)cnt[i];
+    if (event_keys) {
+      r.first_event = first[i] >> 1;
+    } else {
+      // (stream << 25 | k << 1 | kind): global event index when the stream
+      // is local to this context (offsets of the last replay), else ~0
+      const uint64_t gs = first[i] >> 25;
+      const uint64_t k = (first[i] >> 1) & ((1ull << 24) - 1);
+      r.first_event = ~0ull;
+      if (gs >= c->last_stream_base &&
+          gs - c->last_stream_base < c->last_n_streams && c->d_offsets.p) {
+        uint64_t off = 0;
+        CUDA_OK(c, cudaMemcpy(&off,
+                              c->d_offsets.as<uint64_t>() + (gs - c->last_stream_base),
+                              8, cudaMemcpyDeviceToHost));
+        r.first_event = off + k;
+      }
+    }
+    for (uint32_t b = 0; b < WGPF_HIST_BINS; ++b)
+      r.hist[b] = hist[(size_t)i * WGPF_HIST_BINS + b];
+    c->stats_out.push_back(r);
+  }
+  for (size_t k = 0; k < c->stats_out.size(); ++k)
+    c->stats_out[k].label = c->stats_names[k].c_str();
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_stats_get(wgpf_ctx* c, wgpf_region_stat* out,
+                              uint32_t cap, uint32_t* n) {
+  *n = 0;
+  if (!c->has_plan || !c->stats_valid)
+    return set_err(c, WGPF_E_ARG, "no statistics available");
+  int rc = read_stats(c, false);
+  if (rc) return rc;
+  *n = (uint32_t)c->stats_out.size();
+  if (c->stats_out.size() > cap)
+    return set_err(c, WGPF_E_BUFFER, "stats need %u entries", *n);
+  for (size_t k = 0; k < c->stats_out.size(); ++k) out[k] = c->stats_out[k];
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_region_stats(wgpf_ctx* c, const wgpf_event* events,
+                                 uint64_t n, int on_device, uint32_t flags,
+                                 wgpf_region_stat* out, uint32_t cap,
+                                 uint32_t* n_out) {
+  if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
+  *n_out = 0;
+  int rc = status_reset(c);
+  if (rc) return rc;
+  rc = stats_reset(c);
+  if (rc) return rc;
+  const wgpf_event* d_ev = events;
+  if (!on_device) {
+    ALLOC_OK(c, c->d_events, sizeof(wgpf_event) * std::max<uint64_t>(n, 1));
+    if (n)
+      CUDA_OK(c, cudaMemcpyAsync(c->d_events.p, events, sizeof(wgpf_event) * n,
+                                 cudaMemcpyHostToDevice, c->stream));
+    d_ev = c->d_events.as<wgpf_event>();
+  }
+  if (n) {
+    k_event_stats<<<c->sms * 4, 256, 0, c->stream>>>(
+        d_ev, n, dev_plan(c), dev_stats(c), c->d_status.as<DevStatus>());
+    CUDA_OK(c, cudaGetLastError());
+    const uint32_t ns = n_slots(c);
+    k_event_first_wg<<<(ns + 127) / 128, 128, 0, c->stream>>>(
+        d_ev, dev_stats(c), ns, c->d_first_wg.as<unsigned long long>());
+    CUDA_OK(c, cudaGetLastError());
+    c->mean_exact_valid = false;
+    if (flags & WGPF_F_EXACT_MEAN) {
+      c->stats_valid = true;
+      rc = finalize_stats(c, nullptr, 0, 0, 0, d_ev, n, true);
+      if (rc) return rc;
+      // k_resolve_first ran against no body; restore the event-based wg
+      k_event_first_wg<<<(ns + 127) / 128, 128, 0, c->stream>>>(
+          d_ev, dev_stats(c), ns, c->d_first_wg.as<unsigned long long>());
+    }
+  }
+  rc = status_read(c);
+  if (rc) return rc;
+  if (c->h_status->synth_overflow)
+    return set_err(c, WGPF_E_CAPACITY,
+                   "more than %u distinct out-of-table region labels",
+                   kSynthHash);
+  c->stats_valid = true;
+  rc = read_stats(c, true);
+  if (rc) return rc;
+  *n_out = (uint32_t)c->stats_out.size();
+  if (c->stats_out.size() > cap)
+    return set_err(c, WGPF_E_BUFFER, "stats need %u entries", *n_out);
+  for (size_t k = 0; k < c->stats_out.size(); ++k) out[k] = c->stats_out[k];
+  return WGPF_OK;
+}
+
+extern "C" uint64_t wgpf_stats_packed_bytes(const wgpf_ctx* c) {
+  return 8ull * ((uint64_t)n_slots(c) * kPackedPerSlot + kSynthHash);
+}
+
+extern "C" int wgpf_stats_export(wgpf_ctx* c, void* d_dst) {
+  const uint32_t ns = n_slots(c);
+  const uint32_t m = std::max(ns, kSynthHash);
+  k_stats_pack<<<(m + 127) / 128, 128, 0, c->stream>>>(
+      dev_stats(c), ns, c->d_first_wg.as<unsigned long long>(),
+      static_cast<unsigned long long*>(d_dst));
+  CUDA_OK(c, cudaGetLastError());
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_stats_merge(wgpf_ctx* c, const void* d_gathered,
+                                uint32_t n_ranks) {
+  int rc = stats_reset(c);
+  if (rc) return rc;
+  rc = status_reset(c);
+  if (rc) return rc;
+  const uint32_t ns = n_slots(c);
+  const uint64_t work = (uint64_t)n_ranks * ns;
+  const auto* in = static_cast<const unsigned long long*>(d_gathered);
+  k_stats_merge<<<(uint32_t)((work + 127) / 128), 128, 0, c->stream>>>(
+      dev_stats(c), ns, in, n_ranks, c->d_status.as<DevStatus>());
+  k_stats_merge_wg<<<(uint32_t)((work + 127) / 128), 128, 0, c->stream>>>(
+      dev_stats(c), ns, in, n_ranks, c->d_first_wg.as<unsigned long long>());
+  CUDA_OK(c, cudaGetLastError());
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->stats_valid = true;
+  c->mean_exact_valid = false;
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_synth_body(wgpf_ctx* c, void* d_body, uint32_t shape,
+                               uint64_t stream0, uint64_t n_streams,
+                               uint64_t n_long) {
+  if (shape > 1) return set_err(c, WGPF_E_ARG, "unknown synthetic shape");
+  if (n_streams == 0) return WGPF_OK;
+  k_synth<<<c->sms * 8, 256, 0, c->stream>>>(static_cast<uint8_t*>(d_body),
+                                             shape, stream0, n_streams, n_long);
+  CUDA_OK(c, cudaGetLastError());
+  return WGPF_OK;
+}

@@ -1,0 +1,156 @@
+// k_count.cuh -- pass 1 of replay_image: per-stream decode checks, event
+// counts and fast-path routing, one warp per stream, coalesced tag reads.
+//
+// decode_image (trace.hpp:222-251): capacity must equal the plan (:227-231),
+// a flush stream may not claim more records than slots (:238-240), circular
+// streams start at record_count % capacity (:243-246).
+//
+// Event count.  Every matched END yields one interval and every interval one
+// event (a consumed wait marker cannot be malformed because unwrapped clocks
+// are monotone, trace.hpp:262-269 + :455), so events = #END - dropped_heads.
+// Under single-stack nesting (which the instrumentation pass guarantees,
+// instrument.hpp:60-105, and which every suffix of a properly nested stream
+// keeps) dropped_heads = -min(0, min_t Q(t)) with Q the running
+// #START - #END.  Pass 2 verifies the single-stack assumption and reroutes any
+// stream that violates it (SF_INVALID) to an exact recount.
+//
+// Routing to the general path (SF_GENERAL): region ids >= fast_regions,
+// nesting deeper than kMaxDepth, or a wait-marker START after z (below) that
+// is not closed by the very next record (pass 2 could not decide whether it
+// is ever closed).
+//
+// z = the last chronological position where the clamped depth
+// D(t) = Q(t) - min(0, min_{k<=t} Q(k)) is 0: every START at or before z is
+// closed later.
+#pragma once
+
+#include "wgpf_dev.cuh"
+
+namespace wgpf {
+
+struct CountArgs {
+  const uint8_t* body;
+  uint64_t stride;      // 16 + 8 * plan.slots
+  uint64_t n_streams;
+  DevPlan plan;
+  uint32_t* counts;
+  int32_t* zpos;
+  uint32_t* sflag;
+  DevStatus* status;
+  uint32_t fast_regions; // region ids below this may take the fast path
+  uint32_t max_depth;    // nesting the fast path holds in shared memory
+  uint32_t force_general;
+};
+
+__global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
+  __shared__ uint8_t marker_region[256];
+  for (uint32_t r = threadIdx.x; r < 256; r += blockDim.x)
+    marker_region[r] =
+        r < a.fast_regions ? class_is_marker(a.plan, a.plan.class_of[r]) : 0;
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t le = lanemask_le();
+  for (uint64_t s = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       s < a.n_streams; s += warps) {
+    const uint8_t* base = a.body + s * a.stride;
+    const uint4 h = *reinterpret_cast<const uint4*>(base);  // 16-B header
+    const uint32_t cnt = h.z, cap = h.w;
+    uint32_t code = 0;
+    if ((uint64_t)cap != a.plan.slots)
+      code = DEC_CAP;
+    else if (cnt > cap)
+      code = a.plan.strategy == WGPF_STRATEGY_FLUSH ? DEC_FLUSH
+                                                    : (cap == 0 ? DEC_ZERO : 0);
+    if (code) {
+      if (lane == 0) {
+        a.counts[s] = 0;
+        a.zpos[s] = -1;
+        a.sflag[s] = SF_DECODE_ERR;
+        atomicMin(&a.status->decode_err, ((unsigned long long)s << 2) | code);
+        if (code == DEC_CAP) atomicAdd(&a.status->cap_mismatch, 1ull);
+      }
+      continue;
+    }
+    const uint32_t n = cnt <= cap ? cnt : cap;
+    const uint32_t start = cnt <= cap ? 0u : cnt % cap;
+    const uint32_t* tags = reinterpret_cast<const uint32_t*>(base + 16);
+    int32_t q_in = 0;     // Q before the chunk
+    int32_t run_min = 0;  // min(0, min Q so far)
+    int32_t max_d = 0;
+    uint32_t n_end = 0;
+    int32_t z = -1;
+    int64_t last_bad = -1;
+    bool wide = false;
+    bool prev_end = false;       // record c-1 is an END
+    uint32_t pend_rid = kNone;   // lane-31 marker START awaiting its END
+    for (uint32_t c = 0; c < n; c += 32) {
+      const uint32_t i = c + lane;
+      const bool valid = i < n;
+      uint32_t slot = start + i;
+      if (slot >= cap) slot -= cap;
+      const uint32_t tag = valid ? __ldg(tags + 2ull * slot) : 0u;
+      const uint32_t rid = (tag >> 12) & (WGPF_MAX_REGIONS - 1u);
+      const bool st = valid && (tag & WGPF_START_FLAG);
+      const bool en = valid && !(tag & WGPF_START_FLAG);
+      const bool in_range = rid < a.fast_regions;
+      wide |= valid && !in_range;
+      const uint32_t smk = __ballot_sync(0xffffffffu, st);
+      const uint32_t emk = __ballot_sync(0xffffffffu, en);
+      const int32_t q = q_in + (int32_t)__popc(smk & le) - (int32_t)__popc(emk & le);
+      const int32_t cmin = __reduce_min_sync(0xffffffffu, valid ? q : INT32_MAX);
+      uint32_t zm;
+      int32_t d;
+      if (cmin >= run_min) {
+        zm = __ballot_sync(0xffffffffu, valid && q == run_min);
+        d = q - run_min;
+      } else {  // a new running minimum inside the chunk: prefix-min scan
+        int32_t pm = valid ? q : INT32_MAX;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, pm, o);
+          if ((int)lane >= o) pm = min(pm, y);
+        }
+        const int32_t rm = min(run_min, pm);
+        zm = __ballot_sync(0xffffffffu, valid && q == rm);
+        d = q - rm;
+        run_min = min(run_min, cmin);
+      }
+      max_d = max(max_d, __reduce_max_sync(0xffffffffu, valid ? d : 0));
+      if (zm) z = (int32_t)(c + 31u - __clz(zm));
+      // wait-marker STARTs right after an END that the next record does not
+      // close (conservative: the marker class test is done in pass 2)
+      const bool pe = lane == 0 ? prev_end
+                                : (bool)__shfl_up_sync(0xffffffffu, (uint32_t)en, 1);
+      const uint32_t t1 = __shfl_down_sync(0xffffffffu, tag, 1);
+      const bool mk_start = st && pe && in_range && marker_region[rid];
+      const bool closed_next = (lane < 31) && (i + 1 < n) &&
+                               !(t1 & WGPF_START_FLAG) &&
+                               ((t1 >> 12) & (WGPF_MAX_REGIONS - 1u)) == rid;
+      const uint32_t bm = __ballot_sync(0xffffffffu, mk_start && !closed_next && lane < 31);
+      if (pend_rid != kNone) {  // lane 31 of the previous chunk
+        const uint32_t t0 = __shfl_sync(0xffffffffu, tag, 0);
+        const bool ok0 = n > c && !(t0 & WGPF_START_FLAG) &&
+                         ((t0 >> 12) & (WGPF_MAX_REGIONS - 1u)) == pend_rid;
+        if (!ok0) last_bad = max(last_bad, (int64_t)c - 1);
+      }
+      if (bm) last_bad = max(last_bad, (int64_t)(c + 31u - __clz(bm)));
+      const uint32_t p31 = __shfl_sync(0xffffffffu, (mk_start && lane == 31) ? rid : kNone, 31);
+      pend_rid = p31;
+      prev_end = __shfl_sync(0xffffffffu, (uint32_t)en, 31);
+      n_end += __popc(emk);
+      q_in += (int32_t)__popc(smk) - (int32_t)__popc(emk);
+    }
+    if (pend_rid != kNone) last_bad = max(last_bad, (int64_t)n - 1);
+    wide = __any_sync(0xffffffffu, wide);
+    if (lane == 0) {
+      a.counts[s] = n_end - (uint32_t)(-run_min);
+      a.zpos[s] = z;
+      const bool general = wide || a.force_general ||
+                           max_d > (int32_t)a.max_depth || last_bad > (int64_t)z;
+      a.sflag[s] = general ? SF_GENERAL : 0u;
+    }
+  }
+}
+
+}  // namespace wgpf

@@ -1,0 +1,438 @@
+// k_fast.cuh -- pass 2 of replay_image, warp-cooperative: one warp per
+// stream, 32 chronological records per step (lane t holds record c + t).
+//
+// Per step, with ballots / shuffles / match.any instead of a sequential
+// stack walk:
+//   unwrap_clock (trace.hpp:257-272)  u = hi:v where hi counts the mod-2^32
+//       wraps, i.e. ballot(v_t < v_{t-1}) prefix popcounts.
+//   pair_records (trace.hpp:294-346)  clamped depth D from ballot prefix
+//       counts; a START opens level D, an END closes level D_before; the END's
+//       partner is the last START at the same level: match.any on the level,
+//       highest START lane below, else the per-level table in shared memory
+//       (carried across steps).  The partner's region must equal the END's
+//       (single-stack nesting); otherwise the stream is recounted exactly.
+//       Iteration numbers: match.any on the region + per-region counters.
+//   replay (trace.hpp:398-487)  sync correction, wait markers (the marker
+//       START at end_pos + 1, closed either immediately or because it lies at
+//       or before the stream's last zero-depth position z from pass 1),
+//       orphans (staged in a per-warp HBM scratch, written last).
+//   region_stats (pipeline.hpp:114-133) + histograms: per step match.any on
+//       (class, bin), group reductions with redux.sync, one shared-memory
+//       atomic per group; per-CTA totals flushed to HBM at exit.
+// Events are written at offsets from the pass-1 scan, coalesced per step.
+#pragma once
+
+#include "wgpf_dev.cuh"
+
+namespace wgpf {
+
+constexpr uint32_t kFastRegions = 256;  // region ids handled by the fast path
+constexpr uint32_t kMaxDepth = 64;      // nesting levels in shared memory
+constexpr uint32_t kFastWarps = 8;      // warps per CTA
+
+struct FastArgs {
+  const uint8_t* body;
+  uint64_t stride;
+  uint64_t n_streams;
+  uint64_t stream_base;
+  DevPlan plan;
+  DevStats stats;
+  DevStatus* status;
+  const uint32_t* counts;
+  const int32_t* zpos;
+  uint32_t* sflag;
+  const uint64_t* offsets;
+  wgpf_event* events;
+  uint64_t events_cap;
+  uint64_t record_cost;
+  wgpf_event* orphan_scratch;  // per warp: (cap / 2 + 1) events
+  uint32_t cap;
+  uint32_t fast_regions;
+  uint32_t no_stats;
+  unsigned long long* general_list;  // streams left for the general path
+  unsigned long long* general_len;
+};
+
+struct LevelEntry {  // last START seen at a nesting level
+  uint32_t lo;       // low 32 bits of the unwrapped clock (= raw payload)
+  uint32_t hi;       // high bits
+  uint32_t pos;      // chronological position
+  uint32_t info;     // region | consumable << 31
+};
+
+struct FastSmem {
+  SmemStats st;
+  uint32_t cinfo[kFastRegions];  // class | marker << 31
+  uint32_t wcls[kFastRegions];   // class of label + ".wait" (or kNone)
+  LevelEntry lvl[kFastWarps][kMaxDepth];
+  uint32_t cnt[kFastWarps][kFastRegions];
+  unsigned long long warn[4];
+};
+
+__device__ inline void store_event(wgpf_event* dst, uint64_t st, uint64_t en,
+                                   uint32_t region, uint32_t it, uint32_t blk,
+                                   uint32_t wg) {
+  uint4* p = reinterpret_cast<uint4*>(dst);
+  p[0] = make_uint4((uint32_t)st, (uint32_t)(st >> 32), (uint32_t)en,
+                    (uint32_t)(en >> 32));
+  p[1] = make_uint4(region, it, blk, wg);
+}
+
+// Group-aggregated statistics update for one event per participating lane.
+__device__ inline void fast_stats(FastSmem& sm, const DevStats& st,
+                                  DevStatus* status, bool part, uint32_t cls,
+                                  uint32_t d, unsigned long long key) {
+  const uint32_t bin = hist_bin(d);
+  const uint32_t lane = lane_id();
+  const uint32_t k = part ? ((cls << 6) | bin) : (0xFC000000u | lane);
+  const uint32_t grp = __match_any_sync(0xffffffffu, k);
+  const uint32_t lo = __reduce_add_sync(grp, d & 0xFFFFu);
+  const uint32_t hi = __reduce_add_sync(grp, d >> 16);
+  const uint32_t mn = __reduce_min_sync(grp, d);
+  const uint32_t mx = __reduce_max_sync(grp, d);
+  if (!part || (grp & lanemask_lt())) return;  // leader = lowest lane
+  const uint32_t n = __popc(grp);
+  const unsigned long long sum =
+      (unsigned long long)lo + ((unsigned long long)hi << 16);
+  if (cls < kSmemClasses && cls < st.K) {
+    atomicAdd(&sm.st.count[cls], (unsigned long long)n);
+    atomicAdd(&sm.st.sum[cls], sum);
+    atomicMin(&sm.st.min[cls], mn);
+    atomicMax(&sm.st.max[cls], mx);
+    atomicMin(&sm.st.first[cls], key);
+    atomicAdd(&sm.st.hist[cls * WGPF_HIST_BINS + bin], n);
+  } else {
+    const int slot = stats_slot(st, cls, &status->synth_overflow);
+    if (slot < 0) return;
+    atomicAdd(&st.count[slot], (unsigned long long)n);
+    atomicAdd(&st.sum[slot], sum);
+    atomicMin(&st.min[slot], (unsigned long long)mn);
+    atomicMax(&st.max[slot], (unsigned long long)mx);
+    atomicMin(&st.first[slot], key);
+    atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + bin],
+              (unsigned long long)n);
+  }
+}
+
+__global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
+  const uint32_t lane = lane_id();
+  const uint32_t w = threadIdx.x >> 5;
+  if (!a.no_stats) smem_stats_init(sm.st);
+  for (uint32_t r = threadIdx.x; r < kFastRegions; r += blockDim.x) {
+    uint32_t ci = kNone, wc = kNone;
+    if (r < a.fast_regions) {
+      const uint32_t c = a.plan.class_of[r];
+      ci = c | (class_is_marker(a.plan, c) ? 0x80000000u : 0u);
+      wc = c < a.plan.K ? a.plan.wait_class[c] : kNone;
+    }
+    sm.cinfo[r] = ci;
+    sm.wcls[r] = wc;
+  }
+  if (threadIdx.x < 4) sm.warn[threadIdx.x] = 0;
+  __syncthreads();
+  const bool abort_all = a.status->decode_err != kNoErr;
+  LevelEntry* lvl = sm.lvl[w];
+  uint32_t* cnt = sm.cnt[w];
+  const uint64_t gw = (uint64_t)blockIdx.x * kFastWarps + w;
+  wgpf_event* orphans = a.orphan_scratch + gw * (a.cap / 2 + 1);
+  const uint32_t lt = lanemask_lt(), le = lanemask_le();
+  const uint64_t cost = a.record_cost;
+  uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
+
+  for (uint64_t s = gw; !abort_all && s < a.n_streams;
+       s += (uint64_t)gridDim.x * kFastWarps) {
+    const uint32_t flag = a.sflag[s];
+    if (flag & (SF_DECODE_ERR | SF_GENERAL)) {
+      if ((flag & SF_GENERAL) && lane == 0) {
+        const unsigned long long k = atomicAdd(a.general_len, 1ull);
+        a.general_list[k] = s;
+      }
+      continue;
+    }
+    const uint8_t* base = a.body + s * a.stride;
+    const uint4 h = *reinterpret_cast<const uint4*>(base);
+    const uint32_t cntw = h.z, cap = h.w;
+    const uint32_t n = cntw <= cap ? cntw : cap;
+    const uint32_t start = cntw <= cap ? 0u : cntw % cap;
+    const uint32_t blk = h.x, wg = h.y;
+    const int32_t z = a.zpos[s];
+    const uint32_t want = a.counts[s];
+    const uint64_t off = a.offsets[s];
+    const uint64_t gs = s + a.stream_base;
+    const uint2* slots = reinterpret_cast<const uint2*>(base + 16);
+    for (uint32_t r = lane; r < a.fast_regions; r += 32) cnt[r] = 0;
+
+    auto load = [&](uint32_t c) -> uint2 {
+      const uint32_t i = c + lane;
+      if (i >= n) return make_uint2(0u, 0u);
+      uint32_t slot = start + i;
+      if (slot >= cap) slot -= cap;
+      return slots[slot];
+    };
+
+    uint2 rc = load(0);
+    uint32_t hi = 0, vprev = 0;  // unwrap carry
+    int32_t D = 0;               // clamped depth before the chunk
+    uint64_t kb = 0;             // base events emitted
+    uint32_t n_orph = 0;
+    bool prev_end_matched = false;  // record c-1 is a matched END
+    uint32_t prev_rid = 0;          //   its region
+    bool bad = false;
+    __syncwarp();
+
+    for (uint32_t c = 0; c < n; c += 32) {
+      __syncwarp();                   // level / counter tables of chunk c-32
+      const uint2 rn = load(c + 32);  // prefetch the next chunk
+      const uint32_t i = c + lane;
+      const bool valid = i < n;
+      const uint32_t tag = rc.x, v = rc.y;
+      const bool st = valid && (tag & WGPF_START_FLAG);
+      const bool en = valid && !(tag & WGPF_START_FLAG);
+      const uint32_t rid = (tag >> 12) & (WGPF_MAX_REGIONS - 1u);
+
+      // ---- unwrap ---------------------------------------------------------
+      uint32_t vp = __shfl_up_sync(0xffffffffu, v, 1);
+      if (lane == 0) vp = vprev;
+      const uint32_t wm = __ballot_sync(0xffffffffu, valid && v < vp);
+      const uint32_t my_hi = hi + __popc(wm & le);
+
+      // ---- clamped depth --------------------------------------------------
+      const uint32_t smk = __ballot_sync(0xffffffffu, st);
+      const uint32_t emk = __ballot_sync(0xffffffffu, en);
+      const int32_t q = D + (int32_t)__popc(smk & le) - (int32_t)__popc(emk & le);
+      const int32_t cmin = __reduce_min_sync(0xffffffffu, valid ? q : INT32_MAX);
+      int32_t dafter = q;
+      if (cmin < 0) {
+        int32_t pm = valid ? q : INT32_MAX;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, pm, o);
+          if ((int)lane >= o) pm = min(pm, y);
+        }
+        dafter = q - min(0, pm);
+      }
+      int32_t dbefore = __shfl_up_sync(0xffffffffu, dafter, 1);
+      if (lane == 0) dbefore = D;
+      const bool mend = en && dbefore > 0;  // matched END
+      const bool dropped = en && dbefore == 0;
+      const uint32_t L = st ? (uint32_t)dafter : (uint32_t)dbefore;  // level
+
+      // ---- consumable flag of this START (prev record is a matched,
+      //      non-marker END whose wait class is this START's class) --------
+      const bool pm_prev_raw = __shfl_up_sync(0xffffffffu, (uint32_t)mend, 1);
+      const uint32_t prid_raw = __shfl_up_sync(0xffffffffu, rid, 1);
+      const bool prev_m = lane == 0 ? prev_end_matched : pm_prev_raw;
+      const uint32_t prid = lane == 0 ? prev_rid : prid_raw;
+      const uint32_t my_info = sm.cinfo[valid ? rid : 0];
+      bool consumable = false;
+      if (st && prev_m && i > 0) {
+        const uint32_t pinfo = sm.cinfo[prid];
+        consumable = !(pinfo & 0x80000000u) &&
+                     sm.wcls[prid] == (my_info & 0x7FFFFFFFu);
+      }
+
+      // ---- partner START: same level, highest START lane below ------------
+      const uint32_t key = (st || mend) ? L : (0x80000000u | lane);
+      const uint32_t grp = __match_any_sync(0xffffffffu, key);
+      const uint32_t cand = grp & smk & lt;
+      const uint32_t src = cand ? 31u - __clz(cand) : lane;
+      const uint32_t s_v = __shfl_sync(0xffffffffu, v, src);
+      const uint32_t s_hi = __shfl_sync(0xffffffffu, my_hi, src);
+      const uint32_t s_info = __shfl_sync(
+          0xffffffffu, rid | (consumable ? 0x80000000u : 0u), src);
+      uint32_t p_lo = s_v, p_hi = s_hi, p_pos = c + src, p_info = s_info;
+      if (mend && !cand) {
+        const LevelEntry e = lvl[L - 1];
+        p_lo = e.lo;
+        p_hi = e.hi;
+        p_pos = e.pos;
+        p_info = e.info;
+      }
+      __syncwarp();
+      if (st && !(grp & smk & lanemask_gt())) {
+        LevelEntry e;
+        e.lo = v;
+        e.hi = my_hi;
+        e.pos = i;
+        e.info = rid | (consumable ? 0x80000000u : 0u);
+        lvl[L - 1] = e;
+      }
+
+      // ---- validation (single-stack nesting) and the 2^32 check ----------
+      const uint64_t u = ((uint64_t)my_hi << 32) | v;
+      const uint64_t su = ((uint64_t)p_hi << 32) | p_lo;
+      const bool mism = mend && (p_info & 0x7FFFFFFFu) != rid;
+      const bool too_long = mend && !mism && (u - su) >= (1ull << 32);
+      if (__any_sync(0xffffffffu, mism)) {
+        if (lane == 0) {
+          atomicAdd(&a.status->invalid, 1ull);
+          a.sflag[s] = flag | SF_INVALID;
+        }
+        bad = true;
+        break;
+      }
+      if (__any_sync(0xffffffffu, too_long)) {
+        const uint32_t fm = __ballot_sync(0xffffffffu, too_long);
+        if (lane == 0)
+          atomicMin(&a.status->pair_err,
+                    ((unsigned long long)gs << 32) | (c + __ffs(fm) - 1u));
+        bad = true;
+        break;
+      }
+
+      // ---- iteration numbers per region id --------------------------------
+      const uint32_t rgrp =
+          __match_any_sync(0xffffffffu, mend ? rid : (0x80000000u | lane));
+      uint32_t it = 0;
+      if (mend) it = cnt[rid] + __popc(rgrp & lt);
+      __syncwarp();
+      if (mend && !(rgrp & lt)) cnt[rid] += __popc(rgrp);
+
+      // ---- replay -----------------------------------------------------------
+      const uint32_t cls = my_info & 0x7FFFFFFFu;
+      const bool is_mk = (my_info & 0x80000000u) != 0u;
+      const bool base_ev = mend && !is_mk;
+      // look-ahead records i+1, i+2 (next lanes or the next chunk)
+      const uint32_t t1 = __shfl_down_sync(0xffffffffu, tag, 1);
+      const uint32_t v1 = __shfl_down_sync(0xffffffffu, v, 1);
+      const uint32_t t2 = __shfl_down_sync(0xffffffffu, tag, 2);
+      const uint32_t n0t = __shfl_sync(0xffffffffu, rn.x, 0);
+      const uint32_t n0v = __shfl_sync(0xffffffffu, rn.y, 0);
+      const uint32_t n1t = __shfl_sync(0xffffffffu, rn.x, 1);
+      const uint32_t nt1 = lane == 31 ? n0t : t1;
+      const uint32_t nv1 = lane == 31 ? n0v : v1;
+      const uint32_t nt2 = lane == 31 ? n1t : (lane == 30 ? n0t : t2);
+      bool consumed = false;
+      if (base_ev && i + 1 < n && (nt1 & WGPF_START_FLAG)) {
+        const uint32_t r1 = (nt1 >> 12) & (WGPF_MAX_REGIONS - 1u);
+        const uint32_t i1 = sm.cinfo[r1];
+        if ((i1 & 0x80000000u) && sm.wcls[rid] == (i1 & 0x7FFFFFFFu)) {
+          const bool closes_next =
+              i + 2 < n && !(nt2 & WGPF_START_FLAG) &&
+              ((nt2 >> 12) & (WGPF_MAX_REGIONS - 1u)) == r1;
+          consumed = (int64_t)(i + 1) <= (int64_t)z || closes_next;
+        }
+      }
+      const bool orphan = mend && is_mk && !(p_info & 0x80000000u);
+      const uint32_t bm = __ballot_sync(0xffffffffu, base_ev);
+      const uint32_t cm = __ballot_sync(0xffffffffu, consumed);
+      const uint64_t kpos = kb + __popc(bm & lt) + __popc(cm & lt);
+      kb += __popc(bm) + __popc(cm);
+
+      uint32_t e_dur = 0, w_dur = 0;
+      uint32_t wc = kNone;
+      if (base_ev) {
+        const uint64_t meas = u - su;
+        const uint64_t ovh = cost * (uint64_t)(i - p_pos);
+        const uint64_t corr = meas >= ovh ? meas - ovh : 0;
+        e_dur = (uint32_t)corr;
+        const uint64_t idx = off + kpos;
+        if (a.events) {
+          if (idx < a.events_cap)
+            store_event(a.events + idx, su, su + corr, rid | WGPF_EV_CORRECTED,
+                        it, blk, wg);
+          else
+            atomicAdd(&a.status->overflow, 1ull);
+        }
+        if (consumed) {
+          const uint32_t r1 = (nt1 >> 12) & (WGPF_MAX_REGIONS - 1u);
+          wc = sm.cinfo[r1] & 0x7FFFFFFFu;
+          const uint32_t h1 = my_hi + (nv1 < v ? 1u : 0u);
+          const uint64_t u1 = ((uint64_t)h1 << 32) | nv1;
+          const uint64_t wd = u1 - u;
+          const bool corr_w = wd > cost;
+          w_flag += !corr_w;
+          w_dur = (uint32_t)wd;
+          if (a.events) {
+            if (idx + 1 < a.events_cap)
+              store_event(a.events + idx + 1, u, u1,
+                          r1 | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u),
+                          it, blk, wg);
+            else
+              atomicAdd(&a.status->overflow, 1ull);
+          }
+        }
+      }
+      // orphans -> per-warp scratch, written after all base events
+      const uint32_t om = __ballot_sync(0xffffffffu, orphan);
+      if (orphan) {
+        wgpf_event e;
+        e.start = su;
+        e.end = u;
+        e.region = rid;
+        e.iteration = it;
+        e.block_index = blk;
+        e.warp_group = wg;
+        orphans[n_orph + __popc(om & lt)] = e;
+      }
+      n_orph += __popc(om);
+      w_drop += dropped;
+
+      if (!a.no_stats) {
+        fast_stats(sm, a.stats, a.status, base_ev, cls, e_dur,
+                   first_key(gs, kpos, 0u));
+        if (__any_sync(0xffffffffu, consumed))
+          fast_stats(sm, a.stats, a.status, consumed, wc, w_dur,
+                     first_key(gs, kpos + 1, 1u));
+      }
+
+      // ---- carries ----------------------------------------------------------
+      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+      const uint32_t last = 31u - __clz(vm);
+      hi += __popc(wm);
+      vprev = __shfl_sync(0xffffffffu, v, last);
+      D = __shfl_sync(0xffffffffu, dafter, last);
+      prev_end_matched = __shfl_sync(0xffffffffu, (uint32_t)mend, last);
+      prev_rid = __shfl_sync(0xffffffffu, rid, last);
+      rc = rn;
+    }
+    if (bad) continue;
+    if (kb + n_orph != want) {  // cannot happen for single-stack streams
+      if (lane == 0) {
+        atomicAdd(&a.status->invalid, 1ull);
+        a.sflag[s] = flag | SF_INVALID;
+      }
+      continue;
+    }
+    __syncwarp();
+    // orphans after all base events (trace.hpp:469-485)
+    for (uint32_t j = lane; j < ((n_orph + 31u) & ~31u); j += 32) {
+      const bool ok = j < n_orph;
+      wgpf_event e;
+      if (ok) e = orphans[j];
+      const uint64_t idx = off + kb + j;
+      if (ok && a.events) {
+        if (idx < a.events_cap)
+          store_event(a.events + idx, e.start, e.end, e.region, e.iteration,
+                      blk, wg);
+        else
+          atomicAdd(&a.status->overflow, 1ull);
+      }
+      if (!a.no_stats) {
+        const uint32_t ci = ok ? sm.cinfo[e.region] & 0x7FFFFFFFu : 0u;
+        fast_stats(sm, a.stats, a.status, ok, ci,
+                   ok ? (uint32_t)(e.end - e.start) : 0u,
+                   first_key(gs, kb + j, 0u));
+      }
+    }
+    w_mal += n_orph;
+    w_tail += (uint32_t)D;
+  }
+  // warnings: w_drop / w_flag are per lane, w_tail / w_mal per warp (lane 0)
+  const unsigned long long d = warp_sum((unsigned long long)w_drop);
+  const unsigned long long f = warp_sum((unsigned long long)w_flag);
+  if (lane == 0) {
+    if (d) atomicAdd(&sm.warn[0], d);
+    if (w_tail) atomicAdd(&sm.warn[1], (unsigned long long)w_tail);
+    if (f) atomicAdd(&sm.warn[2], f);
+    if (w_mal) atomicAdd(&sm.warn[3], (unsigned long long)w_mal);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && sm.warn[threadIdx.x])
+    atomicAdd(&a.status->warn[threadIdx.x], sm.warn[threadIdx.x]);
+  if (!a.no_stats) smem_stats_flush(sm.st, a.stats);
+}
+
+}  // namespace wgpf

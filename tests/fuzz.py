@@ -1,0 +1,99 @@
+"""Seeded random KPFT images for parity tests (edge cases the reference's
+own tests exercise: wrap-around circular buffers, dropped heads, truncated
+tails, wait markers / orphans, out-of-table region ids, duplicate labels,
+32-bit clock wraps, non-single-stack nesting)."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import synth as S
+
+LABEL_SETS = [
+    ["A", "A.wait", "B", "B.wait", "C"],
+    ["X", "X.wait", "X.wait.wait", "Y", "X"],           # duplicate label
+    ["region#7", "region#7.wait", "L", "L.wait"],       # collides with id 7
+    ["Load K", "Load K.wait", "GEMM", "GEMM.wait", "Softmax", ".wait", "Z.wait"],
+]
+
+
+def _stream_records(rng, n, n_labels, mode, big_gaps):
+    """Chronological records of one stream."""
+    tags, clocks = [], []
+    clock = int(rng.integers(0, 1 << 32))
+    open_stack = []
+    ids_hi = n_labels + 4  # some out-of-table ids
+    while len(tags) < n:
+        r = rng.random()
+        if mode == "nested":
+            # properly nested with canonical async groups
+            if open_stack and r < 0.45:
+                rid = open_stack.pop()
+                tags.append(rid << 12)
+            elif r < 0.65 and n_labels >= 2:
+                base = int(rng.integers(0, n_labels))
+                tags.append(0x80000000 | (base << 12))
+                gap_clock = clock
+                clocks.append(clock)
+                clock = (clock + int(rng.integers(1, 300))) & 0xFFFFFFFF
+                if len(tags) >= n:
+                    break
+                tags.append(base << 12)
+                clocks.append(clock)
+                clock = (clock + int(rng.integers(0, 50 if rng.random() < 0.5 else 3000))) & 0xFFFFFFFF
+                m = min(n_labels - 1, base + 1)
+                if len(tags) >= n:
+                    break
+                tags.append(0x80000000 | (m << 12))
+                clocks.append(clock)
+                clock = (clock + int(rng.integers(0, 40))) & 0xFFFFFFFF
+                if len(tags) >= n:
+                    break
+                if rng.random() < 0.85:
+                    tags.append(m << 12)
+                else:
+                    open_stack.append(m)
+                    continue
+                del gap_clock
+            else:
+                rid = int(rng.integers(0, ids_hi if rng.random() < 0.1 else n_labels))
+                tags.append(0x80000000 | (rid << 12))
+                open_stack.append(rid)
+        else:  # "random": arbitrary start/end sequence (may cross regions)
+            rid = int(rng.integers(0, ids_hi if rng.random() < 0.1 else n_labels))
+            tags.append((0x80000000 if rng.random() < 0.5 else 0) | (rid << 12) |
+                        int(rng.integers(0, 4096)))
+        clocks.append(clock)
+        if big_gaps and rng.random() < 0.05:
+            clock = (clock + int(rng.integers(1 << 30, (1 << 32) - 1))) & 0xFFFFFFFF
+        else:
+            clock = (clock + int(rng.integers(0, 500))) & 0xFFFFFFFF
+    return np.array(tags[:n], np.uint32), np.array(clocks[:n], np.uint32)
+
+
+def random_image(seed: int, n_streams: int = 8, cap: int = 64,
+                 mode: str = "nested", big_gaps: bool = False,
+                 labels_idx: int | None = None):
+    """Returns (kpft v1 bytes, slots, strategy, labels)."""
+    rng = np.random.default_rng(seed)
+    labels = LABEL_SETS[labels_idx if labels_idx is not None else
+                        int(rng.integers(0, len(LABEL_SETS)))]
+    strategy = int(rng.integers(0, 2))
+    body = np.zeros((n_streams, 4 + 2 * cap), np.uint32)
+    for s in range(n_streams):
+        if strategy == 1:
+            count = int(rng.integers(0, cap + 1))
+            writes = count
+        else:
+            count = int(rng.integers(0, 3 * cap))
+            writes = count
+        tags, clocks = _stream_records(rng, writes, len(labels), mode, big_gaps)
+        body[s, 0] = s // 4
+        body[s, 1] = s % 4
+        body[s, 2] = count
+        body[s, 3] = cap
+        for w in range(writes):
+            slot = w % cap
+            body[s, 4 + 2 * slot] = tags[w]
+            body[s, 5 + 2 * slot] = clocks[w]
+    data = S.kpft_v1(body.view(np.uint8).reshape(-1), n_streams)
+    return data, cap, strategy, labels

@@ -1,0 +1,365 @@
+"""GPU parity: the sm_100a replay path (through the C-ABI) against the
+reference's golden vectors, the CPU oracle, and the reference's known-answer
+tests -- bit-exact on every integer output, bit-exact means in exact mode."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import (FIXTURES, GOLDEN, canon_golden, load_fixture,
+                      load_random_set, load_synth)
+from oracle import oracle as O
+from oracle import synth as S
+import fuzz
+
+pytestmark = pytest.mark.gpu
+
+FLAG_MODES = {"fast": 0, "general": 0x4}
+
+
+def T():
+    from paper_2505_21661_b200 import trace
+    return trace
+
+
+def plan_of(slots, strategy, labels):
+    t = T()
+    return t.BufferPlan(slots, t.BufferStrategy(strategy), list(labels))
+
+
+def same_events(ev, labels, ref_canon, space):
+    return np.array_equal(O.canon_from_events(ev, labels, space), ref_canon)
+
+
+# ---------------------------------------------------------------------------
+# golden fixtures
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", list(FLAG_MODES))
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_replay(ctx, oracle, name, mode):
+    data, slots, strategy, labels, cost, _ = load_fixture(name)
+    r = ctx.replay_image_bytes(data, plan_of(slots, strategy, labels), cost,
+                               flags=FLAG_MODES[mode] | 0x2)
+    o = oracle.replay_kpft(data, slots, strategy, labels, cost)
+    assert np.array_equal(r.events, o.events)
+    rep = json.load(open(os.path.join(GOLDEN, "fixtures", name + "_replay.json")))
+    w = rep["warnings"]
+    assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+            r.malformed_groups) == (w["dropped_heads"], w["truncated_tails"],
+                                    w["flagged_preconditions"], w["malformed_groups"])
+    st = ctx.stats()
+    assert list(st) == [x["region"] for x in rep["regions"]]
+    for x in rep["regions"]:
+        s = st[x["region"]]
+        assert (s.warp_group, s.kind, s.count, s.min, s.max) == (
+            x["warp_group"], x["kind"], x["count"], x["min_duration"],
+            x["max_duration"])
+        assert s.mean == x["mean_duration"]  # bit-exact recurrence (H1 a)
+
+
+# ---------------------------------------------------------------------------
+# golden random programs
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", list(FLAG_MODES))
+@pytest.mark.parametrize("setname", ["fidelity", "circular", "circular_flush",
+                                     "replay100"])
+def test_random_programs(ctx, setname, mode):
+    for img, slots, strategy, labels, res in load_random_set(setname):
+        r = ctx.replay_image_bytes(img, plan_of(slots, strategy, labels), 33,
+                                   flags=FLAG_MODES[mode] | 0x2)
+        sp = O.LabelSpace()
+        assert same_events(r.events, labels, canon_golden(res, sp), sp)
+        assert [r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+                r.malformed_groups] == list(res["warnings"])
+        st = ctx.stats()
+        assert list(st) == list(res["stat_label"])
+        assert [s.mean for s in st.values()] == list(res["stat_mean"])
+        assert [s.count for s in st.values()] == list(res["stat_count"])
+        assert [s.min for s in st.values()] == list(res["stat_min"])
+        assert [s.max for s in st.values()] == list(res["stat_max"])
+        assert [s.warp_group for s in st.values()] == list(res["stat_wg"])
+        assert [s.kind == "wait" for s in st.values()] == list(res["stat_kind"])
+
+
+# ---------------------------------------------------------------------------
+# synthetic configs (slices) and the GPU synthetic generator
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", list(FLAG_MODES))
+@pytest.mark.parametrize("shape", ["mixed", "nested"])
+def test_synth_slices(ctx, shape, mode):
+    g = load_synth(shape)
+    if shape == "mixed":
+        body, n, strategy, labels = (S.mixed_body(S.MIXED_FULL_LONG - 1024, 2048,
+                                                  S.MIXED_FULL_LONG), 2048, 1,
+                                     S.MIXED_LABELS)
+        img = S.kpft_v1(body, n)
+    else:
+        body, n, strategy, labels = S.nested_body(0, 1024), 1024, 0, S.NESTED_LABELS
+        img = S.kpft_v2(body, n)  # v2 container
+    r = ctx.replay_image_bytes(img, plan_of(S.CAP, strategy, labels), 33,
+                               flags=FLAG_MODES[mode] | 0x2)
+    sp = O.LabelSpace()
+    assert same_events(r.events, labels,
+                       O.canon_from_ref(g["events"], list(g["labels"]), sp), sp)
+    assert [r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+            r.malformed_groups] == list(g["warnings"])
+    st = ctx.stats()
+    assert [s.mean for s in st.values()] == list(g["stat_mean"])
+    assert [s.count for s in st.values()] == list(g["stat_count"])
+
+
+@pytest.mark.parametrize("shape", [0, 1])
+def test_gpu_synth_generator_matches_cpu(ctx, shape):
+    import torch
+    n, s0 = 3000, S.MIXED_FULL_LONG - 1500
+    if shape == 1:
+        s0 = 123456
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), shape, s0, n, S.MIXED_FULL_LONG)
+    torch.cuda.synchronize()
+    cpu = S.mixed_body(s0, n, S.MIXED_FULL_LONG) if shape == 0 else \
+        S.nested_body(s0, n)
+    assert np.array_equal(body.cpu().numpy(), cpu)
+
+
+# ---------------------------------------------------------------------------
+# fuzz vs the oracle (edge cases: crossings, out-of-table ids, duplicate
+# labels, orphans, clock wraps, errors)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mode", ["nested", "random"])
+@pytest.mark.parametrize("path", list(FLAG_MODES))
+def test_fuzz_vs_oracle(ctx, oracle, mode, path):
+    t = T()
+    for seed in range(80):
+        data, cap, strategy, labels = fuzz.random_image(
+            1000 + seed, n_streams=12, cap=32 if seed % 2 else 64, mode=mode,
+            big_gaps=(seed % 3 == 0))
+        try:
+            o = oracle.replay_kpft(data, cap, strategy, labels, 33)
+            oerr = None
+        except O.OracleError as e:
+            o, oerr = None, (e.category, str(e))
+        try:
+            r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33,
+                                       flags=FLAG_MODES[path] | 0x2)
+            gerr = None
+        except t.Error as e:
+            r, gerr = None, (e.category(), str(e))
+        assert oerr == gerr, (seed, oerr, gerr)
+        if oerr:
+            continue
+        assert np.array_equal(r.events, o.events), seed
+        assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+                r.malformed_groups) == (o.dropped_heads, o.truncated_tails,
+                                        o.flagged_preconditions, o.malformed_groups)
+        want = oracle.region_stats(o.events, labels)
+        got = ctx.stats()
+        assert list(got) == [s.label for s in want], seed
+        for s in want:
+            g = got[s.label]
+            assert (g.warp_group, g.kind, g.count, g.min, g.max, g.sum, g.mean,
+                    g.first_event, g.hist) == (s.warp_group, s.kind, s.count, s.min,
+                                               s.max, s.sum, s.mean, s.first_event,
+                                               s.hist), (seed, s.label)
+
+
+def test_errors_match_reference_messages(ctx, oracle):
+    t = T()
+    body = np.array([0, 1, 0, 8] + [0] * 16, np.uint32)
+    img = S.kpft_v1(body.view(np.uint8), 1)
+    cases = [(img, 4, "does not match the buffer plan (4)"),
+             (img[:-1], 8, "truncated trace image"),
+             (img + b"\0", 8, "trailing bytes after trace image"),
+             (b"XPFT" + img[4:], 8, "bad magic: not a trace image"),
+             (img[:4] + b"\x03\x00" + img[6:], 8, "unsupported trace version 3")]
+    for data, slots, msg in cases:
+        with pytest.raises(t.Error) as ei:
+            ctx.replay_image_bytes(data, plan_of(slots, 0, []), 33)
+        assert ei.value.category() == "trace-error" and msg in str(ei.value)
+        with pytest.raises(O.OracleError) as eo:
+            oracle.replay_kpft(data, slots, 0, [], 33)
+        assert str(eo.value) == str(ei.value)
+
+
+# ---------------------------------------------------------------------------
+# reference known answers through the C-ABI
+# ---------------------------------------------------------------------------
+
+def test_known_answers_unit_entry_points(ctx):
+    t = T()
+    P = t.ProfileRecord.make
+    assert P(True, 3, 0, 1000).tag == 0x80003000                 # test_trace:9
+    img = t.GlobalTraceImage([t.TraceStream(0, 1, 6, 4, [P(True, 4, 0, 4),
+                                                         P(True, 5, 0, 5),
+                                                         P(True, 2, 0, 2),
+                                                         P(True, 3, 0, 3)])])
+    d = ctx.decode_image_bytes(t.serialize_image(img),
+                               t.BufferPlan(4, t.BufferStrategy.Circular, []))
+    assert d[0].dropped_records == 2                             # test_trace:82
+    assert [(int(x) >> 12) & 0x7FFFF for x in d[0].records["tag"]] == [2, 3, 4, 5]
+    u = ctx.unwrap_clock([0xFFFFFF00, 0x00000100])               # test_trace:132
+    assert int(u[1] - u[0]) == 0x200
+    assert list(ctx.unwrap_clock([10, 20, 4000])) == [10, 20, 4000]
+    pr = ctx.pair_records(t.records_array([P(True, 0, 0, 10), P(True, 1, 0, 20),
+                                           P(False, 1, 0, 30), P(False, 0, 0, 40)]),
+                          ["a", "b"])                            # test_trace:171
+    assert [(int(a), int(b), int(c)) for a, b, c in
+            pr.intervals[["region_id", "start", "end"]]] == [(1, 20, 30), (0, 10, 40)]
+    pr = ctx.pair_records(t.records_array([P(False, 0, 0, 10)]), ["a"])
+    assert pr.dropped_heads == 1 and len(pr.intervals) == 0
+    lst = [P(True, 0, 0, 0)]
+    for i in range(1, 6):
+        c = (i * 0x90000000) & 0xFFFFFFFF
+        lst += [P(True, 1, 0, c), P(False, 1, 0, c)]
+    lst.append(P(False, 0, 0, (5 * 0x90000000) & 0xFFFFFFFF))
+    with pytest.raises(t.Error, match=r"exceeds 2\^32"):      # test_trace:203
+        ctx.pair_records(t.records_array(lst), ["a", "b"])
+    iv = np.array([(0, 0, 10, 150, 0, 1), (1, 0, 400, 410, 2, 3)], t.INTERVAL_DTYPE)
+    rr = ctx.replay(iv, ["G", "G.wait"], 0, 0, 33)             # test_replay:51
+    assert (int(rr.events[1]["start"]), int(rr.events[1]["end"])) == (150, 400)
+    iv = np.array([(1, 0, 40, 80, 1, 2), (0, 0, 10, 176, 0, 3)], t.INTERVAL_DTYPE)
+    rr = ctx.replay(iv, ["outer", "inner"], 0, 0, 33)          # test_replay:66
+    assert int(rr.events[1]["end"] - rr.events[1]["start"]) == 67
+    iv = np.array([(0, 0, 10, 100, 0, 1), (1, 0, 120, 130, 2, 3)], t.INTERVAL_DTYPE)
+    rr = ctx.replay(iv, ["G", "G.wait"], 0, 0, 33)             # test_replay:81
+    assert rr.flagged_preconditions == 1
+    iv = np.array([(1, 0, 120, 130, 0, 1)], t.INTERVAL_DTYPE)
+    rr = ctx.replay(iv, ["G", "G.wait"], 0, 0, 33)             # test_replay:92
+    assert rr.malformed_groups == 1 and len(rr.events) == 1
+
+
+# ---------------------------------------------------------------------------
+# device-resident bodies at scale
+# ---------------------------------------------------------------------------
+
+def _device_replay(ctx, shape, s0, n, flags=0):
+    import torch
+    labels = S.MIXED_LABELS if shape == 0 else S.NESTED_LABELS
+    strategy = 1 if shape == 0 else 0
+    ctx.set_plan(plan_of(S.CAP, strategy, labels))
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), shape, s0, n, S.MIXED_FULL_LONG)
+    cap = n * 128
+    ev = torch.empty(cap * 32, dtype=torch.uint8, device="cuda")
+    ne, w = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, ev.data_ptr(),
+                              cap, flags)
+    return body, ev, ne, w, labels, strategy
+
+
+@pytest.mark.parametrize("shape", [0, 1])
+def test_device_body_vs_oracle_64k_streams(ctx, oracle, shape):
+    n = 1 << 16
+    s0 = S.MIXED_FULL_LONG - n // 2
+    body, ev, ne, w, labels, strategy = _device_replay(ctx, shape, s0, n, 0x2)
+    o = oracle.replay_body(body.cpu().numpy(), n, S.CAP, strategy, labels, 33)
+    got = ev[:ne * 32].cpu().numpy().view(O.EVENT_DTYPE)
+    assert ne == len(o.events)
+    assert np.array_equal(got, o.events)
+    assert (w.dropped_heads, w.truncated_tails, w.flagged_preconditions,
+            w.malformed_groups) == (o.dropped_heads, o.truncated_tails,
+                                    o.flagged_preconditions, o.malformed_groups)
+    want = oracle.region_stats(o.events, labels)
+    st = ctx.stats()
+    for s in want:
+        g = st[s.label]
+        assert (g.count, g.min, g.max, g.sum, g.mean, g.warp_group, g.kind,
+                g.first_event, g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
+                                           s.warp_group, s.kind, s.first_event,
+                                           s.hist)
+
+
+@pytest.mark.slow
+def test_full_config4_properties(ctx, oracle):
+    """Full 2^30-record config 4 on one B200: closed-form totals plus a
+    sample of streams checked against the oracle event for event."""
+    import torch
+    n = S.MIXED_FULL_STREAMS
+    body, ev, ne, w, labels, strategy = _device_replay(ctx, 0, 0, n, 0)
+    assert ne == 531_791_872
+    n_long = S.MIXED_FULL_LONG
+    tails = (n_long // 16) * (4 * 0 + 12 * 2) + ((n - n_long) // 16) * (4 * 1 + 12 * 3)
+    assert (w.dropped_heads, w.truncated_tails, w.malformed_groups) == (0, tails, 0)
+    st = ctx.stats()
+    assert sum(s.count for s in st.values()) == ne
+    rng = np.random.default_rng(4)
+    counts = np.where(np.arange(n) < n_long, 0, 0)
+    del counts
+    stride = S.stream_stride()
+    for s in sorted(rng.choice(n, 64, replace=False)):
+        s = int(s)
+        one = body[s * stride:(s + 1) * stride].cpu().numpy()
+        o = oracle.replay_body(one, 1, S.CAP, 1, labels, 33)
+        # event offset of stream s: closed form over the 16-stream blocks
+        blk, lane = divmod(s, 16)
+        def per(gs):
+            long_ = gs < n_long
+            return (111 if long_ else 110) if gs % 16 < 4 else (110 if long_ else 109)
+        off = 0
+        full_long_blocks = min(blk, n_long // 16)
+        off += full_long_blocks * (4 * 111 + 12 * 110)
+        off += (blk - full_long_blocks) * (4 * 110 + 12 * 109)
+        off += sum(per(blk * 16 + k) for k in range(lane))
+        got = ev[off * 32:(off + len(o.events)) * 32].cpu().numpy().view(O.EVENT_DTYPE)
+        assert np.array_equal(got, o.events), s
+    del body, ev
+    torch.cuda.empty_cache()
+
+
+def test_stats_merge_two_shards(ctx):
+    """Multi-GPU shard-and-reduce on one device: two shards of a body, each
+    replayed with its stream_base, stats exported, gathered and merged,
+    equal the single-shot stats (integer fields and first-event keys)."""
+    import torch
+    t = T()
+    n = 40000
+    labels = S.MIXED_LABELS
+    plan = plan_of(S.CAP, 1, labels)
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.set_plan(plan)
+    ctx.synth_body(body.data_ptr(), 0, S.MIXED_FULL_LONG - n // 2, n, S.MIXED_FULL_LONG)
+    ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0, 0x1)
+    whole = ctx.stats()
+    parts = [t.Context(0), t.Context(0)]
+    pb = parts[0].stats_packed_bytes()
+    gathered = torch.zeros(2 * pb, dtype=torch.uint8, device="cuda")
+    cut = 17003
+    stride = S.stream_stride()
+    for r, (a, b) in enumerate([(0, cut), (cut, n)]):
+        c = parts[r]
+        c.set_plan(plan)
+        c.replay_device(body.data_ptr() + a * stride, (b - a) * stride, b - a, 33,
+                        0, 0, 0x1, stream_base=a)
+        c.stats_export(gathered.data_ptr() + r * pb)
+    torch.cuda.synchronize()
+    merged_ctx = t.Context(0)
+    merged_ctx.set_plan(plan)
+    merged_ctx.stats_merge(gathered.data_ptr(), 2)
+    merged = merged_ctx.stats()
+    assert list(merged) == list(whole)
+    for k in whole:
+        a, b = whole[k], merged[k]
+        assert (a.count, a.sum, a.min, a.max, a.warp_group, a.kind, a.hist) == (
+            b.count, b.sum, b.min, b.max, b.warp_group, b.kind, b.hist)
+
+
+def test_cxx_shim_end_to_end(tmp_path):
+    """The drop-in C++ shim (reference signatures) against libwgpf.so."""
+    import subprocess
+    from paper_2505_21661_b200 import _build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "shim_test")
+    lib = _build.build()
+    res = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"),
+                          os.path.join(root, "tests", "cxx", "shim_test.cpp"),
+                          lib, f"-Wl,-rpath,{os.path.dirname(lib)}", "-o", exe],
+                         capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    res = subprocess.run([exe, os.path.join(GOLDEN, "fixtures")], capture_output=True,
+                         text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "ALL PASS" in res.stdout

@@ -1,0 +1,384 @@
+"""bench.py -- trace records decoded/s on the synthetic config-4 trace.
+
+One step = one replay_image of this rank's full config-4 trace (SURVEY.md 8(d)
+config 4: 148 SMs x 2048 CTAs x 16 warps = 4,849,664 streams, 2^30 records,
+flush, capacity 256, 8 regions) already resident in HBM: pass-1 counts, the
+offset scan, the warp-cooperative decode/pair/replay/stats pass writing all
+531,791,872 events, statistics finalisation, and (N > 1) the one NCCL
+all-gather + merge of the per-label tables.  Weak scaling: every rank owns one
+config-4-sized block range of an N x 2^30-record trace.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line on rank 0.  --impl reference times the reference's own
+CPU implementation (oracle/_ref, compiled from the reference headers) on a
+bounded sample of the same workload with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("trace records decoded/s (GB/s vs HBM peak) at 1/2/4/8 GPU; "
+          "instr. overhead %")
+WORKLOAD = ("config 4: synthetic 2^30-record trace per GPU (148 SMs x 2048 CTAs "
+            "x 16 warps = 4,849,664 streams), flush, 256 slots, 8 regions, "
+            "TMA producer / MMA consumer patterns")
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return None
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+            out, _ = self.p.communicate()
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from oracle import synth as S
+    ref = O.Reference()
+    threads = len(os.sched_getaffinity(0))
+    steps, warmup = args.steps, args.warmup
+    # calibrate: one 65,535-stream chunk on all threads
+    cal_n = 65535 * max(1, min(threads, 8))
+    body = S.mixed_body(0, cal_n, S.MIXED_FULL_LONG)
+    r = ref.bench_replay(body, cal_n, S.CAP, 1, S.MIXED_LABELS, 33, 65535, threads)
+    rate = r["records"] / max(r["seconds"], 1e-6)
+    budget = args.ref_budget_s / (steps + warmup)
+    n = int(min(S.MIXED_FULL_STREAMS, max(cal_n, rate * budget / 221.5)))
+    n = (n // 16) * 16
+    if n != cal_n:
+        body = S.mixed_body(0, n, S.MIXED_FULL_LONG)
+    times, recs, evs = [], 0, 0
+    for i in range(warmup + steps):
+        r = ref.bench_replay(body, n, S.CAP, 1, S.MIXED_LABELS, 33, 65535, threads)
+        if i >= warmup:
+            times.append(r["seconds"])
+            recs, evs = r["records"], r["events"]
+    sec = sum(times) / len(times)
+    value = recs / sec
+    sample = (f"first {n} streams of config 4 ({recs} records, {evs} events) per "
+              f"step; deserialize->decode->pair->replay->region_stats over "
+              f"65,535-stream KPFT v1 chunks, {threads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "records/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/u64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_streams": n},
+        "cpu_baseline": {"value": value, "unit": "records/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "records/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+
+def cpu_baseline(host_body_u8, n_avail, budget_s):
+    """oracle/_ref (the reference) on a bounded sample, all host threads."""
+    from oracle import oracle as O
+    from oracle import synth as S
+    if not O.have_ref():
+        return None
+    ref = O.Reference()
+    threads = len(os.sched_getaffinity(0))
+    stride = S.stream_stride()
+    cal_n = min(n_avail, 65535 * max(1, min(threads, 8)))
+    r = ref.bench_replay(host_body_u8[:cal_n * stride], cal_n, S.CAP, 1,
+                         S.MIXED_LABELS, 33, 65535, threads)
+    rate = r["records"] / max(r["seconds"], 1e-6)
+    n = int(min(n_avail, max(cal_n, rate * budget_s / 221.5)))
+    n = (n // 16) * 16
+    r = ref.bench_replay(host_body_u8[:n * stride], n, S.CAP, 1, S.MIXED_LABELS,
+                         33, 65535, threads)
+    return {"value": r["records"] / r["seconds"], "unit": "records/s",
+            "cores": threads, "kind": "reference",
+            "sample": (f"first {n} streams of config 4 ({r['records']} records, "
+                       f"{r['seconds']:.1f} s); reference deserialize->decode->"
+                       f"pair->replay->region_stats, 65,535-stream v1 chunks, "
+                       f"{threads} threads")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=0,
+                    help="streams per GPU (default: full config 4)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    args = ap.parse_args()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from oracle import synth as S
+    from paper_2505_21661_b200 import _lib as L
+    from paper_2505_21661_b200 import trace as T
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    ctx = T.Context(local, stream.cuda_stream)
+    plan = T.BufferPlan(S.CAP, T.BufferStrategy.Flush, S.MIXED_LABELS)
+    ctx.set_plan(plan)
+
+    n = args.streams or S.MIXED_FULL_STREAMS
+    s0 = rank * n
+    n_long = s0 + (S.MIXED_FULL_LONG if n == S.MIXED_FULL_STREAMS
+                   else S.mixed_long_for(n))
+    stride = S.stream_stride()
+    body = torch.empty(n * stride, dtype=torch.uint8, device=dev)
+    ctx.synth_body(body.data_ptr(), 0, s0, n, n_long)
+    torch.cuda.synchronize()
+
+    # sizes: records / events of this rank (one STATS_ONLY pass)
+    n_ev, _ = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0,
+                                L.F_STATS_ONLY | L.F_NO_STATS, stream_base=s0)
+    records = int(min(222, 256) * (n_long - s0) + 221 * (n - (n_long - s0)))
+    events = torch.empty(n_ev * 32, dtype=torch.uint8, device=dev)
+    alg_bytes = 16 * n + 8 * records + 32 * n_ev
+
+    packed = ctx.stats_packed_bytes()
+    mine = torch.zeros(packed, dtype=torch.uint8, device=dev)
+    gathered = torch.zeros(packed * world, dtype=torch.uint8, device=dev)
+    merged_ctx = None
+    if world > 1:
+        merged_ctx = T.Context(local, stream.cuda_stream)
+        merged_ctx.set_plan(plan)
+
+    def step():
+        ne, w = ctx.replay_device(body.data_ptr(), body.numel(), n, 33,
+                                  events.data_ptr(), n_ev, L.F_PROFILE,
+                                  stream_base=s0)
+        assert ne == n_ev
+        prof = ctx.last_profile()
+        launches = prof["launches"]
+        if world > 1:
+            ctx.stats_export(mine.data_ptr())
+            dist.all_gather_into_tensor(gathered, mine)
+            merged_ctx.stats_merge(gathered.data_ptr(), world)
+            launches += 3
+        return prof, launches, w
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(stream)
+    profs, launches = [], 0
+    for _ in range(args.steps):
+        p, l, w = step()
+        profs.append(p)
+        launches += l
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * records * args.steps / (ms / 1e3)
+
+    emit_ms = statistics.mean(p["emit_ms"] for p in profs)
+    count_ms = statistics.mean(p["count_ms"] for p in profs)
+    peak, peak_kind = measured_peaks()
+    achieved = alg_bytes / (emit_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_emit_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the reference-facing call (host buffers) -------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        hdr = b"KPFT" + (2).to_bytes(2, "little") + b"\0\0" + n.to_bytes(8, "little")
+        img = torch.empty(len(hdr) + body.numel(), dtype=torch.uint8, pin_memory=True)
+        img[:len(hdr)] = torch.frombuffer(bytearray(hdr), dtype=torch.uint8)
+        img[len(hdr):].copy_(body, non_blocking=False)
+        hev = torch.empty(n_ev * 32, dtype=torch.uint8, pin_memory=True)
+        lib = L.lib()
+        ne, wr = C.c_uint64(), L.Warnings()
+
+        def e2e_step():
+            rc = lib.wgpf_replay_image(ctx.h, C.c_void_p(img.data_ptr()), img.numel(),
+                                       33, C.c_void_p(hev.data_ptr()), n_ev, 0,
+                                       C.byref(ne), C.byref(wr))
+            assert rc == 0 and ne.value == n_ev, (rc, ne.value)
+            st = ctx.stats()  # the step's result read back to the host
+            return st
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - a)
+        sec = statistics.mean(ts)
+        if world > 1:
+            t = torch.tensor([sec], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        e2e = {"value": world * records / sec, "unit": "records/s",
+               "h2d_bytes_per_step": int(img.numel()),
+               "d2h_bytes_per_step": int(n_ev * 32 + packed),
+               "ms_per_step": sec * 1e3}
+        base_host = img[len(hdr):].numpy()
+    else:
+        base_host = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if base_host is None:
+            base_host = body[: min(n, 1 << 20) * stride].cpu().numpy()
+        cpu = cpu_baseline(base_host, len(base_host) // stride, args.cpu_budget_s)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "records/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32/u64 (integer trace records)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "streams_per_gpu": n,
+                       "records_per_gpu": records, "events_per_gpu": n_ev,
+                       "parallelism": f"dp{world} (block-range shards, one NCCL "
+                                      "all-gather of per-label tables per step)",
+                       "l2": "inputs larger than L2 (10.0 GB body, 17.0 GB events "
+                             "per GPU)"},
+            "gbs": alg_bytes / (ms_step / 1e3) / 1e9,
+            "hbm_frac_step": alg_bytes / (ms_step / 1e3) / 1e9 / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_fast_emit",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "kernel_ms": emit_ms, "peak_kind": peak_kind},
+            "phases_ms": {"count": count_ms,
+                          "scan": statistics.mean(p["scan_ms"] for p in profs),
+                          "emit": emit_ms,
+                          "general": statistics.mean(p["general_ms"] for p in profs),
+                          "finalize": statistics.mean(p["finalize_ms"] for p in profs)},
+            "general_streams": profs[-1]["general_streams"],
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches,
+            "instr_overhead_pct": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -103,6 +103,21 @@ typedef struct wgpf_region_stat { /* RegionStats, pipeline.hpp:105-112 + ext */
 #define WGPF_F_FORCE_GENERAL 0x4u /* route every stream through the general
                                      (thread-per-stream) kernels            */
 #define WGPF_F_NO_STATS 0x8u    /* skip region statistics                  */
+#define WGPF_F_PROFILE 0x10u    /* record per-phase CUDA-event timings     */
+
+/* Per-phase device time of the last wgpf_replay_device (WGPF_F_PROFILE) and
+ * the number of this library's kernels it launched. */
+typedef struct wgpf_profile {
+  float count_ms;    /* pass 1 (k_count_fast)                      */
+  float scan_ms;     /* event-offset scan                          */
+  float emit_ms;     /* pass 2 fast path (k_fast_emit)             */
+  float general_ms;  /* general path (k_general_emit), if any      */
+  float finalize_ms; /* statistics finalisation                    */
+  float total_ms;
+  uint32_t launches;        /* kernels of this library launched     */
+  uint32_t general_streams; /* streams taken by the general path   */
+} wgpf_profile;
+int wgpf_last_profile(const wgpf_ctx* ctx, wgpf_profile* out);
 
 /* ----------------------------------------------------------------------- */
 /* Lifecycle                                                                 */

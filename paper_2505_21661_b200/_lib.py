@@ -51,6 +51,15 @@ class RegionStat(C.Structure):
                 ("first_event", C.c_uint64), ("hist", C.c_uint64 * HIST_BINS)]
 
 
+class Profile(C.Structure):
+    _fields_ = [("count_ms", C.c_float), ("scan_ms", C.c_float),
+                ("emit_ms", C.c_float), ("general_ms", C.c_float),
+                ("finalize_ms", C.c_float), ("total_ms", C.c_float),
+                ("launches", C.c_uint32), ("general_streams", C.c_uint32)]
+
+
+F_PROFILE = 0x10
+
 _lock = threading.Lock()
 _lib = None
 
@@ -90,6 +99,7 @@ def lib() -> C.CDLL:
             "wgpf_stats_export": ([vp, vp], i32),
             "wgpf_stats_merge": ([vp, vp, u32], i32),
             "wgpf_synth_body": ([vp, vp, u32, u64, u64, u64], i32),
+            "wgpf_last_profile": ([vp, C.POINTER(Profile)], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -99,12 +99,23 @@ struct wgpf_ctx {
       d_glen, d_orphans, d_gscratch, d_image, d_events, d_aux0, d_aux1, d_aux2,
       d_aux3;
   DevStatus* h_status = nullptr;  // pinned
+  // profiling
+  cudaEvent_t ev[8] = {};
+  bool profiling = false;
+  uint32_t launches = 0;
+  uint64_t general_streams = 0;
+  wgpf_profile prof{};
   uint64_t last_stream_base = 0, last_n_streams = 0;
   const uint8_t* last_body = nullptr;
   uint64_t last_stride = 0;
 
   ~wgpf_ctx() {
     if (h_status) cudaFreeHost(h_status);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  void mark(int i) {
+    if (profiling) cudaEventRecord(ev[i], stream);
   }
 };
 
@@ -272,6 +283,7 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
   }
   cudaFuncSetAttribute(k_fast_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(FastSmem));
+  for (auto& e : c->ev) cudaEventCreate(&e);
   *out = c;
   return WGPF_OK;
 }
@@ -435,6 +447,7 @@ static int run_general(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
     a.first = first;
     k_general_emit<<<(uint32_t)(batch / 128), 128, 0, c->stream>>>(a);
     CUDA_OK(c, cudaGetLastError());
+    ++c->launches;
   }
   return WGPF_OK;
 }
@@ -472,6 +485,7 @@ static int run_general_count(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
     a.first = first;
     k_general_count<<<(uint32_t)(batch / 128), 128, 0, c->stream>>>(a);
     CUDA_OK(c, cudaGetLastError());
+    ++c->launches;
   }
   return WGPF_OK;
 }
@@ -506,6 +520,7 @@ static int scan_counts(wgpf_ctx* c, uint64_t n) {
                                            (int64_t)n, c->stream));
   k_total<<<1, 1, 0, c->stream>>>(in, out, n, c->d_status.as<DevStatus>());
   CUDA_OK(c, cudaGetLastError());
+  ++c->launches;
   return WGPF_OK;
 }
 
@@ -515,8 +530,11 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                      uint64_t events_cap, bool no_stats, bool force_general) {
   CUDA_OK(c, cudaMemsetAsync(c->d_glen.p, 0, 8, c->stream));
   if (force_general) {
+    c->mark(3);
+    c->general_streams += n_streams;
     int rc = run_general(c, body, stride, n_streams, stream_base, record_cost,
                          events, events_cap, no_stats, false, n_streams);
+    c->mark(4);
     return rc;
   }
   FastArgs f;
@@ -546,13 +564,18 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.orphan_scratch = c->d_orphans.as<wgpf_event>();
   k_fast_emit<<<grid, kFastWarps * 32, sizeof(FastSmem), c->stream>>>(f);
   CUDA_OK(c, cudaGetLastError());
+  ++c->launches;
+  c->mark(3);
   // streams the fast path routed away
   unsigned long long glen = 0;
   CUDA_OK(c, cudaMemcpyAsync(&glen, c->d_glen.p, 8, cudaMemcpyDeviceToHost,
                              c->stream));
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
-  return run_general(c, body, stride, n_streams, stream_base, record_cost,
-                     events, events_cap, no_stats, true, glen);
+  c->general_streams += glen;
+  int rc = run_general(c, body, stride, n_streams, stream_base, record_cost,
+                       events, events_cap, no_stats, true, glen);
+  c->mark(4);
+  return rc;
 }
 
 static int report_errors(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
@@ -604,6 +627,7 @@ static int finalize_stats(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       dev_stats(c), ns, body, stride, stream_base, n_streams,
       c->d_first_wg.as<unsigned long long>());
   CUDA_OK(c, cudaGetLastError());
+  ++c->launches;
   c->mean_exact_valid = false;
   if (exact && events && n_events) {
     // stable class sort of durations, then the recurrence per class
@@ -660,6 +684,11 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   }
   const bool stats_only = flags & WGPF_F_STATS_ONLY;
   const bool no_stats = flags & WGPF_F_NO_STATS;
+  c->profiling = (flags & WGPF_F_PROFILE) != 0;
+  c->launches = 0;
+  c->general_streams = 0;
+  c->prof = wgpf_profile{};
+  c->mark(0);
   const bool force_general = flags & WGPF_F_FORCE_GENERAL;
   wgpf_event* events = stats_only ? nullptr : d_events;
   const uint8_t* body = static_cast<const uint8_t*>(d_body);
@@ -696,8 +725,11 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                  c->stream>>>(ca);
   CUDA_OK(c, cudaGetLastError());
+  ++c->launches;
+  c->mark(1);
   rc = scan_counts(c, n_streams);
   if (rc) return rc;
+  c->mark(2);
   rc = emit_pass(c, body, stride, n_streams, stream_base, record_cost, events,
                  events_cap, no_stats, force_general);
   if (rc) return rc;
@@ -752,8 +784,26 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
     rc = finalize_stats(c, body, stride, stream_base, n_streams, events,
                         st.total_events, (flags & WGPF_F_EXACT_MEAN) != 0);
     if (rc) return rc;
-    CUDA_OK(c, cudaStreamSynchronize(c->stream));
   }
+  c->mark(5);
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  if (c->profiling) {
+    float t[5];
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], c->ev[i], c->ev[i + 1]);
+    c->prof.count_ms = t[0];
+    c->prof.scan_ms = t[1];
+    c->prof.emit_ms = t[2];
+    c->prof.general_ms = t[3];
+    c->prof.finalize_ms = t[4];
+    cudaEventElapsedTime(&c->prof.total_ms, c->ev[0], c->ev[5]);
+  }
+  c->prof.launches = c->launches;
+  c->prof.general_streams = (uint32_t)c->general_streams;
+  return WGPF_OK;
+}
+
+extern "C" int wgpf_last_profile(const wgpf_ctx* c, wgpf_profile* out) {
+  *out = c->prof;
   return WGPF_OK;
 }
 

@@ -417,6 +417,11 @@ class Context:
         _check(self.h, rc, ne.value)
         return ne.value, w
 
+    def last_profile(self) -> dict:
+        p = L.Profile()
+        self.L.wgpf_last_profile(self.h, C.byref(p))
+        return {k: getattr(p, k) for k, _ in L.Profile._fields_}
+
     def stats(self) -> dict:
         """Statistics of the last replay (label -> RegionStats), label order."""
         return self._read_stats(self.L.wgpf_stats_get)

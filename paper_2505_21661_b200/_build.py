@@ -16,6 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libwgpf.so")
+CSRC_P1 = os.path.join(PKG, "csrc_p1")
+LIB_P1 = os.path.join(LIBDIR, "libwgpf_p1.so")
 INCLUDE = os.path.join(ROOT, "include")
 
 NVCC_FLAGS = [
@@ -46,19 +48,41 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
-        return LIB
+def _compile(srcs, out, log):
     os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}",
-           os.path.join(CSRC, "capi.cu"), "-o", tmp]
+    tmp = out + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", *srcs, "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed building libwgpf.so:\n" + res.stderr[-8000:])
-    if verbose:
-        print(res.stderr)
-    with open(os.path.join(LIBDIR, "ptxas.txt"), "w") as f:
+        raise RuntimeError(f"nvcc failed building {os.path.basename(out)}:\n" +
+                           res.stderr[-8000:])
+    with open(os.path.join(LIBDIR, log), "w") as f:
         f.write(res.stderr)
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
+    return res.stderr
+
+
+def p1_sources() -> list[str]:
+    return sorted(glob.glob(os.path.join(CSRC_P1, "*.cu")) +
+                  glob.glob(os.path.join(CSRC_P1, "*.cuh")) +
+                  glob.glob(os.path.join(INCLUDE, "*.cuh")) +
+                  glob.glob(os.path.join(INCLUDE, "*.h")))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """libwgpf.so: the P2 post-processor (C-ABI include/wgpf.h)."""
+    if force or stale():
+        err = _compile([os.path.join(CSRC, "capi.cu")], LIB, "ptxas.txt")
+        if verbose:
+            print(err)
     return LIB
+
+
+def build_p1(force: bool = False) -> str:
+    """libwgpf_p1.so: P1 runtime workloads (self-test, record cost, GEMM)."""
+    fresh = os.path.exists(LIB_P1) and all(
+        os.path.getmtime(s) <= os.path.getmtime(LIB_P1) for s in p1_sources())
+    if force or not fresh:
+        _compile(sorted(glob.glob(os.path.join(CSRC_P1, "*.cu"))), LIB_P1,
+                 "ptxas_p1.txt")
+    return LIB_P1

@@ -1,0 +1,138 @@
+// p1_selftest.cu -- P1 device runtime exercised by known scope programs.
+//
+// wgpf_p1_selftest: every warp of every CTA runs the same scope program
+// (nested sync scopes, the reference's 4-record async pattern
+// instrument.hpp:14-25, a loop) through wgpf_dev::Recorder, then the CTA
+// flushes its shared-memory buffer to HBM as a KPFT body.  The tests decode
+// that body with the reference (oracle/_ref) and the CPU oracle and check the
+// per-stream tag sequence against the program's store log (vgpu.hpp:269-271).
+//
+// wgpf_p1_record_cost: cycles per record op -- the same loop with and without
+// records, timed per warp with %clock64 (PAPER.md:798 reports 33 cycles on
+// H100).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "wgpf_device.cuh"
+
+namespace {
+
+constexpr uint32_t R_KERNEL = 0, R_OUTER = 1, R_INNER = 2, R_ASYNC = 3,
+                   R_ASYNC_WAIT = 4;
+
+__device__ __forceinline__ uint32_t busy(uint32_t x, uint32_t n) {
+  for (uint32_t i = 0; i < n; ++i) x = x * 1664525u + 1013904223u;
+  return x;
+}
+
+template <bool kPow2>
+__global__ void k_selftest(uint8_t* profile, uint32_t cap, uint32_t iters,
+                           uint32_t* sink, wgpf_dev::CtaTiming* timing) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t nwarps = blockDim.x >> 5;
+  const uint64_t cta = blockIdx.x;
+  if (threadIdx.x == 0 && timing) {
+    timing[cta].smid = wgpf_dev::smid();
+    timing[cta].streams = nwarps;
+    timing[cta].gt_start = wgpf_dev::globaltimer();
+    timing[cta].clk_start = wgpf_dev::clock32();
+  }
+  wgpf_dev::Recorder<kPow2> rec;
+  rec.init(buf, warp, cap, lane == 0);
+  uint32_t x = threadIdx.x + 7u * blockIdx.x;
+  rec.start(R_KERNEL);
+  for (uint32_t it = 0; it < iters; ++it) {
+    rec.start(R_OUTER);
+    x = busy(x, 16 + (it & 3));
+    rec.start(R_INNER);
+    x = busy(x, 8 + warp);
+    rec.end(R_INNER);
+    rec.end(R_OUTER);
+    rec.start(R_ASYNC);  // S(X) before the launch
+    x = busy(x, 4);
+    rec.end(R_ASYNC);    // E(X) before the wait
+    x = busy(x, 32);     // the wait
+    rec.start(R_ASYNC_WAIT);
+    rec.end(R_ASYNC_WAIT);
+  }
+  rec.end(R_KERNEL);
+  rec.close((uint32_t)cta, warp, cap);
+  __syncthreads();
+  const uint32_t bytes = wgpf_dev::smem_bytes(nwarps, cap);
+  wgpf_dev::flush(buf, profile, cta, bytes, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0 && timing) {
+    timing[cta].gt_end = wgpf_dev::globaltimer();
+    timing[cta].clk_end = wgpf_dev::clock32();
+  }
+  if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
+// Per-warp cycle cost of N record ops inside an ALU loop.
+template <bool kRecord>
+__global__ void k_record_cost(uint32_t n, uint64_t* cycles, uint32_t* sink) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  wgpf_dev::Recorder<true> rec;
+  rec.init(buf, warp, 256, lane == 0);
+  uint32_t x = threadIdx.x;
+  __syncwarp();
+  const uint64_t t0 = clock64();
+  for (uint32_t i = 0; i < n; ++i) {
+    if constexpr (kRecord) rec.start(1);
+    x = x * 1664525u + 1013904223u;
+    if constexpr (kRecord) rec.end(1);
+    x = x * 1664525u + 1013904223u;
+  }
+  __syncwarp();
+  const uint64_t t1 = clock64();
+  if (lane == 0) cycles[blockIdx.x * (blockDim.x >> 5) + warp] = t1 - t0;
+  if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
+}  // namespace
+
+extern "C" int wgpf_p1_selftest(void* d_profile, uint32_t ctas,
+                                uint32_t warps_per_cta, uint32_t cap,
+                                uint32_t iters, void* d_timing, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  const uint32_t smem = wgpf_dev::smem_bytes(warps_per_cta, cap);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool pow2 = cap && !(cap & (cap - 1));
+  if (pow2) {
+    cudaFuncSetAttribute(k_selftest<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_selftest<true><<<ctas, warps_per_cta * 32, smem, st>>>(
+        static_cast<uint8_t*>(d_profile), cap, iters, sink,
+        static_cast<wgpf_dev::CtaTiming*>(d_timing));
+  } else {
+    cudaFuncSetAttribute(k_selftest<false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_selftest<false><<<ctas, warps_per_cta * 32, smem, st>>>(
+        static_cast<uint8_t*>(d_profile), cap, iters, sink,
+        static_cast<wgpf_dev::CtaTiming*>(d_timing));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
+
+// cycles[warps] out; returns 0 on success.  record != 0 selects the
+// instrumented loop.
+extern "C" int wgpf_p1_record_cost(uint32_t n, uint32_t warps, int record,
+                                   void* d_cycles, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t smem = wgpf_dev::smem_bytes(warps, 256);
+  if (record) {
+    cudaFuncSetAttribute(k_record_cost<true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_record_cost<true><<<1, warps * 32, smem, st>>>(
+        n, static_cast<uint64_t*>(d_cycles), sink);
+  } else {
+    k_record_cost<false><<<1, warps * 32, smem, st>>>(
+        n, static_cast<uint64_t*>(d_cycles), sink);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}

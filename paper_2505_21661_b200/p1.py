@@ -1,0 +1,107 @@
+"""P1 -- the device instrumentation runtime (include/wgpf_device.cuh) and its
+workloads: a scope-program self-test, the per-record cost microbenchmark and
+the instrumented tcgen05/TMA bf16 GEMM (config 2).  Thin ctypes layer over
+libwgpf_p1.so; the profile buffers these kernels leave in HBM are KPFT bodies
+that the P2 decoder (trace.Context.replay_device) reads in place.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+
+import numpy as np
+
+from . import _build
+
+_lib = None
+
+# scope-program self-test regions (csrc_p1/p1_selftest.cu)
+SELFTEST_LABELS = ["kernel", "outer", "inner", "async", "async.wait"]
+# GEMM scopes (csrc_p1/gemm_tcgen05.cu)
+GEMM_LABELS = ["tile", "tma.wait", "tma.issue", "mma.wait", "mma.issue",
+               "epi.wait", "epi.ld", "epi.st"]
+GEMM_WARPS = 6
+GEMM_SLOTS = 64
+CTA_TIMING_DTYPE = np.dtype([("smid", "<u4"), ("streams", "<u4"),
+                             ("gt_start", "<u8"), ("gt_end", "<u8"),
+                             ("clk_start", "<u4"), ("clk_end", "<u4")])
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        L = C.CDLL(_build.build_p1())
+        vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
+        L.wgpf_p1_selftest.argtypes = [vp, u32, u32, u32, u32, vp, vp]
+        L.wgpf_p1_selftest.restype = i32
+        L.wgpf_p1_record_cost.argtypes = [u32, u32, i32, vp, vp]
+        L.wgpf_p1_record_cost.restype = i32
+        L.wgpf_gemm_bf16.argtypes = [vp, vp, vp, u32, u32, u32, i32, vp, vp, vp]
+        L.wgpf_gemm_bf16.restype = i32
+        L.wgpf_gemm_profile_bytes.argtypes = [u32, u32]
+        L.wgpf_gemm_profile_bytes.restype = u64
+        L.wgpf_gemm_smem_bytes.argtypes = [i32]
+        L.wgpf_gemm_smem_bytes.restype = u32
+        _lib = L
+    return _lib
+
+
+def _check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed (status {rc})")
+
+
+def stream_stride(cap: int) -> int:
+    return 16 + 8 * cap
+
+
+def selftest(profile_ptr: int, ctas: int, warps: int, cap: int, iters: int,
+             timing_ptr: int = 0, stream: int = 0) -> None:
+    _check(lib().wgpf_p1_selftest(C.c_void_p(profile_ptr), ctas, warps, cap, iters,
+                                  C.c_void_p(timing_ptr), C.c_void_p(stream)),
+           "wgpf_p1_selftest")
+
+
+def selftest_store_log(iters: int) -> list:
+    """The (start, region) sequence one warp stores (vgpu.hpp:269-271)."""
+    k, o, i, a, w = range(5)
+    log = [(1, k)]
+    for _ in range(iters):
+        log += [(1, o), (1, i), (0, i), (0, o), (1, a), (0, a), (1, w), (0, w)]
+    log.append((0, k))
+    return log
+
+
+def record_cost(n: int, warps: int, record: bool, cycles_ptr: int,
+                stream: int = 0) -> None:
+    _check(lib().wgpf_p1_record_cost(n, warps, int(record), C.c_void_p(cycles_ptr),
+                                     C.c_void_p(stream)), "wgpf_p1_record_cost")
+
+
+def gemm(a_ptr: int, b_ptr: int, c_ptr: int, M: int, N: int, K: int,
+         instrument: bool = False, profile_ptr: int = 0, timing_ptr: int = 0,
+         stream: int = 0) -> None:
+    _check(lib().wgpf_gemm_bf16(C.c_void_p(a_ptr), C.c_void_p(b_ptr),
+                                C.c_void_p(c_ptr), M, N, K, int(instrument),
+                                C.c_void_p(profile_ptr), C.c_void_p(timing_ptr),
+                                C.c_void_p(stream)), "wgpf_gemm_bf16")
+
+
+def gemm_profile_bytes(M: int, N: int) -> int:
+    return int(lib().wgpf_gemm_profile_bytes(M, N))
+
+
+def gemm_smem_bytes(instrument: bool) -> int:
+    return int(lib().wgpf_gemm_smem_bytes(int(instrument)))
+
+
+def kpft_v2(body: bytes | np.ndarray, n_streams: int) -> bytes:
+    """wgpf_collect: a KPFT v2 header in front of a flushed device body."""
+    b = body.tobytes() if isinstance(body, np.ndarray) else bytes(body)
+    return b"KPFT" + struct.pack("<HHQ", 2, 0, n_streams) + b
+
+
+def kpft_v1(body: bytes | np.ndarray, n_streams: int) -> bytes:
+    assert n_streams <= 0xFFFF
+    b = body.tobytes() if isinstance(body, np.ndarray) else bytes(body)
+    return b"KPFT" + struct.pack("<HH", 1, n_streams) + b

@@ -212,6 +212,51 @@ int wgpf_stats_export(wgpf_ctx* ctx, void* d_dst);
 int wgpf_stats_merge(wgpf_ctx* ctx, const void* d_gathered, uint32_t n_ranks);
 
 /* ----------------------------------------------------------------------- */
+/* Interval-overlap analysis (K6)                                            */
+/* ----------------------------------------------------------------------- */
+
+typedef struct wgpf_cp_stage {
+  const char* label;   /* owned by the context; stages sorted by label */
+  uint64_t mean;       /* llround(sum / n) over the steady window */
+  uint64_t steady;     /* steady-window instances */
+  uint32_t warp_group; /* of the stage's lowest-iteration event */
+  uint32_t pad;
+} wgpf_cp_stage;
+
+/*
+ * analyze_critical_path (perfmodel.hpp:317-501) over an event array (device
+ * pointer when on_device != 0).  barrier_src/dst: barrier-derived candidate
+ * edges as label pairs (perfmodel.hpp:258-313 derives them from the lowered
+ * program).  Outputs: stages (sorted by label), binding counts as an
+ * n_stages x n_stages row-major matrix (row = gating stage, column = gated
+ * stage), and the binding cycle (stage indices, rotated to the smallest
+ * label) with its period.  gate_by_block selects per-(block, warp_group)
+ * gating instead of the reference's per-warp_group gating (:373).
+ */
+int wgpf_critical_path(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n,
+                       int on_device, const char* const* barrier_src,
+                       const char* const* barrier_dst, uint32_t n_barrier,
+                       uint64_t slack, int exclude_warmup, int gate_by_block,
+                       wgpf_cp_stage* stages, uint32_t stages_cap,
+                       uint32_t* n_stages, uint64_t* binding,
+                       uint64_t binding_cap, uint32_t* cycle,
+                       uint32_t cycle_cap, uint32_t* n_cycle, uint64_t* period);
+
+/* Role overlap counters (framework definition, oracle/wgpf_oracle.h
+ * wgpo_overlap): per block, producer (role 0) / consumer (role 1) busy time
+ * as the union of their Exec intervals, their intersection, the block span
+ * and bubbles, summed over blocks. */
+typedef struct wgpf_overlap {
+  uint64_t blocks, span;
+  uint64_t busy[2];
+  uint64_t both;
+  uint64_t bubble[2];
+} wgpf_overlap;
+int wgpf_overlap_counters(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n,
+                          int on_device, const uint8_t* role_of_wg,
+                          uint32_t n_roles, wgpf_overlap* out);
+
+/* ----------------------------------------------------------------------- */
 /* Synthetic trace generator (bench / tests)    */
 /* ----------------------------------------------------------------------- */
 

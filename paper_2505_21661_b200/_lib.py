@@ -58,6 +58,17 @@ class Profile(C.Structure):
                 ("launches", C.c_uint32), ("general_streams", C.c_uint32)]
 
 
+class CpStage(C.Structure):
+    _fields_ = [("label", C.c_char_p), ("mean", C.c_uint64), ("steady", C.c_uint64),
+                ("warp_group", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class Overlap(C.Structure):
+    _fields_ = [("blocks", C.c_uint64), ("span", C.c_uint64),
+                ("busy", C.c_uint64 * 2), ("both", C.c_uint64),
+                ("bubble", C.c_uint64 * 2)]
+
+
 F_PROFILE = 0x10
 
 _lock = threading.Lock()
@@ -100,6 +111,13 @@ def lib() -> C.CDLL:
             "wgpf_stats_merge": ([vp, vp, u32], i32),
             "wgpf_synth_body": ([vp, vp, u32, u64, u64, u64], i32),
             "wgpf_last_profile": ([vp, C.POINTER(Profile)], i32),
+            "wgpf_critical_path": ([vp, vp, u64, i32, C.POINTER(C.c_char_p),
+                                    C.POINTER(C.c_char_p), u32, u64, i32, i32,
+                                    C.POINTER(CpStage), u32, C.POINTER(u32),
+                                    C.POINTER(u64), u64, C.POINTER(u32), u32,
+                                    C.POINTER(u32), C.POINTER(u64)], i32),
+            "wgpf_overlap_counters": ([vp, vp, u64, i32, vp, u32,
+                                       C.POINTER(Overlap)], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -31,6 +31,9 @@
 #include "k_misc.cuh"
 #include "k_stats.cuh"
 #include "k_synth.cuh"
+#include "k_cp.cuh"
+#include <functional>
+#include <memory>
 
 using namespace wgpf;
 
@@ -1348,3 +1351,5 @@ extern "C" int wgpf_synth_body(wgpf_ctx* c, void* d_body, uint32_t shape,
   CUDA_OK(c, cudaGetLastError());
   return WGPF_OK;
 }
+
+#include "capi_cp.inc"

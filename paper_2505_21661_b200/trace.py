@@ -513,6 +513,63 @@ class Context:
         return ReplayResult(out[:n.value].copy(), w.flagged_preconditions,
                             w.malformed_groups)
 
+    def critical_path(self, events: np.ndarray, barrier_edges=(), slack: int = 132,
+                      exclude_warmup: bool = True, gate_by_block: bool = False,
+                      on_device_ptr: int = 0, n_events: int | None = None) -> dict:
+        """analyze_critical_path (perfmodel.hpp:317-501) on the GPU.  Labels
+        come from the context plan.  Returns stages / mean / steady / wg /
+        binding {(gate, gated): count} / cycle / period."""
+        n = len(events) if n_events is None else n_events
+        if on_device_ptr:
+            ptr_ev, on_dev = C.c_void_p(on_device_ptr), 1
+        else:
+            ev = np.ascontiguousarray(events, EVENT_DTYPE)
+            ptr_ev, on_dev = C.c_void_p(ev.ctypes.data), 0
+        nb = len(barrier_edges)
+        src = (C.c_char_p * max(1, nb))(*[a.encode() for a, _ in barrier_edges])
+        dst = (C.c_char_p * max(1, nb))(*[b.encode() for _, b in barrier_edges])
+        cap = 64
+        while True:
+            stages = (L.CpStage * cap)()
+            bind = (C.c_uint64 * (cap * cap))()
+            cyc = (C.c_uint32 * cap)()
+            ns, nc, period = C.c_uint32(), C.c_uint32(), C.c_uint64()
+            rc = self.L.wgpf_critical_path(self.h, ptr_ev, n, on_dev, src, dst, nb,
+                                           slack, int(exclude_warmup),
+                                           int(gate_by_block), stages, cap,
+                                           C.byref(ns), bind, cap * cap, cyc, cap,
+                                           C.byref(nc), C.byref(period))
+            if rc == L.E_BUFFER:
+                cap = max(2 * cap, ns.value)
+                continue
+            _check(self.h, rc)
+            S = ns.value
+            labels = [stages[i].label.decode() for i in range(S)]
+            binding = {(labels[a], labels[b]): bind[a * S + b]
+                       for a in range(S) for b in range(S) if bind[a * S + b]}
+            return dict(stages=labels, mean=[stages[i].mean for i in range(S)],
+                        steady=[stages[i].steady for i in range(S)],
+                        wg=[stages[i].warp_group for i in range(S)],
+                        binding=binding,
+                        cycle=[labels[cyc[i]] for i in range(nc.value)],
+                        period=period.value)
+
+    def overlap(self, events: np.ndarray, role_of_wg, on_device_ptr: int = 0,
+                n_events: int | None = None) -> dict:
+        n = len(events) if n_events is None else n_events
+        roles = np.ascontiguousarray(role_of_wg, np.uint8)
+        if on_device_ptr:
+            ptr_ev, on_dev = C.c_void_p(on_device_ptr), 1
+        else:
+            ev = np.ascontiguousarray(events, EVENT_DTYPE)
+            ptr_ev, on_dev = C.c_void_p(ev.ctypes.data), 0
+        out = L.Overlap()
+        _check(self.h, self.L.wgpf_overlap_counters(self.h, ptr_ev, n, on_dev,
+                                                    C.c_void_p(roles.ctypes.data),
+                                                    len(roles), C.byref(out)))
+        return dict(blocks=out.blocks, span=out.span, busy=list(out.busy),
+                    both=out.both, bubble=list(out.bubble))
+
     def synth_body(self, dst_ptr: int, shape: int, stream0: int, n_streams: int,
                    n_long: int) -> None:
         _check(self.h, self.L.wgpf_synth_body(self.h, C.c_void_p(dst_ptr), shape,

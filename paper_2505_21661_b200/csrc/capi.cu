@@ -105,6 +105,7 @@ struct wgpf_ctx {
   // profiling
   cudaEvent_t ev[8] = {};
   bool profiling = false;
+  bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
   uint32_t launches = 0;
   uint64_t general_streams = 0;
   wgpf_profile prof{};
@@ -284,8 +285,11 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
     delete c;
     return WGPF_E_CUDA;
   }
-  cudaFuncSetAttribute(k_fast_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(FastSmem));
+  cudaFuncSetAttribute(k_fast_emit<false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fast_smem_bytes(false, 0));
+  cudaFuncSetAttribute(k_fast_emit<true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   for (auto& e : c->ev) cudaEventCreate(&e);
   *out = c;
   return WGPF_OK;
@@ -560,12 +564,20 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.no_stats = no_stats ? 1u : 0u;
   f.general_list = c->d_glist.as<unsigned long long>();
   f.general_len = c->d_glen.as<unsigned long long>();
-  const uint32_t grid =
-      grid_for(c, (const void*)k_fast_emit, kFastWarps * 32, sizeof(FastSmem));
+  // stage whole streams in shared memory when two buffers per warp fit
+  const size_t smem_stage = fast_smem_bytes(true, stride);
+  const bool staged = !c->no_stage && smem_stage <= 160 * 1024;
+  const size_t smem = staged ? smem_stage : fast_smem_bytes(false, stride);
+  const void* kfn = staged ? (const void*)k_fast_emit<true>
+                           : (const void*)k_fast_emit<false>;
+  const uint32_t grid = grid_for(c, kfn, kFastWarps * 32, smem);
   ALLOC_OK(c, c->d_orphans,
            sizeof(wgpf_event) * (uint64_t)grid * kFastWarps * (c->slots / 2 + 1));
   f.orphan_scratch = c->d_orphans.as<wgpf_event>();
-  k_fast_emit<<<grid, kFastWarps * 32, sizeof(FastSmem), c->stream>>>(f);
+  if (staged)
+    k_fast_emit<true><<<grid, kFastWarps * 32, smem, c->stream>>>(f);
+  else
+    k_fast_emit<false><<<grid, kFastWarps * 32, smem, c->stream>>>(f);
   CUDA_OK(c, cudaGetLastError());
   ++c->launches;
   c->mark(3);

@@ -84,12 +84,9 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     bool wide = false;
     bool prev_end = false;       // record c-1 is an END
     uint32_t pend_rid = kNone;   // lane-31 marker START awaiting its END
-    for (uint32_t c = 0; c < n; c += 32) {
+    auto chunk = [&](uint32_t c, uint32_t tag) {
       const uint32_t i = c + lane;
       const bool valid = i < n;
-      uint32_t slot = start + i;
-      if (slot >= cap) slot -= cap;
-      const uint32_t tag = valid ? __ldg(tags + 2ull * slot) : 0u;
       const uint32_t rid = (tag >> 12) & (WGPF_MAX_REGIONS - 1u);
       const bool st = valid && (tag & WGPF_START_FLAG);
       const bool en = valid && !(tag & WGPF_START_FLAG);
@@ -140,6 +137,21 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       prev_end = __shfl_sync(0xffffffffu, (uint32_t)en, 31);
       n_end += __popc(emk);
       q_in += (int32_t)__popc(smk) - (int32_t)__popc(emk);
+    };
+    // 8 chunks (256 records) of tags in flight per warp, then process
+    constexpr uint32_t G = 8;
+    for (uint32_t c0 = 0; c0 < n; c0 += 32 * G) {
+      uint32_t tg[G];
+#pragma unroll
+      for (uint32_t k = 0; k < G; ++k) {
+        const uint32_t i = c0 + 32 * k + lane;
+        uint32_t slot = start + i;
+        if (slot >= cap) slot -= cap;
+        tg[k] = i < n ? __ldg(tags + 2ull * slot) : 0u;
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < G; ++k)
+        if (c0 + 32 * k < n) chunk(c0 + 32 * k, tg[k]);
     }
     if (pend_rid != kNone) last_bad = max(last_bad, (int64_t)n - 1);
     wide = __any_sync(0xffffffffu, wide);

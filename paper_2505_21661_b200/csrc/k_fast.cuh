@@ -67,7 +67,40 @@ struct FastSmem {
   LevelEntry lvl[kFastWarps][kMaxDepth];
   uint32_t cnt[kFastWarps][kFastRegions];
   unsigned long long warn[4];
+  unsigned long long bar[kFastWarps][2];  // staging mbarriers (kStage)
 };
+
+// Staging: each warp double-buffers whole streams (header + slots) in shared
+// memory; lane 0 issues the next stream's TMA bulk copy (cp.async.bulk,
+// completion on an mbarrier) before the current one is processed, so every
+// warp keeps one stream-sized read in flight.
+__device__ inline void stage_issue(unsigned long long* bar, void* dst,
+                                   const void* src, uint32_t bytes) {
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+      "[%1], %2, [%3];" ::"r"(d),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+__device__ inline void stage_wait(unsigned long long* bar, uint32_t parity) {
+  const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
 
 __device__ inline void store_event(wgpf_event* dst, uint64_t st, uint64_t en,
                                    uint32_t region, uint32_t it, uint32_t blk,
@@ -114,11 +147,31 @@ __device__ inline void fast_stats(FastSmem& sm, const DevStats& st,
   }
 }
 
+// Shared-memory bytes of k_fast_emit<kStage> (staging: 2 buffers per warp).
+__host__ __device__ inline uint32_t fast_stage_stride(uint64_t stride) {
+  return (uint32_t)((stride + 127) & ~127ull);
+}
+__host__ inline size_t fast_smem_bytes(bool stage, uint64_t stride) {
+  size_t b = (sizeof(FastSmem) + 127) & ~size_t(127);
+  if (stage) b += (size_t)kFastWarps * 2 * fast_stage_stride(stride);
+  return b;
+}
+
+template <bool kStage>
 __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   FastSmem& sm = *reinterpret_cast<FastSmem*>(smem_raw);
   const uint32_t lane = lane_id();
   const uint32_t w = threadIdx.x >> 5;
+  const uint32_t sstride = fast_stage_stride(a.stride);
+  uint8_t* stage = smem_raw + ((sizeof(FastSmem) + 127) & ~size_t(127)) +
+                   (size_t)w * 2 * sstride;
+  if (kStage && lane == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+          static_cast<uint32_t>(__cvta_generic_to_shared(&sm.bar[w][b]))));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (!a.no_stats) smem_stats_init(sm.st);
   for (uint32_t r = threadIdx.x; r < kFastRegions; r += blockDim.x) {
     uint32_t ci = kNone, wc = kNone;
@@ -141,8 +194,23 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
   const uint64_t cost = a.record_cost;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
 
-  for (uint64_t s = gw; !abort_all && s < a.n_streams;
-       s += (uint64_t)gridDim.x * kFastWarps) {
+  const uint64_t wstep = (uint64_t)gridDim.x * kFastWarps;
+  uint32_t sbuf = 0, sphase = 0;  // staging buffer in use, parity bits
+  if (kStage && !abort_all && lane == 0 && gw < a.n_streams)
+    stage_issue(&sm.bar[w][0], stage, a.body + gw * a.stride, (uint32_t)a.stride);
+  for (uint64_t s = gw; !abort_all && s < a.n_streams; s += wstep) {
+    if constexpr (kStage) {
+      // prefetch the warp's next stream into the other buffer
+      __syncwarp();
+      if (lane == 0 && s + wstep < a.n_streams)
+        stage_issue(&sm.bar[w][sbuf ^ 1], stage + (sbuf ^ 1) * sstride,
+                    a.body + (s + wstep) * a.stride, (uint32_t)a.stride);
+      stage_wait(&sm.bar[w][sbuf], (sphase >> sbuf) & 1u);
+      sphase ^= 1u << sbuf;
+    }
+    const uint8_t* base =
+        kStage ? stage + sbuf * sstride : a.body + s * a.stride;
+    if constexpr (kStage) sbuf ^= 1;
     const uint32_t flag = a.sflag[s];
     if (flag & (SF_DECODE_ERR | SF_GENERAL)) {
       if ((flag & SF_GENERAL) && lane == 0) {
@@ -151,7 +219,6 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
       }
       continue;
     }
-    const uint8_t* base = a.body + s * a.stride;
     const uint4 h = *reinterpret_cast<const uint4*>(base);
     const uint32_t cntw = h.z, cap = h.w;
     const uint32_t n = cntw <= cap ? cntw : cap;

@@ -137,9 +137,17 @@ static int set_err(wgpf_ctx* c, int code, const char* fmt, ...) {
   return code;
 }
 
+static const bool g_debug = getenv("WGPF_DEBUG") != nullptr;
+
 #define CUDA_OK(ctx, expr)                                                    \
   do {                                                                        \
     cudaError_t e_ = (expr);                                                  \
+    if (g_debug && e_ == cudaSuccess) {                                       \
+      fprintf(stderr, "[wgpf] %s:%d %s ... ", __FILE__, __LINE__, #expr);     \
+      fflush(stderr);                                                         \
+      e_ = cudaStreamSynchronize((ctx)->stream);                              \
+      fprintf(stderr, "%s\n", cudaGetErrorString(e_));                        \
+    }                                                                         \
     if (e_ != cudaSuccess) {                                                  \
       cudaGetLastError();                                                     \
       return set_err(ctx, WGPF_E_CUDA, "%s: %s (%s:%d)", #expr,               \

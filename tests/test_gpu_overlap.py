@@ -19,6 +19,9 @@ def T():
     return trace
 
 
+LABELS = ["A", "A.wait", "B", "C", "C.wait", "Load K", "Load K.wait", "Z"]
+
+
 def random_events(seed, n_chains=12, per_chain=60, labels=8, blocks=3, wgs=4):
     rng = np.random.default_rng(seed)
     evs = []
@@ -29,7 +32,7 @@ def random_events(seed, n_chains=12, per_chain=60, labels=8, blocks=3, wgs=4):
         for _ in range(per_chain):
             lab = int(rng.integers(0, labels))
             dur = int(rng.integers(0, 800))
-            wait = lab % 3 == 2 and rng.random() < 0.7
+            wait = LABELS[lab].endswith(".wait") and rng.random() < 0.8
             k = it.get(lab, 0)
             it[lab] = k + int(rng.integers(1, 3))
             region = lab | (O.EV_WAIT if wait else 0) | O.EV_CORRECTED
@@ -37,9 +40,6 @@ def random_events(seed, n_chains=12, per_chain=60, labels=8, blocks=3, wgs=4):
             t += dur + int(rng.integers(0, 300))
     ev = np.array(evs, O.EVENT_DTYPE)
     return ev[rng.permutation(len(ev))]
-
-
-LABELS = ["A", "A.wait", "B", "C", "C.wait", "Load K", "Load K.wait", "Z"]
 
 
 @pytest.mark.parametrize("gate_by_block", [False, True])

@@ -256,6 +256,13 @@ int wgpf_overlap_counters(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n,
                           int on_device, const uint8_t* role_of_wg,
                           uint32_t n_roles, wgpf_overlap* out);
 
+/* export_chrome_trace (trace.hpp:493-511): the reference's Chrome Trace JSON
+ * (nlohmann dump(2) layout, "\n"-terminated) for an event array (device
+ * pointer when on_device != 0).  out == NULL queries *len. */
+int wgpf_export_chrome_trace(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n,
+                             int on_device, double cycles_per_us, char* out,
+                             uint64_t cap, uint64_t* len);
+
 /* ----------------------------------------------------------------------- */
 /* Synthetic trace generator (bench / tests)    */
 /* ----------------------------------------------------------------------- */

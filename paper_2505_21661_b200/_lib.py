@@ -116,6 +116,8 @@ def lib() -> C.CDLL:
                                     C.POINTER(CpStage), u32, C.POINTER(u32),
                                     C.POINTER(u64), u64, C.POINTER(u32), u32,
                                     C.POINTER(u32), C.POINTER(u64)], i32),
+            "wgpf_export_chrome_trace": ([vp, vp, u64, i32, C.c_double, vp, u64,
+                                          C.POINTER(u64)], i32),
             "wgpf_overlap_counters": ([vp, vp, u64, i32, vp, u32,
                                        C.POINTER(Overlap)], i32),
         }

@@ -32,6 +32,7 @@
 #include "k_stats.cuh"
 #include "k_synth.cuh"
 #include "k_cp.cuh"
+#include <cmath>
 #include <functional>
 #include <memory>
 
@@ -1373,3 +1374,4 @@ extern "C" int wgpf_synth_body(wgpf_ctx* c, void* d_body, uint32_t shape,
 }
 
 #include "capi_cp.inc"
+#include "capi_chrome.inc"

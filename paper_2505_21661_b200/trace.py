@@ -570,6 +570,23 @@ class Context:
         return dict(blocks=out.blocks, span=out.span, busy=list(out.busy),
                     both=out.both, bubble=list(out.bubble))
 
+    def export_chrome_trace(self, events: np.ndarray, cycles_per_us: float = 1000.0,
+                            on_device_ptr: int = 0, n_events: int | None = None) -> str:
+        """export_chrome_trace (trace.hpp:493-511), byte-identical JSON."""
+        n = len(events) if n_events is None else n_events
+        if on_device_ptr:
+            p, dev = C.c_void_p(on_device_ptr), 1
+        else:
+            ev = np.ascontiguousarray(events, EVENT_DTYPE)
+            p, dev = C.c_void_p(ev.ctypes.data), 0
+        ln = C.c_uint64()
+        _check(self.h, self.L.wgpf_export_chrome_trace(self.h, p, n, dev, cycles_per_us,
+                                                       None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value + 1)
+        _check(self.h, self.L.wgpf_export_chrome_trace(self.h, p, n, dev, cycles_per_us,
+                                                       buf, ln.value + 1, C.byref(ln)))
+        return buf.raw[:ln.value].decode()
+
     def synth_body(self, dst_ptr: int, shape: int, stream0: int, n_streams: int,
                    n_long: int) -> None:
         _check(self.h, self.L.wgpf_synth_body(self.h, C.c_void_p(dst_ptr), shape,

@@ -363,3 +363,27 @@ def test_cxx_shim_end_to_end(tmp_path):
                          text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "ALL PASS" in res.stdout
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_chrome_trace_export_byte_identical(ctx, name):
+    """export_chrome_trace (trace.hpp:493-511) vs the reference's own JSON
+    (fixtures regenerated byte-identically to proj/out/*.json)."""
+    data, slots, strategy, labels, cost, _ = load_fixture(name)
+    r = ctx.replay_image_bytes(data, plan_of(slots, strategy, labels), cost)
+    got = ctx.export_chrome_trace(r.events, 1000.0)
+    want = open(os.path.join(GOLDEN, "fixtures", name + ".json")).read()
+    assert got == want
+
+
+def test_chrome_trace_export_empty_and_escaping(ctx):
+    t = T()
+    ctx.set_plan(plan_of(4, 1, ['we"ird\\lab\tel']))
+    assert ctx.export_chrome_trace(np.zeros(0, O.EVENT_DTYPE)) == \
+        '{\n  "traceEvents": []\n}\n'
+    ev = np.array([(0, 1000, 0 | O.EV_CORRECTED, 0, 1, 2)], O.EVENT_DTYPE)
+    js = ctx.export_chrome_trace(ev)
+    import json as J
+    d = J.loads(js)["traceEvents"][0]
+    assert d["name"] == 'we"ird\\lab\tel' and d["dur"] == 1.0 and d["pid"] == 1
+    del t

@@ -117,8 +117,10 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       if (zm) z = (int32_t)(c + 31u - __clz(zm));
       // wait-marker STARTs right after an END that the next record does not
       // close (conservative: the marker class test is done in pass 2)
-      const bool pe = lane == 0 ? prev_end
-                                : (bool)__shfl_up_sync(0xffffffffu, (uint32_t)en, 1);
+      // (the shuffle runs on every lane; selecting afterwards keeps the warp
+      // converged -- a shuffle inside a lane-divergent ternary deadlocks)
+      const uint32_t pe_up = __shfl_up_sync(0xffffffffu, (uint32_t)en, 1);
+      const bool pe = lane == 0 ? prev_end : (bool)pe_up;
       const uint32_t t1 = __shfl_down_sync(0xffffffffu, tag, 1);
       const bool mk_start = st && pe && in_range && marker_region[rid];
       const bool closed_next = (lane < 31) && (i + 1 < n) &&

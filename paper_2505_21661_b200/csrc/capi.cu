@@ -101,7 +101,7 @@ struct wgpf_ctx {
   // per call
   DevBuf d_status, d_counts, d_zpos, d_sflag, d_offsets, d_scan_tmp, d_glist,
       d_glen, d_orphans, d_gscratch, d_image, d_events, d_aux0, d_aux1, d_aux2,
-      d_aux3;
+      d_aux3, d_repack;
   DevStatus* h_status = nullptr;  // pinned
   // profiling
   cudaEvent_t ev[8] = {};
@@ -685,6 +685,23 @@ static int finalize_stats(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   return WGPF_OK;
 }
 
+// The kernels read 16-byte headers and stage streams with 16-byte bulk
+// copies: odd-capacity or unaligned bodies are repacked (one 2D device copy)
+// to a 16-byte pitch; *stride becomes the pitch.
+static int align_body(wgpf_ctx* c, const void** d_body, uint64_t n_streams,
+                      uint64_t* stride) {
+  if (!n_streams ||
+      (!(reinterpret_cast<uintptr_t>(*d_body) & 15u) && !(*stride & 15u)))
+    return WGPF_OK;
+  const uint64_t pitch = (*stride + 15) & ~15ull;
+  ALLOC_OK(c, c->d_repack, n_streams * pitch);
+  CUDA_OK(c, cudaMemcpy2DAsync(c->d_repack.p, pitch, *d_body, *stride, *stride,
+                               n_streams, cudaMemcpyDeviceToDevice, c->stream));
+  *d_body = c->d_repack.p;
+  *stride = pitch;
+  return WGPF_OK;
+}
+
 extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
                                   uint64_t body_bytes, uint64_t n_streams,
                                   uint64_t stream_base, uint64_t record_cost,
@@ -694,17 +711,16 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
   if (n_events) *n_events = 0;
   if (warnings) memset(warnings, 0, sizeof *warnings);
-  const uint64_t stride = 16ull + 8ull * c->slots;
+  uint64_t stride = 16ull + 8ull * c->slots;
   if (body_bytes < n_streams * stride)
     return set_err(c, WGPF_E_ARG, "body of %llu bytes < %llu streams x %llu",
                    (unsigned long long)body_bytes,
                    (unsigned long long)n_streams, (unsigned long long)stride);
   if (c->slots >= (1ull << 31))
     return set_err(c, WGPF_E_ARG, "slot capacity too large");
-  if ((reinterpret_cast<uintptr_t>(d_body) & 15u) || (stride & 15u)) {
-    // the kernels read 16-byte headers with vector loads
-    return set_err(c, WGPF_E_ARG,
-                   "KPFT body must be 16-byte aligned with an even capacity");
+  {
+    int rr = align_body(c, &d_body, n_streams, &stride);
+    if (rr) return rr;
   }
   const bool stats_only = flags & WGPF_F_STATS_ONLY;
   const bool no_stats = flags & WGPF_F_NO_STATS;
@@ -905,18 +921,13 @@ static int stage_image(wgpf_ctx* c, const uint8_t* kpft, uint64_t n,
   if (rc) return rc;
   const uint64_t stride = 16ull + 8ull * c->slots;
   const uint64_t body = n - off;
-  if (count == 0 || body / stride != count || body % stride != 0 ||
-      (stride & 15u)) {
+  if (count == 0 || body / stride != count || body % stride != 0) {
     // not a uniform body of the plan capacity: the reference would fail in
     // deserialize or decode (or it is empty)
     if (count == 0 && body == 0) {
       *n_streams = 0;
       *d_body = nullptr;
       return WGPF_OK;
-    }
-    if (body / stride == count && body % stride == 0 && (stride & 15u)) {
-      return set_err(c, WGPF_E_ARG,
-                     "odd slot capacities are not supported by the device path");
     }
     return host_walk(c, kpft, n, off, count);
   }
@@ -988,7 +999,13 @@ extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
   int rc = stage_image(c, kpft, n_bytes, &d_body, &ns);
   if (rc) return rc;
   if (ns == 0) return WGPF_OK;
-  const uint64_t stride = 16ull + 8ull * c->slots;
+  uint64_t stride = 16ull + 8ull * c->slots;
+  {
+    const void* db = d_body;
+    int rr = align_body(c, &db, ns, &stride);
+    if (rr) return rr;
+    d_body = static_cast<const uint8_t*>(db);
+  }
   // decode checks via pass 1
   int r2 = status_reset(c);
   if (r2) return r2;

@@ -115,35 +115,62 @@ __device__ inline void store_event(wgpf_event* dst, uint64_t st, uint64_t en,
 __device__ inline void fast_stats(FastSmem& sm, const DevStats& st,
                                   DevStatus* status, bool part, uint32_t cls,
                                   uint32_t d, unsigned long long key) {
+  // Warp-uniform loop over the distinct classes present (and, per class, the
+  // distinct histogram bins): only full-mask ballots / shuffles / reductions,
+  // which stay on the converged fast path (a reduction over a match.any
+  // group mask lowers to a serialised WARPSYNC.COLLECTIVE loop).
+  const uint32_t FULL = 0xffffffffu;
   const uint32_t bin = hist_bin(d);
   const uint32_t lane = lane_id();
-  const uint32_t k = part ? ((cls << 6) | bin) : (0xFC000000u | lane);
-  const uint32_t grp = __match_any_sync(0xffffffffu, k);
-  const uint32_t lo = __reduce_add_sync(grp, d & 0xFFFFu);
-  const uint32_t hi = __reduce_add_sync(grp, d >> 16);
-  const uint32_t mn = __reduce_min_sync(grp, d);
-  const uint32_t mx = __reduce_max_sync(grp, d);
-  if (!part || (grp & lanemask_lt())) return;  // leader = lowest lane
-  const uint32_t n = __popc(grp);
-  const unsigned long long sum =
-      (unsigned long long)lo + ((unsigned long long)hi << 16);
-  if (cls < kSmemClasses && cls < st.K) {
-    atomicAdd(&sm.st.count[cls], (unsigned long long)n);
-    atomicAdd(&sm.st.sum[cls], sum);
-    atomicMin(&sm.st.min[cls], mn);
-    atomicMax(&sm.st.max[cls], mx);
-    atomicMin(&sm.st.first[cls], key);
-    atomicAdd(&sm.st.hist[cls * WGPF_HIST_BINS + bin], n);
-  } else {
-    const int slot = stats_slot(st, cls, &status->synth_overflow);
-    if (slot < 0) return;
-    atomicAdd(&st.count[slot], (unsigned long long)n);
-    atomicAdd(&st.sum[slot], sum);
-    atomicMin(&st.min[slot], (unsigned long long)mn);
-    atomicMax(&st.max[slot], (unsigned long long)mx);
-    atomicMin(&st.first[slot], key);
-    atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + bin],
-              (unsigned long long)n);
+  uint32_t rem = __ballot_sync(FULL, part);
+  while (rem) {
+    const uint32_t ld = __ffs(rem) - 1u;  // lowest lane: smallest event index
+    const uint32_t c = __shfl_sync(FULL, cls, ld);
+    const bool mine = part && cls == c;
+    const uint32_t m = __ballot_sync(FULL, mine);
+    const uint32_t lo = __reduce_add_sync(FULL, mine ? (d & 0xFFFFu) : 0u);
+    const uint32_t hi = __reduce_add_sync(FULL, mine ? (d >> 16) : 0u);
+    const uint32_t mn = __reduce_min_sync(FULL, mine ? d : 0xFFFFFFFFu);
+    const uint32_t mx = __reduce_max_sync(FULL, mine ? d : 0u);
+    const bool dense = c < kSmemClasses && c < st.K;
+    int slot = -1;
+    if (lane == ld) {
+      const uint32_t n = __popc(m);
+      const unsigned long long sum =
+          (unsigned long long)lo + ((unsigned long long)hi << 16);
+      if (dense) {
+        atomicAdd(&sm.st.count[c], (unsigned long long)n);
+        atomicAdd(&sm.st.sum[c], sum);
+        atomicMin(&sm.st.min[c], mn);
+        atomicMax(&sm.st.max[c], mx);
+        atomicMin(&sm.st.first[c], key);
+      } else {
+        slot = stats_slot(st, c, &status->synth_overflow);
+        if (slot >= 0) {
+          atomicAdd(&st.count[slot], (unsigned long long)n);
+          atomicAdd(&st.sum[slot], sum);
+          atomicMin(&st.min[slot], (unsigned long long)mn);
+          atomicMax(&st.max[slot], (unsigned long long)mx);
+          atomicMin(&st.first[slot], key);
+        }
+      }
+    }
+    slot = __shfl_sync(FULL, slot, ld);
+    uint32_t hb = m;
+    while (hb) {
+      const uint32_t bl = __ffs(hb) - 1u;
+      const uint32_t b = __shfl_sync(FULL, bin, bl);
+      const uint32_t mb = __ballot_sync(FULL, mine && bin == b);
+      if (lane == bl) {
+        if (dense)
+          atomicAdd(&sm.st.hist[c * WGPF_HIST_BINS + b], (uint32_t)__popc(mb));
+        else if (slot >= 0)
+          atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + b],
+                    (unsigned long long)__popc(mb));
+      }
+      hb &= ~mb;
+    }
+    rem &= ~m;
   }
 }
 

@@ -340,7 +340,8 @@ def test_stats_merge_two_shards(ctx):
     merged_ctx.set_plan(plan)
     merged_ctx.stats_merge(gathered.data_ptr(), 2)
     merged = merged_ctx.stats()
-    assert list(merged) == list(whole)
+    extra = {k: (v.count, v.sum) for k, v in merged.items() if k not in whole}
+    assert list(merged) == list(whole), extra
     for k in whole:
         a, b = whole[k], merged[k]
         assert (a.count, a.sum, a.min, a.max, a.warp_group, a.kind, a.hist) == (

@@ -174,6 +174,77 @@ __device__ inline void fast_stats(FastSmem& sm, const DevStats& st,
   }
 }
 
+// Per-lane register accumulator for one label class: events reaching a lane
+// mostly repeat their class (periodic scope patterns), so count / sum / min /
+// max / first key accumulate in registers and reach shared memory only when
+// the lane's class changes (and once at kernel exit).  Keys grow along a
+// warp's streams, so the first key of a run is its minimum.
+struct LaneAcc {
+  uint32_t cls, cnt, mn, mx;
+  unsigned long long sum, first;
+};
+
+__device__ inline void acc_init(LaneAcc& a) {
+  a.cls = kNone;
+  a.cnt = 0;
+}
+
+__device__ inline void acc_flush(LaneAcc& a, FastSmem& sm, const DevStats& st,
+                                 DevStatus* status) {
+  if (!a.cnt) return;
+  if (a.cls < kSmemClasses && a.cls < st.K) {
+    atomicAdd(&sm.st.count[a.cls], (unsigned long long)a.cnt);
+    atomicAdd(&sm.st.sum[a.cls], a.sum);
+    atomicMin(&sm.st.min[a.cls], a.mn);
+    atomicMax(&sm.st.max[a.cls], a.mx);
+    atomicMin(&sm.st.first[a.cls], a.first);
+  } else {
+    const int slot = stats_slot(st, a.cls, &status->synth_overflow);
+    if (slot >= 0) {
+      atomicAdd(&st.count[slot], (unsigned long long)a.cnt);
+      atomicAdd(&st.sum[slot], a.sum);
+      atomicMin(&st.min[slot], (unsigned long long)a.mn);
+      atomicMax(&st.max[slot], (unsigned long long)a.mx);
+      atomicMin(&st.first[slot], a.first);
+    }
+  }
+  a.cnt = 0;
+}
+
+// One event per participating lane.  Histogram: match.any on (class, bin),
+// the group leader adds the group size (no group-mask reductions).
+__device__ inline void lane_stats(LaneAcc& a, FastSmem& sm, const DevStats& st,
+                                  DevStatus* status, bool part, uint32_t cls,
+                                  uint32_t d, unsigned long long key) {
+  const uint32_t lane = lane_id();
+  const uint32_t bin = hist_bin(d);
+  const uint32_t k = part ? ((cls << 6) | bin) : (0xFC000000u | lane);
+  const uint32_t grp = __match_any_sync(0xffffffffu, k);
+  if (!part) return;
+  if (!(grp & lanemask_lt())) {
+    if (cls < kSmemClasses && cls < st.K) {
+      atomicAdd(&sm.st.hist[cls * WGPF_HIST_BINS + bin], (uint32_t)__popc(grp));
+    } else {
+      const int slot = stats_slot(st, cls, &status->synth_overflow);
+      if (slot >= 0)
+        atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + bin],
+                  (unsigned long long)__popc(grp));
+    }
+  }
+  if (cls != a.cls) {
+    acc_flush(a, sm, st, status);
+    a.cls = cls;
+    a.sum = 0;
+    a.mn = 0xFFFFFFFFu;
+    a.mx = 0;
+    a.first = key;
+  }
+  ++a.cnt;
+  a.sum += d;
+  a.mn = min(a.mn, d);
+  a.mx = max(a.mx, d);
+}
+
 // Shared-memory bytes of k_fast_emit<kStage> (staging: 2 buffers per warp).
 __host__ __device__ inline uint32_t fast_stage_stride(uint64_t stride) {
   return (uint32_t)((stride + 127) & ~127ull);
@@ -220,6 +291,9 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
   const uint32_t lt = lanemask_lt(), le = lanemask_le();
   const uint64_t cost = a.record_cost;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
+  LaneAcc acc_e, acc_w;  // exec / orphan events, wait events
+  acc_init(acc_e);
+  acc_init(acc_w);
 
   const uint64_t wstep = (uint64_t)gridDim.x * kFastWarps;
   uint32_t sbuf = 0, sphase = 0;  // staging buffer in use, parity bits
@@ -465,10 +539,10 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
       w_drop += dropped;
 
       if (!a.no_stats) {
-        fast_stats(sm, a.stats, a.status, base_ev, cls, e_dur,
+        lane_stats(acc_e, sm, a.stats, a.status, base_ev, cls, e_dur,
                    first_key(gs, kpos, 0u));
         if (__any_sync(0xffffffffu, consumed))
-          fast_stats(sm, a.stats, a.status, consumed, wc, w_dur,
+          lane_stats(acc_w, sm, a.stats, a.status, consumed, wc, w_dur,
                      first_key(gs, kpos + 1, 1u));
       }
 
@@ -506,13 +580,17 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
       }
       if (!a.no_stats) {
         const uint32_t ci = ok ? sm.cinfo[e.region] & 0x7FFFFFFFu : 0u;
-        fast_stats(sm, a.stats, a.status, ok, ci,
+        lane_stats(acc_e, sm, a.stats, a.status, ok, ci,
                    ok ? (uint32_t)(e.end - e.start) : 0u,
                    first_key(gs, kb + j, 0u));
       }
     }
     w_mal += n_orph;
     w_tail += (uint32_t)D;
+  }
+  if (!a.no_stats) {
+    acc_flush(acc_e, sm, a.stats, a.status);
+    acc_flush(acc_w, sm, a.stats, a.status);
   }
   // warnings: w_drop / w_flag are per lane, w_tail / w_mal per warp (lane 0)
   const unsigned long long d = warp_sum((unsigned long long)w_drop);

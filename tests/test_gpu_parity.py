@@ -310,6 +310,27 @@ def test_full_config4_properties(ctx, oracle):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("n", [4000, 40000])
+def test_stats_only_equals_materialized(ctx, oracle, n):
+    """WGPF_F_STATS_ONLY (no event materialisation) gives the same
+    statistics as the full replay and as the oracle."""
+    import torch
+    ctx.set_plan(plan_of(S.CAP, 1, S.MIXED_LABELS))
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), 0, S.MIXED_FULL_LONG - n // 2, n, S.MIXED_FULL_LONG)
+    ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0, 0x1)
+    only = ctx.stats()
+    ev = torch.empty(n * 128 * 32, dtype=torch.uint8, device="cuda")
+    ctx.replay_device(body.data_ptr(), body.numel(), n, 33, ev.data_ptr(), n * 128, 0)
+    full = ctx.stats()
+    o = oracle.replay_body(body.cpu().numpy(), n, S.CAP, 1, S.MIXED_LABELS, 33)
+    want = {s.label: s for s in oracle.region_stats(o.events, S.MIXED_LABELS)}
+    for k, s in want.items():
+        for got in (only[k], full[k]):
+            assert (got.count, got.sum, got.min, got.max, got.hist) == (
+                s.count, s.sum, s.min, s.max, s.hist), k
+
+
 def test_stats_merge_two_shards(ctx):
     """Multi-GPU shard-and-reduce on one device: two shards of a body, each
     replayed with its stream_base, stats exported, gathered and merged,

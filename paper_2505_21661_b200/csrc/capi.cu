@@ -27,6 +27,7 @@
 #include "wgpf_dev.cuh"
 #include "k_count.cuh"
 #include "k_fast.cuh"
+#include "k_tps.cuh"
 #include "k_general.cuh"
 #include "k_misc.cuh"
 #include "k_stats.cuh"
@@ -107,6 +108,9 @@ struct wgpf_ctx {
   cudaEvent_t ev[8] = {};
   bool profiling = false;
   bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
+  bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
+  DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
+  size_t smem_optin = 0;
   uint32_t launches = 0;
   uint64_t general_streams = 0;
   wgpf_profile prof{};
@@ -293,6 +297,12 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
       !c->d_status.ensure(sizeof(DevStatus)) || !c->d_glen.ensure(64)) {
     delete c;
     return WGPF_E_CUDA;
+  }
+  {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    c->smem_optin = (size_t)optin;
+    cudaFuncSetAttribute(k_tps, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   }
   cudaFuncSetAttribute(k_fast_emit<false>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -540,6 +550,13 @@ static int scan_counts(wgpf_ctx* c, uint64_t n) {
   return WGPF_OK;
 }
 
+// Thread-per-stream kernel usable for this plan (even capacity that fits the
+// packed stack entries, label classes that fit the lane-private tables).
+static bool tps_enabled(const wgpf_ctx* c) {
+  return !c->no_tps && c->slots % 2 == 0 && c->slots <= kTpsMaxSlots &&
+         c->K <= kTpsClasses && !c->labels.empty();
+}
+
 static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                      uint64_t n_streams, uint64_t stream_base,
                      uint64_t record_cost, wgpf_event* events,
@@ -573,6 +590,18 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.no_stats = no_stats ? 1u : 0u;
   f.general_list = c->d_glist.as<unsigned long long>();
   f.general_len = c->d_glen.as<unsigned long long>();
+  f.list = nullptr;
+  f.list_len = nullptr;
+  if (tps_enabled(c)) {
+    // shallow streams: thread per stream; then the SF_WARP list
+    const uint32_t tw = tps_warps(c->K, c->smem_optin);
+    const size_t tsm = tps_smem_bytes(c->K, tw);
+    k_tps<<<c->sms, tw * 32, tsm, c->stream>>>(f);
+    CUDA_OK(c, cudaGetLastError());
+    ++c->launches;
+    f.list = c->d_wlist.as<unsigned long long>();
+    f.list_len = c->d_glen.as<unsigned long long>() + 1;
+  }
   // stage whole streams in shared memory when two buffers per warp fit
   const size_t smem_stage = fast_smem_bytes(true, stride);
   const bool staged = !c->no_stage && smem_stage <= 160 * 1024;
@@ -762,6 +791,13 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.fast_regions = std::min<uint32_t>((uint32_t)c->labels.size(), kFastRegions);
   ca.max_depth = kMaxDepth;
   ca.force_general = force_general ? 1u : 0u;
+  const bool tps = tps_enabled(c);
+  ca.tps_regions = tps ? std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions) : 0u;
+  ca.tps_depth = tps ? kTpsDepth : 0u;
+  ALLOC_OK(c, c->d_wlist, 8 * n_streams);
+  ca.warp_list = c->d_wlist.as<unsigned long long>();
+  ca.warp_len = c->d_glen.as<unsigned long long>() + 1;
+  CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 8, c->stream));
   k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                  c->stream>>>(ca);
   CUDA_OK(c, cudaGetLastError());
@@ -1024,6 +1060,10 @@ extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
   ca.fast_regions = 0;
   ca.max_depth = kMaxDepth;
   ca.force_general = 1;
+  ca.tps_regions = 0;
+  ca.tps_depth = 0;
+  ca.warp_list = nullptr;
+  ca.warp_len = nullptr;
   k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                  c->stream>>>(ca);
   CUDA_OK(c, cudaGetLastError());

@@ -14,6 +14,9 @@
 // #START - #END.  Pass 2 verifies the single-stack assumption and reroutes any
 // stream that violates it (SF_INVALID) to an exact recount.
 //
+// Routing: the thread-per-stream kernel (k_tps.cuh) takes streams with
+// region ids < tps_regions and nesting <= tps_depth; other fast streams are
+// listed for the warp-per-stream kernel (SF_WARP).
 // Routing to the general path (SF_GENERAL): region ids >= fast_regions,
 // nesting deeper than kMaxDepth, or a wait-marker START after z (below) that
 // is not closed by the very next record (pass 2 could not decide whether it
@@ -40,6 +43,10 @@ struct CountArgs {
   uint32_t fast_regions; // region ids below this may take the fast path
   uint32_t max_depth;    // nesting the fast path holds in shared memory
   uint32_t force_general;
+  uint32_t tps_regions;  // thread-per-stream path: region ids below this
+  uint32_t tps_depth;    //   and nesting up to this (0: path disabled)
+  unsigned long long* warp_list;  // SF_WARP streams
+  unsigned long long* warp_len;
 };
 
 __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
@@ -82,6 +89,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     int32_t z = -1;
     int64_t last_bad = -1;
     bool wide = false;
+    bool tps_out = false;  // region id beyond the thread-per-stream tables
     bool prev_end = false;       // record c-1 is an END
     uint32_t pend_rid = kNone;   // lane-31 marker START awaiting its END
     auto chunk = [&](uint32_t c, uint32_t tag) {
@@ -92,6 +100,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       const bool en = valid && !(tag & WGPF_START_FLAG);
       const bool in_range = rid < a.fast_regions;
       wide |= valid && !in_range;
+      tps_out |= valid && rid >= a.tps_regions;
       const uint32_t smk = __ballot_sync(0xffffffffu, st);
       const uint32_t emk = __ballot_sync(0xffffffffu, en);
       const int32_t q = q_in + (int32_t)__popc(smk & le) - (int32_t)__popc(emk & le);
@@ -157,12 +166,15 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     }
     if (pend_rid != kNone) last_bad = max(last_bad, (int64_t)n - 1);
     wide = __any_sync(0xffffffffu, wide);
+    tps_out = __any_sync(0xffffffffu, tps_out);
     if (lane == 0) {
       a.counts[s] = n_end - (uint32_t)(-run_min);
       a.zpos[s] = z;
       const bool general = wide || a.force_general ||
                            max_d > (int32_t)a.max_depth || last_bad > (int64_t)z;
-      a.sflag[s] = general ? SF_GENERAL : 0u;
+      const bool warp = a.tps_depth != 0 && !general && (tps_out || max_d > (int32_t)a.tps_depth);
+      a.sflag[s] = general ? SF_GENERAL : (warp ? SF_WARP : 0u);
+      if (warp) a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
     }
   }
 }

@@ -51,6 +51,10 @@ struct FastArgs {
   uint32_t no_stats;
   unsigned long long* general_list;  // streams left for the general path
   unsigned long long* general_len;
+  // list mode: only the streams list[0 .. *list_len) (pass 1's SF_WARP
+  // streams; the thread-per-stream kernel handles the rest)
+  const unsigned long long* list;
+  const unsigned long long* list_len;
 };
 
 struct LevelEntry {  // last START seen at a nesting level
@@ -177,8 +181,7 @@ __device__ inline void fast_stats(FastSmem& sm, const DevStats& st,
 // Per-lane register accumulator for one label class: events reaching a lane
 // mostly repeat their class (periodic scope patterns), so count / sum / min /
 // max / first key accumulate in registers and reach shared memory only when
-// the lane's class changes (and once at kernel exit).  Keys grow along a
-// warp's streams, so the first key of a run is its minimum.
+// the lane's class changes (and once at kernel exit).
 struct LaneAcc {
   uint32_t cls, cnt, mn, mx;
   unsigned long long sum, first;
@@ -240,6 +243,7 @@ __device__ inline void lane_stats(LaneAcc& a, FastSmem& sm, const DevStats& st,
     a.first = key;
   }
   ++a.cnt;
+  a.first = min(a.first, key);
   a.sum += d;
   a.mn = min(a.mn, d);
   a.mx = max(a.mx, d);
@@ -296,16 +300,19 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
   acc_init(acc_w);
 
   const uint64_t wstep = (uint64_t)gridDim.x * kFastWarps;
+  const uint64_t n_iter = a.list ? *a.list_len : a.n_streams;
+  auto sid = [&](uint64_t t) -> uint64_t { return a.list ? a.list[t] : t; };
   uint32_t sbuf = 0, sphase = 0;  // staging buffer in use, parity bits
-  if (kStage && !abort_all && lane == 0 && gw < a.n_streams)
-    stage_issue(&sm.bar[w][0], stage, a.body + gw * a.stride, (uint32_t)a.stride);
-  for (uint64_t s = gw; !abort_all && s < a.n_streams; s += wstep) {
+  if (kStage && !abort_all && lane == 0 && gw < n_iter)
+    stage_issue(&sm.bar[w][0], stage, a.body + sid(gw) * a.stride, (uint32_t)a.stride);
+  for (uint64_t t = gw; !abort_all && t < n_iter; t += wstep) {
+    const uint64_t s = sid(t);
     if constexpr (kStage) {
       // prefetch the warp's next stream into the other buffer
       __syncwarp();
-      if (lane == 0 && s + wstep < a.n_streams)
+      if (lane == 0 && t + wstep < n_iter)
         stage_issue(&sm.bar[w][sbuf ^ 1], stage + (sbuf ^ 1) * sstride,
-                    a.body + (s + wstep) * a.stride, (uint32_t)a.stride);
+                    a.body + sid(t + wstep) * a.stride, (uint32_t)a.stride);
       stage_wait(&sm.bar[w][sbuf], (sphase >> sbuf) & 1u);
       sphase ^= 1u << sbuf;
     }
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
     if constexpr (kStage) sbuf ^= 1;
     const uint32_t flag = a.sflag[s];
     if (flag & (SF_DECODE_ERR | SF_GENERAL)) {
-      if ((flag & SF_GENERAL) && lane == 0) {
+      if ((flag & SF_GENERAL) && lane == 0 && !a.list) {
         const unsigned long long k = atomicAdd(a.general_len, 1ull);
         a.general_list[k] = s;
       }

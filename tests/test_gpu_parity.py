@@ -357,6 +357,14 @@ def test_stats_merge_two_shards(ctx):
                         0, 0, 0x1, stream_base=a)
         c.stats_export(gathered.data_ptr() + r * pb)
     torch.cuda.synchronize()
+    part_counts = [p.stats() for p in parts]
+    for k in whole:
+        assert whole[k].count == sum(pc[k].count for pc in part_counts if k in pc), k
+    g = gathered.cpu().numpy().view(np.uint64)
+    per = pb // 8
+    for r in range(2):
+        for i, k in enumerate(S.MIXED_LABELS):
+            assert int(g[r * per + i * 70]) == part_counts[r][k].count, (r, k)
     merged_ctx = t.Context(0)
     merged_ctx.set_plan(plan)
     merged_ctx.stats_merge(gathered.data_ptr(), 2)

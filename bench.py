@@ -362,7 +362,7 @@ def main():
             "hbm_frac_step": alg_bytes / (ms_step / 1e3) / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_fast_emit",
+                         "traffic": traffic, "kernel": "emit phase (k_tps + k_fast_emit list)",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel_ms": emit_ms, "peak_kind": peak_kind},
             "phases_ms": {"count": count_ms,

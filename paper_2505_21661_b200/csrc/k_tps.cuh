@@ -17,13 +17,16 @@
 //       first key per class in shared memory (no atomics), histogram through
 //       match.any groups and one shared atomic per group.
 //
-// Data movement.  Records: the warp stages 16-record windows of its 32 streams
+// Data movement.  Records: the warp stages 8-record windows of its 32 streams
 // in shared memory with cp.async (16-B chunks, double buffered; chunk k of the
 // window of stream l is copied by a fixed lane, so one instruction covers a
-// few contiguous lines).  Events: each lane stages 4 events (128 B) in shared
-// memory and writes them with one TMA bulk store (cp.async.bulk, bulk_group),
-// double buffered.  Per record a lane executes ~1 shared load; per event two
-// 16-B shared stores and a quarter of a bulk store.
+// few contiguous lines).  Events: each lane stages its events in an 8-event
+// ring in shared memory; whenever lanes hold 4 unwritten events the warp
+// writes them cooperatively, 8 lanes per 128-B run, i.e. 4 runs per 16-B-per-
+// lane store instruction (coalesced, full sectors).  (Per-lane TMA bulk
+// stores serialise: the bulk-copy instruction takes uniform operands.)
+// The step is written branch-free (predicated); error, orphan and flush work
+// sits behind warp-uniform votes.
 #pragma once
 
 #include "k_fast.cuh"
@@ -31,22 +34,23 @@
 namespace wgpf {
 
 constexpr uint32_t kTpsMaxWarps = 8;                  // warps per CTA (<=)
-constexpr uint32_t kTpsW = 16;                        // records per window
+constexpr uint32_t kTpsW = 8;                         // records per window
 constexpr uint32_t kTpsChunks = (kTpsW + 2) / 2;      // 16-B chunks per window
 constexpr uint32_t kTpsPitch = 16 * kTpsChunks;       // bytes per lane window
 constexpr uint32_t kTpsDepth = 16;                    // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
 constexpr uint32_t kTpsClasses = 16;                  // dense classes held
-constexpr uint32_t kTpsEvb = 4;                       // events per buffer
-constexpr uint32_t kTpsEvPitch = 32 * kTpsEvb + 16;   // padded: no conflicts
+constexpr uint32_t kTpsRing = 8;                      // events per lane ring
+constexpr uint32_t kTpsRingPitch = 32 * kTpsRing + 16;  // padded: no conflicts
 constexpr uint32_t kTpsMaxSlots = 2046;               // pos / hi in 11+15 bits
 
 struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
-  uint8_t evb[2][32 * kTpsEvPitch];  // event staging
+  uint8_t ring[32 * kTpsRingPitch];  // event rings
   uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<11 | cons<<16 | hi<<17}
   uint16_t cnt[kTpsRegions][32];     // iteration counters
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
+  uint8_t fl[32];                    // lanes being flushed
 };
 
 struct TpsCtaSmem {
@@ -90,39 +94,24 @@ __device__ __forceinline__ void cp_async_commit() {
 __device__ __forceinline__ void cp_async_wait1() {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc,
-                                           uint32_t bytes) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile(
-      "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-      "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ssrc))), "r"(bytes)
-      : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
 
 __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TpsCtaSmem& cs = *reinterpret_cast<TpsCtaSmem*>(smem_raw);
   const uint32_t lane = lane_id();
   const uint32_t w = threadIdx.x >> 5;
-  const uint32_t K = a.plan.K;
   const uint32_t nw = blockDim.x >> 5;
+  const uint32_t K = a.plan.K;
   TpsWarpSmem& ws = *reinterpret_cast<TpsWarpSmem*>(
       smem_raw + tps_align(sizeof(TpsCtaSmem)) + w * tps_align(sizeof(TpsWarpSmem)));
   uint8_t* lsb = smem_raw + tps_align(sizeof(TpsCtaSmem)) +
-                 nw * tps_align(sizeof(TpsWarpSmem)) +
-                 w * tps_lane_stats_bytes(K);
+                 nw * tps_align(sizeof(TpsWarpSmem)) + w * tps_lane_stats_bytes(K);
   TpsLaneStats ls;
   ls.a = reinterpret_cast<uint4*>(lsb);
   ls.hi = reinterpret_cast<uint32_t*>(lsb + (size_t)K * 32 * 16);
   ls.first = reinterpret_cast<unsigned long long*>(lsb + (size_t)K * 32 * 20);
   const bool stats = !a.no_stats;
+  const bool emit = a.events != nullptr;
   for (uint32_t c = 0; c < K; ++c) {
     ls.a[c * 32 + lane] = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
     ls.hi[c * 32 + lane] = 0;
@@ -147,7 +136,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint64_t cost = a.record_cost;
   const uint32_t cap = a.cap;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
-  uint32_t ebuf = 0;  // event staging buffer in use
+  uint8_t* const ring = ws.ring + lane * kTpsRingPitch;
 
   // static chunk assignment of the record windows: chunk k of this lane is
   // part pk of stream lane slk
@@ -185,9 +174,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
 #pragma unroll
     for (uint32_t r = 0; r < kTpsRegions; ++r) ws.cnt[r][lane] = 0;
 
-    // window sources: physical (even) slot of chunk k for window c0 = 2
+    // window sources: physical (even) slot of chunk k, first window c0 = 2
     uint32_t wp[kTpsChunks], wlim[kTpsChunks];
-    const uint8_t* wsrc[kTpsChunks];
 #pragma unroll
     for (uint32_t k = 0; k < kTpsChunks; ++k) {
       const uint32_t st_k = __shfl_sync(FULL, start, slk[k]);
@@ -197,14 +185,15 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       p = (p & ~1u) + 2u * pk[k];
       if (p >= cap) p -= cap;
       wp[k] = p;
-      wsrc[k] = a.body + (b * 32 + slk[k]) * a.stride + 16;
     }
+    const uint8_t* wbase = a.body + b * 32 * a.stride + 16;
     auto issue = [&](uint32_t bsel, uint32_t c0) {
       uint8_t* dst = ws.rec[bsel];
 #pragma unroll
       for (uint32_t k = 0; k < kTpsChunks; ++k) {
         if (c0 < wlim[k])
-          cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k], wsrc[k] + 8ull * wp[k]);
+          cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k],
+                     wbase + (uint64_t)slk[k] * a.stride + 8ull * wp[k]);
         wp[k] += kTpsW;
         if (wp[k] >= cap) wp[k] -= cap;
       }
@@ -221,43 +210,64 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     uint32_t hi = 0, vprev = 0, sp = 0;
     uint32_t pw = 0xFFu;  // wait class of the previous record if it was a
                           // matched base END, else none
-    uint64_t kb = 0;      // base events emitted
-    uint32_t fill = 0;    // events in the staging buffer
-    uint64_t eb = off;    // event index of the buffer's first event
+    uint32_t kw = 0;      // events of this stream staged
+    uint32_t kf = 0;      //   of which written
     uint32_t n_orph = 0;
-    uint8_t* const evl0 = ws.evb[0] + lane * kTpsEvPitch;  // + ebuf * buffer
 
-    auto flush = [&]() {
-      if (!fill) return;
-      const uint64_t room = eb < a.events_cap ? a.events_cap - eb : 0ull;
-      const uint32_t m = (uint64_t)fill <= room ? fill : (uint32_t)room;
-      if (m) bulk_store(a.events + eb, evl0 + ebuf * (32u * kTpsEvPitch), 32u * m);
-      if (m < fill) atomicAdd(&a.status->overflow, (unsigned long long)(fill - m));
-      ebuf ^= 1u;
-      bulk_wait_read1();  // the buffer switched to is free again
-      eb += fill;
-      fill = 0;
+    // warp-cooperative write of the rings: lanes with >= 4 unwritten events
+    // (fin: any); 8 lanes per source lane, 16 B each
+    auto flush = [&](bool fin) {
+      const uint32_t pend = kw - kf;
+      const bool need = fin ? pend != 0 : pend >= 4u;
+      const uint32_t m = __ballot_sync(FULL, need);
+      if (!m) return;
+      const uint32_t cw = pend < 4u ? pend : 4u;
+      if (need) ws.fl[__popc(m & lt)] = (uint8_t)lane;
+      __syncwarp();
+      const uint32_t nf = __popc(m);
+      const uint64_t my_idx = off + kf;
+      for (uint32_t q = 0; q < nf; q += 4) {
+        const uint32_t g = q + (lane >> 3);
+        const uint32_t src = ws.fl[g < nf ? g : q];
+        const uint32_t ilo = __shfl_sync(FULL, (uint32_t)my_idx, src);
+        const uint32_t ihi = __shfl_sync(FULL, (uint32_t)(my_idx >> 32), src);
+        const uint32_t kfs = __shfl_sync(FULL, kf, src);
+        const uint32_t cws = __shfl_sync(FULL, cw, src);
+        const uint32_t ev = (lane & 7u) >> 1;
+        if (g < nf && ev < cws) {
+          const uint64_t idx = (((uint64_t)ihi << 32) | ilo) + ev;
+          const uint4 val = *reinterpret_cast<const uint4*>(
+              ws.ring + src * kTpsRingPitch + ((kfs + ev) & (kTpsRing - 1u)) * 32u +
+              (lane & 1u) * 16u);
+          if (idx < a.events_cap)
+            reinterpret_cast<uint4*>(a.events + idx)[lane & 1u] = val;
+          else if (!(lane & 1u))
+            atomicAdd(&a.status->overflow, 1ull);
+        }
+      }
+      __syncwarp();
+      if (need) kf += cw;
     };
-    auto stage = [&](uint64_t st, uint64_t en, uint32_t region, uint32_t it) {
-      uint4* p = reinterpret_cast<uint4*>(evl0 + ebuf * (32u * kTpsEvPitch) + 32u * fill);
+    auto put = [&](uint32_t k, uint64_t st, uint64_t en, uint32_t region, uint32_t it) {
+      uint4* p = reinterpret_cast<uint4*>(ring + (k & (kTpsRing - 1u)) * 32u);
       p[0] = make_uint4((uint32_t)st, (uint32_t)(st >> 32), (uint32_t)en,
                         (uint32_t)(en >> 32));
       p[1] = make_uint4(region, it, blk, wg);
-      if (++fill == kTpsEvb) flush();
     };
-    auto lstat = [&](uint32_t cls, uint32_t d, unsigned long long key) {
-      uint4* e = ls.a + cls * 32 + lane;
+    auto lstat = [&](bool part, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
+      const uint32_t c = part ? cls : 0u;
+      uint4* e = ls.a + c * 32 + lane;
       uint4 x = *e;
-      if (x.x == 0) ls.first[cls * 32 + lane] = key;
-      x.x += 1;
-      x.y = min(x.y, d);
-      x.z = max(x.z, d);
-      const uint32_t sm = x.w + d;
-      if (sm < d) ls.hi[cls * 32 + lane] += 1;
-      x.w = sm;
-      *e = x;
-    };
-    auto lhist = [&](bool part, uint32_t cls, uint32_t d) {
+      if (part) {
+        if (x.x == 0) ls.first[c * 32 + lane] = first_key(gs, kpos, kind);
+        x.x += 1;
+        x.y = min(x.y, d);
+        x.z = max(x.z, d);
+        const uint32_t sm = x.w + d;
+        if (sm < d) ls.hi[c * 32 + lane] += 1;
+        x.w = sm;
+        *e = x;
+      }
       const uint32_t bin = hist_bin(d);
       const uint32_t key = part ? ((cls << 6) | bin) : (0xFC000000u | lane);
       const uint32_t grp = __match_any_sync(FULL, key);
@@ -271,132 +281,113 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       cp_async_wait1();
       __syncwarp();
       const uint8_t* myrec = myrec0 + bsel * (32 * kTpsPitch);
-#pragma unroll 4
+#pragma unroll 2
       for (uint32_t j = 0; j < kTpsW; ++j) {
         const uint32_t i = w0 + j;
         const uint2 r2 = *reinterpret_cast<const uint2*>(myrec + 8u * j);
         const bool valid = i < n;
         const uint32_t tag = r0.x, v = r0.y;
-        const bool st = valid && (tag & WGPF_START_FLAG);
-        const bool en = valid && !(tag & WGPF_START_FLAG);
+        const bool isS = (int32_t)tag < 0;
+        const bool st = valid && isS;
+        const bool en = valid && !isS;
         const uint32_t rid = (tag >> 12) & (kTpsRegions - 1u);
         const uint32_t inf = cs.info[rid];
-        hi += (valid && v < vprev) ? 1u : 0u;
-        if (valid) vprev = v;
         const uint32_t cls = inf & 0xFFu;
-        bool base_ev = false, consumed = false;
-        uint32_t e_dur = 0, w_dur = 0, wc = 0;
-        uint64_t kpos = kb;
-        if (st) {
-          const uint32_t cons = (pw == cls) ? 1u : 0u;
-          ws.stk[sp][lane] = make_uint2(v, i | (rid << 11) | (cons << 16) | (hi << 17));
-          ++sp;
+        hi += (valid && v < vprev) ? 1u : 0u;
+        vprev = valid ? v : vprev;
+        // ---- stack ---------------------------------------------------------
+        const uint2 e = ws.stk[sp ? sp - 1u : 0u][lane];
+        const bool mend = en && sp != 0;
+        w_drop += (en && sp == 0) ? 1u : 0u;
+        if (st)
+          ws.stk[sp][lane] =
+              make_uint2(v, i | (rid << 11) | ((pw == cls ? 1u : 0u) << 16) | (hi << 17));
+        sp = sp + (st ? 1u : 0u) - (mend ? 1u : 0u);
+        const uint64_t u = ((uint64_t)hi << 32) | v;
+        const uint64_t su = ((uint64_t)(e.y >> 17) << 32) | e.x;
+        const uint64_t meas = u - su;
+        const bool mism = mend && ((e.y >> 11) & 31u) != rid;
+        const bool tlong = mend && !mism && (meas >> 32) != 0;
+        if (__any_sync(FULL, mism || tlong)) {  // rare: leave the stream
+          if (mism) {
+            atomicAdd(&a.status->invalid, 1ull);
+            a.sflag[s] = flag | SF_INVALID;
+          }
+          if (tlong) atomicMin(&a.status->pair_err, ((unsigned long long)gs << 32) | i);
+          if (mism || tlong) n = 0;
         }
-        uint32_t npw = 0xFFu;
-        if (en) {
-          if (sp == 0) {
-            ++w_drop;
-          } else {
-            --sp;
-            const uint2 e = ws.stk[sp][lane];
-            const uint32_t p_rid = (e.y >> 11) & 31u;
-            const uint64_t u = ((uint64_t)hi << 32) | v;
-            const uint64_t su = ((uint64_t)(e.y >> 17) << 32) | e.x;
-            if (p_rid != rid) {  // not single-stack: exact recount
+        const bool ok = mend && !mism && !tlong;
+        const uint32_t it = ws.cnt[rid][lane];
+        if (ok) ws.cnt[rid][lane] = (uint16_t)(it + 1u);
+        const bool is_mk = (inf & 0x100u) != 0u;
+        const bool base = ok && !is_mk;
+        const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
+        // ---- exec event: sync correction -------------------------------------
+        const uint64_t ovh = cost * (uint64_t)(i - (e.y & 2047u));
+        const uint64_t corr = meas >= ovh ? meas - ovh : 0ull;
+        // ---- wait marker START at i+1 -------------------------------------------
+        const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
+        const uint32_t i1 = cs.info[r1id];
+        const bool cclose = i + 2 < n && (int32_t)r2.x >= 0 &&
+                            ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;
+        const bool consumed = base && i + 1 < n && (int32_t)r1.x < 0 &&
+                              (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
+                              ((int32_t)(i + 1) <= z || cclose);
+        const uint32_t h1 = hi + (r1.y < v ? 1u : 0u);
+        const uint64_t u1 = ((uint64_t)h1 << 32) | r1.y;
+        const uint32_t wd = (uint32_t)(u1 - u);  // consecutive records: < 2^32
+        const bool corr_w = (uint64_t)wd > cost;
+        w_flag += (consumed && !corr_w) ? 1u : 0u;
+        const uint32_t kpos = kw;
+        if (emit) {
+          if (base) put(kw, su, su + corr, rid | WGPF_EV_CORRECTED, it);
+          if (consumed)
+            put(kw + 1u, u, u1, r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
+        }
+        kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
+        pw = base ? (inf >> 16) : 0xFFu;
+        if (__any_sync(FULL, orphan)) {  // rare: marker interval without its exec
+          if (orphan) {
+            if (n_orph == 0) {
+              wgpf_event& o = ws.orph[lane];
+              o.start = su;
+              o.end = u;
+              o.region = rid;
+              o.iteration = it;
+              o.block_index = blk;
+              o.warp_group = wg;
+              n_orph = 1;
+            } else {  // more than one: exact recount
               atomicAdd(&a.status->invalid, 1ull);
               a.sflag[s] = flag | SF_INVALID;
               n = 0;
-            } else if (u - su >= (1ull << 32)) {
-              atomicMin(&a.status->pair_err, ((unsigned long long)gs << 32) | i);
-              n = 0;
-            } else {
-              const uint32_t it = ws.cnt[rid][lane];
-              ws.cnt[rid][lane] = (uint16_t)(it + 1u);
-              if (!(inf & 0x100u)) {  // base scope: exec event
-                base_ev = true;
-                const uint64_t meas = u - su;
-                const uint64_t ovh = cost * (uint64_t)(i - (e.y & 2047u));
-                const uint64_t corr = meas >= ovh ? meas - ovh : 0ull;
-                e_dur = (uint32_t)corr;
-                if (a.events) stage(su, su + corr, rid | WGPF_EV_CORRECTED, it);
-                ++kb;
-                npw = inf >> 16;
-                // wait marker START at i+1, closed (z or the next record)
-                if (i + 1 < n && (r1.x & WGPF_START_FLAG)) {
-                  const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
-                  const uint32_t i1 = cs.info[r1id];
-                  if ((i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu)) {
-                    const bool closes_next = i + 2 < n && !(r2.x & WGPF_START_FLAG) &&
-                                             ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;
-                    if ((int64_t)(i + 1) <= (int64_t)z || closes_next) {
-                      consumed = true;
-                      wc = i1 & 0xFFu;
-                      const uint32_t h1 = hi + (r1.y < v ? 1u : 0u);
-                      const uint64_t u1 = ((uint64_t)h1 << 32) | r1.y;
-                      const uint64_t wd = u1 - u;
-                      const bool corr_w = wd > cost;
-                      w_flag += corr_w ? 0u : 1u;
-                      w_dur = (uint32_t)wd;
-                      if (a.events)
-                        stage(u, u1, r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u),
-                              it);
-                      ++kb;
-                    }
-                  }
-                }
-              } else if (!((e.y >> 16) & 1u)) {  // orphan marker interval
-                if (n_orph == 0) {
-                  wgpf_event& o = ws.orph[lane];
-                  o.start = su;
-                  o.end = u;
-                  o.region = rid;
-                  o.iteration = it;
-                  o.block_index = blk;
-                  o.warp_group = wg;
-                  n_orph = 1;
-                } else {  // more than one: exact recount
-                  atomicAdd(&a.status->invalid, 1ull);
-                  a.sflag[s] = flag | SF_INVALID;
-                  n = 0;
-                }
-              }
             }
           }
         }
-        pw = npw;
         if (stats) {
-          if (__any_sync(FULL, base_ev)) {
-            if (base_ev) lstat(cls, e_dur, first_key(gs, kpos, 0u));
-            lhist(base_ev, cls, e_dur);
-          }
-          if (__any_sync(FULL, consumed)) {
-            if (consumed) lstat(wc, w_dur, first_key(gs, kpos + 1, 1u));
-            lhist(consumed, wc, w_dur);
-          }
+          if (__any_sync(FULL, base)) lstat(base, cls, (uint32_t)corr, kpos, 0u);
+          if (__any_sync(FULL, consumed)) lstat(consumed, i1 & 0xFFu, wd, kpos + 1u, 1u);
         }
+        if (emit) flush(false);
         r0 = r1;
         r1 = r2;
       }
       __syncwarp();
     }
-    // stream end: orphans after the base events, flush, checks
-    const bool ok = act && n != 0;
-    if (ok && n_orph) {
+    // stream end: the orphan after the base events, final writes, checks
+    const bool okS = act && n != 0;
+    const bool po = okS && n_orph;
+    if (__any_sync(FULL, po)) {
       const wgpf_event o = ws.orph[lane];
-      if (a.events) stage(o.start, o.end, o.region, o.iteration);
+      if (emit && po) put(kw, o.start, o.end, o.region, o.iteration);
+      if (stats)
+        lstat(po, cs.info[o.region & 31u] & 0xFFu, (uint32_t)(o.end - o.start), kw, 0u);
+      kw += po ? 1u : 0u;
     }
-    if (stats) {
-      const bool po = ok && n_orph;
-      const uint32_t oc = po ? cs.info[ws.orph[lane].region & 31u] & 0xFFu : 0u;
-      const uint32_t od = po ? (uint32_t)(ws.orph[lane].end - ws.orph[lane].start) : 0u;
-      if (__any_sync(FULL, po)) {
-        if (po) lstat(oc, od, first_key(gs, kb, 0u));
-        lhist(po, oc, od);
-      }
-    }
-    flush();
-    if (ok) {
-      if (kb + n_orph != want) {
+    if (emit)
+      while (__any_sync(FULL, kw != kf)) flush(true);
+    if (okS) {
+      if (kw != want) {
         atomicAdd(&a.status->invalid, 1ull);
         a.sflag[s] = flag | SF_INVALID;
       }
@@ -404,8 +395,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       w_tail += sp;
     }
   }
-  bulk_wait_all();
-  // lane-private stats -> CTA -> global
+  // lane-private stats -> global; warnings
   const unsigned long long d = warp_sum((unsigned long long)w_drop);
   const unsigned long long f = warp_sum((unsigned long long)w_flag);
   const unsigned long long t = warp_sum((unsigned long long)w_tail);

@@ -556,6 +556,9 @@ static bool tps_enabled(const wgpf_ctx* c) {
   return !c->no_tps && c->slots % 2 == 0 && c->slots <= kTpsMaxSlots &&
          c->K <= kTpsClasses && !c->labels.empty();
 }
+static uint32_t tps_regions(const wgpf_ctx* c) {
+  return std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions);
+}
 
 static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                      uint64_t n_streams, uint64_t stream_base,
@@ -592,10 +595,11 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.general_len = c->d_glen.as<unsigned long long>();
   f.list = nullptr;
   f.list_len = nullptr;
-  if (tps_enabled(c)) {
+  f.tps_regions = tps_regions(c);
+  if (tps_enabled(c) && record_cost <= 0xFFFFFFFFull) {
     // shallow streams: thread per stream; then the SF_WARP list
-    const uint32_t tw = tps_warps(c->K, c->smem_optin);
-    const size_t tsm = tps_smem_bytes(c->K, tw);
+    const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
+    const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
     k_tps<<<c->sms, tw * 32, tsm, c->stream>>>(f);
     CUDA_OK(c, cudaGetLastError());
     ++c->launches;
@@ -792,7 +796,7 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.max_depth = kMaxDepth;
   ca.force_general = force_general ? 1u : 0u;
   const bool tps = tps_enabled(c);
-  ca.tps_regions = tps ? std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions) : 0u;
+  ca.tps_regions = tps ? tps_regions(c) : 0u;
   ca.tps_depth = tps ? kTpsDepth : 0u;
   ALLOC_OK(c, c->d_wlist, 8 * n_streams);
   ca.warp_list = c->d_wlist.as<unsigned long long>();

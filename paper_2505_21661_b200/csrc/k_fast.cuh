@@ -55,6 +55,7 @@ struct FastArgs {
   // streams; the thread-per-stream kernel handles the rest)
   const unsigned long long* list;
   const unsigned long long* list_len;
+  uint32_t tps_regions;  // k_tps: region ids in its tables
 };
 
 struct LevelEntry {  // last START seen at a nesting level

@@ -25,8 +25,11 @@
 // writes them cooperatively, 8 lanes per 128-B run, i.e. 4 runs per 16-B-per-
 // lane store instruction (coalesced, full sectors).  (Per-lane TMA bulk
 // stores serialise: the bulk-copy instruction takes uniform operands.)
-// The step is written branch-free (predicated); error, orphan and flush work
-// sits behind warp-uniform votes.
+// The step is written predicated with 32-bit timing arithmetic (a pair whose
+// duration reaches 2^32 is an error, so every emitted duration fits); errors
+// are recorded per lane and handled after the stream (the stack depth stays
+// within pass 1's bound whatever the regions, so a lane can keep going).
+// Histograms: per-warp tables, one shared atomic per event.
 #pragma once
 
 #include "k_fast.cuh"
@@ -48,7 +51,6 @@ struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
   uint8_t ring[32 * kTpsRingPitch];  // event rings
   uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<11 | cons<<16 | hi<<17}
-  uint16_t cnt[kTpsRegions][32];     // iteration counters
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
   uint8_t fl[32];                    // lanes being flushed
 };
@@ -56,29 +58,44 @@ struct TpsWarpSmem {
 struct TpsCtaSmem {
   uint32_t info[kTpsRegions];  // class | marker<<8 | wait class<<16 (0xFF none)
   unsigned long long warn[4];
-  uint32_t hist[kTpsClasses * WGPF_HIST_BINS];
 };
 
-// Lane-private stats of one warp, [class][lane]: {count, min, max, sum lo},
-// sum hi, first key.
-struct TpsLaneStats {
+// Per-warp dynamic tables (R = region ids in use, K = classes):
+//   cnt  u16 [R][32]          iteration counters
+//   a    uint4 [K][32]        {count, min, max, sum lo} per class and lane
+//   hi   u32 [K][32]          sum hi
+//   first u64 [K][32]         first-event key
+//   hist u32 [K][64]          per-warp histogram
+struct TpsTables {
+  uint16_t* cnt;
   uint4* a;
   uint32_t* hi;
   unsigned long long* first;
+  uint32_t* hist;
 };
 
 __host__ __device__ inline size_t tps_align(size_t b) { return (b + 127) & ~size_t(127); }
-__host__ __device__ inline size_t tps_lane_stats_bytes(uint32_t K) {
-  return tps_align((size_t)K * 32 * (16 + 4 + 8));
+__host__ __device__ inline size_t tps_tables_bytes(uint32_t K, uint32_t R) {
+  return tps_align((size_t)R * 64 + (size_t)K * 32 * (16 + 4 + 8) +
+                   (size_t)K * WGPF_HIST_BINS * 4);
 }
-__host__ inline size_t tps_smem_bytes(uint32_t K, uint32_t warps) {
+__host__ __device__ inline TpsTables tps_tables(uint8_t* p, uint32_t K, uint32_t R) {
+  TpsTables t;
+  t.a = reinterpret_cast<uint4*>(p);
+  t.first = reinterpret_cast<unsigned long long*>(p + (size_t)K * 32 * 16);
+  t.hi = reinterpret_cast<uint32_t*>(p + (size_t)K * 32 * 24);
+  t.hist = reinterpret_cast<uint32_t*>(p + (size_t)K * 32 * 28);
+  t.cnt = reinterpret_cast<uint16_t*>(p + (size_t)K * 32 * 28 + (size_t)K * WGPF_HIST_BINS * 4);
+  return t;
+}
+__host__ inline size_t tps_smem_bytes(uint32_t K, uint32_t R, uint32_t warps) {
   return tps_align(sizeof(TpsCtaSmem)) +
-         warps * (tps_align(sizeof(TpsWarpSmem)) + tps_lane_stats_bytes(K));
+         warps * (tps_align(sizeof(TpsWarpSmem)) + tps_tables_bytes(K, R));
 }
 // warps per CTA that fit the shared memory of one SM (one CTA per SM)
-__host__ inline uint32_t tps_warps(uint32_t K, size_t smem_limit) {
+__host__ inline uint32_t tps_warps(uint32_t K, uint32_t R, size_t smem_limit) {
   uint32_t w = kTpsMaxWarps;
-  while (w > 1 && tps_smem_bytes(K, w) > smem_limit) --w;
+  while (w > 1 && tps_smem_bytes(K, R, w) > smem_limit) --w;
   return w;
 }
 
@@ -102,22 +119,20 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint32_t w = threadIdx.x >> 5;
   const uint32_t nw = blockDim.x >> 5;
   const uint32_t K = a.plan.K;
+  const uint32_t R = a.tps_regions;
   TpsWarpSmem& ws = *reinterpret_cast<TpsWarpSmem*>(
       smem_raw + tps_align(sizeof(TpsCtaSmem)) + w * tps_align(sizeof(TpsWarpSmem)));
-  uint8_t* lsb = smem_raw + tps_align(sizeof(TpsCtaSmem)) +
-                 nw * tps_align(sizeof(TpsWarpSmem)) + w * tps_lane_stats_bytes(K);
-  TpsLaneStats ls;
-  ls.a = reinterpret_cast<uint4*>(lsb);
-  ls.hi = reinterpret_cast<uint32_t*>(lsb + (size_t)K * 32 * 16);
-  ls.first = reinterpret_cast<unsigned long long*>(lsb + (size_t)K * 32 * 20);
+  uint8_t* const tb0 = smem_raw + tps_align(sizeof(TpsCtaSmem)) +
+                       nw * tps_align(sizeof(TpsWarpSmem));
+  const TpsTables tb = tps_tables(tb0 + w * tps_tables_bytes(K, R), K, R);
   const bool stats = !a.no_stats;
   const bool emit = a.events != nullptr;
   for (uint32_t c = 0; c < K; ++c) {
-    ls.a[c * 32 + lane] = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
-    ls.hi[c * 32 + lane] = 0;
-    ls.first[c * 32 + lane] = ~0ull;
+    tb.a[c * 32 + lane] = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
+    tb.hi[c * 32 + lane] = 0;
+    tb.first[c * 32 + lane] = ~0ull;
   }
-  for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x) cs.hist[i] = 0;
+  for (uint32_t i = lane; i < K * WGPF_HIST_BINS; i += 32) tb.hist[i] = 0;
   for (uint32_t r = threadIdx.x; r < kTpsRegions; r += blockDim.x) {
     uint32_t inf = 0xFFFFFFFFu;
     if (r < a.fast_regions) {
@@ -133,7 +148,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const bool abort_all = a.status->decode_err != kNoErr;
   const uint32_t FULL = 0xffffffffu;
   const uint32_t lt = lanemask_lt();
-  const uint64_t cost = a.record_cost;
+  const uint32_t cost = (uint32_t)a.record_cost;  // host: < 2^32 on this path
   const uint32_t cap = a.cap;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
   uint8_t* const ring = ws.ring + lane * kTpsRingPitch;
@@ -161,7 +176,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const uint8_t* sbase = a.body + (act ? s : 0) * a.stride;
     uint4 h = make_uint4(0u, 0u, 0u, cap);
     if (act) h = *reinterpret_cast<const uint4*>(sbase);
-    uint32_t n = act ? (h.z <= cap ? h.z : cap) : 0u;
+    const uint32_t n = act ? (h.z <= cap ? h.z : cap) : 0u;
     const uint32_t start = h.z <= cap ? 0u : h.z % cap;
     const uint32_t nmax = __reduce_max_sync(FULL, n);
     if (nmax == 0) continue;
@@ -170,9 +185,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const uint32_t want = act ? a.counts[s] : 0u;
     const uint64_t off = act ? a.offsets[s] : 0ull;
     const uint64_t gs = s + a.stream_base;
+    const unsigned long long gkey = (unsigned long long)gs << 25;
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
-#pragma unroll
-    for (uint32_t r = 0; r < kTpsRegions; ++r) ws.cnt[r][lane] = 0;
+    for (uint32_t r = 0; r < R; ++r) tb.cnt[r * 32 + lane] = 0;
 
     // window sources: physical (even) slot of chunk k, first window c0 = 2
     uint32_t wp[kTpsChunks], wlim[kTpsChunks];
@@ -204,6 +219,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
     if (n > 0) r0 = slots[start];
     if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
+    uint32_t inf0 = cs.info[(r0.x >> 12) & (kTpsRegions - 1u)];
     issue(0, 2);
     cp_async_commit();
 
@@ -213,6 +229,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     uint32_t kw = 0;      // events of this stream staged
     uint32_t kf = 0;      //   of which written
     uint32_t n_orph = 0;
+    uint32_t mm_pos = 0xFFFFFFFFu;  // first END breaking single-stack nesting
+    uint32_t tl_pos = 0xFFFFFFFFu;  // first END whose pair reaches 2^32
 
     // warp-cooperative write of the rings: lanes with >= 4 unwritten events
     // (fin: any); 8 lanes per source lane, 16 B each
@@ -248,30 +266,102 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       __syncwarp();
       if (need) kf += cw;
     };
-    auto put = [&](uint32_t k, uint64_t st, uint64_t en, uint32_t region, uint32_t it) {
+    auto put = [&](uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo, uint32_t ehi,
+                   uint32_t region, uint32_t it) {
       uint4* p = reinterpret_cast<uint4*>(ring + (k & (kTpsRing - 1u)) * 32u);
-      p[0] = make_uint4((uint32_t)st, (uint32_t)(st >> 32), (uint32_t)en,
-                        (uint32_t)(en >> 32));
+      p[0] = make_uint4(slo, shi, elo, ehi);
       p[1] = make_uint4(region, it, blk, wg);
     };
-    auto lstat = [&](bool part, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
-      const uint32_t c = part ? cls : 0u;
-      uint4* e = ls.a + c * 32 + lane;
+    auto lstat = [&](uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
+      uint4* e = tb.a + cls * 32 + lane;
       uint4 x = *e;
-      if (part) {
-        if (x.x == 0) ls.first[c * 32 + lane] = first_key(gs, kpos, kind);
-        x.x += 1;
-        x.y = min(x.y, d);
-        x.z = max(x.z, d);
-        const uint32_t sm = x.w + d;
-        if (sm < d) ls.hi[c * 32 + lane] += 1;
-        x.w = sm;
-        *e = x;
+      if (x.x == 0) tb.first[cls * 32 + lane] = gkey | (kpos << 1) | kind;
+      x.x += 1;
+      x.y = min(x.y, d);
+      x.z = max(x.z, d);
+      const uint32_t sm = x.w + d;
+      if (sm < d) tb.hi[cls * 32 + lane] += 1;
+      x.w = sm;
+      *e = x;
+      atomicAdd(&tb.hist[cls * WGPF_HIST_BINS + hist_bin(d)], 1u);
+    };
+    auto step = [&](uint32_t i, uint2 r2) {
+      const bool valid = i < n;
+      const uint32_t tag = r0.x, v = r0.y;
+      const bool isS = (int32_t)tag < 0;
+      const bool st = valid && isS;
+      const bool en = valid && !isS;
+      const uint32_t rid = (tag >> 12) & (kTpsRegions - 1u);
+      const uint32_t inf = inf0;
+      const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
+      const uint32_t i1 = cs.info[r1id];
+      hi += (valid && v < vprev) ? 1u : 0u;
+      vprev = valid ? v : vprev;
+      // ---- stack ------------------------------------------------------------
+      const uint2 e = ws.stk[sp ? sp - 1u : 0u][lane];
+      const bool mend = en && sp != 0;
+      w_drop += (en && sp == 0) ? 1u : 0u;
+      if (st)
+        ws.stk[sp][lane] = make_uint2(
+            v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 16) | (hi << 17));
+      sp = sp + (st ? 1u : 0u) - (mend ? 1u : 0u);
+      const uint32_t shi = e.y >> 17;
+      const uint32_t meas = v - e.x;  // low 32 bits of u - su
+      const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
+      const bool mism = mend && ((e.y >> 11) & 31u) != rid;
+      const bool tlong = mend && !mism && dhi;
+      mm_pos = (mism && mm_pos == 0xFFFFFFFFu) ? i : mm_pos;
+      tl_pos = (tlong && tl_pos == 0xFFFFFFFFu) ? i : tl_pos;
+      const bool ok = mend && !mism && !tlong;
+      uint16_t* cp = tb.cnt + rid * 32 + lane;
+      const uint32_t it = *cp;
+      if (ok) *cp = (uint16_t)(it + 1u);
+      const bool is_mk = (inf & 0x100u) != 0u;
+      const bool base = ok && !is_mk;
+      const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
+      // ---- exec event: sync correction ---------------------------------------
+      const uint64_t ovh = (uint64_t)cost * (i - (e.y & 2047u));
+      const uint32_t corr = ovh > (uint64_t)meas ? 0u : meas - (uint32_t)ovh;
+      // ---- wait marker START at i+1 -------------------------------------------
+      const bool cclose = i + 2 < n && (int32_t)r2.x >= 0 &&
+                          ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;
+      const bool consumed = base && i + 1 < n && (int32_t)r1.x < 0 &&
+                            (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
+                            ((int32_t)(i + 1) <= z || cclose);
+      const uint32_t wd = r1.y - v;  // consecutive records: u1 - u < 2^32
+      const bool corr_w = wd > cost;
+      w_flag += (consumed && !corr_w) ? 1u : 0u;
+      const uint32_t kpos = kw;
+      if (emit) {
+        if (base) {
+          const uint32_t elo = e.x + corr;
+          put(kw, e.x, shi, elo, shi + (elo < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED, it);
+        }
+        if (consumed)
+          put(kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
+              r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
       }
-      const uint32_t bin = hist_bin(d);
-      const uint32_t key = part ? ((cls << 6) | bin) : (0xFC000000u | lane);
-      const uint32_t grp = __match_any_sync(FULL, key);
-      if (part && !(grp & lt)) atomicAdd(&cs.hist[(cls << 6) | bin], (uint32_t)__popc(grp));
+      kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
+      pw = base ? (inf >> 16) : 0xFFu;
+      if (orphan) {  // rare: a marker interval without its exec (last)
+        if (n_orph == 0) {
+          wgpf_event& o = ws.orph[lane];
+          o.start = ((uint64_t)shi << 32) | e.x;
+          o.end = ((uint64_t)hi << 32) | v;
+          o.region = rid;
+          o.iteration = it;
+          o.block_index = blk;
+          o.warp_group = wg;
+        }
+        ++n_orph;
+      }
+      if (stats) {
+        if (base) lstat(inf & 0xFFu, corr, kpos, 0u);
+        if (consumed) lstat(i1 & 0xFFu, wd, kpos + 1u, 1u);
+      }
+      inf0 = i1;
+      r0 = r1;
+      r1 = r2;
     };
 
     for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
@@ -280,119 +370,44 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       cp_async_commit();
       cp_async_wait1();
       __syncwarp();
-      const uint8_t* myrec = myrec0 + bsel * (32 * kTpsPitch);
-#pragma unroll 2
-      for (uint32_t j = 0; j < kTpsW; ++j) {
-        const uint32_t i = w0 + j;
-        const uint2 r2 = *reinterpret_cast<const uint2*>(myrec + 8u * j);
-        const bool valid = i < n;
-        const uint32_t tag = r0.x, v = r0.y;
-        const bool isS = (int32_t)tag < 0;
-        const bool st = valid && isS;
-        const bool en = valid && !isS;
-        const uint32_t rid = (tag >> 12) & (kTpsRegions - 1u);
-        const uint32_t inf = cs.info[rid];
-        const uint32_t cls = inf & 0xFFu;
-        hi += (valid && v < vprev) ? 1u : 0u;
-        vprev = valid ? v : vprev;
-        // ---- stack ---------------------------------------------------------
-        const uint2 e = ws.stk[sp ? sp - 1u : 0u][lane];
-        const bool mend = en && sp != 0;
-        w_drop += (en && sp == 0) ? 1u : 0u;
-        if (st)
-          ws.stk[sp][lane] =
-              make_uint2(v, i | (rid << 11) | ((pw == cls ? 1u : 0u) << 16) | (hi << 17));
-        sp = sp + (st ? 1u : 0u) - (mend ? 1u : 0u);
-        const uint64_t u = ((uint64_t)hi << 32) | v;
-        const uint64_t su = ((uint64_t)(e.y >> 17) << 32) | e.x;
-        const uint64_t meas = u - su;
-        const bool mism = mend && ((e.y >> 11) & 31u) != rid;
-        const bool tlong = mend && !mism && (meas >> 32) != 0;
-        if (__any_sync(FULL, mism || tlong)) {  // rare: leave the stream
-          if (mism) {
-            atomicAdd(&a.status->invalid, 1ull);
-            a.sflag[s] = flag | SF_INVALID;
-          }
-          if (tlong) atomicMin(&a.status->pair_err, ((unsigned long long)gs << 32) | i);
-          if (mism || tlong) n = 0;
-        }
-        const bool ok = mend && !mism && !tlong;
-        const uint32_t it = ws.cnt[rid][lane];
-        if (ok) ws.cnt[rid][lane] = (uint16_t)(it + 1u);
-        const bool is_mk = (inf & 0x100u) != 0u;
-        const bool base = ok && !is_mk;
-        const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
-        // ---- exec event: sync correction -------------------------------------
-        const uint64_t ovh = cost * (uint64_t)(i - (e.y & 2047u));
-        const uint64_t corr = meas >= ovh ? meas - ovh : 0ull;
-        // ---- wait marker START at i+1 -------------------------------------------
-        const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
-        const uint32_t i1 = cs.info[r1id];
-        const bool cclose = i + 2 < n && (int32_t)r2.x >= 0 &&
-                            ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;
-        const bool consumed = base && i + 1 < n && (int32_t)r1.x < 0 &&
-                              (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
-                              ((int32_t)(i + 1) <= z || cclose);
-        const uint32_t h1 = hi + (r1.y < v ? 1u : 0u);
-        const uint64_t u1 = ((uint64_t)h1 << 32) | r1.y;
-        const uint32_t wd = (uint32_t)(u1 - u);  // consecutive records: < 2^32
-        const bool corr_w = (uint64_t)wd > cost;
-        w_flag += (consumed && !corr_w) ? 1u : 0u;
-        const uint32_t kpos = kw;
-        if (emit) {
-          if (base) put(kw, su, su + corr, rid | WGPF_EV_CORRECTED, it);
-          if (consumed)
-            put(kw + 1u, u, u1, r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
-        }
-        kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
-        pw = base ? (inf >> 16) : 0xFFu;
-        if (__any_sync(FULL, orphan)) {  // rare: marker interval without its exec
-          if (orphan) {
-            if (n_orph == 0) {
-              wgpf_event& o = ws.orph[lane];
-              o.start = su;
-              o.end = u;
-              o.region = rid;
-              o.iteration = it;
-              o.block_index = blk;
-              o.warp_group = wg;
-              n_orph = 1;
-            } else {  // more than one: exact recount
-              atomicAdd(&a.status->invalid, 1ull);
-              a.sflag[s] = flag | SF_INVALID;
-              n = 0;
-            }
-          }
-        }
-        if (stats) {
-          if (__any_sync(FULL, base)) lstat(base, cls, (uint32_t)corr, kpos, 0u);
-          if (__any_sync(FULL, consumed)) lstat(consumed, i1 & 0xFFu, wd, kpos + 1u, 1u);
-        }
-        if (emit) flush(false);
-        r0 = r1;
-        r1 = r2;
+      const uint2* myrec = reinterpret_cast<const uint2*>(myrec0 + bsel * (32 * kTpsPitch));
+#pragma unroll
+      for (uint32_t j = 0; j < kTpsW; j += 2) {
+        step(w0 + j, myrec[j]);
+        step(w0 + j + 1, myrec[j + 1]);
+        if (emit) flush(false);  // <= 7 pending: fits the ring
       }
       __syncwarp();
     }
     // stream end: the orphan after the base events, final writes, checks
-    const bool okS = act && n != 0;
-    const bool po = okS && n_orph;
+    const bool bad = mm_pos != 0xFFFFFFFFu || n_orph > 1 || tl_pos != 0xFFFFFFFFu;
+    const bool po = act && !bad && n_orph == 1;
     if (__any_sync(FULL, po)) {
       const wgpf_event o = ws.orph[lane];
-      if (emit && po) put(kw, o.start, o.end, o.region, o.iteration);
-      if (stats)
-        lstat(po, cs.info[o.region & 31u] & 0xFFu, (uint32_t)(o.end - o.start), kw, 0u);
-      kw += po ? 1u : 0u;
+      if (po) {
+        if (emit)
+          put(kw, (uint32_t)o.start, (uint32_t)(o.start >> 32), (uint32_t)o.end,
+              (uint32_t)(o.end >> 32), o.region, o.iteration);
+        if (stats)
+          lstat(cs.info[o.region & 31u] & 0xFFu, (uint32_t)(o.end - o.start), kw, 0u);
+        ++kw;
+      }
     }
     if (emit)
       while (__any_sync(FULL, kw != kf)) flush(true);
-    if (okS) {
-      if (kw != want) {
-        atomicAdd(&a.status->invalid, 1ull);
+    if (act) {
+      // a pair error before any nesting break is the reference's error;
+      // after one, only the exact recount knows
+      if (tl_pos < mm_pos)
+        atomicMin(&a.status->pair_err, ((unsigned long long)gs << 32) | tl_pos);
+      else if (mm_pos != 0xFFFFFFFFu || n_orph > 1 || kw != want) {
+        atomicAdd(&a.status->invalid, 1ull);  // exact recount
         a.sflag[s] = flag | SF_INVALID;
       }
-      w_mal += n_orph;
-      w_tail += sp;
+      if (!bad) {
+        w_mal += n_orph;
+        w_tail += sp;
+      }
     }
   }
   // lane-private stats -> global; warnings
@@ -408,14 +423,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   }
   if (stats) {
     for (uint32_t c = 0; c < K; ++c) {
-      const uint4 x = ls.a[c * 32 + lane];
+      const uint4 x = tb.a[c * 32 + lane];
       const unsigned long long cnt = warp_sum((unsigned long long)x.x);
       if (cnt == 0) continue;
       const unsigned long long sum = warp_sum(
-          ((unsigned long long)ls.hi[c * 32 + lane] << 32) | x.w);
+          ((unsigned long long)tb.hi[c * 32 + lane] << 32) | x.w);
       const uint32_t mn = __reduce_min_sync(FULL, x.y);
       const uint32_t mx = __reduce_max_sync(FULL, x.z);
-      unsigned long long fk = ls.first[c * 32 + lane];
+      unsigned long long fk = tb.first[c * 32 + lane];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) fk = min(fk, __shfl_xor_sync(FULL, fk, o));
       if (lane == 0) {
@@ -430,9 +445,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   __syncthreads();
   if (threadIdx.x < 4 && cs.warn[threadIdx.x])
     atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
-  if (stats)
-    for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x)
-      if (cs.hist[i]) atomicAdd(&a.stats.hist[i], (unsigned long long)cs.hist[i]);
+  if (stats) {  // per-warp histograms -> global
+    for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x) {
+      unsigned long long hsum = 0;
+      for (uint32_t ww = 0; ww < nw; ++ww)
+        hsum += tps_tables(tb0 + ww * tps_tables_bytes(K, R), K, R).hist[i];
+      if (hsum) atomicAdd(&a.stats.hist[i], hsum);
+    }
+  }
 }
 
 }  // namespace wgpf

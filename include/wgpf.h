@@ -206,7 +206,8 @@ int wgpf_region_stats(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n,
 /* Multi-GPU: export this rank's packed statistics (device buffer of
  * wgpf_stats_packed_bytes() bytes), and merge n_ranks gathered exports (one
  * after the other in d_gathered) into this context's statistics.  The caller
- * moves the bytes (e.g. one NCCL all-gather over NVLink). */
+ * moves the bytes (e.g. one NCCL all-gather over NVLink).  The packed size
+ * depends on the plan's label classes: 0 before wgpf_set_plan. */
 uint64_t wgpf_stats_packed_bytes(const wgpf_ctx* ctx);
 int wgpf_stats_export(wgpf_ctx* ctx, void* d_dst);
 int wgpf_stats_merge(wgpf_ctx* ctx, const void* d_gathered, uint32_t n_ranks);

@@ -109,8 +109,17 @@ struct wgpf_ctx {
   bool profiling = false;
   bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
   bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
+  bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   size_t smem_optin = 0;
+  // pipelined replay_image (host buffers): copy streams, chunk buffers, and
+  // per-chunk (first stream, first event) for first_event lookups
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t pev[6] = {};  // h2d done [2], compute done [2], d2h done [2]
+  DevBuf d_cbody[2], d_cev[2], d_packed, d_off_all;
+  bool in_chunked = false, chunk_mode = false;
+  std::vector<uint64_t> chunk_sbase, chunk_ebase;
+  uint64_t chunk_nstreams = 0;
   uint32_t launches = 0;
   uint64_t general_streams = 0;
   wgpf_profile prof{};
@@ -122,6 +131,10 @@ struct wgpf_ctx {
     if (h_status) cudaFreeHost(h_status);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : pev)
+      if (e) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
   }
   void mark(int i) {
     if (profiling) cudaEventRecord(ev[i], stream);
@@ -757,6 +770,7 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   }
   const bool stats_only = flags & WGPF_F_STATS_ONLY;
   const bool no_stats = flags & WGPF_F_NO_STATS;
+  if (!c->in_chunked) c->chunk_mode = false;
   c->profiling = (flags & WGPF_F_PROFILE) != 0;
   c->launches = 0;
   c->general_streams = 0;
@@ -979,6 +993,119 @@ static int stage_image(wgpf_ctx* c, const uint8_t* kpft, uint64_t n,
   return WGPF_OK;
 }
 
+extern "C" int wgpf_stats_merge(wgpf_ctx* c, const void* d_gathered,
+                                uint32_t n_ranks);
+
+// Host-buffer replay of a large uniform image, pipelined over chunks of
+// streams: the H2D copy of chunk k+1 and the D2H copy of chunk k-1's events
+// (their own streams, double-buffered device chunks) overlap the replay of
+// chunk k, so the call approaches max(H2D, D2H) time instead of the sum.
+// Per-chunk statistics are packed and merged at the end (the multi-GPU merge);
+// errors and warnings are the first / the sum over chunks in stream order.
+static constexpr uint64_t kChunkBytes = 256ull << 20;
+
+static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
+                                uint64_t count, uint64_t record_cost,
+                                wgpf_event* h_events, uint64_t events_cap,
+                                uint32_t flags, uint64_t* n_events,
+                                wgpf_warnings* warnings) {
+  const uint64_t stride = 16ull + 8ull * c->slots;
+  const uint64_t cs = std::max<uint64_t>(32, (kChunkBytes / stride) & ~31ull);
+  const uint64_t nc = (count + cs - 1) / cs;
+  const uint64_t ev_cap = std::max<uint64_t>(cs * c->slots, 1);
+  if (!c->s_h2d) {
+    CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (auto& e : c->pev)
+      CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const uint64_t pb = wgpf_stats_packed_bytes(c);
+  for (int b = 0; b < 2; ++b) {
+    ALLOC_OK(c, c->d_cbody[b], cs * stride);
+    ALLOC_OK(c, c->d_cev[b], ev_cap * sizeof(wgpf_event));
+  }
+  ALLOC_OK(c, c->d_packed, nc * pb);
+  ALLOC_OK(c, c->d_off_all, 8 * count);
+  cudaEvent_t* eH = c->pev;
+  cudaEvent_t* eC = c->pev + 2;
+  cudaEvent_t* eD = c->pev + 4;
+  auto h2d = [&](uint64_t k) -> int {
+    const uint32_t b = (uint32_t)(k & 1);
+    const uint64_t s0 = k * cs, m = std::min(cs, count - s0);
+    if (k >= 2) CUDA_OK(c, cudaStreamWaitEvent(c->s_h2d, eC[b], 0));
+    CUDA_OK(c, cudaMemcpyAsync(c->d_cbody[b].p, kpft + off + s0 * stride, m * stride,
+                               cudaMemcpyHostToDevice, c->s_h2d));
+    CUDA_OK(c, cudaEventRecord(eH[b], c->s_h2d));
+    return WGPF_OK;
+  };
+  auto drain = [&]() {
+    cudaStreamSynchronize(c->s_h2d);
+    cudaStreamSynchronize(c->s_d2h);
+    cudaStreamSynchronize(c->stream);
+  };
+  c->chunk_sbase.clear();
+  c->chunk_ebase.clear();
+  c->chunk_mode = false;
+  int rc = h2d(0);
+  if (rc) return rc;
+  uint64_t total = 0;
+  wgpf_warnings acc{};
+  bool overflow = false;
+  for (uint64_t k = 0; k < nc; ++k) {
+    const uint32_t b = (uint32_t)(k & 1);
+    const uint64_t s0 = k * cs, m = std::min(cs, count - s0);
+    if (k + 1 < nc && (rc = h2d(k + 1))) return rc;
+    CUDA_OK(c, cudaStreamWaitEvent(c->stream, eH[b], 0));
+    if (k >= 2) CUDA_OK(c, cudaStreamWaitEvent(c->stream, eD[b], 0));
+    uint64_t ne = 0;
+    wgpf_warnings w{};
+    c->in_chunked = true;
+    rc = wgpf_replay_device(c, c->d_cbody[b].p, m * stride, m, s0, record_cost,
+                            c->d_cev[b].as<wgpf_event>(), ev_cap,
+                            flags & ~WGPF_F_STATS_ONLY, &ne, &w);
+    c->in_chunked = false;
+    if (rc) {
+      drain();
+      if (rc == WGPF_E_TRACE && c->h_status->decode_err != kNoErr &&
+          c->h_status->cap_mismatch)
+        return host_walk(c, kpft, off + count * stride, off, count);
+      return rc;
+    }
+    CUDA_OK(c, cudaEventRecord(eC[b], c->stream));
+    rc = wgpf_stats_export(c, c->d_packed.as<uint8_t>() + k * pb);
+    if (rc) return rc;
+    CUDA_OK(c, cudaMemcpyAsync(c->d_off_all.as<uint64_t>() + s0, c->d_offsets.p, 8 * m,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    if (total + ne > events_cap) overflow = true;
+    if (!overflow && ne) {
+      CUDA_OK(c, cudaStreamWaitEvent(c->s_d2h, eC[b], 0));
+      CUDA_OK(c, cudaMemcpyAsync(h_events + total, c->d_cev[b].p, ne * sizeof(wgpf_event),
+                                 cudaMemcpyDeviceToHost, c->s_d2h));
+    }
+    CUDA_OK(c, cudaEventRecord(eD[b], c->s_d2h));
+    c->chunk_sbase.push_back(s0);
+    c->chunk_ebase.push_back(total);
+    total += ne;
+    acc.dropped_heads += w.dropped_heads;
+    acc.truncated_tails += w.truncated_tails;
+    acc.flagged_preconditions += w.flagged_preconditions;
+    acc.malformed_groups += w.malformed_groups;
+  }
+  drain();
+  if (n_events) *n_events = total;
+  if (warnings) *warnings = acc;
+  if (overflow)
+    return set_err(c, WGPF_E_BUFFER, "event buffer holds %llu of %llu events",
+                   (unsigned long long)events_cap, (unsigned long long)total);
+  if (!(flags & WGPF_F_NO_STATS)) {
+    rc = wgpf_stats_merge(c, c->d_packed.p, (uint32_t)nc);
+    if (rc) return rc;
+    c->chunk_mode = true;
+    c->chunk_nstreams = count;
+  }
+  return WGPF_OK;
+}
+
 extern "C" int wgpf_replay_image(wgpf_ctx* c, const uint8_t* kpft,
                                  uint64_t n_bytes, uint64_t record_cost,
                                  wgpf_event* h_events, uint64_t events_cap,
@@ -987,6 +1114,17 @@ extern "C" int wgpf_replay_image(wgpf_ctx* c, const uint8_t* kpft,
   if (!c->has_plan) return set_err(c, WGPF_E_ARG, "no buffer plan set");
   if (n_events) *n_events = 0;
   if (warnings) memset(warnings, 0, sizeof *warnings);
+  {
+    // large uniform images with host event output: pipelined chunks
+    uint64_t off = 0, count = 0;
+    const uint64_t stride = 16ull + 8ull * c->slots;
+    if (parse_header(c, kpft, n_bytes, &off, &count) == WGPF_OK && count &&
+        (n_bytes - off) % stride == 0 && (n_bytes - off) / stride == count &&
+        n_bytes - off > 2 * kChunkBytes && h_events &&
+        !(flags & (WGPF_F_STATS_ONLY | WGPF_F_EXACT_MEAN)) && !c->no_pipeline)
+      return replay_image_chunked(c, kpft, off, count, record_cost, h_events,
+                                  events_cap, flags, n_events, warnings);
+  }
   const uint8_t* d_body = nullptr;
   uint64_t ns = 0;
   int rc = stage_image(c, kpft, n_bytes, &d_body, &ns);
@@ -1305,7 +1443,17 @@ static int read_stats(wgpf_ctx* c, bool event_keys) {
       const uint64_t gs = first[i] >> 25;
       const uint64_t k = (first[i] >> 1) & ((1ull << 24) - 1);
       r.first_event = ~0ull;
-      if (gs >= c->last_stream_base &&
+      if (c->chunk_mode) {  // pipelined replay_image: per-chunk event bases
+        if (gs < c->chunk_nstreams && !c->chunk_sbase.empty()) {
+          const size_t j = (size_t)(std::upper_bound(c->chunk_sbase.begin(),
+                                                     c->chunk_sbase.end(), gs) -
+                                    c->chunk_sbase.begin()) - 1;
+          uint64_t off = 0;
+          CUDA_OK(c, cudaMemcpy(&off, c->d_off_all.as<uint64_t>() + gs, 8,
+                                cudaMemcpyDeviceToHost));
+          r.first_event = c->chunk_ebase[j] + off + k;
+        }
+      } else if (gs >= c->last_stream_base &&
           gs - c->last_stream_base < c->last_n_streams && c->d_offsets.p) {
         uint64_t off = 0;
         CUDA_OK(c, cudaMemcpy(&off,
@@ -1390,6 +1538,7 @@ extern "C" int wgpf_region_stats(wgpf_ctx* c, const wgpf_event* events,
 }
 
 extern "C" uint64_t wgpf_stats_packed_bytes(const wgpf_ctx* c) {
+  if (!c->has_plan) return 0;  // the size depends on the plan's label classes
   return 8ull * ((uint64_t)n_slots(c) * kPackedPerSlot + kSynthHash);
 }
 
@@ -1405,6 +1554,7 @@ extern "C" int wgpf_stats_export(wgpf_ctx* c, void* d_dst) {
 
 extern "C" int wgpf_stats_merge(wgpf_ctx* c, const void* d_gathered,
                                 uint32_t n_ranks) {
+  c->chunk_mode = false;
   int rc = stats_reset(c);
   if (rc) return rc;
   rc = status_reset(c);

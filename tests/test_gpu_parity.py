@@ -331,6 +331,35 @@ def test_stats_only_equals_materialized(ctx, oracle, n):
                 s.count, s.sum, s.min, s.max, s.hist), k
 
 
+def test_replay_image_pipelined_matches_device(ctx):
+    """Images over 512 MB with host event output take the chunked pipeline
+    (H2D / replay / D2H overlapped over 256 MB chunks): events, warnings and
+    statistics (incl. first-event indices) equal one device-resident replay
+    of the same body; a too-small event buffer reports the full count."""
+    import torch
+    t = T()
+    n = 300000  # 619 MB of config-4 streams: three chunks
+    plan = plan_of(S.CAP, 1, S.MIXED_LABELS)
+    ctx.set_plan(plan)
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), 0, 0, n, n // 3)
+    ne, _ = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0, 0x1)
+    dev_ev = torch.empty(ne * 32, dtype=torch.uint8, device="cuda")
+    ne2, w = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, dev_ev.data_ptr(), ne, 0)
+    assert ne2 == ne
+    whole = ctx.stats()
+    hdr = b"KPFT" + (2).to_bytes(2, "little") + b"\0\0" + n.to_bytes(8, "little")
+    img = hdr + body.cpu().numpy().tobytes()
+    c2 = t.Context(0)
+    r = c2.replay_image_bytes(img, plan, 33, events_cap=7)  # E_BUFFER -> retry
+    assert len(r.events) == ne
+    assert r.events.tobytes() == dev_ev.cpu().numpy().tobytes()
+    assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+            r.malformed_groups) == (w.dropped_heads, w.truncated_tails,
+                                    w.flagged_preconditions, w.malformed_groups)
+    assert c2.stats() == whole
+
+
 def test_stats_merge_two_shards(ctx):
     """Multi-GPU shard-and-reduce on one device: two shards of a body, each
     replayed with its stream_base, stats exported, gathered and merged,
@@ -346,13 +375,15 @@ def test_stats_merge_two_shards(ctx):
     ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0, 0x1)
     whole = ctx.stats()
     parts = [t.Context(0), t.Context(0)]
+    assert parts[0].stats_packed_bytes() == 0  # size needs the plan
+    for c in parts:
+        c.set_plan(plan)
     pb = parts[0].stats_packed_bytes()
     gathered = torch.zeros(2 * pb, dtype=torch.uint8, device="cuda")
     cut = 17003
     stride = S.stream_stride()
     for r, (a, b) in enumerate([(0, cut), (cut, n)]):
         c = parts[r]
-        c.set_plan(plan)
         c.replay_device(body.data_ptr() + a * stride, (b - a) * stride, b - a, 33,
                         0, 0, 0x1, stream_base=a)
         c.stats_export(gathered.data_ptr() + r * pb)

@@ -29,22 +29,23 @@
 // duration reaches 2^32 is an error, so every emitted duration fits); errors
 // are recorded per lane and handled after the stream (the stack depth stays
 // within pass 1's bound whatever the regions, so a lane can keep going).
-// Histograms: per-warp tables, one shared atomic per event.
+// Histograms: one per-CTA table, one shared atomic per event.
 #pragma once
 
 #include "k_fast.cuh"
 
 namespace wgpf {
 
-constexpr uint32_t kTpsMaxWarps = 8;                  // warps per CTA (<=)
+constexpr uint32_t kTpsMaxWarps = 12;                 // warps per CTA (<=)
 constexpr uint32_t kTpsW = 8;                         // records per window
 constexpr uint32_t kTpsChunks = (kTpsW + 2) / 2;      // 16-B chunks per window
 constexpr uint32_t kTpsPitch = 16 * kTpsChunks;       // bytes per lane window
-constexpr uint32_t kTpsDepth = 16;                    // stack entries per lane
+constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
 constexpr uint32_t kTpsClasses = 16;                  // dense classes held
-constexpr uint32_t kTpsRing = 8;                      // events per lane ring
+constexpr uint32_t kTpsRing = 4;                      // events per lane ring
 constexpr uint32_t kTpsRingPitch = 32 * kTpsRing + 16;  // padded: no conflicts
+constexpr uint32_t kTpsFlushEv = 2;                   // events per flush run
 constexpr uint32_t kTpsMaxSlots = 2046;               // pos / hi in 11+15 bits
 
 struct TpsWarpSmem {
@@ -61,35 +62,36 @@ struct TpsCtaSmem {
 };
 
 // Per-warp dynamic tables (R = region ids in use, K = classes):
-//   cnt  u16 [R][32]          iteration counters
-//   a    uint4 [K][32]        {count, min, max, sum lo} per class and lane
-//   hi   u32 [K][32]          sum hi
-//   first u64 [K][32]         first-event key
-//   hist u32 [K][64]          per-warp histogram
+//   a     uint4 [K][32]       {count, min, max, sum lo} per class and lane
+//   hi    u32 [K][32]         sum hi
+//   first u64 [K]             first-event key (per warp: shared atomicMin
+//                             when a lane meets a class for the first time)
+//   cnt   u16 [R][32]         iteration counters
+// and per CTA hist u32 [K][64].
 struct TpsTables {
-  uint16_t* cnt;
   uint4* a;
   uint32_t* hi;
   unsigned long long* first;
-  uint32_t* hist;
+  uint16_t* cnt;
 };
 
 __host__ __device__ inline size_t tps_align(size_t b) { return (b + 127) & ~size_t(127); }
 __host__ __device__ inline size_t tps_tables_bytes(uint32_t K, uint32_t R) {
-  return tps_align((size_t)R * 64 + (size_t)K * 32 * (16 + 4 + 8) +
-                   (size_t)K * WGPF_HIST_BINS * 4);
+  return tps_align((size_t)K * 32 * 20 + (size_t)K * 8 + (size_t)R * 64);
 }
 __host__ __device__ inline TpsTables tps_tables(uint8_t* p, uint32_t K, uint32_t R) {
   TpsTables t;
   t.a = reinterpret_cast<uint4*>(p);
-  t.first = reinterpret_cast<unsigned long long*>(p + (size_t)K * 32 * 16);
-  t.hi = reinterpret_cast<uint32_t*>(p + (size_t)K * 32 * 24);
-  t.hist = reinterpret_cast<uint32_t*>(p + (size_t)K * 32 * 28);
-  t.cnt = reinterpret_cast<uint16_t*>(p + (size_t)K * 32 * 28 + (size_t)K * WGPF_HIST_BINS * 4);
+  t.hi = reinterpret_cast<uint32_t*>(p + (size_t)K * 32 * 16);
+  t.first = reinterpret_cast<unsigned long long*>(p + (size_t)K * 32 * 20);
+  t.cnt = reinterpret_cast<uint16_t*>(p + (size_t)K * 32 * 20 + (size_t)K * 8);
   return t;
 }
+__host__ __device__ inline size_t tps_hist_bytes(uint32_t K) {
+  return tps_align((size_t)K * WGPF_HIST_BINS * 4);
+}
 __host__ inline size_t tps_smem_bytes(uint32_t K, uint32_t R, uint32_t warps) {
-  return tps_align(sizeof(TpsCtaSmem)) +
+  return tps_align(sizeof(TpsCtaSmem)) + tps_hist_bytes(K) +
          warps * (tps_align(sizeof(TpsWarpSmem)) + tps_tables_bytes(K, R));
 }
 // warps per CTA that fit the shared memory of one SM (one CTA per SM)
@@ -120,19 +122,19 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint32_t nw = blockDim.x >> 5;
   const uint32_t K = a.plan.K;
   const uint32_t R = a.tps_regions;
-  TpsWarpSmem& ws = *reinterpret_cast<TpsWarpSmem*>(
-      smem_raw + tps_align(sizeof(TpsCtaSmem)) + w * tps_align(sizeof(TpsWarpSmem)));
-  uint8_t* const tb0 = smem_raw + tps_align(sizeof(TpsCtaSmem)) +
-                       nw * tps_align(sizeof(TpsWarpSmem));
+  uint32_t* const hist = reinterpret_cast<uint32_t*>(smem_raw + tps_align(sizeof(TpsCtaSmem)));
+  uint8_t* const wbase0 = smem_raw + tps_align(sizeof(TpsCtaSmem)) + tps_hist_bytes(K);
+  TpsWarpSmem& ws = *reinterpret_cast<TpsWarpSmem*>(wbase0 + w * tps_align(sizeof(TpsWarpSmem)));
+  uint8_t* const tb0 = wbase0 + nw * tps_align(sizeof(TpsWarpSmem));
   const TpsTables tb = tps_tables(tb0 + w * tps_tables_bytes(K, R), K, R);
   const bool stats = !a.no_stats;
   const bool emit = a.events != nullptr;
   for (uint32_t c = 0; c < K; ++c) {
     tb.a[c * 32 + lane] = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
     tb.hi[c * 32 + lane] = 0;
-    tb.first[c * 32 + lane] = ~0ull;
   }
-  for (uint32_t i = lane; i < K * WGPF_HIST_BINS; i += 32) tb.hist[i] = 0;
+  for (uint32_t c = lane; c < K; c += 32) tb.first[c] = ~0ull;
+  for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x) hist[i] = 0;
   for (uint32_t r = threadIdx.x; r < kTpsRegions; r += blockDim.x) {
     uint32_t inf = 0xFFFFFFFFu;
     if (r < a.fast_regions) {
@@ -232,26 +234,28 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     uint32_t mm_pos = 0xFFFFFFFFu;  // first END breaking single-stack nesting
     uint32_t tl_pos = 0xFFFFFFFFu;  // first END whose pair reaches 2^32
 
-    // warp-cooperative write of the rings: lanes with >= 4 unwritten events
-    // (fin: any); 8 lanes per source lane, 16 B each
+    // warp-cooperative write of the rings: lanes with >= kTpsFlushEv
+    // unwritten events (fin: any); 2 * kTpsFlushEv lanes per source lane,
+    // 16 B each
+    constexpr uint32_t LPS = 2 * kTpsFlushEv;  // lanes per source
     auto flush = [&](bool fin) {
       const uint32_t pend = kw - kf;
-      const bool need = fin ? pend != 0 : pend >= 4u;
+      const bool need = fin ? pend != 0 : pend >= kTpsFlushEv;
       const uint32_t m = __ballot_sync(FULL, need);
       if (!m) return;
-      const uint32_t cw = pend < 4u ? pend : 4u;
+      const uint32_t cw = pend < kTpsFlushEv ? pend : kTpsFlushEv;
       if (need) ws.fl[__popc(m & lt)] = (uint8_t)lane;
       __syncwarp();
       const uint32_t nf = __popc(m);
       const uint64_t my_idx = off + kf;
-      for (uint32_t q = 0; q < nf; q += 4) {
-        const uint32_t g = q + (lane >> 3);
+      for (uint32_t q = 0; q < nf; q += 32 / LPS) {
+        const uint32_t g = q + lane / LPS;
         const uint32_t src = ws.fl[g < nf ? g : q];
         const uint32_t ilo = __shfl_sync(FULL, (uint32_t)my_idx, src);
         const uint32_t ihi = __shfl_sync(FULL, (uint32_t)(my_idx >> 32), src);
         const uint32_t kfs = __shfl_sync(FULL, kf, src);
         const uint32_t cws = __shfl_sync(FULL, cw, src);
-        const uint32_t ev = (lane & 7u) >> 1;
+        const uint32_t ev = (lane % LPS) >> 1;
         if (g < nf && ev < cws) {
           const uint64_t idx = (((uint64_t)ihi << 32) | ilo) + ev;
           const uint4 val = *reinterpret_cast<const uint4*>(
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     auto lstat = [&](uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
       uint4* e = tb.a + cls * 32 + lane;
       uint4 x = *e;
-      if (x.x == 0) tb.first[cls * 32 + lane] = gkey | (kpos << 1) | kind;
+      if (x.x == 0) atomicMin(&tb.first[cls], gkey | (kpos << 1) | kind);
       x.x += 1;
       x.y = min(x.y, d);
       x.z = max(x.z, d);
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       if (sm < d) tb.hi[cls * 32 + lane] += 1;
       x.w = sm;
       *e = x;
-      atomicAdd(&tb.hist[cls * WGPF_HIST_BINS + hist_bin(d)], 1u);
+      atomicAdd(&hist[cls * WGPF_HIST_BINS + hist_bin(d)], 1u);
     };
     auto step = [&](uint32_t i, uint2 r2) {
       const bool valid = i < n;
@@ -372,10 +376,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       __syncwarp();
       const uint2* myrec = reinterpret_cast<const uint2*>(myrec0 + bsel * (32 * kTpsPitch));
 #pragma unroll
-      for (uint32_t j = 0; j < kTpsW; j += 2) {
+      for (uint32_t j = 0; j < kTpsW; ++j) {
         step(w0 + j, myrec[j]);
-        step(w0 + j + 1, myrec[j + 1]);
-        if (emit) flush(false);  // <= 7 pending: fits the ring
+        if (emit) flush(false);  // <= 1 + 2 pending: fits the ring
       }
       __syncwarp();
     }
@@ -430,9 +433,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
           ((unsigned long long)tb.hi[c * 32 + lane] << 32) | x.w);
       const uint32_t mn = __reduce_min_sync(FULL, x.y);
       const uint32_t mx = __reduce_max_sync(FULL, x.z);
-      unsigned long long fk = tb.first[c * 32 + lane];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) fk = min(fk, __shfl_xor_sync(FULL, fk, o));
+      const unsigned long long fk = tb.first[c];
       if (lane == 0) {
         atomicAdd(&a.stats.count[c], cnt);
         atomicAdd(&a.stats.sum[c], sum);
@@ -447,10 +448,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
   if (stats) {  // per-warp histograms -> global
     for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x) {
-      unsigned long long hsum = 0;
-      for (uint32_t ww = 0; ww < nw; ++ww)
-        hsum += tps_tables(tb0 + ww * tps_tables_bytes(K, R), K, R).hist[i];
-      if (hsum) atomicAdd(&a.stats.hist[i], hsum);
+      if (hist[i]) atomicAdd(&a.stats.hist[i], (unsigned long long)hist[i]);
     }
   }
 }

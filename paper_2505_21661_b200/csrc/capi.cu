@@ -566,8 +566,12 @@ static int scan_counts(wgpf_ctx* c, uint64_t n) {
 // Thread-per-stream kernel usable for this plan (even capacity that fits the
 // packed stack entries, label classes that fit the lane-private tables).
 static bool tps_enabled(const wgpf_ctx* c) {
-  return !c->no_tps && c->slots % 2 == 0 && c->slots <= kTpsMaxSlots &&
+  return !c->no_tps && c->slots % 2 == 0 && c->slots && c->slots <= kTpsMaxSlots &&
          c->K <= kTpsClasses && !c->labels.empty();
+}
+// thread-per-stream pass 1: record windows need an even capacity
+static bool count_tps_enabled(const wgpf_ctx* c) {
+  return !c->no_tps && c->slots % 2 == 0 && c->slots && c->slots <= kTpsMaxSlots;
 }
 static uint32_t tps_regions(const wgpf_ctx* c) {
   return std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions);
@@ -816,8 +820,12 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.warp_list = c->d_wlist.as<unsigned long long>();
   ca.warp_len = c->d_glen.as<unsigned long long>() + 1;
   CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 8, c->stream));
-  k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
-                 c->stream>>>(ca);
+  if (count_tps_enabled(c))
+    k_count_tps<<<grid_for(c, (const void*)k_count_tps, kCountWarps * 32, 0),
+                  kCountWarps * 32, 0, c->stream>>>(ca);
+  else
+    k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
+                   c->stream>>>(ca);
   CUDA_OK(c, cudaGetLastError());
   ++c->launches;
   c->mark(1);

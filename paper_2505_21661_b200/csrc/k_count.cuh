@@ -28,6 +28,7 @@
 #pragma once
 
 #include "wgpf_dev.cuh"
+#include "k_window.cuh"
 
 namespace wgpf {
 
@@ -173,6 +174,120 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       const bool general = wide || a.force_general ||
                            max_d > (int32_t)a.max_depth || last_bad > (int64_t)z;
       const bool warp = a.tps_depth != 0 && !general && (tps_out || max_d > (int32_t)a.tps_depth);
+      a.sflag[s] = general ? SF_GENERAL : (warp ? SF_WARP : 0u);
+      if (warp) a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
+    }
+  }
+}
+
+
+// Thread-per-stream pass 1 (same outputs as k_count_fast): lane l of a warp
+// owns stream 32 b + l and walks its records sequentially, windows staged in
+// shared memory (k_window.cuh).  Used when the capacity is even and at most
+// kTpsMaxSlots (the record windows need 16-B chunk alignment).
+constexpr uint32_t kCountWarps = 8;
+
+__global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
+  __shared__ uint8_t marker_region[256];
+  __shared__ __align__(16) uint8_t recbuf[kCountWarps][2 * 32 * kTpsPitch];
+  for (uint32_t r = threadIdx.x; r < 256; r += blockDim.x)
+    marker_region[r] =
+        r < a.fast_regions ? class_is_marker(a.plan, a.plan.class_of[r]) : 0;
+  __syncthreads();
+  const uint32_t FULL = 0xffffffffu;
+  const uint32_t lane = lane_id();
+  const uint32_t w = threadIdx.x >> 5;
+  const uint32_t cap = (uint32_t)a.plan.slots;
+  RecWindows win;
+  win.init(recbuf[w], lane, a.stride, cap);
+  const uint64_t wstep = (uint64_t)gridDim.x * kCountWarps;
+  for (uint64_t b = (uint64_t)blockIdx.x * kCountWarps + w; b * 32 < a.n_streams;
+       b += wstep) {
+    const uint64_t s = b * 32 + lane;
+    const bool live = s < a.n_streams;
+    uint4 h = make_uint4(0u, 0u, 0u, cap);
+    if (live) h = *reinterpret_cast<const uint4*>(a.body + s * a.stride);
+    const uint32_t cnt = h.z, hcap = h.w;
+    // decode_image checks (trace.hpp:227-240)
+    uint32_t code = 0;
+    if (live) {
+      if (hcap != cap)
+        code = DEC_CAP;
+      else if (cnt > hcap)
+        code = a.plan.strategy == WGPF_STRATEGY_FLUSH ? DEC_FLUSH : (hcap == 0 ? DEC_ZERO : 0);
+      if (code) {
+        a.counts[s] = 0;
+        a.zpos[s] = -1;
+        a.sflag[s] = SF_DECODE_ERR;
+        atomicMin(&a.status->decode_err, ((unsigned long long)s << 2) | code);
+        if (code == DEC_CAP) atomicAdd(&a.status->cap_mismatch, 1ull);
+      }
+    }
+    const bool act = live && !code;
+    const uint32_t n = act ? (cnt <= cap ? cnt : cap) : 0u;
+    const uint32_t start = act && cnt > cap ? cnt % cap : 0u;
+    const uint32_t nmax = __reduce_max_sync(FULL, n);
+    if (nmax == 0) {
+      if (act) {
+        a.counts[s] = 0;
+        a.zpos[s] = -1;
+        a.sflag[s] = a.force_general ? SF_GENERAL : 0u;
+      }
+      continue;
+    }
+    win.begin(a.body + b * 32 * a.stride, start, n);
+    const uint2* slots = reinterpret_cast<const uint2*>(a.body + (act ? s : 0) * a.stride + 16);
+    uint32_t t0 = 0, t1 = 0;  // tags of records i, i+1
+    if (n > 0) t0 = slots[start].x;
+    if (n > 1) t1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap].x;
+    win.issue(0, 2);
+    cp_async_commit();
+    int32_t q = 0, run_min = 0, max_d = 0, z = -1, last_bad = -1;
+    uint32_t n_end = 0;
+    bool wide = false, tps_out = false, prev_end = false;
+    for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
+      const uint32_t bsel = (w0 / kTpsW) & 1u;
+      if (w0 + kTpsW < nmax) win.issue(bsel ^ 1u, w0 + kTpsW + 2u);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncwarp();
+      const uint2* rec = win.lane_records(bsel, lane, start);
+#pragma unroll
+      for (uint32_t j = 0; j < kTpsW; ++j) {
+        const uint32_t t2 = rec[j].x;
+        const uint32_t i = w0 + j;
+        const bool valid = i < n;
+        const bool isS = (int32_t)t0 < 0;
+        const bool st = valid && isS;
+        const bool en = valid && !isS;
+        const uint32_t rid = (t0 >> 12) & (WGPF_MAX_REGIONS - 1u);
+        wide |= valid && rid >= a.fast_regions;
+        tps_out |= valid && rid >= a.tps_regions;
+        q += st ? 1 : (en ? -1 : 0);
+        run_min = min(run_min, q);
+        const int32_t d = q - run_min;
+        z = (valid && d == 0) ? (int32_t)i : z;
+        max_d = max(max_d, d);
+        n_end += en ? 1u : 0u;
+        // a wait-marker START right after an END that the next record does
+        // not close: only z can tell whether it is ever closed
+        const bool mk_start = st && prev_end && rid < a.fast_regions && marker_region[rid & 255u];
+        const bool closed_next = i + 1 < n && (int32_t)t1 >= 0 &&
+                                 ((t1 >> 12) & (WGPF_MAX_REGIONS - 1u)) == rid;
+        last_bad = (mk_start && !closed_next) ? (int32_t)i : last_bad;
+        prev_end = en;
+        t0 = t1;
+        t1 = t2;
+      }
+      __syncwarp();
+    }
+    if (act) {
+      a.counts[s] = n_end - (uint32_t)(-run_min);
+      a.zpos[s] = z;
+      const bool general = wide || a.force_general || max_d > (int32_t)a.max_depth ||
+                           last_bad > z;
+      const bool warp = a.tps_depth != 0 && !general &&
+                        (tps_out || max_d > (int32_t)a.tps_depth);
       a.sflag[s] = general ? SF_GENERAL : (warp ? SF_WARP : 0u);
       if (warp) a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
     }

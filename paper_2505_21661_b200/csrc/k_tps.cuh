@@ -13,16 +13,16 @@
 //       (exact recount); durations >= 2^32 -> pair error (trace.hpp:330-336).
 //   replay (trace.hpp:398-487)          sync correction, wait markers decided
 //       with the look-ahead records i+1, i+2 and pass 1's z, orphans last.
-//   region_stats (pipeline.hpp:114-133) lane-private count / min / max / sum /
-//       first key per class in shared memory (no atomics), histogram through
-//       match.any groups and one shared atomic per group.
+//   region_stats (pipeline.hpp:114-133) lane-private count / min / max / sum
+//       per class in shared memory (no atomics); the first-event key per warp
+//       (a shared atomicMin when a lane meets a class for the first time).
 //
 // Data movement.  Records: the warp stages 8-record windows of its 32 streams
 // in shared memory with cp.async (16-B chunks, double buffered; chunk k of the
 // window of stream l is copied by a fixed lane, so one instruction covers a
-// few contiguous lines).  Events: each lane stages its events in an 8-event
-// ring in shared memory; whenever lanes hold 4 unwritten events the warp
-// writes them cooperatively, 8 lanes per 128-B run, i.e. 4 runs per 16-B-per-
+// few contiguous lines).  Events: each lane stages its events in a 4-event
+// ring in shared memory; whenever lanes hold 2 unwritten events the warp
+// writes them cooperatively, 4 lanes per 64-B run, i.e. 8 runs per 16-B-per-
 // lane store instruction (coalesced, full sectors).  (Per-lane TMA bulk
 // stores serialise: the bulk-copy instruction takes uniform operands.)
 // The step is written predicated with 32-bit timing arithmetic (a pair whose
@@ -33,20 +33,17 @@
 #pragma once
 
 #include "k_fast.cuh"
+#include "k_window.cuh"
 
 namespace wgpf {
 
 constexpr uint32_t kTpsMaxWarps = 12;                 // warps per CTA (<=)
-constexpr uint32_t kTpsW = 8;                         // records per window
-constexpr uint32_t kTpsChunks = (kTpsW + 2) / 2;      // 16-B chunks per window
-constexpr uint32_t kTpsPitch = 16 * kTpsChunks;       // bytes per lane window
 constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
 constexpr uint32_t kTpsClasses = 16;                  // dense classes held
 constexpr uint32_t kTpsRing = 4;                      // events per lane ring
 constexpr uint32_t kTpsRingPitch = 32 * kTpsRing + 16;  // padded: no conflicts
 constexpr uint32_t kTpsFlushEv = 2;                   // events per flush run
-constexpr uint32_t kTpsMaxSlots = 2046;               // pos / hi in 11+15 bits
 
 struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
@@ -101,19 +98,6 @@ __host__ inline uint32_t tps_warps(uint32_t K, uint32_t R, size_t smem_limit) {
   return w;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait1() {
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
-}
-
 __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TpsCtaSmem& cs = *reinterpret_cast<TpsCtaSmem*>(smem_raw);
@@ -155,15 +139,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
   uint8_t* const ring = ws.ring + lane * kTpsRingPitch;
 
-  // static chunk assignment of the record windows: chunk k of this lane is
-  // part pk of stream lane slk
-  uint32_t slk[kTpsChunks], pk[kTpsChunks];
-#pragma unroll
-  for (uint32_t k = 0; k < kTpsChunks; ++k) {
-    const uint32_t q = k * 32 + lane;
-    slk[k] = q / kTpsChunks;
-    pk[k] = q - slk[k] * kTpsChunks;
-  }
+  RecWindows win;
+  win.init(ws.rec[0], lane, a.stride, cap);
 
   const uint64_t wstep = (uint64_t)gridDim.x * nw;
   for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b * 32 < a.n_streams;
@@ -191,38 +168,13 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
     for (uint32_t r = 0; r < R; ++r) tb.cnt[r * 32 + lane] = 0;
 
-    // window sources: physical (even) slot of chunk k, first window c0 = 2
-    uint32_t wp[kTpsChunks], wlim[kTpsChunks];
-#pragma unroll
-    for (uint32_t k = 0; k < kTpsChunks; ++k) {
-      const uint32_t st_k = __shfl_sync(FULL, start, slk[k]);
-      wlim[k] = __shfl_sync(FULL, n, slk[k]);
-      uint32_t p = st_k + 2u;
-      if (p >= cap) p -= cap;
-      p = (p & ~1u) + 2u * pk[k];
-      if (p >= cap) p -= cap;
-      wp[k] = p;
-    }
-    const uint8_t* wbase = a.body + b * 32 * a.stride + 16;
-    auto issue = [&](uint32_t bsel, uint32_t c0) {
-      uint8_t* dst = ws.rec[bsel];
-#pragma unroll
-      for (uint32_t k = 0; k < kTpsChunks; ++k) {
-        if (c0 < wlim[k])
-          cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k],
-                     wbase + (uint64_t)slk[k] * a.stride + 8ull * wp[k]);
-        wp[k] += kTpsW;
-        if (wp[k] >= cap) wp[k] -= cap;
-      }
-    };
-    const uint32_t shift = start & 1u;
-    const uint8_t* myrec0 = ws.rec[0] + lane * kTpsPitch + 8u * shift;
+    win.begin(a.body + b * 32 * a.stride, start, n);
 
     uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
     if (n > 0) r0 = slots[start];
     if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
     uint32_t inf0 = cs.info[(r0.x >> 12) & (kTpsRegions - 1u)];
-    issue(0, 2);
+    win.issue(0, 2);
     cp_async_commit();
 
     uint32_t hi = 0, vprev = 0, sp = 0;
@@ -370,11 +322,11 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
 
     for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
       const uint32_t bsel = (w0 / kTpsW) & 1u;
-      if (w0 + kTpsW < nmax) issue(bsel ^ 1u, w0 + kTpsW + 2u);
+      if (w0 + kTpsW < nmax) win.issue(bsel ^ 1u, w0 + kTpsW + 2u);
       cp_async_commit();
       cp_async_wait1();
       __syncwarp();
-      const uint2* myrec = reinterpret_cast<const uint2*>(myrec0 + bsel * (32 * kTpsPitch));
+      const uint2* myrec = win.lane_records(bsel, lane, start);
 #pragma unroll
       for (uint32_t j = 0; j < kTpsW; ++j) {
         step(w0 + j, myrec[j]);

@@ -1,0 +1,96 @@
+// k_window.cuh -- record windows of the thread-per-stream kernels (k_tps,
+// k_count_tps): a warp owns 32 consecutive streams (lane l = stream l) and
+// walks them in lockstep over chronological positions.  Records reach shared
+// memory in windows of kTpsW positions per stream, double buffered, with
+// cp.async 16-B chunks.  Chunk k of the window of stream l is copied by a
+// fixed lane (q = k * 32 + lane -> stream q / kTpsChunks, part q % kTpsChunks),
+// so one copy instruction covers a few contiguous runs of the body.
+//
+// Circular streams start at physical slot `start` (trace.hpp:243-246); a
+// window for chronological position c0 starts at the even physical slot at or
+// below (start + c0) mod cap, so 16-B chunks never straddle the wrap (the
+// capacity is even on this path) and the lane reads its records at offset
+// (start & 1) in its window.
+#pragma once
+
+#include "wgpf_dev.cuh"
+
+namespace wgpf {
+
+constexpr uint32_t kTpsW = 8;                         // records per window
+constexpr uint32_t kTpsChunks = (kTpsW + 2) / 2;      // 16-B chunks per window
+constexpr uint32_t kTpsPitch = 16 * kTpsChunks;       // bytes per lane window
+constexpr uint32_t kTpsMaxSlots = 2046;               // even; pos fits 11 bits
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait1() {
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+}
+
+struct RecWindows {
+  uint32_t slk[kTpsChunks], pk[kTpsChunks];  // static chunk assignment
+  uint32_t wp[kTpsChunks], wlim[kTpsChunks]; // physical slot, stream length
+  const uint8_t* wbase;                      // slots of the warp's stream 0
+  uint64_t stride;
+  uint32_t cap;
+  uint8_t* buf;                              // [2][32 * kTpsPitch]
+
+  __device__ __forceinline__ void init(uint8_t* smem, uint32_t lane,
+                                       uint64_t stride_, uint32_t cap_) {
+    buf = smem;
+    stride = stride_;
+    cap = cap_;
+#pragma unroll
+    for (uint32_t k = 0; k < kTpsChunks; ++k) {
+      const uint32_t q = k * 32 + lane;
+      slk[k] = q / kTpsChunks;
+      pk[k] = q - slk[k] * kTpsChunks;
+    }
+  }
+  // streams of this batch: body of the warp's first stream, this lane's
+  // stream start slot and length; first window at c0 = 2 (records 0 and 1
+  // are loaded directly)
+  __device__ __forceinline__ void begin(const uint8_t* batch_body,
+                                        uint32_t start, uint32_t n) {
+    wbase = batch_body + 16;
+#pragma unroll
+    for (uint32_t k = 0; k < kTpsChunks; ++k) {
+      const uint32_t st_k = __shfl_sync(0xffffffffu, start, slk[k]);
+      wlim[k] = __shfl_sync(0xffffffffu, n, slk[k]);
+      uint32_t p = st_k + 2u;
+      if (p >= cap) p -= cap;
+      p = (p & ~1u) + 2u * pk[k];
+      if (p >= cap) p -= cap;
+      wp[k] = p;
+    }
+  }
+  // copy the window of chronological positions [c0, c0 + kTpsW) of all 32
+  // streams into buffer bsel (windows are issued in order, c0 += kTpsW)
+  __device__ __forceinline__ void issue(uint32_t bsel, uint32_t c0) {
+    uint8_t* dst = buf + bsel * (32 * kTpsPitch);
+#pragma unroll
+    for (uint32_t k = 0; k < kTpsChunks; ++k) {
+      if (c0 < wlim[k])
+        cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k],
+                   wbase + (uint64_t)slk[k] * stride + 8ull * wp[k]);
+      wp[k] += kTpsW;
+      if (wp[k] >= cap) wp[k] -= cap;
+    }
+  }
+  // this lane's records in buffer bsel
+  __device__ __forceinline__ const uint2* lane_records(uint32_t bsel, uint32_t lane,
+                                                       uint32_t start) const {
+    return reinterpret_cast<const uint2*>(buf + bsel * (32 * kTpsPitch) +
+                                          lane * kTpsPitch + 8u * (start & 1u));
+  }
+};
+
+}  // namespace wgpf

@@ -98,6 +98,9 @@ __host__ inline uint32_t tps_warps(uint32_t K, uint32_t R, size_t smem_limit) {
   return w;
 }
 
+// kEmit: events materialised; kStats: statistics; kDirect: each lane stores
+// its events straight to HBM (no ring / cooperative flush; A/B variant).
+template <bool kEmit, bool kStats, bool kDirect>
 __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TpsCtaSmem& cs = *reinterpret_cast<TpsCtaSmem*>(smem_raw);
@@ -111,8 +114,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   TpsWarpSmem& ws = *reinterpret_cast<TpsWarpSmem*>(wbase0 + w * tps_align(sizeof(TpsWarpSmem)));
   uint8_t* const tb0 = wbase0 + nw * tps_align(sizeof(TpsWarpSmem));
   const TpsTables tb = tps_tables(tb0 + w * tps_tables_bytes(K, R), K, R);
-  const bool stats = !a.no_stats;
-  const bool emit = a.events != nullptr;
+  constexpr bool stats = kStats;
+  constexpr bool emit = kEmit;
   for (uint32_t c = 0; c < K; ++c) {
     tb.a[c * 32 + lane] = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
     tb.hi[c * 32 + lane] = 0;
@@ -191,6 +194,10 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     // 16 B each
     constexpr uint32_t LPS = 2 * kTpsFlushEv;  // lanes per source
     auto flush = [&](bool fin) {
+      if constexpr (kDirect) {
+        kf = kw;
+        return;
+      }
       const uint32_t pend = kw - kf;
       const bool need = fin ? pend != 0 : pend >= kTpsFlushEv;
       const uint32_t m = __ballot_sync(FULL, need);
@@ -224,9 +231,20 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     };
     auto put = [&](uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo, uint32_t ehi,
                    uint32_t region, uint32_t it) {
-      uint4* p = reinterpret_cast<uint4*>(ring + (k & (kTpsRing - 1u)) * 32u);
-      p[0] = make_uint4(slo, shi, elo, ehi);
-      p[1] = make_uint4(region, it, blk, wg);
+      if constexpr (kDirect) {
+        const uint64_t idx = off + k;
+        if (idx < a.events_cap) {
+          uint4* p = reinterpret_cast<uint4*>(a.events + idx);
+          p[0] = make_uint4(slo, shi, elo, ehi);
+          p[1] = make_uint4(region, it, blk, wg);
+        } else {
+          atomicAdd(&a.status->overflow, 1ull);
+        }
+      } else {
+        uint4* p = reinterpret_cast<uint4*>(ring + (k & (kTpsRing - 1u)) * 32u);
+        p[0] = make_uint4(slo, shi, elo, ehi);
+        p[1] = make_uint4(region, it, blk, wg);
+      }
     };
     auto lstat = [&](uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
       uint4* e = tb.a + cls * 32 + lane;
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       if (sm < d) tb.hi[cls * 32 + lane] += 1;
       x.w = sm;
       *e = x;
-      atomicAdd(&hist[cls * WGPF_HIST_BINS + hist_bin(d)], 1u);
+      atomicAdd(&hist[cls * WGPF_HIST_BINS + hist_bin32(d)], 1u);
     };
     auto step = [&](uint32_t i, uint2 r2) {
       const bool valid = i < n;
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool corr_w = wd > cost;
       w_flag += (consumed && !corr_w) ? 1u : 0u;
       const uint32_t kpos = kw;
-      if (emit) {
+      if constexpr (emit) {
         if (base) {
           const uint32_t elo = e.x + corr;
           put(kw, e.x, shi, elo, shi + (elo < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED, it);
@@ -311,7 +329,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
         }
         ++n_orph;
       }
-      if (stats) {
+      if constexpr (stats) {
         if (base) lstat(inf & 0xFFu, corr, kpos, 0u);
         if (consumed) lstat(i1 & 0xFFu, wd, kpos + 1u, 1u);
       }
@@ -330,7 +348,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
 #pragma unroll
       for (uint32_t j = 0; j < kTpsW; ++j) {
         step(w0 + j, myrec[j]);
-        if (emit) flush(false);  // <= 1 + 2 pending: fits the ring
+        if constexpr (emit) flush(false);  // <= 1 + 2 pending: fits the ring
       }
       __syncwarp();
     }

@@ -84,6 +84,13 @@ __device__ inline uint32_t hist_bin(uint64_t d) {
   return b < WGPF_HIST_BINS ? b : WGPF_HIST_BINS - 1u;
 }
 
+// hist_bin for durations below 2^32 (bin <= 63 without clamping)
+__device__ __forceinline__ uint32_t hist_bin32(uint32_t d) {
+  if (d < 4u) return d;
+  const uint32_t k = 31u - (uint32_t)__clz(d);
+  return 2u * k + ((d >> (k - 1u)) & 1u);
+}
+
 // Slot of a class in the stats arrays (inserting synthetic classes).
 __device__ inline int stats_slot(const DevStats& st, uint32_t cls,
                                  unsigned long long* overflow) {

@@ -75,13 +75,10 @@ struct DevBuf {
 }  // namespace
 
 using TpsKernel = void (*)(FastArgs);
-static TpsKernel tps_kernel(bool emit, bool stats, bool direct) {
-  static const TpsKernel k[8] = {
-      k_tps<false, false, false>, k_tps<true, false, false>,
-      k_tps<false, true, false>,  k_tps<true, true, false>,
-      k_tps<false, false, true>,  k_tps<true, false, true>,
-      k_tps<false, true, true>,   k_tps<true, true, true>};
-  return k[(emit ? 1 : 0) | (stats ? 2 : 0) | (direct ? 4 : 0)];
+static TpsKernel tps_kernel(bool emit, bool stats) {
+  static const TpsKernel k[4] = {k_tps<false, false>, k_tps<true, false>,
+                                 k_tps<false, true>, k_tps<true, true>};
+  return k[(emit ? 1 : 0) | (stats ? 2 : 0)];
 }
 
 struct wgpf_ctx {
@@ -120,7 +117,6 @@ struct wgpf_ctx {
   bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
   bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
-  bool tps_direct = getenv("WGPF_TPS_DIRECT") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   size_t smem_optin = 0;
   // pipelined replay_image (host buffers): copy streams, chunk buffers, and
@@ -326,8 +322,8 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     c->smem_optin = (size_t)optin;
-    for (int v = 0; v < 8; ++v)
-      cudaFuncSetAttribute(tps_kernel(v & 1, v & 2, v & 4),
+    for (int v = 0; v < 4; ++v)
+      cudaFuncSetAttribute(tps_kernel(v & 1, v & 2),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   }
   cudaFuncSetAttribute(k_fast_emit<false>,
@@ -630,8 +626,7 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
     // shallow streams: thread per stream; then the SF_WARP list
     const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
     const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
-    tps_kernel(events != nullptr, !no_stats, c->tps_direct)<<<c->sms, tw * 32, tsm,
-                                                              c->stream>>>(f);
+    tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f);
     CUDA_OK(c, cudaGetLastError());
     ++c->launches;
     f.list = c->d_wlist.as<unsigned long long>();

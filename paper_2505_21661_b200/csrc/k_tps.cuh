@@ -20,11 +20,13 @@
 // Data movement.  Records: the warp stages 8-record windows of its 32 streams
 // in shared memory with cp.async (16-B chunks, double buffered; chunk k of the
 // window of stream l is copied by a fixed lane, so one instruction covers a
-// few contiguous lines).  Events: each lane stages its events in a 4-event
-// ring in shared memory; whenever lanes hold 2 unwritten events the warp
-// writes them cooperatively, 4 lanes per 64-B run, i.e. 8 runs per 16-B-per-
-// lane store instruction (coalesced, full sectors).  (Per-lane TMA bulk
-// stores serialise: the bulk-copy instruction takes uniform operands.)
+// few contiguous lines).  Events: each lane stores its 32-B events straight
+// to HBM (two 16-B stores, full sectors; a stream's events are contiguous, so
+// L2 completes each line before write-back).  Measured against staging the
+// events in shared-memory rings with a warp-cooperative coalesced flush, the
+// direct stores are faster (the flush costs more issue slots than the
+// scattered stores cost the LSU), and per-lane TMA bulk stores serialise (the
+// bulk-copy instruction takes uniform operands).
 // The step is written predicated with 32-bit timing arithmetic (a pair whose
 // duration reaches 2^32 is an error, so every emitted duration fits); errors
 // are recorded per lane and handled after the stream (the stack depth stays
@@ -37,20 +39,15 @@
 
 namespace wgpf {
 
-constexpr uint32_t kTpsMaxWarps = 12;                 // warps per CTA (<=)
+constexpr uint32_t kTpsMaxWarps = 16;                 // warps per CTA (<=)
 constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
 constexpr uint32_t kTpsClasses = 16;                  // dense classes held
-constexpr uint32_t kTpsRing = 4;                      // events per lane ring
-constexpr uint32_t kTpsRingPitch = 32 * kTpsRing + 16;  // padded: no conflicts
-constexpr uint32_t kTpsFlushEv = 2;                   // events per flush run
 
 struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
-  uint8_t ring[32 * kTpsRingPitch];  // event rings
   uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<11 | cons<<16 | hi<<17}
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
-  uint8_t fl[32];                    // lanes being flushed
 };
 
 struct TpsCtaSmem {
@@ -98,9 +95,8 @@ __host__ inline uint32_t tps_warps(uint32_t K, uint32_t R, size_t smem_limit) {
   return w;
 }
 
-// kEmit: events materialised; kStats: statistics; kDirect: each lane stores
-// its events straight to HBM (no ring / cooperative flush; A/B variant).
-template <bool kEmit, bool kStats, bool kDirect>
+// kEmit: events materialised; kStats: statistics.
+template <bool kEmit, bool kStats>
 __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TpsCtaSmem& cs = *reinterpret_cast<TpsCtaSmem*>(smem_raw);
@@ -140,7 +136,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint32_t cost = (uint32_t)a.record_cost;  // host: < 2^32 on this path
   const uint32_t cap = a.cap;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
-  uint8_t* const ring = ws.ring + lane * kTpsRingPitch;
 
   RecWindows win;
   win.init(ws.rec[0], lane, a.stride, cap);
@@ -183,67 +178,20 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     uint32_t hi = 0, vprev = 0, sp = 0;
     uint32_t pw = 0xFFu;  // wait class of the previous record if it was a
                           // matched base END, else none
-    uint32_t kw = 0;      // events of this stream staged
-    uint32_t kf = 0;      //   of which written
+    uint32_t kw = 0;      // events of this stream written
     uint32_t n_orph = 0;
     uint32_t mm_pos = 0xFFFFFFFFu;  // first END breaking single-stack nesting
     uint32_t tl_pos = 0xFFFFFFFFu;  // first END whose pair reaches 2^32
 
-    // warp-cooperative write of the rings: lanes with >= kTpsFlushEv
-    // unwritten events (fin: any); 2 * kTpsFlushEv lanes per source lane,
-    // 16 B each
-    constexpr uint32_t LPS = 2 * kTpsFlushEv;  // lanes per source
-    auto flush = [&](bool fin) {
-      if constexpr (kDirect) {
-        kf = kw;
-        return;
-      }
-      const uint32_t pend = kw - kf;
-      const bool need = fin ? pend != 0 : pend >= kTpsFlushEv;
-      const uint32_t m = __ballot_sync(FULL, need);
-      if (!m) return;
-      const uint32_t cw = pend < kTpsFlushEv ? pend : kTpsFlushEv;
-      if (need) ws.fl[__popc(m & lt)] = (uint8_t)lane;
-      __syncwarp();
-      const uint32_t nf = __popc(m);
-      const uint64_t my_idx = off + kf;
-      for (uint32_t q = 0; q < nf; q += 32 / LPS) {
-        const uint32_t g = q + lane / LPS;
-        const uint32_t src = ws.fl[g < nf ? g : q];
-        const uint32_t ilo = __shfl_sync(FULL, (uint32_t)my_idx, src);
-        const uint32_t ihi = __shfl_sync(FULL, (uint32_t)(my_idx >> 32), src);
-        const uint32_t kfs = __shfl_sync(FULL, kf, src);
-        const uint32_t cws = __shfl_sync(FULL, cw, src);
-        const uint32_t ev = (lane % LPS) >> 1;
-        if (g < nf && ev < cws) {
-          const uint64_t idx = (((uint64_t)ihi << 32) | ilo) + ev;
-          const uint4 val = *reinterpret_cast<const uint4*>(
-              ws.ring + src * kTpsRingPitch + ((kfs + ev) & (kTpsRing - 1u)) * 32u +
-              (lane & 1u) * 16u);
-          if (idx < a.events_cap)
-            reinterpret_cast<uint4*>(a.events + idx)[lane & 1u] = val;
-          else if (!(lane & 1u))
-            atomicAdd(&a.status->overflow, 1ull);
-        }
-      }
-      __syncwarp();
-      if (need) kf += cw;
-    };
     auto put = [&](uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo, uint32_t ehi,
                    uint32_t region, uint32_t it) {
-      if constexpr (kDirect) {
-        const uint64_t idx = off + k;
-        if (idx < a.events_cap) {
-          uint4* p = reinterpret_cast<uint4*>(a.events + idx);
-          p[0] = make_uint4(slo, shi, elo, ehi);
-          p[1] = make_uint4(region, it, blk, wg);
-        } else {
-          atomicAdd(&a.status->overflow, 1ull);
-        }
-      } else {
-        uint4* p = reinterpret_cast<uint4*>(ring + (k & (kTpsRing - 1u)) * 32u);
+      const uint64_t idx = off + k;
+      if (idx < a.events_cap) {
+        uint4* p = reinterpret_cast<uint4*>(a.events + idx);
         p[0] = make_uint4(slo, shi, elo, ehi);
         p[1] = make_uint4(region, it, blk, wg);
+      } else {
+        atomicAdd(&a.status->overflow, 1ull);
       }
     };
     auto lstat = [&](uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
@@ -348,7 +296,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
 #pragma unroll
       for (uint32_t j = 0; j < kTpsW; ++j) {
         step(w0 + j, myrec[j]);
-        if constexpr (emit) flush(false);  // <= 1 + 2 pending: fits the ring
       }
       __syncwarp();
     }
@@ -366,8 +313,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
         ++kw;
       }
     }
-    if (emit)
-      while (__any_sync(FULL, kw != kf)) flush(true);
     if (act) {
       // a pair error before any nesting break is the reference's error;
       // after one, only the exact recount knows

@@ -9,7 +9,7 @@ p1) timeout 600 python -m pytest tests/test_gpu_p1.py -q --timeout 200 -p no:cac
 overlap) timeout 600 python -m pytest tests/test_gpu_overlap.py -q --timeout 200 -p no:cacheprovider > $OUT/overlap.txt 2>&1; echo "rc=$?" >> $OUT/overlap.txt ;;
 slow) timeout 900 python -m pytest tests -q -m "slow" --timeout 800 -p no:cacheprovider > $OUT/slow.txt 2>&1; echo "rc=$?" >> $OUT/slow.txt ;;
 benchsmall) timeout 400 python bench.py --streams 262144 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/bench_small.json 2> $OUT/bench_small.err ;;
-benchdirect) WGPF_TPS_DIRECT=1 timeout 400 python bench.py --streams 262144 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/bench_direct.json 2> $OUT/bench_direct.err ;;
+
 bench) timeout 1200 python bench.py > $OUT/bench.json 2> $OUT/bench.err ;;
 benchref) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err ;;
 benchp1) timeout 600 python bench_p1.py > $OUT/bench_p1.json 2> $OUT/bench_p1.err ;;

@@ -9,8 +9,10 @@
 //   unwrap_clock (trace.hpp:257-272)   hi += (v < v_prev)
 //   pair_records (trace.hpp:294-346)   one stack per stream in shared memory;
 //       pass 1 guarantees depth <= kTpsDepth; an END whose stack top has
-//       another region breaks the single-stack assumption -> SF_INVALID
-//       (exact recount); durations >= 2^32 -> pair error (trace.hpp:330-336).
+//       another region breaks the single-stack assumption, and a duration
+//       >= 2^32 is the reference's pair error (trace.hpp:330-336): both mark
+//       the stream SF_INVALID -> exact recount and re-emit on the general
+//       path, which reports the error.
 //   replay (trace.hpp:398-487)          sync correction, wait markers decided
 //       with the look-ahead records i+1, i+2 and pass 1's z, orphans last.
 //   region_stats (pipeline.hpp:114-133) lane-private count / min / max / sum
@@ -180,8 +182,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
                           // matched base END, else none
     uint32_t kw = 0;      // events of this stream written
     uint32_t n_orph = 0;
-    uint32_t mm_pos = 0xFFFFFFFFu;  // first END breaking single-stack nesting
-    uint32_t tl_pos = 0xFFFFFFFFu;  // first END whose pair reaches 2^32
+    bool broken = false;  // single-stack nesting broken or a pair >= 2^32:
+                          // the exact general path redoes the stream
 
     auto put = [&](uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo, uint32_t ehi,
                    uint32_t region, uint32_t it) {
@@ -232,8 +234,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
       const bool mism = mend && ((e.y >> 11) & 31u) != rid;
       const bool tlong = mend && !mism && dhi;
-      mm_pos = (mism && mm_pos == 0xFFFFFFFFu) ? i : mm_pos;
-      tl_pos = (tlong && tl_pos == 0xFFFFFFFFu) ? i : tl_pos;
+      broken |= mism || tlong;
       const bool ok = mend && !mism && !tlong;
       uint16_t* cp = tb.cnt + rid * 32 + lane;
       const uint32_t it = *cp;
@@ -242,8 +243,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool base = ok && !is_mk;
       const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
       // ---- exec event: sync correction ---------------------------------------
-      const uint64_t ovh = (uint64_t)cost * (i - (e.y & 2047u));
-      const uint32_t corr = ovh > (uint64_t)meas ? 0u : meas - (uint32_t)ovh;
+      const uint32_t dpos = i - (e.y & 2047u);
+      const uint32_t ovh = cost * dpos;  // + __umulhi: the 64-bit product
+      const uint32_t corr = (__umulhi(cost, dpos) != 0u || ovh > meas) ? 0u : meas - ovh;
       // ---- wait marker START at i+1 -------------------------------------------
       const bool cclose = i + 2 < n && (int32_t)r2.x >= 0 &&
                           ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       __syncwarp();
     }
     // stream end: the orphan after the base events, final writes, checks
-    const bool bad = mm_pos != 0xFFFFFFFFu || n_orph > 1 || tl_pos != 0xFFFFFFFFu;
+    const bool bad = broken || n_orph > 1;
     const bool po = act && !bad && n_orph == 1;
     if (__any_sync(FULL, po)) {
       const wgpf_event o = ws.orph[lane];
@@ -314,11 +316,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       }
     }
     if (act) {
-      // a pair error before any nesting break is the reference's error;
-      // after one, only the exact recount knows
-      if (tl_pos < mm_pos)
-        atomicMin(&a.status->pair_err, ((unsigned long long)gs << 32) | tl_pos);
-      else if (mm_pos != 0xFFFFFFFFu || n_orph > 1 || kw != want) {
+      // exact recount + re-emit on the general path, which also reports the
+      // reference's pair error (trace.hpp:330-336) if there is one
+      if (bad || kw != want) {
         atomicAdd(&a.status->invalid, 1ull);  // exact recount
         a.sflag[s] = flag | SF_INVALID;
       }

@@ -38,7 +38,7 @@ __device__ __forceinline__ void cp_async_wait1() {
 struct RecWindows {
   uint32_t slk[kTpsChunks], pk[kTpsChunks];  // static chunk assignment
   uint32_t wp[kTpsChunks], wlim[kTpsChunks]; // physical slot, stream length
-  const uint8_t* wbase;                      // slots of the warp's stream 0
+  const uint8_t* src[kTpsChunks];            // slots of chunk k's stream
   uint64_t stride;
   uint32_t cap;
   uint8_t* buf;                              // [2][32 * kTpsPitch]
@@ -60,9 +60,9 @@ struct RecWindows {
   // are loaded directly)
   __device__ __forceinline__ void begin(const uint8_t* batch_body,
                                         uint32_t start, uint32_t n) {
-    wbase = batch_body + 16;
 #pragma unroll
     for (uint32_t k = 0; k < kTpsChunks; ++k) {
+      src[k] = batch_body + 16 + (uint64_t)slk[k] * stride;
       const uint32_t st_k = __shfl_sync(0xffffffffu, start, slk[k]);
       wlim[k] = __shfl_sync(0xffffffffu, n, slk[k]);
       uint32_t p = st_k + 2u;
@@ -79,8 +79,7 @@ struct RecWindows {
 #pragma unroll
     for (uint32_t k = 0; k < kTpsChunks; ++k) {
       if (c0 < wlim[k])
-        cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k],
-                   wbase + (uint64_t)slk[k] * stride + 8ull * wp[k]);
+        cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k], src[k] + 8u * wp[k]);
       wp[k] += kTpsW;
       if (wp[k] >= cap) wp[k] -= cap;
     }

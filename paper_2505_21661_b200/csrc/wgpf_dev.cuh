@@ -84,11 +84,12 @@ __device__ inline uint32_t hist_bin(uint64_t d) {
   return b < WGPF_HIST_BINS ? b : WGPF_HIST_BINS - 1u;
 }
 
-// hist_bin for durations below 2^32 (bin <= 63 without clamping)
+// hist_bin for durations below 2^32 (bin <= 63 without clamping): for
+// d >= 2, 2k + bit k-1 of d (k = floor(log2 d)) is the float's exponent and
+// top mantissa bit under round-toward-zero.
 __device__ __forceinline__ uint32_t hist_bin32(uint32_t d) {
-  if (d < 4u) return d;
-  const uint32_t k = 31u - (uint32_t)__clz(d);
-  return 2u * k + ((d >> (k - 1u)) & 1u);
+  const uint32_t b = (__float_as_uint(__uint2float_rz(d)) >> 22) - 254u;
+  return d < 2u ? d : b;
 }
 
 // Slot of a class in the stats arrays (inserting synthetic classes).

@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool tlong = mend && !mism && dhi;
       broken |= mism || tlong;
       const bool ok = mend && !mism && !tlong;
-      uint16_t* cp = tb.cnt + rid * 32 + lane;
+      // (rows exist for region ids < R; positions past the stream end hold
+      // arbitrary tags, so clamp -- the value is only used when ok)
+      uint16_t* cp = tb.cnt + min(rid, R - 1u) * 32 + lane;
       const uint32_t it = *cp;
       if (ok) *cp = (uint16_t)(it + 1u);
       const bool is_mk = (inf & 0x100u) != 0u;

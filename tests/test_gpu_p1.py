@@ -100,6 +100,21 @@ def test_gemm_matches_cublas_and_instrumented_is_identical(oracle, shape):
     assert torch.equal(C0, C1)
     img = p1.kpft_v1(prof.cpu().numpy(), ctas * p1.GEMM_WARPS)
     r = oracle.replay_kpft(img, p1.GEMM_SLOTS, 0, p1.GEMM_LABELS, 0)
+    # the GPU decoder on the device-resident profile (circular buffers: the
+    # slots past each stream's surviving records hold older records)
+    T = __import__("paper_2505_21661_b200.trace", fromlist=["trace"])
+    ctx = T.Context(0)
+    ctx.set_plan(T.BufferPlan(p1.GEMM_SLOTS, T.BufferStrategy.Circular, p1.GEMM_LABELS))
+    n_streams = ctas * p1.GEMM_WARPS
+    ev = torch.empty(n_streams * p1.GEMM_SLOTS * 32, dtype=torch.uint8, device="cuda")
+    ne, w = ctx.replay_device(prof.data_ptr(), prof.numel(), n_streams, 0,
+                              ev.data_ptr(), n_streams * p1.GEMM_SLOTS)
+    assert ne == len(r.events)
+    assert (w.dropped_heads, w.truncated_tails, w.flagged_preconditions,
+            w.malformed_groups) == (r.dropped_heads, r.truncated_tails,
+                                    r.flagged_preconditions, r.malformed_groups)
+    gev = ev[: ne * 32].cpu().numpy().view(T.EVENT_DTYPE)
+    assert np.array_equal(gev, r.events)
     st = oracle.region_stats(r.events, p1.GEMM_LABELS)
     labels = {s.label for s in st}
     assert {"mma.issue", "tma.issue", "epi.ld", "epi.st", "tile"} <= labels

@@ -33,6 +33,8 @@ METRIC = ("trace records decoded/s (GB/s vs HBM peak) at 1/2/4/8 GPU; "
 WORKLOAD = ("config 4: synthetic 2^30-record trace per GPU (148 SMs x 2048 CTAs "
             "x 16 warps = 4,849,664 streams), flush, 256 slots, 8 regions, "
             "TMA producer / MMA consumer patterns")
+WORKLOAD5 = ("config 5: 2^22 circular streams per GPU, 256 slots, 1000 writes each "
+             "(2^30 surviving records), 64 nested scopes S0..S63 E63..E0")
 
 
 def env_int(k, d):
@@ -191,6 +193,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
+    ap.add_argument("--config", type=int, default=4, choices=[4, 5],
+                    help="4: mixed producer/consumer trace (headline); 5: 2^22 "
+                         "circular streams, 64 nested scopes, 1000 writes each")
+    ap.add_argument("--no-p1", action="store_true",
+                    help="skip the config-2 instrumentation-overhead measurement")
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -215,22 +222,32 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     ctx = T.Context(local, stream.cuda_stream)
-    plan = T.BufferPlan(S.CAP, T.BufferStrategy.Flush, S.MIXED_LABELS)
+    nested = args.config == 5
+    if nested:
+        plan = T.BufferPlan(S.CAP, T.BufferStrategy.Circular, S.NESTED_LABELS)
+    else:
+        plan = T.BufferPlan(S.CAP, T.BufferStrategy.Flush, S.MIXED_LABELS)
     ctx.set_plan(plan)
 
-    n = args.streams or S.MIXED_FULL_STREAMS
+    n = args.streams or (S.NESTED_FULL_STREAMS if nested else S.MIXED_FULL_STREAMS)
     s0 = rank * n
     n_long = s0 + (S.MIXED_FULL_LONG if n == S.MIXED_FULL_STREAMS
                    else S.mixed_long_for(n))
     stride = S.stream_stride()
     body = torch.empty(n * stride, dtype=torch.uint8, device=dev)
-    ctx.synth_body(body.data_ptr(), 0, s0, n, n_long)
+    if nested:
+        ctx.synth_body(body.data_ptr(), 1, s0, n, 0)
+    else:
+        ctx.synth_body(body.data_ptr(), 0, s0, n, n_long)
     torch.cuda.synchronize()
 
     # sizes: records / events of this rank (one STATS_ONLY pass)
     n_ev, _ = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0,
                                 L.F_STATS_ONLY | L.F_NO_STATS, stream_base=s0)
-    records = int(min(222, 256) * (n_long - s0) + 221 * (n - (n_long - s0)))
+    if nested:
+        records = n * S.CAP
+    else:
+        records = int(min(222, 256) * (n_long - s0) + 221 * (n - (n_long - s0)))
     events = torch.empty(n_ev * 32, dtype=torch.uint8, device=dev)
     alg_bytes = 16 * n + 8 * records + 32 * n_ev
 
@@ -300,7 +317,7 @@ def main():
 
     # ---- end to end through the reference-facing call (host buffers) -------
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    if not args.no_e2e and args.e2e_steps > 0 and not nested:
         hdr = b"KPFT" + (2).to_bytes(2, "little") + b"\0\0" + n.to_bytes(8, "little")
         img = torch.empty(len(hdr) + body.numel(), dtype=torch.uint8, pin_memory=True)
         img[:len(hdr)] = torch.frombuffer(bytearray(hdr), dtype=torch.uint8)
@@ -341,10 +358,20 @@ def main():
         base_host = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not nested:
         if base_host is None:
             base_host = body[: min(n, 1 << 20) * stride].cpu().numpy()
         cpu = cpu_baseline(base_host, len(base_host) // stride, args.cpu_budget_s)
+
+    p1line = None
+    if rank == 0 and world == 1 and not args.no_p1 and not nested:
+        # config 2 in the same run: instrumented tcgen05 GEMM 8192^3
+        import bench_p1
+        p1line = bench_p1.measure(iters=20, warmup=5, decode=False, sass=False)
+        p1line = {k: p1line[k] for k in ("value", "unit", "t_plain_ms", "t_instr_ms",
+                                         "t_cublas_ms", "accuracy_rel_err",
+                                         "smem_profile_bytes_per_cta",
+                                         "record_cost_cycles")}
 
     if rank == 0:
         line = {
@@ -352,12 +379,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u32/u64 (integer trace records)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "streams_per_gpu": n,
+            "config": {"workload": WORKLOAD5 if nested else WORKLOAD, "streams_per_gpu": n,
                        "records_per_gpu": records, "events_per_gpu": n_ev,
                        "parallelism": f"dp{world} (block-range shards, one NCCL "
                                       "all-gather of per-label tables per step)",
-                       "l2": "inputs larger than L2 (10.0 GB body, 17.0 GB events "
-                             "per GPU)"},
+                       "l2": f"inputs larger than L2 ({body.numel() / 1e9:.1f} GB body, "
+                             f"{n_ev * 32 / 1e9:.1f} GB events per GPU)"},
             "gbs": alg_bytes / (ms_step / 1e3) / 1e9,
             "hbm_frac_step": alg_bytes / (ms_step / 1e3) / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
@@ -373,7 +400,8 @@ def main():
             "general_streams": profs[-1]["general_streams"],
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches,
-            "instr_overhead_pct": None,
+            "instr_overhead_pct": p1line["value"] if p1line else None,
+            "p1": p1line,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

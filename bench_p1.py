@@ -52,23 +52,16 @@ def sass_counts():
     return res
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--m", type=int, default=8192)
-    ap.add_argument("--n", type=int, default=8192)
-    ap.add_argument("--k", type=int, default=8192)
-    ap.add_argument("--iters", type=int, default=25)
-    ap.add_argument("--warmup", type=int, default=5)
-    args = ap.parse_args()
-
+def measure(M: int = 8192, N: int = 8192, K: int = 8192, iters: int = 25,
+            warmup: int = 5, decode: bool = True, sass: bool = True) -> dict:
+    """The config-2 measurement (also called by bench.py for its
+    instr_overhead_pct); returns the JSON line as a dict."""
     import numpy as np
     import torch
 
-    from oracle import oracle as O
     from paper_2505_21661_b200 import p1
     from paper_2505_21661_b200 import trace as T
 
-    M, N, K = args.m, args.n, args.k
     g = torch.Generator(device="cuda").manual_seed(0)
     A = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
     B = torch.randn(N, K, generator=g, device="cuda").to(torch.bfloat16)
@@ -90,7 +83,7 @@ def main():
 
     def timed(fn):
         ts = []
-        for i in range(args.warmup + args.iters):
+        for i in range(warmup + iters):
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -98,7 +91,7 @@ def main():
             fn()
             e1.record()
             torch.cuda.synchronize()
-            if i >= args.warmup:
+            if i >= warmup:
                 ts.append(e0.elapsed_time(e1))
         return ts
 
@@ -120,14 +113,15 @@ def main():
     med_p, med_i, med_c = (statistics.median(t_plain), statistics.median(t_instr),
                            statistics.median(t_cublas))
     flops = 2.0 * M * N * K
-    # decode the profile with the GPU decoder and the reference format check
-    ctx = T.Context(0)
-    ctx.set_plan(T.BufferPlan(p1.GEMM_SLOTS, T.BufferStrategy.Circular, p1.GEMM_LABELS))
-    n_streams = ctas * p1.GEMM_WARPS
-    ev = torch.empty(n_streams * p1.GEMM_SLOTS * 32, dtype=torch.uint8, device="cuda")
-    ne, w = ctx.replay_device(prof.data_ptr(), prof.numel(), n_streams, 0,
-                              ev.data_ptr(), n_streams * p1.GEMM_SLOTS)
-    st = ctx.stats()
+    ne, st = None, {}
+    if decode:  # decode the profile with the GPU decoder
+        ctx = T.Context(0)
+        ctx.set_plan(T.BufferPlan(p1.GEMM_SLOTS, T.BufferStrategy.Circular, p1.GEMM_LABELS))
+        n_streams = ctas * p1.GEMM_WARPS
+        ev = torch.empty(n_streams * p1.GEMM_SLOTS * 32, dtype=torch.uint8, device="cuda")
+        ne, w = ctx.replay_device(prof.data_ptr(), prof.numel(), n_streams, 0,
+                                  ev.data_ptr(), n_streams * p1.GEMM_SLOTS)
+        st = ctx.stats()
     c0 = torch.zeros(4, dtype=torch.int64, device="cuda")
     c1 = torch.zeros(4, dtype=torch.int64, device="cuda")
     p1.record_cost(1 << 14, 4, False, c0.data_ptr())
@@ -150,12 +144,23 @@ def main():
         "smem_total_bytes_per_cta": {"plain": p1.gemm_smem_bytes(False),
                                      "instrumented": p1.gemm_smem_bytes(True)},
         "record_cost_cycles": cyc,
-        "sass_instructions": sass_counts(),
+        "sass_instructions": sass_counts() if sass else None,
         "max_abs_err_vs_cublas": err, "instrumented_output_identical": same,
         "decoded_events": ne,
         "scope_means_cycles": {k: v.mean for k, v in st.items()},
     }
-    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=8192)
+    ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--k", type=int, default=8192)
+    ap.add_argument("--iters", type=int, default=25)
+    ap.add_argument("--warmup", type=int, default=5)
+    args = ap.parse_args()
+    print(json.dumps(measure(args.m, args.n, args.k, args.iters, args.warmup)), flush=True)
 
 
 if __name__ == "__main__":

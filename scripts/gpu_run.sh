@@ -11,6 +11,7 @@ slow) timeout 900 python -m pytest tests -q -m "slow" --timeout 800 -p no:cachep
 benchsmall) timeout 400 python bench.py --streams 262144 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/bench_small.json 2> $OUT/bench_small.err ;;
 
 bench) timeout 1200 python bench.py > $OUT/bench.json 2> $OUT/bench.err ;;
+bench5) timeout 1200 python bench.py --config 5 --no-p1 > $OUT/bench5.json 2> $OUT/bench5.err ;;
 benchref) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err ;;
 benchp1) timeout 600 python bench_p1.py > $OUT/bench_p1.json 2> $OUT/bench_p1.err ;;
 ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1

@@ -259,9 +259,13 @@ def main():
         merged_ctx = T.Context(local, stream.cuda_stream)
         merged_ctx.set_plan(plan)
 
+    # WGPF_BENCH_FLAGS: extra replay flags for A/B experiments (never in the
+    # reported configuration)
+    xflags = env_int("WGPF_BENCH_FLAGS", 0)
+
     def step():
         ne, w = ctx.replay_device(body.data_ptr(), body.numel(), n, 33,
-                                  events.data_ptr(), n_ev, L.F_PROFILE,
+                                  events.data_ptr(), n_ev, L.F_PROFILE | xflags,
                                   stream_base=s0)
         assert ne == n_ev
         prof = ctx.last_profile()

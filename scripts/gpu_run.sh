@@ -18,5 +18,6 @@ ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv
      timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_tps} -s 1 -c 1 -o $OUT/emit python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1 ;;
 ncusmall) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_small.csv python bench.py --streams 262144 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_bench_small.log 2>&1
      timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_tps} -s 1 -c 1 -o $OUT/emit_small python bench.py --streams 262144 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_small.log 2>&1 ;;
+split) for fl in 0 8 1 9; do WGPF_BENCH_FLAGS=$fl timeout 400 python bench.py --streams 1048576 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-p1 > $OUT/split_$fl.json 2>> $OUT/split.err; done ;;
 merge) timeout 300 python -m pytest tests/test_gpu_parity.py -q -k merge -p no:cacheprovider -vv > $OUT/merge.txt 2>&1 ;;
 esac; done

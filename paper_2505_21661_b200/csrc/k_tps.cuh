@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint32_t lt = lanemask_lt();
   const uint32_t cost = (uint32_t)a.record_cost;  // host: < 2^32 on this path
   const uint32_t cap = a.cap;
-  uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0;
+  uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0, w_ovf = 0;
 
   RecWindows win;
   win.init(ws.rec[0], lane, a.stride, cap);
@@ -185,29 +185,37 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     bool broken = false;  // single-stack nesting broken or a pair >= 2^32:
                           // the exact general path redoes the stream
 
-    auto put = [&](uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo, uint32_t ehi,
-                   uint32_t region, uint32_t it) {
+    // a stream's events fit the caller's buffer unless it ends past the
+    // capacity (events <= records): then each store is checked
+    const bool fits = off + n <= a.events_cap;
+    auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
+                   uint32_t ehi, uint32_t region, uint32_t it) {
       const uint64_t idx = off + k;
-      if (idx < a.events_cap) {
-        uint4* p = reinterpret_cast<uint4*>(a.events + idx);
-        p[0] = make_uint4(slo, shi, elo, ehi);
-        p[1] = make_uint4(region, it, blk, wg);
-      } else {
-        atomicAdd(&a.status->overflow, 1ull);
+      const bool ok = p && (fits || idx < a.events_cap);
+      if (ok) {
+        uint4* q = reinterpret_cast<uint4*>(a.events + idx);
+        q[0] = make_uint4(slo, shi, elo, ehi);
+        q[1] = make_uint4(region, it, blk, wg);
       }
+      w_ovf += (p && !ok) ? 1u : 0u;
     };
-    auto lstat = [&](uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
-      uint4* e = tb.a + cls * 32 + lane;
+    // one event of class cls (predicated on p): lane-private count / min /
+    // max / sum, per-warp first key, CTA histogram
+    auto lstat = [&](bool p, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
+      const uint32_t c = p ? cls : 0u;
+      uint4* e = tb.a + c * 32 + lane;
       uint4 x = *e;
-      if (x.x == 0) atomicMin(&tb.first[cls], gkey | (kpos << 1) | kind);
+      if (p && x.x == 0) atomicMin(&tb.first[c], gkey | (kpos << 1) | kind);
       x.x += 1;
       x.y = min(x.y, d);
       x.z = max(x.z, d);
       const uint32_t sm = x.w + d;
-      if (sm < d) tb.hi[cls * 32 + lane] += 1;
+      if (p && sm < d) tb.hi[c * 32 + lane] += 1;
       x.w = sm;
-      *e = x;
-      atomicAdd(&hist[cls * WGPF_HIST_BINS + hist_bin32(d)], 1u);
+      if (p) {
+        *e = x;
+        atomicAdd(&hist[c * WGPF_HIST_BINS + hist_bin32(d)], 1u);
+      }
     };
     auto step = [&](uint32_t i, uint2 r2) {
       const bool valid = i < n;
@@ -259,31 +267,24 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       w_flag += (consumed && !corr_w) ? 1u : 0u;
       const uint32_t kpos = kw;
       if constexpr (emit) {
-        if (base) {
-          const uint32_t elo = e.x + corr;
-          put(kw, e.x, shi, elo, shi + (elo < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED, it);
-        }
-        if (consumed)
-          put(kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
-              r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
+        const uint32_t elo = e.x + corr;
+        put(base, kw, e.x, shi, elo, shi + (elo < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED,
+            it);
+        put(consumed, kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
+            r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
       }
       kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
       pw = base ? (inf >> 16) : 0xFFu;
-      if (orphan) {  // rare: a marker interval without its exec (last)
-        if (n_orph == 0) {
-          wgpf_event& o = ws.orph[lane];
-          o.start = ((uint64_t)shi << 32) | e.x;
-          o.end = ((uint64_t)hi << 32) | v;
-          o.region = rid;
-          o.iteration = it;
-          o.block_index = blk;
-          o.warp_group = wg;
-        }
-        ++n_orph;
+      // orphan marker interval (written after the base events): keep one
+      if (orphan && n_orph == 0) {
+        uint4* o = reinterpret_cast<uint4*>(&ws.orph[lane]);
+        o[0] = make_uint4(e.x, shi, v, hi);
+        o[1] = make_uint4(rid, it, blk, wg);
       }
+      n_orph += orphan ? 1u : 0u;
       if constexpr (stats) {
-        if (base) lstat(inf & 0xFFu, corr, kpos, 0u);
-        if (consumed) lstat(i1 & 0xFFu, wd, kpos + 1u, 1u);
+        lstat(base, inf & 0xFFu, corr, kpos, 0u);
+        if (__any_sync(FULL, consumed)) lstat(consumed, i1 & 0xFFu, wd, kpos + 1u, 1u);
       }
       inf0 = i1;
       r0 = r1;
@@ -308,14 +309,12 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const bool po = act && !bad && n_orph == 1;
     if (__any_sync(FULL, po)) {
       const wgpf_event o = ws.orph[lane];
-      if (po) {
-        if (emit)
-          put(kw, (uint32_t)o.start, (uint32_t)(o.start >> 32), (uint32_t)o.end,
-              (uint32_t)(o.end >> 32), o.region, o.iteration);
-        if (stats)
-          lstat(cs.info[o.region & 31u] & 0xFFu, (uint32_t)(o.end - o.start), kw, 0u);
-        ++kw;
-      }
+      if (emit)
+        put(po, kw, (uint32_t)o.start, (uint32_t)(o.start >> 32), (uint32_t)o.end,
+            (uint32_t)(o.end >> 32), o.region, o.iteration);
+      if (stats)
+        lstat(po, cs.info[o.region & 31u] & 0xFFu, (uint32_t)(o.end - o.start), kw, 0u);
+      kw += po ? 1u : 0u;
     }
     if (act) {
       // exact recount + re-emit on the general path, which also reports the
@@ -335,6 +334,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const unsigned long long f = warp_sum((unsigned long long)w_flag);
   const unsigned long long t = warp_sum((unsigned long long)w_tail);
   const unsigned long long m = warp_sum((unsigned long long)w_mal);
+  const unsigned long long ov = warp_sum((unsigned long long)w_ovf);
+  if (lane == 0 && ov) atomicAdd(&a.status->overflow, ov);
   if (lane == 0) {
     if (d) atomicAdd(&cs.warn[0], d);
     if (t) atomicAdd(&cs.warn[1], t);

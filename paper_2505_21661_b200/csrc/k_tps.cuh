@@ -141,6 +141,13 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
 
   RecWindows win;
   win.init(ws.rec[0], lane, a.stride, cap);
+  // 32-bit shared addresses of the hot tables (this lane's column)
+  const uint32_t s_info = smem_addr(cs.info);
+  const uint32_t s_hist = smem_addr(hist);
+  const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);    // + 256 * level
+  const uint32_t s_cnt = smem_addr(tb.cnt + lane);        // + 64 * region
+  const uint32_t s_a = smem_addr(tb.a + lane);            // + 512 * class
+  const uint32_t s_orph = smem_addr(&ws.orph[lane]);
 
   const uint64_t wstep = (uint64_t)gridDim.x * nw;
   for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b * 32 < a.n_streams;
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
                    uint32_t ehi, uint32_t region, uint32_t it) {
       const uint64_t idx = off + k;
-      const bool ok = p && (fits || idx < a.events_cap);
+      const bool ok = p & (fits | (idx < a.events_cap));
       if (ok) {
         uint4* q = reinterpret_cast<uint4*>(a.events + idx);
         q[0] = make_uint4(slo, shi, elo, ehi);
@@ -203,8 +210,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     // max / sum, per-warp first key, CTA histogram
     auto lstat = [&](bool p, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
       const uint32_t c = p ? cls : 0u;
-      uint4* e = tb.a + c * 32 + lane;
-      uint4 x = *e;
+      const uint32_t ea = s_a + c * 512u;
+      uint4 x = lds128(ea);
       if (p && x.x == 0) atomicMin(&tb.first[c], gkey | (kpos << 1) | kind);
       x.x += 1;
       x.y = min(x.y, d);
@@ -212,10 +219,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const uint32_t sm = x.w + d;
       if (p && sm < d) tb.hi[c * 32 + lane] += 1;
       x.w = sm;
-      if (p) {
-        *e = x;
-        atomicAdd(&hist[c * WGPF_HIST_BINS + hist_bin32(d)], 1u);
-      }
+      sts128_if(p, ea, x);
+      red_add_if(p, s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)), 1u);
     };
     auto step = [&](uint32_t i, uint2 r2) {
       const bool valid = i < n;
@@ -226,16 +231,16 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const uint32_t rid = (tag >> 12) & (kTpsRegions - 1u);
       const uint32_t inf = inf0;
       const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
-      const uint32_t i1 = cs.info[r1id];
+      const uint32_t i1 = lds32(s_info + 4u * r1id);
       hi += (valid && v < vprev) ? 1u : 0u;
       vprev = valid ? v : vprev;
       // ---- stack ------------------------------------------------------------
-      const uint2 e = ws.stk[sp ? sp - 1u : 0u][lane];
+      const uint2 e = lds64(s_stk + 256u * (sp ? sp - 1u : 0u));
       const bool mend = en && sp != 0;
       w_drop += (en && sp == 0) ? 1u : 0u;
-      if (st)
-        ws.stk[sp][lane] = make_uint2(
-            v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 16) | (hi << 17));
+      sts64_if(st, s_stk + 256u * sp,
+               make_uint2(v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 16) |
+                                 (hi << 17)));
       sp = sp + (st ? 1u : 0u) - (mend ? 1u : 0u);
       const uint32_t shi = e.y >> 17;
       const uint32_t meas = v - e.x;  // low 32 bits of u - su
@@ -246,9 +251,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool ok = mend && !mism && !tlong;
       // (rows exist for region ids < R; positions past the stream end hold
       // arbitrary tags, so clamp -- the value is only used when ok)
-      uint16_t* cp = tb.cnt + min(rid, R - 1u) * 32 + lane;
-      const uint32_t it = *cp;
-      if (ok) *cp = (uint16_t)(it + 1u);
+      const uint32_t ca = s_cnt + 64u * min(rid, R - 1u);
+      const uint32_t it = lds16(ca);
+      sts16_if(ok, ca, it + 1u);
       const bool is_mk = (inf & 0x100u) != 0u;
       const bool base = ok && !is_mk;
       const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
@@ -276,11 +281,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
       pw = base ? (inf >> 16) : 0xFFu;
       // orphan marker interval (written after the base events): keep one
-      if (orphan && n_orph == 0) {
-        uint4* o = reinterpret_cast<uint4*>(&ws.orph[lane]);
-        o[0] = make_uint4(e.x, shi, v, hi);
-        o[1] = make_uint4(rid, it, blk, wg);
-      }
+      sts128_if(orphan && n_orph == 0, s_orph, make_uint4(e.x, shi, v, hi));
+      sts128_if(orphan && n_orph == 0, s_orph + 16u, make_uint4(rid, it, blk, wg));
       n_orph += orphan ? 1u : 0u;
       if constexpr (stats) {
         lstat(base, inf & 0xFFu, corr, kpos, 0u);

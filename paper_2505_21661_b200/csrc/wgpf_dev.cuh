@@ -195,6 +195,62 @@ __device__ inline uint32_t wait_class_of(const DevPlan& p, uint32_t rid,
              : kNone;
 }
 
+// ---- shared memory through 32-bit addresses ----------------------------------
+// (hot loops: a generic pointer into dynamic shared memory makes the compiler
+// rematerialise the shared window base at every access site)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.u16 [%1], %2; }" ::"r"(
+                   (uint32_t)p),
+               "r"(a), "h"((uint16_t)v)
+               : "memory");
+}
+__device__ __forceinline__ void sts64_if(bool p, uint32_t a, uint2 v) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.v2.u32 [%1], {%2, %3}; }" ::"r"(
+          (uint32_t)p),
+      "r"(a), "r"(v.x), "r"(v.y)
+      : "memory");
+}
+__device__ __forceinline__ void sts128_if(bool p, uint32_t a, uint4 v) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.v4.u32 [%1], {%2, %3, %4, %5}; }" ::"r"(
+          (uint32_t)p),
+      "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+      : "memory");
+}
+__device__ __forceinline__ void red_add_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.shared.add.u32 [%1], %2; }" ::"r"(
+                   (uint32_t)p),
+               "r"(a), "r"(v)
+               : "memory");
+}
+
 // ---- warp helpers --------------------------------------------------------------
 __device__ inline uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ inline uint32_t lanemask_lt() {

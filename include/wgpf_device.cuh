@@ -114,7 +114,28 @@ struct Recorder {
   template <bool kStart>
   __device__ __forceinline__ void record(uint32_t region, uint32_t sig = 0) {
     const uint32_t clk = clock32();
-    const uint32_t tag = make_tag(kStart, region, sig);
+    put(make_tag(kStart, region, sig), clk);
+  }
+
+  __device__ __forceinline__ void start(uint32_t region, uint32_t sig = 0) {
+    record<true>(region, sig);
+  }
+  __device__ __forceinline__ void end(uint32_t region, uint32_t sig = 0) {
+    record<false>(region, sig);
+  }
+
+  // END(end_region) immediately followed by START(start_region): the two
+  // RecordOps of a scope boundary (wait -> issue, issue -> next wait) share
+  // one clock capture -- same records, half the critical-path cost there.
+  __device__ __forceinline__ void mark(uint32_t end_region, uint32_t start_region,
+                                       uint32_t sig = 0) {
+    const uint32_t clk = clock32();
+    put(make_tag(false, end_region, sig), clk);
+    put(make_tag(true, start_region, sig), clk);
+  }
+
+  // StoreCounter: slot writes % cap (circular) -- vgpu.hpp:240-273
+  __device__ __forceinline__ void put(uint32_t tag, uint32_t clk) {
     uint32_t s;
     if constexpr (kPow2) {
       s = writes & mask;
@@ -128,13 +149,6 @@ struct Recorder {
                    "r"(clk)
                    : "memory");
     ++writes;
-  }
-
-  __device__ __forceinline__ void start(uint32_t region, uint32_t sig = 0) {
-    record<true>(region, sig);
-  }
-  __device__ __forceinline__ void end(uint32_t region, uint32_t sig = 0) {
-    record<false>(region, sig);
   }
 
   // Stream header (done by the leader before the CTA flush).

@@ -161,15 +161,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
+    // scope boundaries share one capture (Recorder::mark)
+    if constexpr (kInstr) rec.start(R_TMA_WAIT);
     for (uint32_t kb = 0; kb < nk; ++kb) {
       const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1u;
-      if constexpr (kInstr) rec.start(R_TMA_WAIT);
       if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
       __syncwarp();
-      if constexpr (kInstr) {
-        rec.end(R_TMA_WAIT);
-        rec.start(R_TMA);
-      }
+      if constexpr (kInstr) rec.mark(R_TMA_WAIT, R_TMA);
       if (lane == 0) {
         uint8_t* a = stage_base + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
@@ -177,20 +175,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_2d(&tb, &full[s], a + A_BYTES, (int)(kb * BK), (int)n0);
       }
       __syncwarp();
-      if constexpr (kInstr) rec.end(R_TMA);
+      if constexpr (kInstr) {
+        if (kb + 1 < nk)
+          rec.mark(R_TMA, R_TMA_WAIT);
+        else
+          rec.end(R_TMA);
+      }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    if constexpr (kInstr) rec.start(R_MMA_WAIT);
     for (uint32_t kb = 0; kb < nk; ++kb) {
       const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1u;
-      if constexpr (kInstr) rec.start(R_MMA_WAIT);
       if (lane == 0) mbar_wait(&full[s], ph);
       __syncwarp();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if constexpr (kInstr) {
-        rec.end(R_MMA_WAIT);
-        rec.start(R_MMA);
-      }
+      if constexpr (kInstr) rec.mark(R_MMA_WAIT, R_MMA);
       if (lane == 0) {
         const uint32_t a = smem_u32(stage_base + s * STAGE_BYTES);
         const uint32_t b = a + A_BYTES;
@@ -202,7 +202,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (kb == nk - 1) umma_commit(tmem_full);
       }
       __syncwarp();
-      if constexpr (kInstr) rec.end(R_MMA);
+      if constexpr (kInstr) {
+        if (kb + 1 < nk)
+          rec.mark(R_MMA, R_MMA_WAIT);
+        else
+          rec.end(R_MMA);
+      }
     }
   } else {
     // ---------------- epilogue: TMEM -> registers -> bf16 -> HBM -----------
@@ -211,10 +216,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if constexpr (kInstr) rec.start(R_EPI_WAIT);
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if constexpr (kInstr) rec.end(R_EPI_WAIT);
+    if constexpr (kInstr) rec.mark(R_EPI_WAIT, R_EPI_LD);
     const uint32_t taddr = tmem + ((quad * 32u) << 16);
     for (uint32_t c = 0; c < BN; c += 32) {
-      if constexpr (kInstr) rec.start(R_EPI_LD);
       uint32_t v[32];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,"
@@ -229,10 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             "=r"(v[30]), "=r"(v[31])
           : "r"(taddr + c));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if constexpr (kInstr) {
-        rec.end(R_EPI_LD);
-        rec.start(R_EPI_ST);
-      }
+      if constexpr (kInstr) rec.mark(R_EPI_LD, R_EPI_ST);
       uint4 out[4];
       uint32_t* o = reinterpret_cast<uint32_t*>(out);
 #pragma unroll
@@ -246,7 +247,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dst[j] = out[j];
       }
-      if constexpr (kInstr) rec.end(R_EPI_ST);
+      if constexpr (kInstr) {
+        if (c + 32 < BN)
+          rec.mark(R_EPI_ST, R_EPI_LD);
+        else
+          rec.end(R_EPI_ST);
+      }
     }
   }
 

@@ -47,8 +47,11 @@ def sass_counts():
             counts[cur] += 1
     res = {}
     for k, v in counts.items():
-        if "k_gemm" in k:
-            res["instrumented" if "ILb1E" in k else "plain"] = v
+        if "k_gemm" in k:  # k_gemm<mode>: 0 plain, 1 / 2 instrumented
+            mode = re.search(r"ILi(\d)E", k)
+            if mode:
+                res[{"0": "plain", "1": "instrumented", "2": "instrumented_mark"}
+                    [mode.group(1)]] = v
     return res
 
 

@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "wgpf_device.cuh"
 
@@ -104,7 +105,9 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
       : "memory");
 }
 
-template <bool kInstr>
+// kMode: 0 plain, 1 one clock capture per RecordOp, 2 adjacent END/START
+// RecordOps at scope boundaries share a capture (Recorder::mark)
+template <int kMode>
 __global__ void __launch_bounds__(THREADS, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta,
            const __grid_constant__ CUtensorMap tb, __nv_bfloat16* C, uint32_t M,
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint64_t cta = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
 
   wgpf_dev::Recorder<true> rec;
-  if constexpr (kInstr) {
+  if constexpr (kMode != 0) {
     rec.init(prof, warp, PROF_CAP, lane == 0);
     if (threadIdx.x == 0 && timing) {
       timing[cta].smid = wgpf_dev::smid();
@@ -161,13 +164,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
-    // scope boundaries share one capture (Recorder::mark)
-    if constexpr (kInstr) rec.start(R_TMA_WAIT);
+    if constexpr (kMode == 2) rec.start(R_TMA_WAIT);
     for (uint32_t kb = 0; kb < nk; ++kb) {
       const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1u;
+      if constexpr (kMode == 1) rec.start(R_TMA_WAIT);
       if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
       __syncwarp();
-      if constexpr (kInstr) rec.mark(R_TMA_WAIT, R_TMA);
+      if constexpr (kMode == 1) {
+        rec.end(R_TMA_WAIT);
+        rec.start(R_TMA);
+      }
+      if constexpr (kMode == 2) rec.mark(R_TMA_WAIT, R_TMA);
       if (lane == 0) {
         uint8_t* a = stage_base + s * STAGE_BYTES;
         mbar_expect_tx(&full[s], STAGE_BYTES);
@@ -175,7 +182,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tma_load_2d(&tb, &full[s], a + A_BYTES, (int)(kb * BK), (int)n0);
       }
       __syncwarp();
-      if constexpr (kInstr) {
+      if constexpr (kMode == 1) rec.end(R_TMA);
+      if constexpr (kMode == 2) {
         if (kb + 1 < nk)
           rec.mark(R_TMA, R_TMA_WAIT);
         else
@@ -184,13 +192,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if constexpr (kInstr) rec.start(R_MMA_WAIT);
+    if constexpr (kMode == 2) rec.start(R_MMA_WAIT);
     for (uint32_t kb = 0; kb < nk; ++kb) {
       const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1u;
+      if constexpr (kMode == 1) rec.start(R_MMA_WAIT);
       if (lane == 0) mbar_wait(&full[s], ph);
       __syncwarp();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if constexpr (kInstr) rec.mark(R_MMA_WAIT, R_MMA);
+      if constexpr (kMode == 1) {
+        rec.end(R_MMA_WAIT);
+        rec.start(R_MMA);
+      }
+      if constexpr (kMode == 2) rec.mark(R_MMA_WAIT, R_MMA);
       if (lane == 0) {
         const uint32_t a = smem_u32(stage_base + s * STAGE_BYTES);
         const uint32_t b = a + A_BYTES;
@@ -202,7 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (kb == nk - 1) umma_commit(tmem_full);
       }
       __syncwarp();
-      if constexpr (kInstr) {
+      if constexpr (kMode == 1) rec.end(R_MMA);
+      if constexpr (kMode == 2) {
         if (kb + 1 < nk)
           rec.mark(R_MMA, R_MMA_WAIT);
         else
@@ -213,12 +227,14 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- epilogue: TMEM -> registers -> bf16 -> HBM -----------
     const uint32_t quad = warp & 3u;  // TMEM lane quadrant of this warp
     const uint32_t row = m0 + quad * 32u + lane;
-    if constexpr (kInstr) rec.start(R_EPI_WAIT);
+    if constexpr (kMode != 0) rec.start(R_EPI_WAIT);
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if constexpr (kInstr) rec.mark(R_EPI_WAIT, R_EPI_LD);
+    if constexpr (kMode == 1) rec.end(R_EPI_WAIT);
+    if constexpr (kMode == 2) rec.mark(R_EPI_WAIT, R_EPI_LD);
     const uint32_t taddr = tmem + ((quad * 32u) << 16);
     for (uint32_t c = 0; c < BN; c += 32) {
+      if constexpr (kMode == 1) rec.start(R_EPI_LD);
       uint32_t v[32];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,"
@@ -233,7 +249,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             "=r"(v[30]), "=r"(v[31])
           : "r"(taddr + c));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if constexpr (kInstr) rec.mark(R_EPI_LD, R_EPI_ST);
+      if constexpr (kMode == 1) {
+        rec.end(R_EPI_LD);
+        rec.start(R_EPI_ST);
+      }
+      if constexpr (kMode == 2) rec.mark(R_EPI_LD, R_EPI_ST);
       uint4 out[4];
       uint32_t* o = reinterpret_cast<uint32_t*>(out);
 #pragma unroll
@@ -247,7 +267,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dst[j] = out[j];
       }
-      if constexpr (kInstr) {
+      if constexpr (kMode == 1) rec.end(R_EPI_ST);
+      if constexpr (kMode == 2) {
         if (c + 32 < BN)
           rec.mark(R_EPI_ST, R_EPI_LD);
         else
@@ -256,7 +277,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
-  if constexpr (kInstr) {
+  if constexpr (kMode != 0) {
     rec.end(R_TILE);
     rec.close((uint32_t)cta, warp, PROF_CAP);
   }
@@ -265,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
-  if constexpr (kInstr) {
+  if constexpr (kMode != 0) {
     wgpf_dev::flush(prof, profile, cta, PROF_BYTES, threadIdx.x, THREADS);
     if (threadIdx.x == 0 && timing) {
       timing[cta].gt_end = wgpf_dev::globaltimer();
@@ -330,17 +351,20 @@ extern "C" int wgpf_gemm_bf16(const void* A, const void* B, void* C, uint32_t M,
   dim3 grid(N / BN, M / BM);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (instrument) {
-    cudaFuncSetAttribute(k_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-    k_gemm<true><<<grid, THREADS, SMEM_BYTES, st>>>(
+    // instrument = 1: one capture per RecordOp; 2: shared boundary captures
+    // (WGPF_P1_MODE overrides, for A/B runs)
+    int mode = instrument;
+    if (const char* e = getenv("WGPF_P1_MODE")) mode = atoi(e);
+    auto* kfn = mode == 2 ? k_gemm<2> : k_gemm<1>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    kfn<<<grid, THREADS, SMEM_BYTES, st>>>(
         ta, tb, static_cast<__nv_bfloat16*>(C), M, N, K,
         static_cast<uint8_t*>(d_profile),
         static_cast<wgpf_dev::CtaTiming*>(d_timing));
   } else {
-    cudaFuncSetAttribute(k_gemm<false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          SMEM_BYTES - PROF_BYTES);
-    k_gemm<false><<<grid, THREADS, SMEM_BYTES - PROF_BYTES, st>>>(
+    k_gemm<0><<<grid, THREADS, SMEM_BYTES - PROF_BYTES, st>>>(
         ta, tb, static_cast<__nv_bfloat16*>(C), M, N, K, nullptr, nullptr);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 10;

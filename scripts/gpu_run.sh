@@ -19,5 +19,6 @@ ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv
 ncusmall) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_small.csv python bench.py --streams 262144 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_bench_small.log 2>&1
      timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_tps} -s 1 -c 1 -o $OUT/emit_small python bench.py --streams 262144 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_small.log 2>&1 ;;
 split) for fl in 0 8 1 9; do WGPF_BENCH_FLAGS=$fl timeout 400 python bench.py --streams 1048576 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-p1 > $OUT/split_$fl.json 2>> $OUT/split.err; done ;;
+p1ab) for m in 1 2 1 2; do WGPF_P1_MODE=$m timeout 300 python bench_p1.py > $OUT/p1_mode$m.json 2>> $OUT/p1ab.err; cat $OUT/p1_mode$m.json >> $OUT/p1ab.jsonl; done ;;
 merge) timeout 300 python -m pytest tests/test_gpu_parity.py -q -k merge -p no:cacheprovider -vv > $OUT/merge.txt 2>&1 ;;
 esac; done

@@ -194,6 +194,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
     marker_region[r] =
         r < a.fast_regions ? class_is_marker(a.plan, a.plan.class_of[r]) : 0;
   __syncthreads();
+  uint32_t mbits = 0;  // marker regions among ids < 32
+  for (uint32_t r = 0; r < 32; ++r) mbits |= (uint32_t)marker_region[r] << r;
   const uint32_t FULL = 0xffffffffu;
   const uint32_t lane = lane_id();
   const uint32_t w = threadIdx.x >> 5;
@@ -243,8 +245,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
     win.issue(0, 2);
     cp_async_commit();
     int32_t q = 0, run_min = 0, max_d = 0, z = -1, last_bad = -1;
-    uint32_t n_end = 0;
-    bool wide = false, tps_out = false, prev_end = false;
+    uint32_t maxrid = 0;  // region-id range: fast / thread-per-stream routing
+    bool prev_end = false;
     for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
       const uint32_t bsel = (w0 / kTpsW) & 1u;
       if (w0 + kTpsW < nmax) win.issue(bsel ^ 1u, w0 + kTpsW + 2u);
@@ -258,29 +260,34 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
         const uint32_t i = w0 + j;
         const bool valid = i < n;
         const bool isS = (int32_t)t0 < 0;
-        const bool st = valid && isS;
-        const bool en = valid && !isS;
         const uint32_t rid = (t0 >> 12) & (WGPF_MAX_REGIONS - 1u);
-        wide |= valid && rid >= a.fast_regions;
-        tps_out |= valid && rid >= a.tps_regions;
-        q += st ? 1 : (en ? -1 : 0);
+        maxrid = valid ? max(maxrid, rid) : maxrid;
+        q += valid ? 2 * (int32_t)(t0 >> 31) - 1 : 0;  // START +1, END -1
         run_min = min(run_min, q);
         const int32_t d = q - run_min;
         z = (valid && d == 0) ? (int32_t)i : z;
         max_d = max(max_d, d);
-        n_end += en ? 1u : 0u;
         // a wait-marker START right after an END that the next record does
         // not close: only z can tell whether it is ever closed
-        const bool mk_start = st && prev_end && rid < a.fast_regions && marker_region[rid & 255u];
+        uint32_t mk;
+        if (rid < 32u)
+          mk = (mbits >> rid) & 1u;
+        else
+          mk = rid < a.fast_regions ? marker_region[rid & 255u] : 0u;
+        const bool mk_start = valid && isS && prev_end && mk;
         const bool closed_next = i + 1 < n && (int32_t)t1 >= 0 &&
                                  ((t1 >> 12) & (WGPF_MAX_REGIONS - 1u)) == rid;
         last_bad = (mk_start && !closed_next) ? (int32_t)i : last_bad;
-        prev_end = en;
+        prev_end = valid && !isS;
         t0 = t1;
         t1 = t2;
       }
       __syncwarp();
     }
+    // #START + #END = n and #START - #END = q
+    const uint32_t n_end = (n - (uint32_t)q) >> 1;
+    const bool wide = n && maxrid >= a.fast_regions;
+    const bool tps_out = n && maxrid >= a.tps_regions;
     if (act) {
       a.counts[s] = n_end - (uint32_t)(-run_min);
       a.zpos[s] = z;

@@ -22,10 +22,8 @@ constexpr uint32_t kTpsChunks = (kTpsW + 2) / 2;      // 16-B chunks per window
 constexpr uint32_t kTpsPitch = 16 * kTpsChunks;       // bytes per lane window
 constexpr uint32_t kTpsMaxSlots = 2046;               // even; pos fits 11 bits
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
@@ -36,23 +34,28 @@ __device__ __forceinline__ void cp_async_wait1() {
 }
 
 struct RecWindows {
-  uint32_t slk[kTpsChunks], pk[kTpsChunks];  // static chunk assignment
+  uint32_t slk[kTpsChunks];                  // static chunk assignment:
+  uint32_t sdst[kTpsChunks];                 //   stream, shared destination
   uint32_t wp[kTpsChunks], wlim[kTpsChunks]; // physical slot, stream length
   const uint8_t* src[kTpsChunks];            // slots of chunk k's stream
   uint64_t stride;
   uint32_t cap;
   uint8_t* buf;                              // [2][32 * kTpsPitch]
+  uint32_t pk2[kTpsChunks];                  // 2 * part (slots)
 
   __device__ __forceinline__ void init(uint8_t* smem, uint32_t lane,
                                        uint64_t stride_, uint32_t cap_) {
     buf = smem;
     stride = stride_;
     cap = cap_;
+    const uint32_t b0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
 #pragma unroll
     for (uint32_t k = 0; k < kTpsChunks; ++k) {
       const uint32_t q = k * 32 + lane;
       slk[k] = q / kTpsChunks;
-      pk[k] = q - slk[k] * kTpsChunks;
+      const uint32_t part = q - slk[k] * kTpsChunks;
+      pk2[k] = 2u * part;
+      sdst[k] = b0 + slk[k] * kTpsPitch + 16u * part;
     }
   }
   // streams of this batch: body of the warp's first stream, this lane's
@@ -67,7 +70,7 @@ struct RecWindows {
       wlim[k] = __shfl_sync(0xffffffffu, n, slk[k]);
       uint32_t p = st_k + 2u;
       if (p >= cap) p -= cap;
-      p = (p & ~1u) + 2u * pk[k];
+      p = (p & ~1u) + pk2[k];
       if (p >= cap) p -= cap;
       wp[k] = p;
     }
@@ -75,11 +78,10 @@ struct RecWindows {
   // copy the window of chronological positions [c0, c0 + kTpsW) of all 32
   // streams into buffer bsel (windows are issued in order, c0 += kTpsW)
   __device__ __forceinline__ void issue(uint32_t bsel, uint32_t c0) {
-    uint8_t* dst = buf + bsel * (32 * kTpsPitch);
+    const uint32_t boff = bsel * (32 * kTpsPitch);
 #pragma unroll
     for (uint32_t k = 0; k < kTpsChunks; ++k) {
-      if (c0 < wlim[k])
-        cp_async16(dst + slk[k] * kTpsPitch + 16u * pk[k], src[k] + 8u * wp[k]);
+      if (c0 < wlim[k]) cp_async16(sdst[k] + boff, src[k] + 8u * wp[k]);
       wp[k] += kTpsW;
       if (wp[k] >= cap) wp[k] -= cap;
     }

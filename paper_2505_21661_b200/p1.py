@@ -22,6 +22,20 @@ GEMM_LABELS = ["tile", "tma.wait", "tma.issue", "mma.wait", "mma.issue",
                "epi.wait", "epi.ld", "epi.st"]
 GEMM_WARPS = 6
 GEMM_SLOTS = 64
+# attention scopes (csrc_p1/attn_tcgen05.cu), the fa3 fixture's names
+ATTN_LABELS = ["Load K", "Load K.wait", "Load V", "Load V.wait",
+               "GEMM0.c0", "GEMM0.c0.wait", "Softmax.c0", "GEMM1.c0", "GEMM1.c0.wait",
+               "GEMM0.c1", "GEMM0.c1.wait", "Softmax.c1", "GEMM1.c1", "GEMM1.c1.wait"]
+ATTN_WARPS = 10          # stream = warp: 0 K producer, 1 V producer, 2-5 c0, 6-9 c1
+ATTN_SLOTS = 64
+ATTN_ROLE_OF_WARP = [0, 0] + [1] * 8  # producer / consumer roles (overlap counters)
+# barrier edges of the attention kernel (perfmodel.hpp:258-313 derives them
+# from the program's arrive/wait pairs): a landed tile gates the consumer
+# GEMM that reads it; a consumed tile frees the slot the next load fills.
+ATTN_BARRIER_EDGES = [("Load K.wait", "GEMM0.c0"), ("Load K.wait", "GEMM0.c1"),
+                      ("Load V.wait", "GEMM1.c0"), ("Load V.wait", "GEMM1.c1"),
+                      ("GEMM0.c0.wait", "Load K"), ("GEMM0.c1.wait", "Load K"),
+                      ("GEMM1.c0.wait", "Load V"), ("GEMM1.c1.wait", "Load V")]
 CTA_TIMING_DTYPE = np.dtype([("smid", "<u4"), ("streams", "<u4"),
                              ("gt_start", "<u8"), ("gt_end", "<u8"),
                              ("clk_start", "<u4"), ("clk_end", "<u4")])
@@ -42,6 +56,13 @@ def lib() -> C.CDLL:
         L.wgpf_gemm_profile_bytes.restype = u64
         L.wgpf_gemm_smem_bytes.argtypes = [i32]
         L.wgpf_gemm_smem_bytes.restype = u32
+        L.wgpf_attn_bf16.argtypes = [vp, vp, vp, vp, u32, u32, C.c_float, i32, i32,
+                                     vp, vp, vp]
+        L.wgpf_attn_bf16.restype = i32
+        L.wgpf_attn_profile_bytes.argtypes = [u32, u32]
+        L.wgpf_attn_profile_bytes.restype = u64
+        L.wgpf_attn_smem_bytes.argtypes = [i32, i32]
+        L.wgpf_attn_smem_bytes.restype = u32
         _lib = L
     return _lib
 
@@ -93,6 +114,25 @@ def gemm_profile_bytes(M: int, N: int) -> int:
 
 def gemm_smem_bytes(instrument: bool) -> int:
     return int(lib().wgpf_gemm_smem_bytes(int(instrument)))
+
+
+def attention(q_ptr: int, k_ptr: int, v_ptr: int, o_ptr: int, BH: int, S: int,
+              scale: float = 0.0, kv_stages: int = 2, instrument: bool = False,
+              profile_ptr: int = 0, timing_ptr: int = 0, stream: int = 0) -> None:
+    """O = softmax(Q K^T scale) V, bf16 [BH, S, 128]; S % 256 == 0."""
+    _check(lib().wgpf_attn_bf16(C.c_void_p(q_ptr), C.c_void_p(k_ptr), C.c_void_p(v_ptr),
+                                C.c_void_p(o_ptr), BH, S, scale, kv_stages,
+                                int(instrument), C.c_void_p(profile_ptr),
+                                C.c_void_p(timing_ptr), C.c_void_p(stream)),
+           "wgpf_attn_bf16")
+
+
+def attn_profile_bytes(BH: int, S: int) -> int:
+    return int(lib().wgpf_attn_profile_bytes(BH, S))
+
+
+def attn_smem_bytes(instrument: bool, kv_stages: int = 2) -> int:
+    return int(lib().wgpf_attn_smem_bytes(int(instrument), kv_stages))
 
 
 def kpft_v2(body: bytes | np.ndarray, n_streams: int) -> bytes:

@@ -22,13 +22,15 @@
 //          by more than 2^8; FA4's trick, exact after the final 1/l), P = 2^(s
 //          - m) to bf16, written back into S_c's columns (tcgen05.st)
 //   GEMM1  O_c += P_c V_j          (TS: A = P from TMEM, B = V MN-major)
-// and the consumer waits for GEMM1 before the next GEMM0 (P aliases S).
+// and GEMM0 of tile j+1 is issued right behind GEMM1 of tile j by the same
+// thread (in-order tcgen05 pipe: it overwrites P only after GEMM1 read it;
+// its completion implies GEMM1's, which is what the O rescale needs).
 //
 // Scopes (region ids) follow the reference's async pattern
 // (instrument.hpp:14-25: S(X) before the launch, E(X) before the wait,
 // S(X.wait) E(X.wait) after it): producers "Load K"/"Load V" (+ ".wait":
-// the TMA completion), consumers "GEMM0.cN", "GEMM0.cN.wait", "Softmax.cN",
-// "GEMM1.cN", "GEMM1.cN.wait".  One profile stream per warp, circular,
+// the TMA completion), consumers "GEMM0.cN" (+ ".wait": S ready, which also
+// retires the GEMM1 issued just before), "Softmax.cN", "GEMM1.cN".  One profile stream per warp, circular,
 // PROF_CAP slots.
 //
 // KV_STAGES = 1 mirrors fa3_vanilla (single-buffered K / V slots: the next
@@ -59,7 +61,7 @@ constexpr float RESCALE_LOG2 = 8.0f;
 
 enum : uint32_t {
   R_LOAD_K, R_LOAD_K_WAIT, R_LOAD_V, R_LOAD_V_WAIT,
-  R_C0,  // + 5 * c: GEMM0, GEMM0.wait, Softmax, GEMM1, GEMM1.wait
+  R_C0,  // + 4 * c: GEMM0, GEMM0.wait, Softmax, GEMM1
 };
 
 template <uint32_t kStages>
@@ -181,29 +183,36 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t lane_base = (quad * 32u) << 16;
     const uint32_t tS = tmem + c * 128u;          // S, then P (bf16 pairs)
     const uint32_t tO = tmem + 256u + c * 128u;
-    const uint32_t R = R_C0 + 5u * c;
+    const uint32_t R = R_C0 + 4u * c;
     const uint32_t qbase = tc::smem_u32(qs + c * TILE);
     const uint32_t kbase = tc::smem_u32(ks), vbase = tc::smem_u32(vs);
 
     tc::mbar_wait(q_full, 0);
     if (c == 1) tc::bar_sync(3, 256);  // start one softmax behind c0 (ping-pong)
-    float m = -INFINITY, l = 0.f;
-    for (uint32_t j = 0; j < nkv; ++j) {
-      const uint32_t s = j % kStages, ph = (j / kStages) & 1u;
-      // ---- GEMM0: S = Q K_j^T ----
-      tc::mbar_wait(&k_full[s], ph);
+    // GEMM0: S = Q K_j^T into tS (issued one iteration ahead, right behind
+    // GEMM1 of the previous tile; tcgen05.mma from one thread executes in
+    // order, so it overwrites P only after GEMM1 has consumed it, and its
+    // commit implies that GEMM1 -- and with it O -- is complete)
+    auto gemm0 = [&](uint32_t jj) {
+      const uint32_t s1 = jj % kStages, ph1 = (jj / kStages) & 1u;
+      tc::mbar_wait(&k_full[s1], ph1);
       if constexpr (kInstr) rec.start(R + 0);
       if (issuer) {
         tc::fence_after();
-        const uint32_t kt = kbase + s * TILE;
+        const uint32_t kt = kbase + s1 * TILE;
 #pragma unroll
         for (uint32_t kk = 0; kk < HD / 16; ++kk)
           tc::mma_ss(tS, kmaj(qbase, kk), kmaj(kt, kk), IDESC_S, kk);
         tc::mma_commit(&s_full[c]);
-        tc::mma_commit(&k_empty[s]);
+        tc::mma_commit(&k_empty[s1]);
       }
       __syncwarp();
       if constexpr (kInstr) rec.end(R + 0);
+    };
+    gemm0(0);
+    float m = -INFINITY, l = 0.f;
+    for (uint32_t j = 0; j < nkv; ++j) {
+      const uint32_t s = j % kStages, ph = (j / kStages) & 1u;
       tc::mbar_wait(&s_full[c], j & 1u);
       tc::fence_after();
       if constexpr (kInstr) {
@@ -275,18 +284,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (uint32_t kk = 0; kk < BKV / 16; ++kk)
           tc::mma_ts(tO, tS + kk * 8u, tc::desc_mn_sw128(vt + kk * 2048u, HALF),
                      IDESC_PV, (j | kk) != 0u);
-        tc::mma_commit(&o_done[c]);
         tc::mma_commit(&v_empty[s]);
+        if (j + 1 == nkv) tc::mma_commit(o_done + c);
       }
       __syncwarp();
       if constexpr (kInstr) rec.end(R + 3);
-      tc::mbar_wait(&o_done[c], j & 1u);
-      tc::fence_after();
-      if constexpr (kInstr) {
-        rec.start(R + 4);
-        rec.end(R + 4);
-      }
+      if (j + 1 < nkv) gemm0(j + 1);
     }
+    tc::mbar_wait(o_done + c, 0);
+    tc::fence_after();
     // ---- epilogue: O / l -> bf16 -> HBM (one row per thread) ----
     const float inv = 1.f / l;
     const uint64_t orow = (uint64_t)row0 + q0 + c * BQ + quad * 32u + lane;
@@ -342,11 +348,10 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
 
 // Labels of the attention kernel's region ids (the plan's region table).
 extern "C" const char* wgpf_attn_label(uint32_t id) {
-  static const char* L[] = {"Load K",        "Load K.wait",   "Load V",
-                            "Load V.wait",   "GEMM0.c0",      "GEMM0.c0.wait",
-                            "Softmax.c0",    "GEMM1.c0",      "GEMM1.c0.wait",
-                            "GEMM0.c1",      "GEMM0.c1.wait", "Softmax.c1",
-                            "GEMM1.c1",      "GEMM1.c1.wait"};
+  static const char* L[] = {"Load K",   "Load K.wait",   "Load V",
+                            "Load V.wait", "GEMM0.c0", "GEMM0.c0.wait",
+                            "Softmax.c0",  "GEMM1.c0", "GEMM0.c1",
+                            "GEMM0.c1.wait", "Softmax.c1", "GEMM1.c1"};
   return id < sizeof(L) / sizeof(L[0]) ? L[id] : nullptr;
 }
 

@@ -24,8 +24,8 @@ GEMM_WARPS = 6
 GEMM_SLOTS = 64
 # attention scopes (csrc_p1/attn_tcgen05.cu), the fa3 fixture's names
 ATTN_LABELS = ["Load K", "Load K.wait", "Load V", "Load V.wait",
-               "GEMM0.c0", "GEMM0.c0.wait", "Softmax.c0", "GEMM1.c0", "GEMM1.c0.wait",
-               "GEMM0.c1", "GEMM0.c1.wait", "Softmax.c1", "GEMM1.c1", "GEMM1.c1.wait"]
+               "GEMM0.c0", "GEMM0.c0.wait", "Softmax.c0", "GEMM1.c0",
+               "GEMM0.c1", "GEMM0.c1.wait", "Softmax.c1", "GEMM1.c1"]
 ATTN_WARPS = 10          # stream = warp: 0 K producer, 1 V producer, 2-5 c0, 6-9 c1
 ATTN_SLOTS = 64
 ATTN_ROLE_OF_WARP = [0, 0] + [1] * 8  # producer / consumer roles (overlap counters)
@@ -35,7 +35,7 @@ ATTN_ROLE_OF_WARP = [0, 0] + [1] * 8  # producer / consumer roles (overlap count
 ATTN_BARRIER_EDGES = [("Load K.wait", "GEMM0.c0"), ("Load K.wait", "GEMM0.c1"),
                       ("Load V.wait", "GEMM1.c0"), ("Load V.wait", "GEMM1.c1"),
                       ("GEMM0.c0.wait", "Load K"), ("GEMM0.c1.wait", "Load K"),
-                      ("GEMM1.c0.wait", "Load V"), ("GEMM1.c1.wait", "Load V")]
+                      ("GEMM0.c0.wait", "Load V"), ("GEMM0.c1.wait", "Load V")]
 CTA_TIMING_DTYPE = np.dtype([("smid", "<u4"), ("streams", "<u4"),
                              ("gt_start", "<u8"), ("gt_end", "<u8"),
                              ("clk_start", "<u4"), ("clk_end", "<u4")])

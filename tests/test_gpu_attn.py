@@ -83,6 +83,17 @@ def test_attention_structured_inputs():
     assert ok, err
 
 
+def test_attention_is_deterministic():
+    """GEMM0 of tile j+1 is issued behind GEMM1 of tile j into the TMEM columns
+    GEMM1 reads P from: any ordering race would show as run-to-run noise."""
+    import torch
+    q, k, v = inputs(16, 2048, seed=5, scale_q=2.0)
+    for stages in (1, 2):
+        o0 = run(q, k, v, stages)
+        for _ in range(3):
+            assert torch.equal(run(q, k, v, stages), o0)
+
+
 def test_attention_rejects_bad_shapes():
     import torch
     q = torch.zeros(1, 384, 128, dtype=torch.bfloat16, device="cuda")
@@ -112,7 +123,7 @@ def test_instrumented_attention_trace(ctx, oracle, stages):
     assert np.array_equal(hdr[:, 1], np.tile(np.arange(p1.ATTN_WARPS), ctas))
     nkv = S // 128
     assert np.all(hdr[:2 * 10:10, 2] == 4 * nkv)        # producers: 4 per tile
-    assert np.all(hdr[2:10, 2] == 10 * nkv)             # consumers: 10 per tile
+    assert np.all(hdr[2:10, 2] == 8 * nkv)              # consumers: 8 per tile
 
     want = oracle.replay_body(body, n_streams, p1.ATTN_SLOTS, 0, p1.ATTN_LABELS, 0)
     ctx.set_plan(T.BufferPlan(p1.ATTN_SLOTS, T.BufferStrategy.Circular, p1.ATTN_LABELS))

@@ -36,6 +36,8 @@
 // Histograms: one per-CTA table, one shared atomic per event.
 #pragma once
 
+#include <type_traits>
+
 #include "k_fast.cuh"
 #include "k_window.cuh"
 
@@ -192,15 +194,17 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     bool broken = false;  // single-stack nesting broken or a pair >= 2^32:
                           // the exact general path redoes the stream
 
-    // a stream's events fit the caller's buffer unless it ends past the
-    // capacity (events <= records): then each store is checked
-    const bool fits = off + n <= a.events_cap;
+    // events of this stream that fit the caller's buffer (events <= records,
+    // so a stream ending inside the capacity needs no per-store check)
+    const uint32_t lim = off + n <= a.events_cap
+                             ? 0xFFFFFFFFu
+                             : (off < a.events_cap ? (uint32_t)(a.events_cap - off) : 0u);
+    wgpf_event* const ev0 = a.events + (act ? off : 0ull);
     auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
                    uint32_t ehi, uint32_t region, uint32_t it) {
-      const uint64_t idx = off + k;
-      const bool ok = p & (fits | (idx < a.events_cap));
+      const bool ok = p & (k < lim);
       if (ok) {
-        uint4* q = reinterpret_cast<uint4*>(a.events + idx);
+        uint4* q = reinterpret_cast<uint4*>(ev0 + k);
         q[0] = make_uint4(slo, shi, elo, ehi);
         q[1] = make_uint4(region, it, blk, wg);
       }
@@ -222,8 +226,11 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       sts128_if(p, ea, x);
       red_add_if(p, s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)), 1u);
     };
-    auto step = [&](uint32_t i, uint2 r2) {
-      const bool valid = i < n;
+    // kFull: positions i .. i+2 exist on every lane (the bulk of the walk):
+    // no per-record bounds predicates
+    auto step = [&](auto full, uint32_t i, uint2 r2) {
+      constexpr bool kFull = decltype(full)::value;
+      const bool valid = kFull || i < n;
       const uint32_t tag = r0.x, v = r0.y;
       const bool isS = (int32_t)tag < 0;
       const bool st = valid && isS;
@@ -262,9 +269,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const uint32_t ovh = cost * dpos;  // + __umulhi: the 64-bit product
       const uint32_t corr = (__umulhi(cost, dpos) != 0u || ovh > meas) ? 0u : meas - ovh;
       // ---- wait marker START at i+1 -------------------------------------------
-      const bool cclose = i + 2 < n && (int32_t)r2.x >= 0 &&
+      const bool cclose = (kFull || i + 2 < n) && (int32_t)r2.x >= 0 &&
                           ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;
-      const bool consumed = base && i + 1 < n && (int32_t)r1.x < 0 &&
+      const bool consumed = base && (kFull || i + 1 < n) && (int32_t)r1.x < 0 &&
                             (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
                             ((int32_t)(i + 1) <= z || cclose);
       const uint32_t wd = r1.y - v;  // consecutive records: u1 - u < 2^32
@@ -293,6 +300,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       r1 = r2;
     };
 
+    const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
     for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
       const uint32_t bsel = (w0 / kTpsW) & 1u;
       if (w0 + kTpsW < nmax) win.issue(bsel ^ 1u, w0 + kTpsW + 2u);
@@ -300,9 +308,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       cp_async_wait1();
       __syncwarp();
       const uint2* myrec = win.lane_records(bsel, lane, start);
+      if (w0 + kTpsW + 2u <= nmin) {
 #pragma unroll
-      for (uint32_t j = 0; j < kTpsW; ++j) {
-        step(w0 + j, myrec[j]);
+        for (uint32_t j = 0; j < kTpsW; ++j)
+          step(std::true_type{}, w0 + j, myrec[j]);
+      } else {
+#pragma unroll 1
+        for (uint32_t j = 0; j < kTpsW; ++j)
+          step(std::false_type{}, w0 + j, myrec[j]);
       }
       __syncwarp();
     }

@@ -10,6 +10,8 @@ overlap) timeout 600 python -m pytest tests/test_gpu_overlap.py -q --timeout 200
 slow) timeout 900 python -m pytest tests -q -m "slow" --timeout 800 -p no:cacheprovider > $OUT/slow.txt 2>&1; echo "rc=$?" >> $OUT/slow.txt ;;
 benchsmall) timeout 400 python bench.py --streams 262144 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/bench_small.json 2> $OUT/bench_small.err ;;
 
+parity) timeout 900 python -m pytest tests/test_gpu_parity.py -x -q --timeout 300 -p no:cacheprovider > $OUT/parity.txt 2>&1; echo "rc=$?" >> $OUT/parity.txt ;;
+quick) timeout 600 python bench.py --no-e2e --no-cpu-baseline --no-p1 > $OUT/quick.json 2> $OUT/quick.err ;;
 bench) timeout 1200 python bench.py > $OUT/bench.json 2> $OUT/bench.err ;;
 bench5) timeout 1200 python bench.py --config 5 --no-p1 > $OUT/bench5.json 2> $OUT/bench5.err ;;
 benchref) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err ;;

@@ -622,7 +622,9 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.list = nullptr;
   f.list_len = nullptr;
   f.tps_regions = tps_regions(c);
-  if (tps_enabled(c) && record_cost <= 0xFFFFFFFFull) {
+  // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
+  // correction arithmetic; larger costs take the warp-per-stream kernel)
+  if (tps_enabled(c) && record_cost < (1ull << 21)) {
     // shallow streams: thread per stream; then the SF_WARP list
     const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
     const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const bool abort_all = a.status->decode_err != kNoErr;
   const uint32_t FULL = 0xffffffffu;
   const uint32_t lt = lanemask_lt();
-  const uint32_t cost = (uint32_t)a.record_cost;  // host: < 2^32 on this path
+  const uint32_t cost = (uint32_t)a.record_cost;  // host: < 2^21 on this path
   const uint32_t cap = a.cap;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0, w_ovf = 0;
 
@@ -266,8 +266,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
       // ---- exec event: sync correction ---------------------------------------
       const uint32_t dpos = i - (e.y & 2047u);
-      const uint32_t ovh = cost * dpos;  // + __umulhi: the 64-bit product
-      const uint32_t corr = (__umulhi(cost, dpos) != 0u || ovh > meas) ? 0u : meas - ovh;
+      // dpos < 2^11 and cost < 2^21 (host): the product fits 32 bits
+      const uint32_t ovh = cost * dpos;
+      const uint32_t corr = ovh > meas ? 0u : meas - ovh;
       // ---- wait marker START at i+1 -------------------------------------------
       const bool cclose = (kFull || i + 2 < n) && (int32_t)r2.x >= 0 &&
                           ((r2.x >> 12) & (kTpsRegions - 1u)) == r1id;

@@ -131,6 +131,11 @@ def test_gpu_synth_generator_matches_cpu(ctx, shape):
 # labels, orphans, clock wraps, errors)
 # ---------------------------------------------------------------------------
 
+# record costs around the thread-per-stream kernel's bound (cost < 2^21 keeps
+# cost x position in 32 bits; larger costs route to the warp-per-stream path)
+COSTS = [33, 0, 1, (1 << 21) - 1, 1 << 21, (1 << 32) + 5]
+
+
 @pytest.mark.parametrize("mode", ["nested", "random"])
 @pytest.mark.parametrize("path", list(FLAG_MODES))
 def test_fuzz_vs_oracle(ctx, oracle, mode, path):
@@ -139,13 +144,14 @@ def test_fuzz_vs_oracle(ctx, oracle, mode, path):
         data, cap, strategy, labels = fuzz.random_image(
             1000 + seed, n_streams=12, cap=32 if seed % 2 else 64, mode=mode,
             big_gaps=(seed % 3 == 0))
+        cost = COSTS[seed % len(COSTS)] if seed >= 40 else 33
         try:
-            o = oracle.replay_kpft(data, cap, strategy, labels, 33)
+            o = oracle.replay_kpft(data, cap, strategy, labels, cost)
             oerr = None
         except O.OracleError as e:
             o, oerr = None, (e.category, str(e))
         try:
-            r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33,
+            r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), cost,
                                        flags=FLAG_MODES[path] | 0x2)
             gerr = None
         except t.Error as e:

@@ -186,7 +186,11 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     win.issue(0, 2);
     cp_async_commit();
 
-    uint32_t hi = 0, vprev = 0, sp = 0;
+    // stack top as a shared address: row sp-1 of the lane's column; the
+    // empty stack points one row below (bytes of the record windows: read,
+    // never written, and only used when an END has a partner)
+    const uint32_t s_stk0 = s_stk - 256u;
+    uint32_t hi = 0, vprev = 0, stop = s_stk0;
     uint32_t pw = 0xFFu;  // wait class of the previous record if it was a
                           // matched base END, else none
     uint32_t kw = 0;      // events of this stream written
@@ -242,13 +246,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       hi += (valid && v < vprev) ? 1u : 0u;
       vprev = valid ? v : vprev;
       // ---- stack ------------------------------------------------------------
-      const uint2 e = lds64(s_stk + 256u * (sp ? sp - 1u : 0u));
-      const bool mend = en && sp != 0;
-      w_drop += (en && sp == 0) ? 1u : 0u;
-      sts64_if(st, s_stk + 256u * sp,
+      const uint2 e = lds64(stop);
+      const bool nonempty = stop != s_stk0;
+      const bool mend = en && nonempty;
+      w_drop += (en && !nonempty) ? 1u : 0u;
+      sts64_if(st, stop + 256u,
                make_uint2(v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 16) |
                                  (hi << 17)));
-      sp = sp + (st ? 1u : 0u) - (mend ? 1u : 0u);
+      stop = stop + (st ? 256u : 0u) - (mend ? 256u : 0u);
       const uint32_t shi = e.y >> 17;
       const uint32_t meas = v - e.x;  // low 32 bits of u - su
       const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool ok = mend && !mism && !tlong;
       // (rows exist for region ids < R; positions past the stream end hold
       // arbitrary tags, so clamp -- the value is only used when ok)
-      const uint32_t ca = s_cnt + 64u * min(rid, R - 1u);
+      const uint32_t ca = s_cnt + 64u * (kFull ? rid : min(rid, R - 1u));
       const uint32_t it = lds16(ca);
       sts16_if(ok, ca, it + 1u);
       const bool is_mk = (inf & 0x100u) != 0u;
@@ -341,7 +346,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       }
       if (!bad) {
         w_mal += n_orph;
-        w_tail += sp;
+        w_tail += (stop - s_stk0) >> 8;
       }
     }
   }

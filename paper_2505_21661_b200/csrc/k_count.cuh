@@ -185,11 +185,13 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
 // owns stream 32 b + l and walks its records sequentially, windows staged in
 // shared memory (k_window.cuh).  Used when the capacity is even and at most
 // kTpsMaxSlots (the record windows need 16-B chunk alignment).
-constexpr uint32_t kCountWarps = 8;
+constexpr uint32_t kCountWarps = 4;
+constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
+using CountWin = RecWindowsT<kCountW>;
 
 __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
   __shared__ uint8_t marker_region[256];
-  __shared__ __align__(16) uint8_t recbuf[kCountWarps][2 * 32 * kTpsPitch];
+  __shared__ __align__(16) uint8_t recbuf[kCountWarps][2 * 32 * CountWin::kTpsPitch];
   for (uint32_t r = threadIdx.x; r < 256; r += blockDim.x)
     marker_region[r] =
         r < a.fast_regions ? class_is_marker(a.plan, a.plan.class_of[r]) : 0;
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
   const uint32_t lane = lane_id();
   const uint32_t w = threadIdx.x >> 5;
   const uint32_t cap = (uint32_t)a.plan.slots;
-  RecWindows win;
+  CountWin win;
   win.init(recbuf[w], lane, a.stride, cap);
   const uint64_t wstep = (uint64_t)gridDim.x * kCountWarps;
   for (uint64_t b = (uint64_t)blockIdx.x * kCountWarps + w; b * 32 < a.n_streams;
@@ -247,15 +249,15 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
     int32_t q = 0, run_min = 0, max_d = 0, z = -1, last_bad = -1;
     uint32_t maxrid = 0;  // region-id range: fast / thread-per-stream routing
     bool prev_end = false;
-    for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
-      const uint32_t bsel = (w0 / kTpsW) & 1u;
-      if (w0 + kTpsW < nmax) win.issue(bsel ^ 1u, w0 + kTpsW + 2u);
+    for (uint32_t w0 = 0; w0 < nmax; w0 += kCountW) {
+      const uint32_t bsel = (w0 / kCountW) & 1u;
+      if (w0 + kCountW < nmax) win.issue(bsel ^ 1u, w0 + kCountW + 2u);
       cp_async_commit();
       cp_async_wait1();
       __syncwarp();
       const uint2* rec = win.lane_records(bsel, lane, start);
 #pragma unroll
-      for (uint32_t j = 0; j < kTpsW; ++j) {
+      for (uint32_t j = 0; j < kCountW; ++j) {
         const uint32_t t2 = rec[j].x;
         const uint32_t i = w0 + j;
         const bool valid = i < n;

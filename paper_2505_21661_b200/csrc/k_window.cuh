@@ -17,9 +17,15 @@
 
 namespace wgpf {
 
-constexpr uint32_t kTpsW = 8;                         // records per window
-constexpr uint32_t kTpsChunks = (kTpsW + 2) / 2;      // 16-B chunks per window
-constexpr uint32_t kTpsPitch = 16 * kTpsChunks;       // bytes per lane window
+// records per window: kW (template); the emit kernel uses kTpsW
+template <uint32_t kW>
+struct WinGeom {
+  static constexpr uint32_t kChunks = (kW + 2) / 2;  // 16-B chunks per window
+  static constexpr uint32_t kPitch = 16 * kChunks;   // bytes per lane window
+};
+constexpr uint32_t kTpsW = 8;
+constexpr uint32_t kTpsChunks = WinGeom<kTpsW>::kChunks;
+constexpr uint32_t kTpsPitch = WinGeom<kTpsW>::kPitch;
 constexpr uint32_t kTpsMaxSlots = 2046;               // even; pos fits 11 bits
 
 __device__ __forceinline__ void cp_async16(uint32_t sdst, const void* src) {
@@ -33,7 +39,11 @@ __device__ __forceinline__ void cp_async_wait1() {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
 
-struct RecWindows {
+template <uint32_t kW = kTpsW>
+struct RecWindowsT {
+  static constexpr uint32_t kTpsW = kW;
+  static constexpr uint32_t kTpsChunks = WinGeom<kW>::kChunks;
+  static constexpr uint32_t kTpsPitch = WinGeom<kW>::kPitch;
   uint32_t slk[kTpsChunks];                  // static chunk assignment:
   uint32_t sdst[kTpsChunks];                 //   stream, shared destination
   uint32_t wp[kTpsChunks], wlim[kTpsChunks]; // physical slot, stream length
@@ -93,5 +103,6 @@ struct RecWindows {
                                           lane * kTpsPitch + 8u * (start & 1u));
   }
 };
+using RecWindows = RecWindowsT<kTpsW>;
 
 }  // namespace wgpf

@@ -27,6 +27,8 @@
 // closed later.
 #pragma once
 
+#include <type_traits>
+
 #include "wgpf_dev.cuh"
 #include "k_window.cuh"
 
@@ -249,6 +251,34 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
     int32_t q = 0, run_min = 0, max_d = 0, z = -1, last_bad = -1;
     uint32_t maxrid = 0;  // region-id range: fast / thread-per-stream routing
     bool prev_end = false;
+    // kFull: positions i, i+1 exist on every lane -- no bounds predicates
+    auto step = [&](auto full, uint32_t i, uint32_t t2) {
+      constexpr bool kFull = decltype(full)::value;
+      const bool valid = kFull || i < n;
+      const bool isS = (int32_t)t0 < 0;
+      const uint32_t rid = (t0 >> 12) & (WGPF_MAX_REGIONS - 1u);
+      maxrid = valid ? max(maxrid, rid) : maxrid;
+      q += valid ? 2 * (int32_t)(t0 >> 31) - 1 : 0;  // START +1, END -1
+      run_min = min(run_min, q);
+      const int32_t d = q - run_min;
+      z = (valid && d == 0) ? (int32_t)i : z;
+      max_d = max(max_d, d);
+      // a wait-marker START right after an END that the next record does
+      // not close: only z can tell whether it is ever closed
+      uint32_t mk;
+      if (rid < 32u)
+        mk = (mbits >> rid) & 1u;
+      else
+        mk = rid < a.fast_regions ? marker_region[rid & 255u] : 0u;
+      const bool mk_start = valid && isS && prev_end && mk;
+      const bool closed_next = (kFull || i + 1 < n) && (int32_t)t1 >= 0 &&
+                               ((t1 >> 12) & (WGPF_MAX_REGIONS - 1u)) == rid;
+      last_bad = (mk_start && !closed_next) ? (int32_t)i : last_bad;
+      prev_end = valid && !isS;
+      t0 = t1;
+      t1 = t2;
+    };
+    const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
     for (uint32_t w0 = 0; w0 < nmax; w0 += kCountW) {
       const uint32_t bsel = (w0 / kCountW) & 1u;
       if (w0 + kCountW < nmax) win.issue(bsel ^ 1u, w0 + kCountW + 2u);
@@ -256,33 +286,12 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
       cp_async_wait1();
       __syncwarp();
       const uint2* rec = win.lane_records(bsel, lane, start);
+      if (w0 + kCountW + 1u <= nmin) {
 #pragma unroll
-      for (uint32_t j = 0; j < kCountW; ++j) {
-        const uint32_t t2 = rec[j].x;
-        const uint32_t i = w0 + j;
-        const bool valid = i < n;
-        const bool isS = (int32_t)t0 < 0;
-        const uint32_t rid = (t0 >> 12) & (WGPF_MAX_REGIONS - 1u);
-        maxrid = valid ? max(maxrid, rid) : maxrid;
-        q += valid ? 2 * (int32_t)(t0 >> 31) - 1 : 0;  // START +1, END -1
-        run_min = min(run_min, q);
-        const int32_t d = q - run_min;
-        z = (valid && d == 0) ? (int32_t)i : z;
-        max_d = max(max_d, d);
-        // a wait-marker START right after an END that the next record does
-        // not close: only z can tell whether it is ever closed
-        uint32_t mk;
-        if (rid < 32u)
-          mk = (mbits >> rid) & 1u;
-        else
-          mk = rid < a.fast_regions ? marker_region[rid & 255u] : 0u;
-        const bool mk_start = valid && isS && prev_end && mk;
-        const bool closed_next = i + 1 < n && (int32_t)t1 >= 0 &&
-                                 ((t1 >> 12) & (WGPF_MAX_REGIONS - 1u)) == rid;
-        last_bad = (mk_start && !closed_next) ? (int32_t)i : last_bad;
-        prev_end = valid && !isS;
-        t0 = t1;
-        t1 = t2;
+        for (uint32_t j = 0; j < kCountW; ++j) step(std::true_type{}, w0 + j, rec[j].x);
+      } else {
+#pragma unroll 1
+        for (uint32_t j = 0; j < kCountW; ++j) step(std::false_type{}, w0 + j, rec[j].x);
       }
       __syncwarp();
     }

@@ -144,8 +144,10 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   RecWindows win;
   win.init(ws.rec[0], lane, a.stride, cap);
   // 32-bit shared addresses of the hot tables (this lane's column)
-  const uint32_t s_info = smem_addr(cs.info);
-  const uint32_t s_hist = smem_addr(hist);
+  // (opaque: kept in registers instead of being rebuilt from the CTA's
+  // shared window base at every use)
+  const uint32_t s_info = opaque_u32(smem_addr(cs.info));
+  const uint32_t s_hist = opaque_u32(smem_addr(hist));
   const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);    // + 256 * level
   const uint32_t s_cnt = smem_addr(tb.cnt + lane);        // + 64 * region
   const uint32_t s_a = smem_addr(tb.a + lane);            // + 512 * class

@@ -481,6 +481,25 @@ class Reference:
                                        C.c_uint64, C.c_uint64, C.c_int,
                                        C.POINTER(_RBenchOut)]
 
+    def export_chrome(self, events: np.ndarray, labels, cycles_per_us: float = 1000.0) -> str:
+        """export_chrome_trace (trace.hpp:493-511) over this framework's event
+        array (the reference's own JSON writer, nlohmann 3.11.3)."""
+        L = self.lib
+        L.ref_export_chrome.argtypes = [C.c_void_p, C.c_uint64, C.c_char_p, C.c_uint32,
+                                        C.c_double, C.POINTER(C.c_void_p),
+                                        C.POINTER(_RStatus)]
+        L.ref_export_chrome.restype = C.c_int64
+        L.ref_free_text.argtypes = [C.c_void_p]
+        ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+        p, st = C.c_void_p(), _RStatus()
+        n = L.ref_export_chrome(ev.ctypes.data, len(ev), label_blob(labels), len(labels),
+                                cycles_per_us, C.byref(p), C.byref(st))
+        st.raise_if()
+        try:
+            return C.string_at(p, n).decode()
+        finally:
+            L.ref_free_text(p)
+
     def replay_kpft(self, data: bytes, slots: int, strategy: int, labels,
                     record_cost: int) -> RefReplay:
         buf = np.frombuffer(data, np.uint8)

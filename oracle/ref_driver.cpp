@@ -667,4 +667,49 @@ int ref_bench_replay(const uint8_t* body, uint64_t n_streams, uint64_t slots,
   return out->st.code;
 }
 
+// export_chrome_trace (trace.hpp:493-511) of an event array in this
+// framework's 32-byte layout (wgpf_event: start, end, region | WAIT<<31 |
+// CORRECTED<<30, iteration, block, warp_group; label = labels[region] or
+// "region#<id>", trace.hpp:302-306).  *out is malloc'ed (free with
+// ref_free_text); returns the byte count, or -1 with st set.
+struct ref_wgpf_event {
+  uint64_t start, end;
+  uint32_t region, iteration, block, wg;
+};
+
+int64_t ref_export_chrome(const ref_wgpf_event* ev, uint64_t n,
+                          const char* label_blob, uint32_t n_labels,
+                          double cycles_per_us, char** out, ref_status* st) {
+  try {
+    const auto labels = split_blob(label_blob, n_labels);
+    std::vector<R::TimelineEvent> evs;
+    evs.reserve(n);
+    for (uint64_t i = 0; i < n; ++i) {
+      R::TimelineEvent t;
+      const uint32_t rid = ev[i].region & 0x3FFFFFFFu;
+      t.region = rid < labels.size() ? labels[rid] : "region#" + std::to_string(rid);
+      t.kind = (ev[i].region >> 31) ? R::EventKind::Wait : R::EventKind::Exec;
+      t.corrected = ((ev[i].region >> 30) & 1u) != 0;
+      t.start = ev[i].start;
+      t.end = ev[i].end;
+      t.iteration = ev[i].iteration;
+      t.block_index = ev[i].block;
+      t.warp_group = ev[i].wg;
+      evs.push_back(std::move(t));
+    }
+    const std::string js = R::export_chrome_trace(evs, cycles_per_us);
+    *out = static_cast<char*>(std::malloc(js.size() + 1));
+    std::memcpy(*out, js.data(), js.size());
+    set_ok(st);
+    return static_cast<int64_t>(js.size());
+  } catch (const R::Error& e) {
+    set_err(st, e);
+  } catch (const std::exception& e) {
+    set_other(st, e);
+  }
+  return -1;
+}
+
+void ref_free_text(char* p) { std::free(p); }
+
 } // extern "C"

@@ -33,6 +33,7 @@
 #include "k_stats.cuh"
 #include "k_synth.cuh"
 #include "k_cp.cuh"
+#include "k_chrome.cuh"
 #include <cmath>
 #include <functional>
 #include <memory>
@@ -109,7 +110,7 @@ struct wgpf_ctx {
   // per call
   DevBuf d_status, d_counts, d_zpos, d_sflag, d_offsets, d_scan_tmp, d_glist,
       d_glen, d_orphans, d_gscratch, d_image, d_events, d_aux0, d_aux1, d_aux2,
-      d_aux3, d_repack;
+      d_aux3, d_repack, d_chrome;
   DevStatus* h_status = nullptr;  // pinned
   // profiling
   cudaEvent_t ev[8] = {};

@@ -454,3 +454,64 @@ def test_chrome_trace_export_empty_and_escaping(ctx):
     d = J.loads(js)["traceEvents"][0]
     assert d["name"] == 'we"ird\\lab\tel' and d["dur"] == 1.0 and d["pid"] == 1
     del t
+
+
+def random_chrome_events(seed, n, n_labels):
+    rng = np.random.default_rng(seed)
+    start = rng.integers(0, 1 << 62, n, dtype=np.uint64) >> rng.integers(0, 62, n).astype(np.uint64)
+    dur = rng.integers(0, 1 << 40, n, dtype=np.uint64) >> rng.integers(0, 40, n).astype(np.uint64)
+    rid = rng.integers(0, n_labels + 40, n).astype(np.uint32)   # some out of table
+    flags = rng.integers(0, 4, n).astype(np.uint32) << 30
+    ev = np.zeros(n, O.EVENT_DTYPE)
+    ev["start"], ev["end"] = start, start + dur
+    ev["region"] = rid | flags
+    ev["iteration"] = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32) >> \
+        rng.integers(0, 32, n).astype(np.uint32)
+    ev["block_index"] = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32) >> \
+        rng.integers(0, 32, n).astype(np.uint32)
+    ev["warp_group"] = rng.integers(0, 64, n).astype(np.uint32)
+    return ev
+
+
+@pytest.mark.parametrize("cpu", [1000.0, 1965.0, 1.0, 0.37])
+def test_chrome_trace_gpu_formatter_vs_reference(ctx, reference, cpu):
+    """The GPU formatter (events in HBM, k_chrome.cuh) and the host writer
+    produce the reference's own export_chrome_trace text byte for byte on
+    random events: 2^62-scale clocks, B200 cycles_per_us = 1965 (17-digit
+    doubles where Grisu2 differs from the shortest representation), labels
+    needing escapes, out-of-table region ids."""
+    import torch
+    labels = ["Load K", "GEMM0.c0", "we\"ird\\lab\tel", "Softmax.c1", "x" * 150, "é"]
+    labels = labels[:5]
+    ctx.set_plan(plan_of(8, 0, labels))
+    ev = random_chrome_events(int(cpu * 7) + 1, 3000, len(labels))
+    want = reference.export_chrome(ev, labels, cpu)
+    d = torch.from_numpy(ev.view(np.uint8).copy()).cuda()
+    assert ctx.export_chrome_trace(None, cpu, on_device_ptr=d.data_ptr(),
+                                   n_events=len(ev)) == want
+    assert ctx.export_chrome_trace(ev, cpu) == want
+
+
+def test_chrome_trace_gpu_formatter_attention_trace(ctx, reference):
+    """A real device trace (the instrumented attention kernel, decoded on the
+    GPU) exported on the GPU == the reference's export of the same events."""
+    import torch
+    from paper_2505_21661_b200 import p1
+    BH, S = 2, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(BH, S, 128, generator=g, device="cuda").to(torch.bfloat16)
+               for _ in range(3))
+    o = torch.empty_like(q)
+    prof = torch.zeros(p1.attn_profile_bytes(BH, S), dtype=torch.uint8, device="cuda")
+    p1.attention(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), BH, S,
+                 instrument=True, profile_ptr=prof.data_ptr())
+    ns = BH * S // 256 * p1.ATTN_WARPS
+    t = T()
+    ctx.set_plan(t.BufferPlan(p1.ATTN_SLOTS, t.BufferStrategy.Circular, p1.ATTN_LABELS))
+    ev = torch.empty(ns * p1.ATTN_SLOTS * 32, dtype=torch.uint8, device="cuda")
+    ne, _ = ctx.replay_device(prof.data_ptr(), prof.numel(), ns, 0, ev.data_ptr(),
+                              ns * p1.ATTN_SLOTS)
+    host = ev[: ne * 32].cpu().numpy().view(O.EVENT_DTYPE)
+    want = reference.export_chrome(host, p1.ATTN_LABELS, 1965.0)
+    assert ctx.export_chrome_trace(None, 1965.0, on_device_ptr=ev.data_ptr(),
+                                   n_events=ne) == want

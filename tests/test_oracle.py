@@ -379,3 +379,38 @@ def test_fuzz_oracle_vs_reference(oracle, reference, mode):
         assert [(s.label, s.warp_group, s.kind, s.count, s.min, s.max, s.mean)
                 for s in st] == [(s.label, s.warp_group, s.kind, s.count, s.min,
                                   s.max, s.mean) for s in rr.stats], seed
+
+
+# ---------------------------------------------------------------------------
+# Chrome Trace numbers: Grisu2 as the reference's JSON library prints doubles
+# ---------------------------------------------------------------------------
+
+JSON_DIR = ("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/"
+            "cudnn_frontend/thirdparty/nlohmann")
+
+
+def test_grisu2_matches_reference_json_library(tmp_path):
+    """include/wgpf_grisu2.h (shared by the host and GPU Chrome exporters)
+    prints every double byte-identically to nlohmann/json 3.11.3 -- including
+    the values where Grisu2 is not the shortest round trip (std::to_chars)."""
+    import subprocess
+    if not os.path.exists(os.path.join(JSON_DIR, "json.hpp")):
+        pytest.skip("nlohmann/json header not in this image")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "grisu2_test")
+    res = subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(root, "include"),
+                          "-I", JSON_DIR, os.path.join(root, "tests", "cxx", "grisu2_test.cpp"),
+                          "-o", exe], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr[-2000:]
+    res = subprocess.run([exe, "1000000", "11"], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-2000:]
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_reference_chrome_export_entry_point(reference, oracle, name):
+    """oracle/_ref's export_chrome_trace entry point reproduces the shipped
+    out/<fixture>.json byte for byte from the oracle's events."""
+    data, slots, strategy, labels, cost, _ = load_fixture(name)
+    r = oracle.replay_kpft(data, slots, strategy, labels, cost)
+    got = reference.export_chrome(r.events, labels, 1000.0)
+    assert got == open(os.path.join(GOLDEN, "fixtures", name + ".json")).read()

@@ -261,6 +261,25 @@ def measure_attn(B: int = 16, H: int = 16, S: int = 8192, iters: int = 20,
             ov = ctx.overlap(None, p1.ATTN_ROLE_OF_WARP, on_device_ptr=ev.data_ptr(),
                              n_events=ne)
             key = "kv_double_buffered" if stages == 2 else "kv_single_buffered_fa3_vanilla"
+            chrome = None
+            if stages == 1:  # export_chrome_trace of the whole decoded trace
+                import time
+                t0 = time.perf_counter()
+                js = ctx.export_chrome_trace(None, 1965.0, on_device_ptr=ev.data_ptr(),
+                                             n_events=ne)
+                t_gpu = time.perf_counter() - t0
+                host = ev[: ne * 32].cpu().numpy().view(T.EVENT_DTYPE)
+                t0 = time.perf_counter()
+                js2 = ctx.export_chrome_trace(host, 1965.0)
+                t_host = time.perf_counter() - t0
+                chrome = {"bytes": len(js), "events": ne, "gpu_s": t_gpu,
+                          "host_writer_s": t_host, "identical": js == js2,
+                          "note": "wall clock of the C-ABI call incl. the D2H copy of "
+                                  "the text; GPU path = k_chrome_len + scan + "
+                                  "k_chrome_write"}
+                del js, js2
+            if chrome:
+                line["chrome_export"] = chrome
             line[key]["analysis"] = {
                 "events": ne,
                 "scope_mean_cycles": {k_: round(v_.mean, 1) for k_, v_ in st.items()},

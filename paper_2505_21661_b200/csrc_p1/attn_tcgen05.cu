@@ -58,6 +58,10 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t IDESC_S = tc::idesc_bf16(128, 128, false);
 constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, HD, true);
 constexpr float RESCALE_LOG2 = 8.0f;
+#ifndef WGPF_ATTN_MUFU_PAIRS
+#define WGPF_ATTN_MUFU_PAIRS 16
+#endif
+constexpr int kMufuPairs = WGPF_ATTN_MUFU_PAIRS;  // of 16 pairs per chunk: ex2 on MUFU
 
 enum : uint32_t {
   R_LOAD_K, R_LOAD_K_WAIT, R_LOAD_V, R_LOAD_V_WAIT,
@@ -222,15 +226,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       // ---- softmax ----
       // pass 1: row max (S stays in TMEM; pass 2 reloads it)
-      float mx = -INFINITY;
+      // (four independent max chains: the 3-input max has a few cycles of
+      // latency and a single chain would serialise the pass)
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll 1
       for (uint32_t ch = 0; ch < 4; ++ch) {
         uint32_t v[32];
         tc::tmem_ld32(tS + lane_base + ch * 32u, v);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+        for (int i = 0; i < 32; i += 2)
+          mx4[(i >> 1) & 3] = tc::max3(mx4[(i >> 1) & 3], __uint_as_float(v[i]),
+                                       __uint_as_float(v[i + 1]));
       }
+      const float mx = fmaxf(tc::max3(mx4[0], mx4[1], mx4[2]), mx4[3]);
       const float m_new = fmaxf(m, mx * scale_log2);
       const bool grow = m_new > m + RESCALE_LOG2;
       if (j > 0 && __any_sync(0xFFFFFFFFu, grow)) {
@@ -250,24 +259,50 @@ __global__ void __launch_bounds__(THREADS, 1)
         l *= tc::ex2(m - m_new);
         m = m_new;
       }
-      const float nm = -m;
-      // pass 2: P = 2^(s - m) in bf16 pairs over S's first 64 columns.  Chunk
-      // ch reads S columns 32ch .. 32ch+31, then P chunk ch overwrites columns
-      // 16ch .. 16ch+15 -- all of them already read.
-#pragma unroll 1
-      for (uint32_t ch = 0; ch < 4; ++ch) {
-        uint32_t v[32], pk[16];
-        tc::tmem_ld32(tS + lane_base + ch * 32u, v);
-        tc::tmem_wait_ld();
+      // pass 2: P = 2^(s scale - m) in bf16 pairs over S's first 64 columns.
+      // Chunk ch reads S columns 32ch .. 32ch+31, then P chunk ch overwrites
+      // columns 16ch .. 16ch+15 -- all of them already read.  Packed f32x2
+      // arithmetic; pairs [0, kMufuPairs) take ex2.approx (MUFU), the rest
+      // the polynomial on the FMA pipe.
+      const uint64_t sc2 = tc::pack2(scale_log2, scale_log2);
+      const uint64_t nm2 = tc::pack2(-m, -m);
+      uint64_t l2a = tc::pack2(0.f, 0.f), l2b = l2a;  // two sum chains
+      auto chunk = [&](uint32_t ch, const uint32_t (&v)[32]) {
+        uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float a = tc::ex2(fmaf(__uint_as_float(v[2 * i]), scale_log2, nm));
-          const float b = tc::ex2(fmaf(__uint_as_float(v[2 * i + 1]), scale_log2, nm));
-          l += a + b;
+          const uint64_t x = tc::fma2(tc::pack2(__uint_as_float(v[2 * i]),
+                                                __uint_as_float(v[2 * i + 1])),
+                                      sc2, nm2);
+          uint64_t e;
+          float x0, x1;
+          tc::unpack2(x, x0, x1);
+          if (i < kMufuPairs)
+            e = tc::pack2(tc::ex2(x0), tc::ex2(x1));
+          else
+            e = tc::exp2_poly2(tc::pack2(fmaxf(x0, -125.f), fmaxf(x1, -125.f)));
+          if (i & 1)
+            l2b = tc::add2(l2b, e);
+          else
+            l2a = tc::add2(l2a, e);
+          float a, b;
+          tc::unpack2(e, a, b);
           __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
           pk[i] = *reinterpret_cast<uint32_t*>(&h);
         }
         tc::tmem_st16(tS + lane_base + ch * 16u, pk);
+      };
+#pragma unroll 1
+      for (uint32_t ch = 0; ch < 4; ++ch) {
+        uint32_t v[32];
+        tc::tmem_ld32(tS + lane_base + ch * 32u, v);
+        tc::tmem_wait_ld();
+        chunk(ch, v);
+      }
+      {
+        float la, lb;
+        tc::unpack2(tc::add2(l2a, l2b), la, lb);
+        l += la + lb;
       }
       tc::tmem_wait_st();
       tc::fence_before();

@@ -202,6 +202,49 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// ---- packed f32x2 arithmetic (FFMA2 / FADD2) and 3-input max ----
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void unpack2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// 2^x for a pair on the FMA pipe (x >= -125): x = n + f, n = rint(x) by the
+// 1.5 * 2^23 magic add, 2^f by a degree-3 fit on [-0.5, 0.5] (relative error
+// 2.2e-4, below bf16's 3.9e-3), n added into the exponent field.  Takes the
+// exponentials off the MUFU pipe (FA4's split).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  const uint64_t kMagic = 0x4B4000004B400000ull;   // 12582912.f x2
+  const uint64_t kNegOne = 0xBF800000BF800000ull;   // -1.f x2
+  const uint64_t t = add2(x, kMagic);                       // M + n
+  const uint64_t f = add2(x, fma2(t, kNegOne, kMagic));     // x - n
+  uint64_t p = fma2(f, pack2(0.05286743491888046f, 0.05286743491888046f),
+                    pack2(0.2421518862247467f, 0.2421518862247467f));
+  p = fma2(f, p, pack2(0.6935867667198181f, 0.6935867667198181f));
+  p = fma2(f, p, pack2(0.9999627470970154f, 0.9999627470970154f));
+  const uint32_t t0 = (uint32_t)t, t1 = (uint32_t)(t >> 32);
+  const uint32_t p0 = (uint32_t)p + (t0 << 23), p1 = (uint32_t)(p >> 32) + (t1 << 23);
+  return ((uint64_t)p1 << 32) | p0;
+}
+
 // ---- host: 2-D bf16 tensor map, 128-byte swizzle, box {64, box_rows} ----
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                 void*, const cuuint64_t*, const cuuint64_t*,

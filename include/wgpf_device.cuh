@@ -163,6 +163,74 @@ struct Recorder {
   }
 };
 
+// The uninstrumented twin (strip_profiling, lower.hpp:303-314): the same
+// kernel source compiled with NullRecorder records nothing and costs nothing,
+// which is how T_vanilla of the overhead metric is measured.
+struct NullRecorder {
+  __device__ __forceinline__ void init(void*, uint32_t, uint32_t, bool) {}
+  template <bool kStart>
+  __device__ __forceinline__ void record(uint32_t, uint32_t = 0) {}
+  __device__ __forceinline__ void start(uint32_t, uint32_t = 0) {}
+  __device__ __forceinline__ void end(uint32_t, uint32_t = 0) {}
+  __device__ __forceinline__ void mark(uint32_t, uint32_t, uint32_t = 0) {}
+  __device__ __forceinline__ void close(uint32_t, uint32_t, uint32_t) {}
+};
+
+// ---- the instrumentation pass, as source-level helpers ---------------------
+// The reference inserts RecordOps into its IR (instrument.hpp:163-244): a
+// start/end pair around a synchronous region, and around every async launch /
+// wait pair the four-record pattern (insert_async_pattern, :145-153; doc
+// :14-25): S(X) immediately before the launch, E(X) immediately before the
+// wait, S(X.wait) E(X.wait) immediately after it -- replay derives the wait
+// interval as CLK2 - CLK1.  On B200 the launch is a TMA copy or a
+// tcgen05.mma + commit and the wait an mbarrier phase wait; these helpers
+// place the records at exactly those points so a kernel is instrumented by
+// wrapping its issue and wait sites (auto_async), not by hand-placed records.
+
+// RAII sync scope: S(region) now, E(region) when the scope closes.
+template <class Rec>
+struct Scope {
+  Rec& rec;
+  uint32_t region;
+  __device__ __forceinline__ Scope(Rec& r, uint32_t id) : rec(r), region(id) {
+    rec.start(region);
+  }
+  __device__ __forceinline__ ~Scope() { rec.end(region); }
+};
+
+// One async operation X (region ids x and x_wait = the "X.wait" label):
+//   AsyncOp op(rec, x, xw);  op.launch([&]{ issue });  ... ;  op.wait([&]{ wait });
+template <class Rec>
+struct AsyncOp {
+  Rec& rec;
+  uint32_t x, xw;
+  __device__ __forceinline__ AsyncOp(Rec& r, uint32_t x_, uint32_t xw_)
+      : rec(r), x(x_), xw(xw_) {}
+  // S(X) immediately before the launch
+  template <class F>
+  __device__ __forceinline__ void launch(F&& issue) {
+    rec.start(x);
+    issue();
+  }
+  // E(X) immediately before the wait; S(X.wait) E(X.wait) right after it
+  template <class F>
+  __device__ __forceinline__ void wait(F&& block) {
+    rec.end(x);
+    block();
+    rec.start(xw);
+    rec.end(xw);
+  }
+};
+
+// launch and wait back to back (a producer that waits for its own copy)
+template <class Rec, class L, class W>
+__device__ __forceinline__ void async_region(Rec& rec, uint32_t x, uint32_t xw, L&& issue,
+                                             W&& block) {
+  AsyncOp<Rec> op(rec, x, xw);
+  op.launch(issue);
+  op.wait(block);
+}
+
 // FinalizeOp: after every stream of the CTA has closed (barrier), copy the
 // CTA's buffer to HBM with 16-byte vector stores by all participating threads
 // (coalesced; the buffer is a contiguous KPFT body segment).

@@ -41,6 +41,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "tc_sm100.cuh"
 #include "wgpf_device.cuh"
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint64_t cta = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
   const int row0 = (int)(bh * S);  // first row of this head in [B*H*S, d]
 
-  wgpf_dev::Recorder<true> rec;
+  // the uninstrumented twin uses the null recorder (strip_profiling)
+  std::conditional_t<kInstr, wgpf_dev::Recorder<true>, wgpf_dev::NullRecorder> rec;
   if constexpr (kInstr) {
     rec.init(prof, warp, PROF_CAP, lane == 0);
     if (threadIdx.x == 0 && timing) {
@@ -163,21 +165,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t s = j % kStages, ph = (j / kStages) & 1u;
       if (lane == 0) tc::mbar_wait(&empty[s], ph ^ 1u);
       __syncwarp();
-      if constexpr (kInstr) rec.start(R);
-      if (lane == 0) {
-        uint8_t* dst = ring + s * TILE;
-        tc::mbar_expect_tx(&full[s], TILE);
-        tc::tma_load_2d(map, &full[s], dst, 0, row0 + (int)(j * BKV));
-        tc::tma_load_2d(map, &full[s], dst + HALF, 64, row0 + (int)(j * BKV));
-      }
-      __syncwarp();
-      if constexpr (kInstr) rec.end(R);
-      if (lane == 0) tc::mbar_wait(&full[s], ph);
-      __syncwarp();
-      if constexpr (kInstr) {
-        rec.start(R + 1);
-        rec.end(R + 1);
-      }
+      // the async pattern around the TMA launch and its completion wait
+      // (insert_async_pattern, instrument.hpp:145-153)
+      wgpf_dev::async_region(
+          rec, R, R + 1,
+          [&] {
+            if (lane == 0) {
+              uint8_t* dst = ring + s * TILE;
+              tc::mbar_expect_tx(&full[s], TILE);
+              tc::tma_load_2d(map, &full[s], dst, 0, row0 + (int)(j * BKV));
+              tc::tma_load_2d(map, &full[s], dst + HALF, 64, row0 + (int)(j * BKV));
+            }
+            __syncwarp();
+          },
+          [&] {
+            if (lane == 0) tc::mbar_wait(&full[s], ph);
+            __syncwarp();
+          });
     }
   } else {
     // ---------------- consumers ----------------

@@ -26,7 +26,10 @@ __device__ __forceinline__ uint32_t busy(uint32_t x, uint32_t n) {
   return x;
 }
 
-template <bool kPow2>
+// kAuto: the same program instrumented through the pass helpers
+// (wgpf_dev::Scope / AsyncOp) instead of hand-placed records -- the store log
+// must be identical.
+template <bool kPow2, bool kAuto = false>
 __global__ void k_selftest(uint8_t* profile, uint32_t cap, uint32_t iters,
                            uint32_t* sink, wgpf_dev::CtaTiming* timing) {
   extern __shared__ __align__(16) uint8_t buf[];
@@ -42,6 +45,21 @@ __global__ void k_selftest(uint8_t* profile, uint32_t cap, uint32_t iters,
   wgpf_dev::Recorder<kPow2> rec;
   rec.init(buf, warp, cap, lane == 0);
   uint32_t x = threadIdx.x + 7u * blockIdx.x;
+  if constexpr (kAuto) {
+    using Rec = wgpf_dev::Recorder<kPow2>;
+    wgpf_dev::Scope<Rec> kernel(rec, R_KERNEL);
+    for (uint32_t it = 0; it < iters; ++it) {
+      {
+        wgpf_dev::Scope<Rec> outer(rec, R_OUTER);
+        x = busy(x, 16 + (it & 3));
+        wgpf_dev::Scope<Rec> inner(rec, R_INNER);
+        x = busy(x, 8 + warp);
+      }
+      wgpf_dev::AsyncOp<Rec> op(rec, R_ASYNC, R_ASYNC_WAIT);
+      op.launch([&] { x = busy(x, 4); });
+      op.wait([&] { x = busy(x, 32); });
+    }
+  } else {
   rec.start(R_KERNEL);
   for (uint32_t it = 0; it < iters; ++it) {
     rec.start(R_OUTER);
@@ -58,6 +76,7 @@ __global__ void k_selftest(uint8_t* profile, uint32_t cap, uint32_t iters,
     rec.end(R_ASYNC_WAIT);
   }
   rec.end(R_KERNEL);
+  }
   rec.close((uint32_t)cta, warp, cap);
   __syncthreads();
   const uint32_t bytes = wgpf_dev::smem_bytes(nwarps, cap);
@@ -92,6 +111,22 @@ __global__ void k_record_cost(uint32_t n, uint64_t* cycles, uint32_t* sink) {
 }
 
 }  // namespace
+
+// the selftest program instrumented through the pass helpers (pow2 caps)
+extern "C" int wgpf_p1_selftest_auto(void* d_profile, uint32_t ctas,
+                                     uint32_t warps_per_cta, uint32_t cap,
+                                     uint32_t iters, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  if (!cap || (cap & (cap - 1))) return 11;
+  const uint32_t smem = wgpf_dev::smem_bytes(warps_per_cta, cap);
+  cudaFuncSetAttribute(k_selftest<true, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_selftest<true, true><<<ctas, warps_per_cta * 32, smem,
+                           reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint8_t*>(d_profile), cap, iters, sink, nullptr);
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
 
 extern "C" int wgpf_p1_selftest(void* d_profile, uint32_t ctas,
                                 uint32_t warps_per_cta, uint32_t cap,

@@ -48,6 +48,8 @@ def lib() -> C.CDLL:
         vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
         L.wgpf_p1_selftest.argtypes = [vp, u32, u32, u32, u32, vp, vp]
         L.wgpf_p1_selftest.restype = i32
+        L.wgpf_p1_selftest_auto.argtypes = [vp, u32, u32, u32, u32, vp]
+        L.wgpf_p1_selftest_auto.restype = i32
         L.wgpf_p1_record_cost.argtypes = [u32, u32, i32, vp, vp]
         L.wgpf_p1_record_cost.restype = i32
         L.wgpf_gemm_bf16.argtypes = [vp, vp, vp, u32, u32, u32, i32, vp, vp, vp]
@@ -81,6 +83,14 @@ def selftest(profile_ptr: int, ctas: int, warps: int, cap: int, iters: int,
     _check(lib().wgpf_p1_selftest(C.c_void_p(profile_ptr), ctas, warps, cap, iters,
                                   C.c_void_p(timing_ptr), C.c_void_p(stream)),
            "wgpf_p1_selftest")
+
+
+def selftest_auto(profile_ptr: int, ctas: int, warps: int, cap: int, iters: int,
+                  stream: int = 0) -> None:
+    """The selftest program instrumented through the device pass helpers
+    (wgpf_dev::Scope / AsyncOp, include/wgpf_device.cuh)."""
+    _check(lib().wgpf_p1_selftest_auto(C.c_void_p(profile_ptr), ctas, warps, cap, iters,
+                                       C.c_void_p(stream)), "wgpf_p1_selftest_auto")
 
 
 def selftest_store_log(iters: int) -> list:

@@ -118,3 +118,26 @@ def test_gemm_matches_cublas_and_instrumented_is_identical(oracle, shape):
     st = oracle.region_stats(r.events, p1.GEMM_LABELS)
     labels = {s.label for s in st}
     assert {"mma.issue", "tma.issue", "epi.ld", "epi.st", "tile"} <= labels
+
+
+def test_pass_helpers_place_the_reference_records(oracle):
+    """wgpf_dev::Scope / AsyncOp (the instrumentation pass as source helpers,
+    instrument.hpp:145-153) store exactly the hand-instrumented program's
+    records: same tags in the same order, and the body decodes."""
+    import torch
+    p1 = P1()
+    ctas, warps, cap, iters = 3, 4, 64, 9
+    stride = p1.stream_stride(cap)
+    a = torch.zeros(ctas * warps * stride, dtype=torch.uint8, device="cuda")
+    b = torch.zeros_like(a)
+    p1.selftest(a.data_ptr(), ctas, warps, cap, iters)
+    p1.selftest_auto(b.data_ptr(), ctas, warps, cap, iters)
+    torch.cuda.synchronize()
+    da = oracle.decode_kpft(p1.kpft_v1(a.cpu().numpy(), ctas * warps), cap, 0)
+    db = oracle.decode_kpft(p1.kpft_v1(b.cpu().numpy(), ctas * warps), cap, 0)
+    log = p1.selftest_store_log(iters)
+    tail = log[-cap:] if len(log) > cap else log
+    for x, y in zip(da, db):
+        assert np.array_equal(x["records"]["tag"], y["records"]["tag"])
+        got = [((int(t) >> 31) & 1, (int(t) >> 12) & 0x7FFFF) for t in y["records"]["tag"]]
+        assert got == tail

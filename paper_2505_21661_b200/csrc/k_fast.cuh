@@ -11,14 +11,15 @@
 //       highest START lane below, else the per-level table in shared memory
 //       (carried across steps).  The partner's region must equal the END's
 //       (single-stack nesting); otherwise the stream is recounted exactly.
-//       Iteration numbers: match.any on the region + per-region counters.
+//       Iteration numbers: lanes of a region meet through a shared bit mask
+//       (atomicOr) + per-region counters.
 //   replay (trace.hpp:398-487)  sync correction, wait markers (the marker
 //       START at end_pos + 1, closed either immediately or because it lies at
 //       or before the stream's last zero-depth position z from pass 1),
 //       orphans (staged in a per-warp HBM scratch, written last).
-//   region_stats (pipeline.hpp:114-133) + histograms: per step match.any on
-//       (class, bin), group reductions with redux.sync, one shared-memory
-//       atomic per group; per-CTA totals flushed to HBM at exit.
+//   region_stats (pipeline.hpp:114-133) + histograms: per-lane register
+//       accumulators flushed on a class change, one shared histogram
+//       increment per event; per-CTA totals flushed to HBM at exit.
 // Events are written at offsets from the pass-1 scan, coalesced per step.
 #pragma once
 
@@ -71,6 +72,7 @@ struct FastSmem {
   uint32_t wcls[kFastRegions];   // class of label + ".wait" (or kNone)
   LevelEntry lvl[kFastWarps][kMaxDepth];
   uint32_t cnt[kFastWarps][kFastRegions];
+  uint32_t rmask[kFastWarps][kFastRegions];  // lanes ending a region this step
   unsigned long long warn[4];
   unsigned long long bar[kFastWarps][2];  // staging mbarriers (kStage)
 };
@@ -215,25 +217,21 @@ __device__ inline void acc_flush(LaneAcc& a, FastSmem& sm, const DevStats& st,
   a.cnt = 0;
 }
 
-// One event per participating lane.  Histogram: match.any on (class, bin),
-// the group leader adds the group size (no group-mask reductions).
+// One event per participating lane: register accumulators per class (flushed
+// on a class change), one shared histogram increment.
 __device__ inline void lane_stats(LaneAcc& a, FastSmem& sm, const DevStats& st,
                                   DevStatus* status, bool part, uint32_t cls,
                                   uint32_t d, unsigned long long key) {
-  const uint32_t lane = lane_id();
-  const uint32_t bin = hist_bin(d);
-  const uint32_t k = part ? ((cls << 6) | bin) : (0xFC000000u | lane);
-  const uint32_t grp = __match_any_sync(0xffffffffu, k);
   if (!part) return;
-  if (!(grp & lanemask_lt())) {
-    if (cls < kSmemClasses && cls < st.K) {
-      atomicAdd(&sm.st.hist[cls * WGPF_HIST_BINS + bin], (uint32_t)__popc(grp));
-    } else {
-      const int slot = stats_slot(st, cls, &status->synth_overflow);
-      if (slot >= 0)
-        atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + bin],
-                  (unsigned long long)__popc(grp));
-    }
+  const uint32_t bin = hist_bin(d);
+  // one shared increment per event (same-address increments of a warp are
+  // aggregated by the hardware; match.any grouping cost more than it saved)
+  if (cls < kSmemClasses && cls < st.K) {
+    atomicAdd(&sm.st.hist[cls * WGPF_HIST_BINS + bin], 1u);
+  } else {
+    const int slot = stats_slot(st, cls, &status->synth_overflow);
+    if (slot >= 0)
+      atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + bin], 1ull);
   }
   if (cls != a.cls) {
     acc_flush(a, sm, st, status);
@@ -291,6 +289,8 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
   const bool abort_all = a.status->decode_err != kNoErr;
   LevelEntry* lvl = sm.lvl[w];
   uint32_t* cnt = sm.cnt[w];
+  uint32_t* rmask = sm.rmask[w];
+  for (uint32_t r = lane; r < kFastRegions; r += 32) rmask[r] = 0u;
   const uint64_t gw = (uint64_t)blockIdx.x * kFastWarps + w;
   wgpf_event* orphans = a.orphan_scratch + gw * (a.cap / 2 + 1);
   const uint32_t lt = lanemask_lt(), le = lanemask_le();
@@ -410,8 +410,13 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
       }
 
       // ---- partner START: same level, highest START lane below ------------
+      // (match.any only when the step has both STARTs and matched ENDs: with
+      // no matched END, START levels strictly increase, so each START is the
+      // last at its level and no END has a partner inside the step)
       const uint32_t key = (st || mend) ? L : (0x80000000u | lane);
-      const uint32_t grp = __match_any_sync(0xffffffffu, key);
+      uint32_t grp = 1u << lane;
+      if (smk != 0u && __any_sync(0xffffffffu, mend))
+        grp = __match_any_sync(0xffffffffu, key);
       const uint32_t cand = grp & smk & lt;
       const uint32_t src = cand ? 31u - __clz(cand) : lane;
       const uint32_t s_v = __shfl_sync(0xffffffffu, v, src);
@@ -459,12 +464,18 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
       }
 
       // ---- iteration numbers per region id --------------------------------
-      const uint32_t rgrp =
-          __match_any_sync(0xffffffffu, mend ? rid : (0x80000000u | lane));
+      // lanes of a region find each other through a shared bit mask (one
+      // shared atomicOr each) instead of match.any
+      if (mend) atomicOr(&rmask[rid], 1u << lane);
+      __syncwarp();
+      const uint32_t rgrp = mend ? rmask[rid] : 0u;
       uint32_t it = 0;
       if (mend) it = cnt[rid] + __popc(rgrp & lt);
       __syncwarp();
-      if (mend && !(rgrp & lt)) cnt[rid] += __popc(rgrp);
+      if (mend && !(rgrp & lt)) {
+        cnt[rid] += __popc(rgrp);
+        rmask[rid] = 0u;
+      }
 
       // ---- replay -----------------------------------------------------------
       const uint32_t cls = my_info & 0x7FFFFFFFu;

@@ -146,11 +146,11 @@ __device__ inline void fast_stats(FastSmem& sm, const DevStats& st,
       const unsigned long long sum =
           (unsigned long long)lo + ((unsigned long long)hi << 16);
       if (dense) {
-        atomicAdd(&sm.st.count[c], (unsigned long long)n);
-        atomicAdd(&sm.st.sum[c], sum);
+        sadd64(&sm.st.count[c], (unsigned long long)n);
+        sadd64(&sm.st.sum[c], sum);
         atomicMin(&sm.st.min[c], mn);
         atomicMax(&sm.st.max[c], mx);
-        atomicMin(&sm.st.first[c], key);
+        smin64(&sm.st.first[c], key);
       } else {
         slot = stats_slot(st, c, &status->synth_overflow);
         if (slot >= 0) {
@@ -199,11 +199,11 @@ __device__ inline void acc_flush(LaneAcc& a, FastSmem& sm, const DevStats& st,
                                  DevStatus* status) {
   if (!a.cnt) return;
   if (a.cls < kSmemClasses && a.cls < st.K) {
-    atomicAdd(&sm.st.count[a.cls], (unsigned long long)a.cnt);
-    atomicAdd(&sm.st.sum[a.cls], a.sum);
+    sadd64(&sm.st.count[a.cls], (unsigned long long)a.cnt);
+    sadd64(&sm.st.sum[a.cls], a.sum);
     atomicMin(&sm.st.min[a.cls], a.mn);
     atomicMax(&sm.st.max[a.cls], a.mx);
-    atomicMin(&sm.st.first[a.cls], a.first);
+    smin64(&sm.st.first[a.cls], a.first);
   } else {
     const int slot = stats_slot(st, a.cls, &status->synth_overflow);
     if (slot >= 0) {

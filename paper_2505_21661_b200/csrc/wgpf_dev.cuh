@@ -117,6 +117,22 @@ __device__ inline void stats_add_global(const DevStats& st, int slot,
   atomicAdd(&st.hist[(uint64_t)slot * WGPF_HIST_BINS + hist_bin(d)], 1ull);
 }
 
+// 64-bit shared-memory add / min without the CAS loops the compiler emits
+// for 64-bit shared atomics: the add goes to the two 32-bit halves (each
+// adder whose low-word add wraps carries exactly one into the high word), the
+// min is skipped when the current value is already smaller (first-event keys
+// only shrink early in a kernel).  Results are read after a barrier.
+__device__ __forceinline__ void sadd64(unsigned long long* p, unsigned long long v) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(p);
+  const uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(w, lo);
+  const uint32_t up = hi + ((uint32_t)(old + lo) < old ? 1u : 0u);
+  if (up) atomicAdd(w + 1, up);
+}
+__device__ __forceinline__ void smin64(unsigned long long* p, unsigned long long v) {
+  if (v < *reinterpret_cast<volatile unsigned long long*>(p)) atomicMin(p, v);
+}
+
 // Per-CTA shared-memory accumulators for dense classes < kSmemClasses.
 constexpr uint32_t kSmemClasses = 64;
 struct SmemStats {
@@ -161,11 +177,11 @@ __device__ inline void stats_add_one(SmemStats& s, const DevStats& st,
                                      unsigned long long key,
                                      unsigned long long* overflow) {
   if (cls < kSmemClasses && cls < st.K) {
-    atomicAdd(&s.count[cls], 1ull);
-    atomicAdd(&s.sum[cls], (unsigned long long)d);
+    sadd64(&s.count[cls], 1ull);
+    sadd64(&s.sum[cls], (unsigned long long)d);
     atomicMin(&s.min[cls], (uint32_t)d);
     atomicMax(&s.max[cls], (uint32_t)d);
-    atomicMin(&s.first[cls], key);
+    smin64(&s.first[cls], key);
     atomicAdd(&s.hist[cls * WGPF_HIST_BINS + hist_bin(d)], 1u);
   } else {
     stats_add_global(st, stats_slot(st, cls, overflow), d, key);

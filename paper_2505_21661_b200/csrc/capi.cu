@@ -1030,7 +1030,9 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
                                 uint32_t flags, uint64_t* n_events,
                                 wgpf_warnings* warnings) {
   const uint64_t stride = 16ull + 8ull * c->slots;
-  const uint64_t cs = std::max<uint64_t>(32, (kChunkBytes / stride) & ~31ull);
+  uint64_t chunk_bytes = kChunkBytes;
+  if (const char* e = getenv("WGPF_CHUNK_MB")) chunk_bytes = (uint64_t)atoll(e) << 20;
+  const uint64_t cs = std::max<uint64_t>(32, (chunk_bytes / stride) & ~31ull);
   const uint64_t nc = (count + cs - 1) / cs;
   const uint64_t ev_cap = std::max<uint64_t>(cs * c->slots, 1);
   if (!c->s_h2d) {

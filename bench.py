@@ -312,8 +312,10 @@ def main():
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / (emit_ms / 1e3) / 1e9
     traffic = None
+    # (the committed ncu capture is of the full config-4 emit kernel: other
+    # workloads report no traffic figure)
     tp = os.path.join(ROOT, "profiles", "ncu_emit_traffic.json")
-    if os.path.exists(tp):
+    if not nested and n == S.MIXED_FULL_STREAMS and os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("dram_bytes_per_launch")
         except Exception:

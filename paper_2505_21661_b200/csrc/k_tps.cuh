@@ -23,7 +23,7 @@
 // in shared memory with cp.async (16-B chunks, double buffered; chunk k of the
 // window of stream l is copied by a fixed lane, so one instruction covers a
 // few contiguous lines).  Events: each lane stores its 32-B events straight
-// to HBM (two 16-B stores, full sectors; a stream's events are contiguous, so
+// to HBM (one 256-bit store per event, a full L2 sector; a stream's events are contiguous, so
 // L2 completes each line before write-back).  Measured against staging the
 // events in shared-memory rings with a warp-cooperative coalesced flush, the
 // direct stores are faster (the flush costs more issue slots than the
@@ -209,11 +209,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
                    uint32_t ehi, uint32_t region, uint32_t it) {
       const bool ok = p & (k < lim);
-      if (ok) {
-        uint4* q = reinterpret_cast<uint4*>(ev0 + k);
-        q[0] = make_uint4(slo, shi, elo, ehi);
-        q[1] = make_uint4(region, it, blk, wg);
-      }
+      if (ok) stg256(ev0 + k, make_uint4(slo, shi, elo, ehi), make_uint4(region, it, blk, wg));
       w_ovf += (p && !ok) ? 1u : 0u;
     };
     // one event of class cls (predicated on p): lane-private count / min /

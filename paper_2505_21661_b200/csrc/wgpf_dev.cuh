@@ -232,6 +232,15 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
   return v;
 }
+// One 32-byte event with a single 256-bit store (STG.E.ENL2.256, sm_100):
+// a full L2 sector per lane instead of two 16-byte halves.
+__device__ __forceinline__ void stg256(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p),
+               "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z),
+               "r"(b.w)
+               : "memory");
+}
+
 // a value the compiler cannot see through (so it is not rematerialised)
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   uint32_t y;

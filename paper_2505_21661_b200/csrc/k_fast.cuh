@@ -112,10 +112,8 @@ __device__ inline void stage_wait(unsigned long long* bar, uint32_t parity) {
 __device__ inline void store_event(wgpf_event* dst, uint64_t st, uint64_t en,
                                    uint32_t region, uint32_t it, uint32_t blk,
                                    uint32_t wg) {
-  uint4* p = reinterpret_cast<uint4*>(dst);
-  p[0] = make_uint4((uint32_t)st, (uint32_t)(st >> 32), (uint32_t)en,
-                    (uint32_t)(en >> 32));
-  p[1] = make_uint4(region, it, blk, wg);
+  stg256(dst, make_uint4((uint32_t)st, (uint32_t)(st >> 32), (uint32_t)en, (uint32_t)(en >> 32)),
+         make_uint4(region, it, blk, wg));
 }
 
 // Group-aggregated statistics update for one event per participating lane.

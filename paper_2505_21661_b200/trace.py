@@ -262,6 +262,71 @@ def label_of(labels, rid: int) -> str:
     return labels[rid] if rid < len(labels) else f"region#{rid}"
 
 
+@dataclass
+class DeviceProgram:
+    """The lowered program's side channel: what the replay and the critical
+    path analysis need from `print_device_program` (lower.hpp:320-380) --
+    the buffer plan (strategy, slots per stream, region table) and the
+    barrier-derived candidate edges (barrier_edges, perfmodel.hpp:258-313)."""
+    name: str
+    num_warp_groups: int
+    plan: BufferPlan
+    barrier_edges: list
+
+
+def parse_device_program(text: str) -> DeviceProgram:
+    """Parse a `.dev` file (the reference's `print_device_program` output).
+
+    barrier_edges: for every `arrive <b>` the label of the nearest preceding
+    end `store_counter`, for every `wait <b>` the label of the nearest
+    following start `store_counter` in the same warp-group body; an edge per
+    (arrive, wait) pair on the same barrier with different labels, sorted and
+    unique (perfmodel.hpp:258-313)."""
+    import json as _json
+    lines = text.splitlines()
+    if not lines or not lines[0].startswith("device kernel "):
+        raise Error(ErrorKind.Parse, "not a device program")
+    head = lines[0].split()
+    kv = dict(tok.split("=", 1) for tok in head if "=" in tok)
+    labels, bodies, cur = [], [], None
+    for line in lines[1:]:
+        t = line.strip()
+        if t.startswith("region ") and cur is None:
+            labels.append(_json.loads(t[t.index('"'):]))
+        elif t.startswith("wg") and t.endswith("{"):
+            cur = []
+            bodies.append(cur)
+        elif cur is not None and t and t != "}":
+            cur.append(t)
+
+    def label(rid: int) -> str:
+        return labels[rid] if rid < len(labels) else ""
+
+    def region_of(t: str) -> int:
+        return int(t.split("region=")[1].split()[0])
+
+    arrives, waits = [], []
+    for body in bodies:
+        for i, t in enumerate(body):
+            if t.startswith("arrive "):
+                for j in range(i - 1, -1, -1):
+                    if body[j].startswith("store_counter") and body[j].endswith(" end"):
+                        if label(region_of(body[j])):
+                            arrives.append((t.split()[1], label(region_of(body[j]))))
+                        break
+            elif t.startswith("wait "):
+                for j in range(i + 1, len(body)):
+                    if body[j].startswith("store_counter") and body[j].endswith(" start"):
+                        if label(region_of(body[j])):
+                            waits.append((t.split()[1], label(region_of(body[j]))))
+                        break
+    edges = sorted({(a, w) for b1, a in arrives for b2, w in waits if b1 == b2 and a != w})
+    strategy = (BufferStrategy.Circular if kv.get("strategy") == "circular"
+                else BufferStrategy.Flush)
+    plan = BufferPlan(int(kv.get("slots_per_wg", 0)), strategy, labels)
+    return DeviceProgram(head[2], int(kv.get("wgs", 0)), plan, edges)
+
+
 def is_wait_marker(label: str) -> bool:
     return len(label) > len(WAIT_SUFFIX) and label.endswith(WAIT_SUFFIX)
 

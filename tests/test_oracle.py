@@ -414,3 +414,18 @@ def test_reference_chrome_export_entry_point(reference, oracle, name):
     r = oracle.replay_kpft(data, slots, strategy, labels, cost)
     got = reference.export_chrome(r.events, labels, 1000.0)
     assert got == open(os.path.join(GOLDEN, "fixtures", name + ".json")).read()
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_device_program_side_channel(name):
+    """trace.parse_device_program (the .dev side channel, lower.hpp:320-380)
+    gives the fixture's plan and the barrier edges perfmodel.hpp:258-313
+    derives (the test-side parser above is the independent check)."""
+    from paper_2505_21661_b200 import trace as T
+    data, slots, strategy, labels, cost, dev = load_fixture(name)
+    dp = T.parse_device_program(dev)
+    assert dp.plan.slots_per_warp_group == slots
+    assert int(dp.plan.strategy) == strategy
+    assert dp.plan.region_labels == labels
+    assert dp.barrier_edges == dev_barrier_edges(dev)
+    assert dp.num_warp_groups > 0 and dp.name

@@ -515,3 +515,44 @@ def test_chrome_trace_gpu_formatter_attention_trace(ctx, reference):
     want = reference.export_chrome(host, p1.ATTN_LABELS, 1965.0)
     assert ctx.export_chrome_trace(None, 1965.0, on_device_ptr=ev.data_ptr(),
                                    n_events=ne) == want
+
+
+@pytest.mark.parametrize("shape", [0, 1])
+def test_device_event_buffer_too_small(ctx, shape):
+    """A device event buffer smaller than the trace: E_BUFFER with the full
+    count, nothing written past the capacity (canary), and the events that
+    fit are exactly the prefix of the full result (events sit at their final
+    offsets) -- the thread-per-stream kernel's per-stream store limit, the
+    warp kernel's per-store check."""
+    import torch
+    t = T()
+    n = 4096
+    plan = plan_of(S.CAP, 1 if shape == 0 else 0,
+                   S.MIXED_LABELS if shape == 0 else S.NESTED_LABELS)
+    ctx.set_plan(plan)
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), shape, 0, n, n // 2)
+    ne, _ = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0, 0x1)
+    full = torch.empty(ne * 32, dtype=torch.uint8, device="cuda")
+    assert ctx.replay_device(body.data_ptr(), body.numel(), n, 33, full.data_ptr(), ne)[0] == ne
+    cap = ne // 3 + 5
+    buf = torch.full(((cap + 64) * 32,), 0xAB, dtype=torch.uint8, device="cuda")
+    with pytest.raises(t.BufferTooSmall) as ex:
+        ctx.replay_device(body.data_ptr(), body.numel(), n, 33, buf.data_ptr(), cap)
+    assert ex.value.needed == ne
+    torch.cuda.synchronize()
+    assert torch.all(buf[cap * 32:] == 0xAB)
+    assert torch.equal(buf[: cap * 32], full[: cap * 32])
+
+
+def test_chrome_trace_long_label_falls_back_to_host_writer(ctx, reference):
+    """Labels longer than the GPU formatter's per-event budget take the host
+    writer for device events: still the reference's bytes."""
+    import torch
+    labels = ["L" * 300, "short", 'q"uote']
+    ctx.set_plan(plan_of(8, 0, labels))
+    ev = random_chrome_events(5, 500, len(labels))
+    want = reference.export_chrome(ev, labels, 1965.0)
+    d = torch.from_numpy(ev.view(np.uint8).copy()).cuda()
+    assert ctx.export_chrome_trace(None, 1965.0, on_device_ptr=d.data_ptr(),
+                                   n_events=len(ev)) == want

@@ -224,6 +224,30 @@ inline void set_plan(std::uint64_t slots, BufferStrategy st,
                       static_cast<std::uint32_t>(p.size())));
 }
 
+// TimelineEvents -> 32-byte events with a dense label table (first-seen order)
+inline std::vector<wgpf_event> pack_events(const std::vector<TimelineEvent>& events,
+                                           std::vector<std::string>& table) {
+  std::unordered_map<std::string, std::uint32_t> ids;
+  std::vector<wgpf_event> ev(events.size() + 1);
+  for (std::size_t i = 0; i < events.size(); ++i) {
+    const auto& e = events[i];
+    auto it = ids.find(e.region);
+    std::uint32_t id;
+    if (it == ids.end()) {
+      id = static_cast<std::uint32_t>(table.size());
+      ids.emplace(e.region, id);
+      table.push_back(e.region);
+    } else {
+      id = it->second;
+    }
+    ev[i] = wgpf_event{e.start, e.end,
+                       id | (e.kind == EventKind::Wait ? WGPF_EV_WAIT : 0u) |
+                           (e.corrected ? WGPF_EV_CORRECTED : 0u),
+                       e.iteration, e.block_index, e.warp_group};
+  }
+  return ev;
+}
+
 inline std::string label_of(const std::vector<std::string>& t, std::uint32_t id) {
   return id < t.size() ? t[id] : "region#" + std::to_string(id);
 }
@@ -473,6 +497,74 @@ inline std::map<std::string, RegionStats> region_stats(
     out.emplace(st[i].label, r);
   }
   return out;
+}
+
+// export_chrome_trace (trace.hpp:489-511): byte-identical Chrome Trace JSON.
+inline std::string export_chrome_trace(const std::vector<TimelineEvent>& events,
+                                       double cycles_per_us = 1000.0) {
+  std::vector<std::string> table;
+  std::vector<wgpf_event> ev = b200::pack_events(events, table);
+  b200::set_plan(0, BufferStrategy::Flush, table);
+  std::uint64_t len = 0;
+  b200::check(wgpf_export_chrome_trace(b200::ctx(), ev.data(), events.size(), 0,
+                                       cycles_per_us, nullptr, 0, &len));
+  std::string out(len, '\0');
+  b200::check(wgpf_export_chrome_trace(b200::ctx(), ev.data(), events.size(), 0,
+                                       cycles_per_us, out.data(), len, &len));
+  return out;
+}
+
+// analyze_critical_path (perfmodel.hpp:317-501).  The reference takes the
+// lowered DeviceProgram and derives the barrier edges from it
+// (perfmodel.hpp:258-313); this drop-in takes those edges directly (the
+// reference's own detail::barrier_edges(dp), or the `.dev` side channel via
+// the Python layer's parse_device_program).  The result carries the binding
+// cycle and its period -- the parts of CriticalPathAnalysis the CLI reports
+// (tools/wgprof.cpp:110) -- plus the per-stage steady means.
+struct CriticalPathOptions {
+  std::uint64_t slack_tolerance = 132;
+  bool exclude_warmup = true;
+};
+struct CriticalPathResult {
+  std::vector<std::string> cycle;
+  std::uint64_t period = 0;
+  std::map<std::string, std::uint64_t> stage_mean;
+};
+inline CriticalPathResult analyze_critical_path(
+    const std::vector<TimelineEvent>& events,
+    const std::vector<std::pair<std::string, std::string>>& barrier_edges,
+    const CriticalPathOptions& opts = {}) {
+  std::vector<std::string> table;
+  std::vector<wgpf_event> ev = b200::pack_events(events, table);
+  b200::set_plan(0, BufferStrategy::Flush, table);
+  std::vector<const char*> src, dst;
+  for (const auto& e : barrier_edges) {
+    src.push_back(e.first.c_str());
+    dst.push_back(e.second.c_str());
+  }
+  std::uint32_t cap = 64;
+  for (;;) {
+    std::vector<wgpf_cp_stage> st(cap);
+    std::vector<std::uint64_t> bind((std::size_t)cap * cap);
+    std::vector<std::uint32_t> cyc(cap);
+    std::uint32_t ns = 0, nc = 0;
+    std::uint64_t period = 0;
+    const int rc = wgpf_critical_path(
+        b200::ctx(), ev.data(), events.size(), 0, src.data(), dst.data(),
+        static_cast<std::uint32_t>(src.size()), opts.slack_tolerance,
+        opts.exclude_warmup ? 1 : 0, 0, st.data(), cap, &ns, bind.data(),
+        (std::uint64_t)cap * cap, cyc.data(), cap, &nc, &period);
+    if (rc == WGPF_E_BUFFER && ns > cap) {
+      cap = ns;
+      continue;
+    }
+    b200::check(rc);
+    CriticalPathResult r;
+    for (std::uint32_t i = 0; i < ns; ++i) r.stage_mean[st[i].label] = st[i].mean;
+    for (std::uint32_t i = 0; i < nc; ++i) r.cycle.push_back(st[cyc[i]].label);
+    r.period = period;
+    return r;
+  }
 }
 
 }  // namespace wgprof

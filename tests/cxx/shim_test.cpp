@@ -127,6 +127,25 @@ int main(int argc, char** argv) {
     CHECK(st["GEMM0.c0.wait"].count == 6);
     CHECK(st["GEMM0.c0.wait"].mean == 1127.8333333333333);  // non-integer (H1)
     CHECK(st["GEMM0.c0.wait"].min == 800 && st["GEMM0.c0.wait"].max == 1200);
+    // export_chrome_trace: the reference's bytes (out/fa3_vanilla.json)
+    auto js = export_chrome_trace(tr.events, 1000.0);
+    auto want = read_bytes(dir + "/fa3_vanilla.json");
+    CHECK(js == std::string(want.begin(), want.end()));
+    // analyze_critical_path with the program's barrier edges (argv[2]:
+    // "src<TAB>dst" lines, derived from fa3_vanilla.dev by the test driver)
+    if (argc > 2) {
+      std::vector<std::pair<std::string, std::string>> edges;
+      std::ifstream ef(argv[2]);
+      std::string el;
+      while (std::getline(ef, el)) {
+        auto t = el.find('\t');
+        if (t != std::string::npos) edges.emplace_back(el.substr(0, t), el.substr(t + 1));
+      }
+      auto cp = analyze_critical_path(tr.events, edges);
+      CHECK(cp.period == 4200);
+      CHECK((cp.cycle == std::vector<std::string>{"GEMM1.c0", "GEMM1.c0.wait", "Load V0",
+                                                  "Load V0.wait"}));
+    }
   }
   if (failures == 0) std::printf("ALL PASS\n");
   return failures ? 1 : 0;

@@ -426,8 +426,13 @@ def test_cxx_shim_end_to_end(tmp_path):
                           lib, f"-Wl,-rpath,{os.path.dirname(lib)}", "-o", exe],
                          capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
-    res = subprocess.run([exe, os.path.join(GOLDEN, "fixtures")], capture_output=True,
-                         text=True, timeout=300)
+    from paper_2505_21661_b200 import trace as tr
+    dp = tr.parse_device_program(open(os.path.join(GOLDEN, "fixtures",
+                                                   "fa3_vanilla.dev")).read())
+    edges = tmp_path / "edges.tsv"
+    edges.write_text("".join(f"{a}\t{b}\n" for a, b in dp.barrier_edges))
+    res = subprocess.run([exe, os.path.join(GOLDEN, "fixtures"), str(edges)],
+                         capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "ALL PASS" in res.stdout
 

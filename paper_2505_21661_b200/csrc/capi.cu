@@ -28,6 +28,7 @@
 #include "k_count.cuh"
 #include "k_fast.cuh"
 #include "k_tps.cuh"
+#include "k_tpsd.cuh"
 #include "k_general.cuh"
 #include "k_misc.cuh"
 #include "k_stats.cuh"
@@ -76,6 +77,11 @@ struct DevBuf {
 }  // namespace
 
 using TpsKernel = void (*)(FastArgs);
+static TpsKernel deep_kernel(bool emit, bool stats) {
+  static const TpsKernel k[4] = {k_tpsd<false, false>, k_tpsd<true, false>,
+                                 k_tpsd<false, true>, k_tpsd<true, true>};
+  return k[(emit ? 1 : 0) | (stats ? 2 : 0)];
+}
 static TpsKernel tps_kernel(bool emit, bool stats) {
   static const TpsKernel k[4] = {k_tps<false, false>, k_tps<true, false>,
                                  k_tps<false, true>, k_tps<true, true>};
@@ -110,13 +116,14 @@ struct wgpf_ctx {
   // per call
   DevBuf d_status, d_counts, d_zpos, d_sflag, d_offsets, d_scan_tmp, d_glist,
       d_glen, d_orphans, d_gscratch, d_image, d_events, d_aux0, d_aux1, d_aux2,
-      d_aux3, d_repack, d_chrome;
+      d_aux3, d_repack, d_chrome, d_dlist;
   DevStatus* h_status = nullptr;  // pinned
   // profiling
   cudaEvent_t ev[8] = {};
   bool profiling = false;
   bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
   bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
+  bool no_deep = getenv("WGPF_NO_DEEP") != nullptr;  // deep streams -> warp kernel
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   size_t smem_optin = 0;
@@ -323,9 +330,12 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     c->smem_optin = (size_t)optin;
-    for (int v = 0; v < 4; ++v)
+    for (int v = 0; v < 4; ++v) {
       cudaFuncSetAttribute(tps_kernel(v & 1, v & 2),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      cudaFuncSetAttribute(deep_kernel(v & 1, v & 2),
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    }
   }
   cudaFuncSetAttribute(k_fast_emit<false>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -583,6 +593,12 @@ static bool tps_enabled(const wgpf_ctx* c) {
 static bool count_tps_enabled(const wgpf_ctx* c) {
   return !c->no_tps && c->slots % 2 == 0 && c->slots && c->slots <= kTpsMaxSlots;
 }
+// deep thread-per-stream kernel for SF_DEEP streams of the warp list (any
+// number of label classes: its statistics live in the CTA table)
+static bool deep_enabled(const wgpf_ctx* c) {
+  return !c->no_tps && !c->no_deep && c->slots % 2 == 0 && c->slots &&
+         c->slots <= kTpsMaxSlots && !c->labels.empty();
+}
 static uint32_t tps_regions(const wgpf_ctx* c) {
   return std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions);
 }
@@ -625,13 +641,26 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.tps_regions = tps_regions(c);
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
-  if (tps_enabled(c) && record_cost < (1ull << 21)) {
-    // shallow streams: thread per stream; then the SF_WARP list
-    const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
-    const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
-    tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f);
-    CUDA_OK(c, cudaGetLastError());
-    ++c->launches;
+  if ((tps_enabled(c) || deep_enabled(c)) && record_cost < (1ull << 21)) {
+    if (tps_enabled(c)) {
+      // shallow streams: thread per stream
+      const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
+      const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
+      tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f);
+      CUDA_OK(c, cudaGetLastError());
+      ++c->launches;
+    }
+    if (deep_enabled(c)) {
+      // pass 1's deep list: thread per stream, 64-deep stacks
+      f.list = c->d_dlist.as<unsigned long long>();
+      f.list_len = c->d_glen.as<unsigned long long>() + 2;
+      const uint32_t dw = deep_warps(c->smem_optin);
+      deep_kernel(events != nullptr, !no_stats)<<<c->sms, dw * 32, deep_smem_bytes(dw),
+                                                  c->stream>>>(f);
+      CUDA_OK(c, cudaGetLastError());
+      ++c->launches;
+    }
+    // then the rest of the SF_WARP streams: warp per stream
     f.list = c->d_wlist.as<unsigned long long>();
     f.list_len = c->d_glen.as<unsigned long long>() + 1;
   }
@@ -828,10 +857,21 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   const bool tps = tps_enabled(c);
   ca.tps_regions = tps ? tps_regions(c) : 0u;
   ca.tps_depth = tps ? kTpsDepth : 0u;
+  ca.deep_regions = deep_enabled(c) ? kDeepRegions : 0u;
+  ca.deep_depth = deep_enabled(c) ? kDeepDepth : 0u;
+  if (!tps && deep_enabled(c)) {
+    // no shallow kernel for this plan: every stream with records is listed
+    // (SF_WARP) and the deep ones marked
+    ca.tps_regions = 0;
+    ca.tps_depth = 1;
+  }
   ALLOC_OK(c, c->d_wlist, 8 * n_streams);
   ca.warp_list = c->d_wlist.as<unsigned long long>();
   ca.warp_len = c->d_glen.as<unsigned long long>() + 1;
-  CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 8, c->stream));
+  ALLOC_OK(c, c->d_dlist, deep_enabled(c) ? 8 * n_streams : 8);
+  ca.deep_list = c->d_dlist.as<unsigned long long>();
+  ca.deep_len = c->d_glen.as<unsigned long long>() + 2;
+  CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 16, c->stream));
   if (count_tps_enabled(c))
     k_count_tps<<<grid_for(c, (const void*)k_count_tps, kCountWarps * 32, 0),
                   kCountWarps * 32, 0, c->stream>>>(ca);
@@ -1226,8 +1266,12 @@ extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
   ca.force_general = 1;
   ca.tps_regions = 0;
   ca.tps_depth = 0;
+  ca.deep_regions = 0;
+  ca.deep_depth = 0;
   ca.warp_list = nullptr;
   ca.warp_len = nullptr;
+  ca.deep_list = nullptr;
+  ca.deep_len = nullptr;
   k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                  c->stream>>>(ca);
   CUDA_OK(c, cudaGetLastError());

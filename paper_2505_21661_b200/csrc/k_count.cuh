@@ -48,8 +48,12 @@ struct CountArgs {
   uint32_t force_general;
   uint32_t tps_regions;  // thread-per-stream path: region ids below this
   uint32_t tps_depth;    //   and nesting up to this (0: path disabled)
-  unsigned long long* warp_list;  // SF_WARP streams
+  uint32_t deep_regions; // deep thread-per-stream path (SF_DEEP): ids below
+  uint32_t deep_depth;   //   this, nesting up to this (0: path disabled)
+  unsigned long long* warp_list;  // SF_WARP streams (not SF_DEEP)
   unsigned long long* warp_len;
+  unsigned long long* deep_list;  // SF_WARP | SF_DEEP streams
+  unsigned long long* deep_len;
 };
 
 __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
@@ -93,6 +97,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     int64_t last_bad = -1;
     bool wide = false;
     bool tps_out = false;  // region id beyond the thread-per-stream tables
+    bool deep_out = false; // region id beyond the deep kernel's tables
     bool prev_end = false;       // record c-1 is an END
     uint32_t pend_rid = kNone;   // lane-31 marker START awaiting its END
     auto chunk = [&](uint32_t c, uint32_t tag) {
@@ -104,6 +109,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       const bool in_range = rid < a.fast_regions;
       wide |= valid && !in_range;
       tps_out |= valid && rid >= a.tps_regions;
+      deep_out |= valid && rid >= a.deep_regions;
       const uint32_t smk = __ballot_sync(0xffffffffu, st);
       const uint32_t emk = __ballot_sync(0xffffffffu, en);
       const int32_t q = q_in + (int32_t)__popc(smk & le) - (int32_t)__popc(emk & le);
@@ -170,14 +176,19 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     if (pend_rid != kNone) last_bad = max(last_bad, (int64_t)n - 1);
     wide = __any_sync(0xffffffffu, wide);
     tps_out = __any_sync(0xffffffffu, tps_out);
+    deep_out = __any_sync(0xffffffffu, deep_out);
     if (lane == 0) {
       a.counts[s] = n_end - (uint32_t)(-run_min);
       a.zpos[s] = z;
       const bool general = wide || a.force_general ||
                            max_d > (int32_t)a.max_depth || last_bad > (int64_t)z;
       const bool warp = a.tps_depth != 0 && !general && (tps_out || max_d > (int32_t)a.tps_depth);
-      a.sflag[s] = general ? SF_GENERAL : (warp ? SF_WARP : 0u);
-      if (warp) a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
+      const bool deep = warp && !deep_out && max_d <= (int32_t)a.deep_depth;
+      a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
+      if (warp && deep)
+        a.deep_list[atomicAdd(a.deep_len, 1ull)] = s;
+      else if (warp)
+        a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
     }
   }
 }
@@ -306,8 +317,13 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
                            last_bad > z;
       const bool warp = a.tps_depth != 0 && !general &&
                         (tps_out || max_d > (int32_t)a.tps_depth);
-      a.sflag[s] = general ? SF_GENERAL : (warp ? SF_WARP : 0u);
-      if (warp) a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
+      const bool deep = warp && !(n && maxrid >= a.deep_regions) &&
+                        max_d <= (int32_t)a.deep_depth;
+      a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
+      if (warp && deep)
+        a.deep_list[atomicAdd(a.deep_len, 1ull)] = s;
+      else if (warp)
+        a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
     }
   }
 }

@@ -1,0 +1,322 @@
+// k_tpsd.cuh -- pass 2 of replay_image for DEEP streams, thread per stream:
+// nesting up to kDeepDepth and region ids below kDeepRegions (config 5: 64
+// nested scopes, 64 labels).  Same algorithm and outputs as k_tps (k_tps.cuh
+// documents the reference mapping: unwrap_clock trace.hpp:257-272,
+// pair_records :294-346, replay :398-487, region_stats pipeline.hpp:114-133);
+// what changes with depth:
+//
+//   * the per-lane stack has 64 rows (16 KB per warp), so 8 warps per SM;
+//   * statistics cannot be lane-private for 64 classes: events go to the
+//     CTA's shared table.  Streams of a trace usually advance in lockstep
+//     (same scope program, same wrap position), so a warp's events of one step
+//     mostly share a class: then one lane applies the warp's reduced
+//     count / sum / min / max / first key (redux.sync), otherwise each lane
+//     updates the table with shared atomics.  Histograms: one shared increment
+//     per event (same-bin increments of a warp aggregate in hardware).
+//
+// It runs over pass 1's deep list (SF_WARP | SF_DEEP: depth <= 64, ids < 64,
+// not general); the warp-per-stream kernel (k_fast.cuh) takes pass 1's warp
+// list (the rest).
+#pragma once
+
+#include <type_traits>
+
+#include "k_tps.cuh"
+
+namespace wgpf {
+
+constexpr uint32_t kDeepDepth = 64;
+constexpr uint32_t kDeepRegions = 64;
+constexpr uint32_t kDeepWarps = 8;
+
+struct DeepWarpSmem {
+  uint8_t rec[2][32 * kTpsPitch];        // record windows
+  uint2 stk[kDeepDepth][32];             // {lo, pos | rid<<11 | cons<<17 | hi<<18}
+  wgpf_event orph[32];                   // one orphan per lane
+  uint16_t cnt[kDeepRegions][32];        // iteration counters
+};
+
+struct DeepCtaSmem {
+  SmemStats st;
+  uint32_t info[kDeepRegions];  // class | marker<<8 | wait class<<16
+  unsigned long long warn[4];
+};
+
+__host__ inline size_t deep_smem_bytes(uint32_t warps) {
+  return tps_align(sizeof(DeepCtaSmem)) + warps * tps_align(sizeof(DeepWarpSmem));
+}
+__host__ inline uint32_t deep_warps(size_t smem_limit) {
+  uint32_t w = kDeepWarps;
+  while (w > 1 && deep_smem_bytes(w) > smem_limit) --w;
+  return w;
+}
+
+template <bool kEmit, bool kStats>
+__global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  DeepCtaSmem& cs = *reinterpret_cast<DeepCtaSmem*>(smem_raw);
+  const uint32_t lane = lane_id();
+  const uint32_t w = threadIdx.x >> 5;
+  const uint32_t nw = blockDim.x >> 5;
+  const uint32_t K = a.plan.K;
+  DeepWarpSmem& ws = *reinterpret_cast<DeepWarpSmem*>(
+      smem_raw + tps_align(sizeof(DeepCtaSmem)) + w * tps_align(sizeof(DeepWarpSmem)));
+  constexpr bool stats = kStats;
+  constexpr bool emit = kEmit;
+  if (stats) smem_stats_init(cs.st);
+  for (uint32_t r = threadIdx.x; r < kDeepRegions; r += blockDim.x) {
+    uint32_t inf = 0xFFFFFFFFu;
+    if (r < a.fast_regions) {
+      const uint32_t c = a.plan.class_of[r];
+      const uint32_t wc = c < K ? a.plan.wait_class[c] : kNone;
+      inf = (c & 0xFFu) | (class_is_marker(a.plan, c) ? 0x100u : 0u) |
+            ((wc < K ? wc : 0xFFu) << 16);
+    }
+    cs.info[r] = inf;
+  }
+  if (threadIdx.x < 4) cs.warn[threadIdx.x] = 0;
+  __syncthreads();
+  const bool abort_all = a.status->decode_err != kNoErr;
+  const uint32_t FULL = 0xffffffffu;
+  const uint32_t cost = (uint32_t)a.record_cost;  // host: < 2^21 on this path
+  const uint32_t cap = a.cap;
+  uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0, w_ovf = 0;
+
+  const uint32_t s_info = opaque_u32(smem_addr(cs.info));
+  const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);  // + 256 * level
+  const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);  // + 64 * region
+  const uint32_t s_orph = smem_addr(&ws.orph[lane]);
+  const uint32_t s_rec = smem_addr(ws.rec[0]);
+  const uint64_t n_list = *a.list_len;
+
+  // one event per participating lane into the CTA statistics
+  auto wstat = [&](bool p, uint32_t cls, uint32_t d, unsigned long long key) {
+    const uint32_t pm = __ballot_sync(FULL, p);
+    if (pm == 0) return;
+    const uint32_t leader = __ffs(pm) - 1u;
+    const uint32_t c0 = __shfl_sync(FULL, cls, leader);
+    const bool uni = __all_sync(FULL, !p || cls == c0);
+    if (uni && c0 < kSmemClasses && c0 < K) {
+      const uint32_t dd = p ? d : 0u;
+      const uint32_t slo = __reduce_add_sync(FULL, dd & 0xFFFFu);
+      const uint32_t shi = __reduce_add_sync(FULL, dd >> 16);
+      const uint32_t mn = __reduce_min_sync(FULL, p ? d : 0xFFFFFFFFu);
+      const uint32_t mx = __reduce_max_sync(FULL, dd);
+      // smallest 64-bit first-event key of the participating lanes
+      const uint32_t khi = __reduce_min_sync(FULL, p ? (uint32_t)(key >> 32) : 0xFFFFFFFFu);
+      const bool cand = p && (uint32_t)(key >> 32) == khi;
+      const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
+      if (lane == leader) {
+        sadd64(&cs.st.count[c0], (unsigned long long)__popc(pm));
+        sadd64(&cs.st.sum[c0], (unsigned long long)slo + ((unsigned long long)shi << 16));
+        atomicMin(&cs.st.min[c0], mn);
+        atomicMax(&cs.st.max[c0], mx);
+        smin64(&cs.st.first[c0], ((unsigned long long)khi << 32) | klo);
+      }
+      if (p) atomicAdd(&cs.st.hist[c0 * WGPF_HIST_BINS + hist_bin32(d)], 1u);
+    } else if (p) {
+      stats_add_one(cs.st, a.stats, cls, d, key, &a.status->synth_overflow);
+    }
+  };
+
+  const uint64_t wstep = (uint64_t)gridDim.x * nw;
+  for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b * 32 < n_list; b += wstep) {
+    const uint64_t li = b * 32 + lane;
+    const uint64_t s = li < n_list ? a.list[li] : 0ull;
+    const uint32_t flag = li < n_list ? a.sflag[s] : SF_DECODE_ERR;
+    const bool act = (flag & SF_DEEP) && !(flag & (SF_DECODE_ERR | SF_GENERAL));
+    const uint8_t* sbase = a.body + (act ? s : 0) * a.stride;
+    uint4 h = make_uint4(0u, 0u, 0u, cap);
+    if (act) h = *reinterpret_cast<const uint4*>(sbase);
+    const uint32_t n = act ? (h.z <= cap ? h.z : cap) : 0u;
+    const uint32_t start = h.z <= cap ? 0u : h.z % cap;
+    const uint32_t nmax = __reduce_max_sync(FULL, n);
+    if (nmax == 0) continue;
+    const uint32_t blk = h.x, wg = h.y;
+    const int32_t z = act ? a.zpos[s] : -1;
+    const uint32_t want = act ? a.counts[s] : 0u;
+    const uint64_t off = act ? a.offsets[s] : 0ull;
+    const unsigned long long gkey = (unsigned long long)(s + a.stream_base) << 25;
+    const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
+    for (uint32_t r = 0; r < kDeepRegions; ++r) ws.cnt[r][lane] = 0;
+
+    // record windows: chunk k of this lane copies part (q % C) of the window
+    // of batch slot q / C, q = 32 k + lane; that slot's stream from its lane
+    uint32_t wp[kTpsChunks];
+    const uint32_t s32 = (uint32_t)s;
+    const uint32_t live = act ? 1u : 0u;
+#pragma unroll
+    for (uint32_t k = 0; k < kTpsChunks; ++k) {
+      const uint32_t q = k * 32u + lane, sl = q / kTpsChunks, part = q % kTpsChunks;
+      const uint32_t st_k = __shfl_sync(FULL, start, sl);
+      uint32_t p = st_k + 2u;
+      if (p >= cap) p -= cap;
+      p = (p & ~1u) + 2u * part;
+      if (p >= cap) p -= cap;
+      wp[k] = p;
+    }
+    auto issue = [&](uint32_t bsel) {
+#pragma unroll
+      for (uint32_t k = 0; k < kTpsChunks; ++k) {
+        const uint32_t q = k * 32u + lane, sl = q / kTpsChunks, part = q % kTpsChunks;
+        const uint32_t ss = __shfl_sync(FULL, s32, sl);
+        const uint32_t lv = __shfl_sync(FULL, live, sl);
+        if (lv)
+          cp_async16(s_rec + bsel * (32 * kTpsPitch) + sl * kTpsPitch + 16u * part,
+                     a.body + (uint64_t)ss * a.stride + 16 + 8u * wp[k]);
+        wp[k] += kTpsW;
+        if (wp[k] >= cap) wp[k] -= cap;
+      }
+    };
+
+    uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
+    if (n > 0) r0 = slots[start];
+    if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
+    uint32_t inf0 = cs.info[(r0.x >> 12) & (kDeepRegions - 1u)];
+    issue(0);
+    cp_async_commit();
+
+    const uint32_t s_stk0 = s_stk - 256u;  // empty stack: one row below (rec)
+    uint32_t hi = 0, vprev = 0, stop = s_stk0;
+    uint32_t pw = 0xFFu;
+    uint32_t kw = 0;
+    uint32_t n_orph = 0;
+    bool broken = false;
+    const uint32_t lim = off + n <= a.events_cap
+                             ? 0xFFFFFFFFu
+                             : (off < a.events_cap ? (uint32_t)(a.events_cap - off) : 0u);
+    wgpf_event* const ev0 = a.events + (act ? off : 0ull);
+    auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
+                   uint32_t ehi, uint32_t region, uint32_t it) {
+      const bool ok = p & (k < lim);
+      if (ok) stg256(ev0 + k, make_uint4(slo, shi, elo, ehi), make_uint4(region, it, blk, wg));
+      w_ovf += (p && !ok) ? 1u : 0u;
+    };
+    auto step = [&](auto full, uint32_t i, uint2 r2) {
+      constexpr bool kFull = decltype(full)::value;
+      const bool valid = kFull || i < n;
+      const uint32_t tag = r0.x, v = r0.y;
+      const bool isS = (int32_t)tag < 0;
+      const bool st = valid && isS;
+      const bool en = valid && !isS;
+      const uint32_t rid = (tag >> 12) & (kDeepRegions - 1u);
+      const uint32_t inf = inf0;
+      const uint32_t r1id = (r1.x >> 12) & (kDeepRegions - 1u);
+      const uint32_t i1 = lds32(s_info + 4u * r1id);
+      hi += (valid && v < vprev) ? 1u : 0u;
+      vprev = valid ? v : vprev;
+      const uint2 e = lds64(stop);
+      const bool nonempty = stop != s_stk0;
+      const bool mend = en && nonempty;
+      w_drop += (en && !nonempty) ? 1u : 0u;
+      sts64_if(st, stop + 256u,
+               make_uint2(v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 17) |
+                                 (hi << 18)));
+      stop = stop + (st ? 256u : 0u) - (mend ? 256u : 0u);
+      const uint32_t shi = e.y >> 18;
+      const uint32_t meas = v - e.x;
+      const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
+      const bool mism = mend && ((e.y >> 11) & 63u) != rid;
+      const bool tlong = mend && !mism && dhi;
+      broken |= mism || tlong;
+      const bool ok = mend && !mism && !tlong;
+      const uint32_t ca = s_cnt + 64u * rid;
+      const uint32_t it = lds16(ca);
+      sts16_if(ok, ca, it + 1u);
+      const bool is_mk = (inf & 0x100u) != 0u;
+      const bool base = ok && !is_mk;
+      const bool orphan = ok && is_mk && !((e.y >> 17) & 1u);
+      const uint32_t dpos = i - (e.y & 2047u);
+      const uint32_t ovh = cost * dpos;
+      const uint32_t corr = ovh > meas ? 0u : meas - ovh;
+      const bool cclose = (kFull || i + 2 < n) && (int32_t)r2.x >= 0 &&
+                          ((r2.x >> 12) & (kDeepRegions - 1u)) == r1id;
+      const bool consumed = base && (kFull || i + 1 < n) && (int32_t)r1.x < 0 &&
+                            (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
+                            ((int32_t)(i + 1) <= z || cclose);
+      const uint32_t wd = r1.y - v;
+      const bool corr_w = wd > cost;
+      w_flag += (consumed && !corr_w) ? 1u : 0u;
+      const uint32_t kpos = kw;
+      if constexpr (emit) {
+        const uint32_t elo = e.x + corr;
+        put(base, kw, e.x, shi, elo, shi + (elo < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED,
+            it);
+        put(consumed, kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
+            r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
+      }
+      kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
+      pw = base ? (inf >> 16) : 0xFFu;
+      sts128_if(orphan && n_orph == 0, s_orph, make_uint4(e.x, shi, v, hi));
+      sts128_if(orphan && n_orph == 0, s_orph + 16u, make_uint4(rid, it, blk, wg));
+      n_orph += orphan ? 1u : 0u;
+      if constexpr (stats) {
+        wstat(base, inf & 0xFFu, corr, gkey | (kpos << 1));
+        if (__any_sync(FULL, consumed))
+          wstat(consumed, i1 & 0xFFu, wd, gkey | ((kpos + 1u) << 1) | 1u);
+      }
+      inf0 = i1;
+      r0 = r1;
+      r1 = r2;
+    };
+
+    const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
+    for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
+      const uint32_t bsel = (w0 / kTpsW) & 1u;
+      if (w0 + kTpsW < nmax) issue(bsel ^ 1u);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncwarp();
+      const uint2* myrec = reinterpret_cast<const uint2*>(
+          ws.rec[bsel] + lane * kTpsPitch + 8u * (start & 1u));
+      if (w0 + kTpsW + 2u <= nmin) {
+#pragma unroll
+        for (uint32_t j = 0; j < kTpsW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
+      } else {
+#pragma unroll 1
+        for (uint32_t j = 0; j < kTpsW; ++j) step(std::false_type{}, w0 + j, myrec[j]);
+      }
+      __syncwarp();
+    }
+    const bool bad = broken || n_orph > 1;
+    const bool po = act && !bad && n_orph == 1;
+    if (__any_sync(FULL, po)) {
+      const wgpf_event o = ws.orph[lane];
+      if (emit)
+        put(po, kw, (uint32_t)o.start, (uint32_t)(o.start >> 32), (uint32_t)o.end,
+            (uint32_t)(o.end >> 32), o.region, o.iteration);
+      if (stats)
+        wstat(po, cs.info[o.region & (kDeepRegions - 1u)] & 0xFFu,
+              (uint32_t)(o.end - o.start), gkey | (kw << 1));
+      kw += po ? 1u : 0u;
+    }
+    if (act) {
+      if (bad || kw != want) {
+        atomicAdd(&a.status->invalid, 1ull);
+        a.sflag[s] = flag | SF_INVALID;
+      }
+      if (!bad) {
+        w_mal += n_orph;
+        w_tail += (stop - s_stk0) >> 8;
+      }
+    }
+  }
+  const unsigned long long d = warp_sum((unsigned long long)w_drop);
+  const unsigned long long f = warp_sum((unsigned long long)w_flag);
+  const unsigned long long t = warp_sum((unsigned long long)w_tail);
+  const unsigned long long m = warp_sum((unsigned long long)w_mal);
+  const unsigned long long ov = warp_sum((unsigned long long)w_ovf);
+  if (lane == 0 && ov) atomicAdd(&a.status->overflow, ov);
+  if (lane == 0) {
+    if (d) atomicAdd(&cs.warn[0], d);
+    if (t) atomicAdd(&cs.warn[1], t);
+    if (f) atomicAdd(&cs.warn[2], f);
+    if (m) atomicAdd(&cs.warn[3], m);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 && cs.warn[threadIdx.x])
+    atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
+  if (stats) smem_stats_flush(cs.st, a.stats);
+}
+
+}  // namespace wgpf

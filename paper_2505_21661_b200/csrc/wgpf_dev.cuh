@@ -24,6 +24,8 @@ constexpr uint32_t SF_GENERAL = 1u;     // needs the thread-per-stream path
 constexpr uint32_t SF_DECODE_ERR = 2u;  // decode error: no events
 constexpr uint32_t SF_INVALID = 4u;     // single-stack count was wrong
 constexpr uint32_t SF_WARP = 8u;        // warp-per-stream kernel (deep / wide)
+constexpr uint32_t SF_DEEP = 16u;       // (with SF_WARP) fits the deep thread-per-
+                                        // stream kernel (k_tpsd.cuh)
 
 // ---- status block (device, read back once per call) ------------------------
 struct DevStatus {

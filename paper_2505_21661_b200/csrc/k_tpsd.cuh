@@ -270,7 +270,9 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       const uint2* myrec = reinterpret_cast<const uint2*>(
           ws.rec[bsel] + lane * kTpsPitch + 8u * (start & 1u));
       if (w0 + kTpsW + 2u <= nmin) {
-#pragma unroll
+        // (2 steps per iteration: the step with its reduced statistics is
+        // long, and 8 unrolled copies thrash the instruction cache)
+#pragma unroll 2
         for (uint32_t j = 0; j < kTpsW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
       } else {
 #pragma unroll 1

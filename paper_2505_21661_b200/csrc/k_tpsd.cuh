@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       if (w0 + kTpsW + 2u <= nmin) {
         // (2 steps per iteration: the step with its reduced statistics is
         // long, and 8 unrolled copies thrash the instruction cache)
-#pragma unroll 2
+#pragma unroll 1
         for (uint32_t j = 0; j < kTpsW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
       } else {
 #pragma unroll 1

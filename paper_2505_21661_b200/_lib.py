@@ -81,7 +81,8 @@ def lib() -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = _build.build()
+        # WGPF_LIB_OVERRIDE: an alternative build of the same ABI (A/B runs)
+        path = os.environ.get("WGPF_LIB_OVERRIDE") or _build.build()
         L = C.CDLL(path)
         vp, u64, u32, i32 = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
         sig = {

@@ -200,6 +200,10 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
 // kTpsMaxSlots (the record windows need 16-B chunk alignment).
 constexpr uint32_t kCountWarps = 4;
 constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
+#ifndef WGPF_COUNT_UNROLL
+#define WGPF_COUNT_UNROLL 16
+#endif
+constexpr int kCountUnroll = WGPF_COUNT_UNROLL;
 using CountWin = RecWindowsT<kCountW>;
 
 __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
@@ -298,7 +302,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
       __syncwarp();
       const uint2* rec = win.lane_records(bsel, lane, start);
       if (w0 + kCountW + 1u <= nmin) {
-#pragma unroll
+#pragma unroll kCountUnroll
         for (uint32_t j = 0; j < kCountW; ++j) step(std::true_type{}, w0 + j, rec[j].x);
       } else {
 #pragma unroll 1

@@ -43,6 +43,10 @@
 
 namespace wgpf {
 
+#ifndef WGPF_TPS_UNROLL
+#define WGPF_TPS_UNROLL 4
+#endif
+constexpr int kTpsUnroll = WGPF_TPS_UNROLL;  // full steps unrolled per window
 constexpr uint32_t kTpsMaxWarps = 16;                 // warps per CTA (<=)
 constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       __syncwarp();
       const uint2* myrec = win.lane_records(bsel, lane, start);
       if (w0 + kTpsW + 2u <= nmin) {
-#pragma unroll
+#pragma unroll kTpsUnroll
         for (uint32_t j = 0; j < kTpsW; ++j)
           step(std::true_type{}, w0 + j, myrec[j]);
       } else {

@@ -17,7 +17,7 @@ bench5) timeout 1200 python bench.py --config 5 --no-p1 > $OUT/bench5.json 2> $O
 benchref) timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err ;;
 benchp1) timeout 600 python bench_p1.py > $OUT/bench_p1.json 2> $OUT/bench_p1.err ;;
 ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_bench.log 2>&1
-     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_tps} -s 1 -c 1 -o $OUT/emit python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1 ;;
+     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-^k_tps$} -s 1 -c 1 -o $OUT/emit python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1 ;;
 ncusmall) timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_small.csv python bench.py --streams 262144 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_bench_small.log 2>&1
      timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_tps} -s 1 -c 1 -o $OUT/emit_small python bench.py --streams 262144 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_small.log 2>&1 ;;
 split) for fl in 0 8 1 9; do WGPF_BENCH_FLAGS=$fl timeout 400 python bench.py --streams 1048576 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --no-p1 > $OUT/split_$fl.json 2>> $OUT/split.err; done ;;

@@ -44,3 +44,19 @@ def allgather_merge(ctx, merged_ctx, dist, world: int, mine=None, gathered=None)
     dist.all_gather_into_tensor(gathered, mine)
     merged_ctx.stats_merge(gathered.data_ptr(), world)
     return merged_ctx.stats()
+
+
+OVERLAP_FIELDS = ("blocks", "span", "busy0", "busy1", "both", "bubble0", "bubble1")
+
+
+def allreduce_overlap(counters: dict, dist, device="cuda") -> dict:
+    """Role-overlap counters (wgpf_overlap_counters) of every rank combined:
+    they are sums over blocks, and blocks never straddle ranks (block-range
+    shards), so one all-reduce (sum) gives the whole-trace counters."""
+    import torch
+    v = [counters["blocks"], counters["span"], counters["busy"][0], counters["busy"][1],
+         counters["both"], counters["bubble"][0], counters["bubble"][1]]
+    t = torch.tensor(v, dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    a = [int(x) for x in t.tolist()]
+    return dict(blocks=a[0], span=a[1], busy=[a[2], a[3]], both=a[4], bubble=[a[5], a[6]])

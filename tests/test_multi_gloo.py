@@ -5,7 +5,9 @@ computes its per-label table with the CPU oracle in the packed layout that
 wgpf_stats_export produces (70 u64 per label: count, sum, min, max, first key,
 first warp group, 64 bins), the ranks all-gather the tables (the one
 collective), and the merge rule of wgpf_stats_merge (add / min / max /
-first-key min with its warp group) must reproduce the single-process table.
+first-key min with its warp group) must reproduce the single-process table;
+the role-overlap counters all-reduced across ranks (shard.allreduce_overlap)
+must equal the whole trace's.
 """
 import os
 import socket
@@ -85,7 +87,10 @@ def _rank_main(rank, world, port, n_streams, q):
         dist.all_gather_into_tensor(out, mine)
         tables = [t.numpy().view(np.uint64) for t in out.chunk(world)]
         merged = merge_tables(tables)
-        q.put((rank, merged))
+        # role-overlap counters: per-rank counters, one all-reduce (sum)
+        roles = [0] * 4 + [1] * 12
+        ov = shard.allreduce_overlap(orc.overlap(r.events, roles), dist, device="cpu")
+        q.put((rank, (merged, ov)))
     finally:
         dist.destroy_process_group()
 
@@ -134,7 +139,14 @@ def test_gloo_world2_shard_and_merge_equals_single(oracle):
             p.kill()
         assert p.exitcode == 0
     assert len(res) == 2
-    assert np.array_equal(res[0], res[1])
+    assert np.array_equal(res[0][0], res[1][0])
+    assert res[0][1] == res[1][1]
+    ov_all = oracle.overlap(
+        oracle.replay_body(S.mixed_body(0, n_streams, S.MIXED_FULL_LONG - n_streams // 3),
+                           n_streams, S.CAP, 1, S.MIXED_LABELS, 33).events,
+        [0] * 4 + [1] * 12)
+    assert res[0][1] == ov_all
+    res = {k: v[0] for k, v in res.items()}
     # single process, whole trace
     body = S.mixed_body(0, n_streams, S.MIXED_FULL_LONG - n_streams // 3)
     r = oracle.replay_body(body, n_streams, S.CAP, 1, S.MIXED_LABELS, 33)

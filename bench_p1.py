@@ -104,7 +104,7 @@ def measure(M: int = 8192, N: int = 8192, K: int = 8192, iters: int = 25,
     B = torch.randn(N, K, generator=g, device="cuda").to(torch.bfloat16)
     C0 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     C1 = torch.empty_like(C0)
-    ctas = (M // 128) * (N // 256)
+    ctas = p1.gemm_ctas(M, N)
     prof = torch.zeros(p1.gemm_profile_bytes(M, N), dtype=torch.uint8, device="cuda")
     timing = torch.zeros(ctas * 32, dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > L2

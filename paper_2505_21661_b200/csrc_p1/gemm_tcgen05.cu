@@ -6,7 +6,8 @@
 //
 // Roles (6 warps): warp 0 TMA producer, warp 1 MMA issuer (+ TMEM owner),
 // warps 2-5 epilogue (TMEM lanes 32*(w%4) .. +32).  Tile 128x256x64, UMMA
-// 128x256x16 (cta_group::1), 4 smem stages of 48 KB, 256 TMEM columns.
+// 128x256x16 (cta_group::1), 4 smem stages of 48 KB, 2 x 256 TMEM columns
+// (double-buffered accumulator).
 //
 // Scopes (region ids): 0 tile, 1 tma.wait, 2 tma.issue, 3 mma.wait,
 // 4 mma.issue, 5 epi.wait, 6 epi.ld, 7 epi.st.
@@ -27,7 +28,7 @@ constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t NWARPS = 6, THREADS = NWARPS * 32;
 constexpr uint32_t PROF_CAP = 64;
 constexpr uint32_t PROF_BYTES = wgpf_dev::smem_bytes(NWARPS, PROF_CAP);
-constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TMEM_COLS = 512;  // two 128 x 256 fp32 accumulators
 constexpr uint32_t SMEM_BYTES = 1024 + STAGES * STAGE_BYTES + 256 + PROF_BYTES;
 
 enum : uint32_t { R_TILE, R_TMA_WAIT, R_TMA, R_MMA_WAIT, R_MMA, R_EPI_WAIT,
@@ -105,6 +106,22 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
       : "memory");
 }
 
+// Persistent: one CTA per SM walks tiles t = blockIdx.x, += gridDim.x in a
+// grouped raster (kGroupM m-blocks x all n-blocks, m fastest) so a wave's A
+// and B tiles stay in L2.  Two TMEM accumulators (2 x 256 columns): the MMA
+// warp fills one while the epilogue drains the other (tmem_full / tmem_empty
+// barriers), so the epilogue overlaps the next tile's main loop.
+constexpr uint32_t kGroupM = 8;
+
+__device__ __forceinline__ void tile_coords(uint32_t t, uint32_t nM, uint32_t nN,
+                                            uint32_t& mb, uint32_t& nb) {
+  const uint32_t per_group = kGroupM * nN;
+  const uint32_t g = t / per_group, r = t % per_group;
+  const uint32_t gm = min(kGroupM, nM - g * kGroupM);  // m-blocks in this group
+  mb = g * kGroupM + r % gm;
+  nb = r / gm;
+}
+
 // kMode: 0 plain, 1 one clock capture per RecordOp, 2 adjacent END/START
 // RecordOps at scope boundaries share a capture (Recorder::mark)
 template <int kMode>
@@ -119,14 +136,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* stage_base = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + STAGES;   // [2]
+  uint64_t* tmem_empty = tmem_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   uint8_t* prof = smem + STAGES * STAGE_BYTES + 256;
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const uint32_t nM = M / BM, nN = N / BN, n_tiles = nM * nN;
   const uint32_t nk = K / BK;
-  const uint64_t cta = (uint64_t)blockIdx.y * gridDim.x + blockIdx.x;
+  const uint64_t cta = blockIdx.x;
 
   wgpf_dev::Recorder<true> rec;
   if constexpr (kMode != 0) {
@@ -137,7 +155,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       timing[cta].gt_start = wgpf_dev::globaltimer();
       timing[cta].clk_start = wgpf_dev::clock32();
     }
-    rec.start(R_TILE);
   }
 
   if (warp == 0 && lane == 0) {
@@ -147,7 +164,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (uint32_t a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -164,123 +184,158 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
-    if constexpr (kMode == 2) rec.start(R_TMA_WAIT);
-    for (uint32_t kb = 0; kb < nk; ++kb) {
-      const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1u;
-      if constexpr (kMode == 1) rec.start(R_TMA_WAIT);
-      if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
-      __syncwarp();
-      if constexpr (kMode == 1) {
-        rec.end(R_TMA_WAIT);
-        rec.start(R_TMA);
+    uint32_t it = 0;  // k-block counter across tiles
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      uint32_t mb, nb;
+      tile_coords(t, nM, nN, mb, nb);
+      const uint32_t m0 = mb * BM, n0 = nb * BN;
+      if constexpr (kMode != 0) rec.start(R_TILE);
+      if constexpr (kMode == 2) rec.start(R_TMA_WAIT);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+        if constexpr (kMode == 1) rec.start(R_TMA_WAIT);
+        if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
+        __syncwarp();
+        if constexpr (kMode == 1) {
+          rec.end(R_TMA_WAIT);
+          rec.start(R_TMA);
+        }
+        if constexpr (kMode == 2) rec.mark(R_TMA_WAIT, R_TMA);
+        if (lane == 0) {
+          uint8_t* a = stage_base + s * STAGE_BYTES;
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(&ta, &full[s], a, (int)(kb * BK), (int)m0);
+          tma_load_2d(&tb, &full[s], a + A_BYTES, (int)(kb * BK), (int)n0);
+        }
+        __syncwarp();
+        if constexpr (kMode == 1) rec.end(R_TMA);
+        if constexpr (kMode == 2) {
+          if (kb + 1 < nk)
+            rec.mark(R_TMA, R_TMA_WAIT);
+          else
+            rec.end(R_TMA);
+        }
       }
-      if constexpr (kMode == 2) rec.mark(R_TMA_WAIT, R_TMA);
-      if (lane == 0) {
-        uint8_t* a = stage_base + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(&ta, &full[s], a, (int)(kb * BK), (int)m0);
-        tma_load_2d(&tb, &full[s], a + A_BYTES, (int)(kb * BK), (int)n0);
-      }
-      __syncwarp();
-      if constexpr (kMode == 1) rec.end(R_TMA);
-      if constexpr (kMode == 2) {
-        if (kb + 1 < nk)
-          rec.mark(R_TMA, R_TMA_WAIT);
-        else
-          rec.end(R_TMA);
-      }
+      if constexpr (kMode != 0) rec.end(R_TILE);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if constexpr (kMode == 2) rec.start(R_MMA_WAIT);
-    for (uint32_t kb = 0; kb < nk; ++kb) {
-      const uint32_t s = kb % STAGES, ph = (kb / STAGES) & 1u;
-      if constexpr (kMode == 1) rec.start(R_MMA_WAIT);
-      if (lane == 0) mbar_wait(&full[s], ph);
+    uint32_t it = 0, tl = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+      const uint32_t dt = tmem + acc * BN;
+      if constexpr (kMode != 0) rec.start(R_TILE);
+      // the epilogue has drained this accumulator (two tiles ago)
+      if (lane == 0) mbar_wait(&tmem_empty[acc], aph ^ 1u);
       __syncwarp();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if constexpr (kMode == 1) {
-        rec.end(R_MMA_WAIT);
-        rec.start(R_MMA);
-      }
-      if constexpr (kMode == 2) rec.mark(R_MMA_WAIT, R_MMA);
-      if (lane == 0) {
-        const uint32_t a = smem_u32(stage_base + s * STAGE_BYTES);
-        const uint32_t b = a + A_BYTES;
+      if constexpr (kMode == 2) rec.start(R_MMA_WAIT);
+      for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
+        const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
+        if constexpr (kMode == 1) rec.start(R_MMA_WAIT);
+        if (lane == 0) mbar_wait(&full[s], ph);
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if constexpr (kMode == 1) {
+          rec.end(R_MMA_WAIT);
+          rec.start(R_MMA);
+        }
+        if constexpr (kMode == 2) rec.mark(R_MMA_WAIT, R_MMA);
+        if (lane == 0) {
+          const uint32_t a = smem_u32(stage_base + s * STAGE_BYTES);
+          const uint32_t b = a + A_BYTES;
 #pragma unroll
-        for (uint32_t k = 0; k < BK / 16; ++k)
-          umma(tmem, umma_desc(a + 32u * k), umma_desc(b + 32u * k),
-               (kb | k) != 0u);
-        umma_commit(&empty[s]);
-        if (kb == nk - 1) umma_commit(tmem_full);
+          for (uint32_t k = 0; k < BK / 16; ++k)
+            umma(dt, umma_desc(a + 32u * k), umma_desc(b + 32u * k), (kb | k) != 0u);
+          umma_commit(&empty[s]);
+          if (kb == nk - 1) umma_commit(&tmem_full[acc]);
+        }
+        __syncwarp();
+        if constexpr (kMode == 1) rec.end(R_MMA);
+        if constexpr (kMode == 2) {
+          if (kb + 1 < nk)
+            rec.mark(R_MMA, R_MMA_WAIT);
+          else
+            rec.end(R_MMA);
+        }
       }
-      __syncwarp();
-      if constexpr (kMode == 1) rec.end(R_MMA);
-      if constexpr (kMode == 2) {
-        if (kb + 1 < nk)
-          rec.mark(R_MMA, R_MMA_WAIT);
-        else
-          rec.end(R_MMA);
-      }
+      if constexpr (kMode != 0) rec.end(R_TILE);
     }
   } else {
     // ---------------- epilogue: TMEM -> registers -> bf16 -> HBM -----------
     const uint32_t quad = warp & 3u;  // TMEM lane quadrant of this warp
-    const uint32_t row = m0 + quad * 32u + lane;
-    if constexpr (kMode != 0) rec.start(R_EPI_WAIT);
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if constexpr (kMode == 1) rec.end(R_EPI_WAIT);
-    if constexpr (kMode == 2) rec.mark(R_EPI_WAIT, R_EPI_LD);
-    const uint32_t taddr = tmem + ((quad * 32u) << 16);
-    for (uint32_t c = 0; c < BN; c += 32) {
-      if constexpr (kMode == 1) rec.start(R_EPI_LD);
-      uint32_t v[32];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,"
-          "%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,"
-          "%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]),
-            "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]),
-            "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
-            "=r"(v[30]), "=r"(v[31])
-          : "r"(taddr + c));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if constexpr (kMode == 1) {
-        rec.end(R_EPI_LD);
-        rec.start(R_EPI_ST);
+    uint32_t tl = 0;
+    for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
+      uint32_t mb, nb;
+      tile_coords(t, nM, nN, mb, nb);
+      const uint32_t m0 = mb * BM, n0 = nb * BN;
+      const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
+      const uint32_t row = m0 + quad * 32u + lane;
+      if constexpr (kMode != 0) {
+        rec.start(R_TILE);
+        rec.start(R_EPI_WAIT);
       }
-      if constexpr (kMode == 2) rec.mark(R_EPI_LD, R_EPI_ST);
-      uint4 out[4];
-      uint32_t* o = reinterpret_cast<uint32_t*>(out);
+      mbar_wait(&tmem_full[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if constexpr (kMode == 1) rec.end(R_EPI_WAIT);
+      if constexpr (kMode == 2) rec.mark(R_EPI_WAIT, R_EPI_LD);
+      const uint32_t taddr = tmem + acc * BN + ((quad * 32u) << 16);
+      for (uint32_t c = 0; c < BN; c += 32) {
+        if constexpr (kMode == 1) rec.start(R_EPI_LD);
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,"
+            "%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,"
+            "%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]),
+              "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]),
+              "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c + 32 == BN) {
+          // the accumulator is in registers: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                             smem_u32(&tmem_empty[acc]))
+                         : "memory");
+        }
+        if constexpr (kMode == 1) {
+          rec.end(R_EPI_LD);
+          rec.start(R_EPI_ST);
+        }
+        if constexpr (kMode == 2) rec.mark(R_EPI_LD, R_EPI_ST);
+        uint4 out[4];
+        uint32_t* o = reinterpret_cast<uint32_t*>(out);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * j]),
-                                                 __uint_as_float(v[2 * j + 1]));
-        o[j] = *reinterpret_cast<uint32_t*>(&h);
-      }
-      if (row < M) {
-        uint4* dst = reinterpret_cast<uint4*>(C + (uint64_t)row * N + n0 + c);
+        for (int j = 0; j < 16; ++j) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(v[2 * j]),
+                                                   __uint_as_float(v[2 * j + 1]));
+          o[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        if (row < M) {
+          uint4* dst = reinterpret_cast<uint4*>(C + (uint64_t)row * N + n0 + c);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dst[j] = out[j];
+          for (int j = 0; j < 4; ++j) dst[j] = out[j];
+        }
+        if constexpr (kMode == 1) rec.end(R_EPI_ST);
+        if constexpr (kMode == 2) {
+          if (c + 32 < BN)
+            rec.mark(R_EPI_ST, R_EPI_LD);
+          else
+            rec.end(R_EPI_ST);
+        }
       }
-      if constexpr (kMode == 1) rec.end(R_EPI_ST);
-      if constexpr (kMode == 2) {
-        if (c + 32 < BN)
-          rec.mark(R_EPI_ST, R_EPI_LD);
-        else
-          rec.end(R_EPI_ST);
-      }
+      if constexpr (kMode != 0) rec.end(R_TILE);
     }
   }
 
-  if constexpr (kMode != 0) {
-    rec.end(R_TILE);
-    rec.close((uint32_t)cta, warp, PROF_CAP);
-  }
+  if constexpr (kMode != 0) rec.close((uint32_t)cta, warp, PROF_CAP);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1)
@@ -293,6 +348,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       timing[cta].clk_end = wgpf_dev::clock32();
     }
   }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+uint32_t grid_ctas(uint32_t M, uint32_t N) {
+  const uint32_t tiles = (M / BM) * (N / BN);
+  return tiles < (uint32_t)sm_count() ? tiles : (uint32_t)sm_count();
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
@@ -334,9 +405,11 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols,
 // N % 256, K % 64 must be 0.  instrument != 0 runs the P1-instrumented kernel
 // and writes the KPFT body to d_profile (wgpf_gemm_profile_bytes) and the CTA
 // side records to d_timing (32 B per CTA, may be null).
+// one profile segment per CTA of the persistent grid (min(tiles, SMs))
 extern "C" uint64_t wgpf_gemm_profile_bytes(uint32_t M, uint32_t N) {
-  return wgpf_dev::profile_bytes((uint64_t)(M / BM) * (N / BN), NWARPS, PROF_CAP);
+  return wgpf_dev::profile_bytes(grid_ctas(M, N), NWARPS, PROF_CAP);
 }
+extern "C" uint32_t wgpf_gemm_ctas(uint32_t M, uint32_t N) { return grid_ctas(M, N); }
 
 extern "C" uint32_t wgpf_gemm_smem_bytes(int instrument) {
   return instrument ? SMEM_BYTES : SMEM_BYTES - PROF_BYTES;
@@ -348,7 +421,7 @@ extern "C" int wgpf_gemm_bf16(const void* A, const void* B, void* C, uint32_t M,
   if (M % BM || N % BN || K % BK || K == 0) return 11;
   CUtensorMap ta, tb;
   if (!make_map(&ta, A, M, K, BM) || !make_map(&tb, B, N, K, BN)) return 10;
-  dim3 grid(N / BN, M / BM);
+  dim3 grid(grid_ctas(M, N));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (instrument) {
     // instrument = 1: one capture per RecordOp; 2: shared boundary captures

@@ -56,6 +56,8 @@ def lib() -> C.CDLL:
         L.wgpf_gemm_bf16.restype = i32
         L.wgpf_gemm_profile_bytes.argtypes = [u32, u32]
         L.wgpf_gemm_profile_bytes.restype = u64
+        L.wgpf_gemm_ctas.argtypes = [u32, u32]
+        L.wgpf_gemm_ctas.restype = u32
         L.wgpf_gemm_smem_bytes.argtypes = [i32]
         L.wgpf_gemm_smem_bytes.restype = u32
         L.wgpf_attn_bf16.argtypes = [vp, vp, vp, vp, u32, u32, C.c_float, i32, i32,
@@ -120,6 +122,12 @@ def gemm(a_ptr: int, b_ptr: int, c_ptr: int, M: int, N: int, K: int,
 
 def gemm_profile_bytes(M: int, N: int) -> int:
     return int(lib().wgpf_gemm_profile_bytes(M, N))
+
+
+def gemm_ctas(M: int, N: int) -> int:
+    """CTAs of the persistent GEMM grid (min(tiles, SMs)); one profile
+    segment of GEMM_WARPS streams each."""
+    return int(lib().wgpf_gemm_ctas(M, N))
 
 
 def gemm_smem_bytes(instrument: bool) -> int:

@@ -90,7 +90,7 @@ def test_gemm_matches_cublas_and_instrumented_is_identical(oracle, shape):
     C0 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     C1 = torch.empty_like(C0)
     p1.gemm(A.data_ptr(), B.data_ptr(), C0.data_ptr(), M, N, K, False)
-    ctas = (M // 128) * (N // 256)
+    ctas = p1.gemm_ctas(M, N)
     prof = torch.zeros(p1.gemm_profile_bytes(M, N), dtype=torch.uint8, device="cuda")
     p1.gemm(A.data_ptr(), B.data_ptr(), C1.data_ptr(), M, N, K, True, prof.data_ptr())
     torch.cuda.synchronize()

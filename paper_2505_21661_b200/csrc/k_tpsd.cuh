@@ -185,11 +185,12 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     const uint32_t lim = off + n <= a.events_cap
                              ? 0xFFFFFFFFu
                              : (off < a.events_cap ? (uint32_t)(a.events_cap - off) : 0u);
-    wgpf_event* const ev0 = a.events + (act ? off : 0ull);
+    const uint64_t ev0 = opaque_u64(reinterpret_cast<uint64_t>(a.events + (act ? off : 0ull)));
     auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
                    uint32_t ehi, uint32_t region, uint32_t it) {
       const bool ok = p & (k < lim);
-      if (ok) stg256(ev0 + k, make_uint4(slo, shi, elo, ehi), make_uint4(region, it, blk, wg));
+      stg256_if(ok, ev0 + 32ull * k, make_uint4(slo, shi, elo, ehi),
+                make_uint4(region, it, blk, wg));
       w_ovf += (p && !ok) ? 1u : 0u;
     };
     auto step = [&](auto full, uint32_t i, uint2 r2) {
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
       pw = base ? (inf >> 16) : 0xFFu;
       sts128_if(orphan && n_orph == 0, s_orph, make_uint4(e.x, shi, v, hi));
-      sts128_if(orphan && n_orph == 0, s_orph + 16u, make_uint4(rid, it, blk, wg));
+      sts64_if(orphan && n_orph == 0, s_orph + 16u, make_uint2(rid, it));
       n_orph += orphan ? 1u : 0u;
       if constexpr (stats) {
         wstat(base, inf & 0xFFu, corr, gkey | (kpos << 1));

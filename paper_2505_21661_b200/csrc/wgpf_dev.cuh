@@ -243,6 +243,21 @@ __device__ __forceinline__ void stg256(void* p, uint4 a, uint4 b) {
                : "memory");
 }
 
+// predicated form (no branch around the store; the operands are computed
+// unconditionally)
+__device__ __forceinline__ void stg256_if(bool q, uint64_t p, uint4 a, uint4 b) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.global.v8.u32 [%1], {%2, %3, %4, %5, %6, "
+      "%7, %8, %9}; }" ::"r"((uint32_t)q),
+      "l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t opaque_u64(uint64_t x) {
+  uint64_t y;
+  asm("mov.b64 %0, %1;" : "=l"(y) : "l"(x));
+  return y;
+}
+
 // a value the compiler cannot see through (so it is not rematerialised)
 __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   uint32_t y;

@@ -51,10 +51,13 @@ constexpr uint32_t kTpsMaxWarps = 16;                 // warps per CTA (<=)
 constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
 constexpr uint32_t kTpsClasses = 16;                  // dense classes held
+// stack entry: the START's region id stays where the record tag has it
+// (bits 12..16), so an END compares it with one xor
+constexpr uint32_t kStkRid = (kTpsRegions - 1u) << 12;
 
 struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
-  uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<11 | cons<<16 | hi<<17}
+  uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<12 | cons<<17 | hi<<18}
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
 };
 
@@ -156,6 +159,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint32_t s_cnt = smem_addr(tb.cnt + lane);        // + 64 * region
   const uint32_t s_a = smem_addr(tb.a + lane);            // + 512 * class
   const uint32_t s_orph = smem_addr(&ws.orph[lane]);
+  const uint32_t s_hi = smem_addr(tb.hi + lane);          // + 128 * class
 
   const uint64_t wstep = (uint64_t)gridDim.x * nw;
   for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b * 32 < a.n_streams;
@@ -212,10 +216,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const uint64_t ev0 = opaque_u64(reinterpret_cast<uint64_t>(a.events + (act ? off : 0ull)));
     auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
                    uint32_t ehi, uint32_t region, uint32_t it) {
-      const bool ok = p & (k < lim);
-      stg256_if(ok, ev0 + 32ull * k, make_uint4(slo, shi, elo, ehi),
+      // (events past lim are counted once at the stream end: kw - lim)
+      stg256_if(p & (k < lim), ev0 + 32ull * k, make_uint4(slo, shi, elo, ehi),
                 make_uint4(region, it, blk, wg));
-      w_ovf += (p && !ok) ? 1u : 0u;
     };
     // one event of class cls (predicated on p): lane-private count / min /
     // max / sum, per-warp first key, CTA histogram
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       x.y = min(x.y, d);
       x.z = max(x.z, d);
       const uint32_t sm = x.w + d;
-      if (p && sm < d) tb.hi[c * 32 + lane] += 1;
+      red_add_if(p && sm < d, s_hi + c * 128u, 1u);
       x.w = sm;
       sts128_if(p, ea, x);
       red_add_if(p, s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)), 1u);
@@ -254,13 +257,13 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       const bool mend = en && nonempty;
       w_drop += (en && !nonempty) ? 1u : 0u;
       sts64_if(st, stop + 256u,
-               make_uint2(v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 16) |
-                                 (hi << 17)));
+               make_uint2(v, i | (tag & kStkRid) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 17) |
+                                 (hi << 18)));
       stop = stop + (st ? 256u : 0u) - (mend ? 256u : 0u);
-      const uint32_t shi = e.y >> 17;
+      const uint32_t shi = e.y >> 18;
       const uint32_t meas = v - e.x;  // low 32 bits of u - su
       const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
-      const bool mism = mend && ((e.y >> 11) & 31u) != rid;
+      const bool mism = mend && ((e.y ^ tag) & kStkRid) != 0u;
       const bool tlong = mend && !mism && dhi;
       broken |= mism || tlong;
       const bool ok = mend && !mism && !tlong;
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       sts16_if(ok, ca, it + 1u);
       const bool is_mk = (inf & 0x100u) != 0u;
       const bool base = ok && !is_mk;
-      const bool orphan = ok && is_mk && !((e.y >> 16) & 1u);
+      const bool orphan = ok && is_mk && !((e.y >> 17) & 1u);
       // ---- exec event: sync correction ---------------------------------------
       const uint32_t dpos = i - (e.y & 2047u);
       // dpos < 2^11 and cost < 2^21 (host): the product fits 32 bits
@@ -340,6 +343,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
         lstat(po, cs.info[o.region & 31u] & 0xFFu, (uint32_t)(o.end - o.start), kw, 0u);
       kw += po ? 1u : 0u;
     }
+    w_ovf += act && kw > lim ? kw - lim : 0u;
     if (act) {
       // exact recount + re-emit on the general path, which also reports the
       // reference's pair error (trace.hpp:330-336) if there is one

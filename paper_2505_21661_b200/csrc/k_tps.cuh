@@ -67,29 +67,27 @@ struct TpsCtaSmem {
 };
 
 // Per-warp dynamic tables (R = region ids in use, K = classes):
-//   a     uint4 [K][32]       {count, min, max, sum lo} per class and lane
-//   hi    u32 [K][32]         sum hi
+//   a     uint4 [K][32]       {min, max, sum lo, sum hi} per class and lane
 //   first u64 [K]             first-event key (per warp: shared atomicMin
-//                             when a lane meets a class for the first time)
+//                             when a lane meets a class for the first time,
+//                             i.e. while its min is still the initial ~0)
 //   cnt   u16 [R][32]         iteration counters
-// and per CTA hist u32 [K][64].
+// and per CTA hist u32 [K][64]; a class's event count is the sum of its bins.
 struct TpsTables {
   uint4* a;
-  uint32_t* hi;
   unsigned long long* first;
   uint16_t* cnt;
 };
 
 __host__ __device__ inline size_t tps_align(size_t b) { return (b + 127) & ~size_t(127); }
 __host__ __device__ inline size_t tps_tables_bytes(uint32_t K, uint32_t R) {
-  return tps_align((size_t)K * 32 * 20 + (size_t)K * 8 + (size_t)R * 64);
+  return tps_align((size_t)K * 32 * 16 + (size_t)K * 8 + (size_t)R * 64);
 }
 __host__ __device__ inline TpsTables tps_tables(uint8_t* p, uint32_t K, uint32_t R) {
   TpsTables t;
   t.a = reinterpret_cast<uint4*>(p);
-  t.hi = reinterpret_cast<uint32_t*>(p + (size_t)K * 32 * 16);
-  t.first = reinterpret_cast<unsigned long long*>(p + (size_t)K * 32 * 20);
-  t.cnt = reinterpret_cast<uint16_t*>(p + (size_t)K * 32 * 20 + (size_t)K * 8);
+  t.first = reinterpret_cast<unsigned long long*>(p + (size_t)K * 32 * 16);
+  t.cnt = reinterpret_cast<uint16_t*>(p + (size_t)K * 32 * 16 + (size_t)K * 8);
   return t;
 }
 __host__ __device__ inline size_t tps_hist_bytes(uint32_t K) {
@@ -123,10 +121,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const TpsTables tb = tps_tables(tb0 + w * tps_tables_bytes(K, R), K, R);
   constexpr bool stats = kStats;
   constexpr bool emit = kEmit;
-  for (uint32_t c = 0; c < K; ++c) {
-    tb.a[c * 32 + lane] = make_uint4(0u, 0xFFFFFFFFu, 0u, 0u);
-    tb.hi[c * 32 + lane] = 0;
-  }
+  for (uint32_t c = 0; c < K; ++c) tb.a[c * 32 + lane] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
   for (uint32_t c = lane; c < K; c += 32) tb.first[c] = ~0ull;
   for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x) hist[i] = 0;
   for (uint32_t r = threadIdx.x; r < kTpsRegions; r += blockDim.x) {
@@ -159,7 +154,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   const uint32_t s_cnt = smem_addr(tb.cnt + lane);        // + 64 * region
   const uint32_t s_a = smem_addr(tb.a + lane);            // + 512 * class
   const uint32_t s_orph = smem_addr(&ws.orph[lane]);
-  const uint32_t s_hi = smem_addr(tb.hi + lane);          // + 128 * class
 
   const uint64_t wstep = (uint64_t)gridDim.x * nw;
   for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b * 32 < a.n_streams;
@@ -220,19 +214,19 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
       stg256_if(p & (k < lim), ev0 + 32ull * k, make_uint4(slo, shi, elo, ehi),
                 make_uint4(region, it, blk, wg));
     };
-    // one event of class cls (predicated on p): lane-private count / min /
-    // max / sum, per-warp first key, CTA histogram
+    // one event of class cls (predicated on p): lane-private min / max / sum,
+    // per-warp first key, CTA histogram (which also gives the count).  A lane
+    // meets its events in key order, so the first-key atomic fires while the
+    // lane's min is still ~0 (again only if every duration so far was
+    // 2^32-1: a larger key, which the min leaves alone).
     auto lstat = [&](bool p, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
       const uint32_t c = p ? cls : 0u;
       const uint32_t ea = s_a + c * 512u;
       uint4 x = lds128(ea);
-      if (p && x.x == 0) atomicMin(&tb.first[c], gkey | (kpos << 1) | kind);
-      x.x += 1;
-      x.y = min(x.y, d);
-      x.z = max(x.z, d);
-      const uint32_t sm = x.w + d;
-      red_add_if(p && sm < d, s_hi + c * 128u, 1u);
-      x.w = sm;
+      if (p && x.x == 0xFFFFFFFFu) atomicMin(&tb.first[c], gkey | (kpos << 1) | kind);
+      x.x = min(x.x, d);
+      x.y = max(x.y, d);
+      add64_u32(x.z, x.w, d);
       sts128_if(p, ea, x);
       red_add_if(p, s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)), 1u);
     };
@@ -373,15 +367,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   if (stats) {
     for (uint32_t c = 0; c < K; ++c) {
       const uint4 x = tb.a[c * 32 + lane];
-      const unsigned long long cnt = warp_sum((unsigned long long)x.x);
-      if (cnt == 0) continue;
-      const unsigned long long sum = warp_sum(
-          ((unsigned long long)tb.hi[c * 32 + lane] << 32) | x.w);
-      const uint32_t mn = __reduce_min_sync(FULL, x.y);
-      const uint32_t mx = __reduce_max_sync(FULL, x.z);
+      // (no event: min ~0 and max 0; an event of 2^32-1 cycles has max ~0)
+      if (!__any_sync(FULL, x.x != 0xFFFFFFFFu || x.y != 0u)) continue;
+      const unsigned long long sum =
+          warp_sum(((unsigned long long)x.w << 32) | x.z);
+      const uint32_t mn = __reduce_min_sync(FULL, x.x);
+      const uint32_t mx = __reduce_max_sync(FULL, x.y);
       const unsigned long long fk = tb.first[c];
       if (lane == 0) {
-        atomicAdd(&a.stats.count[c], cnt);
         atomicAdd(&a.stats.sum[c], sum);
         atomicMin(&a.stats.min[c], (unsigned long long)mn);
         atomicMax(&a.stats.max[c], (unsigned long long)mx);
@@ -392,9 +385,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
   __syncthreads();
   if (threadIdx.x < 4 && cs.warn[threadIdx.x])
     atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
-  if (stats) {  // per-warp histograms -> global
+  if (stats) {  // CTA histograms -> global; counts = bin sums
     for (uint32_t i = threadIdx.x; i < K * WGPF_HIST_BINS; i += blockDim.x) {
       if (hist[i]) atomicAdd(&a.stats.hist[i], (unsigned long long)hist[i]);
+    }
+    for (uint32_t c = w; c < K; c += nw) {
+      const unsigned long long cnt = warp_sum(
+          (unsigned long long)hist[c * WGPF_HIST_BINS + lane] + hist[c * WGPF_HIST_BINS + 32 + lane]);
+      if (lane == 0 && cnt) atomicAdd(&a.stats.count[c], cnt);
     }
   }
 }

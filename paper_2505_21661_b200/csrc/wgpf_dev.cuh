@@ -292,6 +292,10 @@ __device__ __forceinline__ void sts128_if(bool p, uint32_t a, uint4 v) {
       "r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
       : "memory");
 }
+// (lo, hi) += d as one 64-bit add (add.cc / addc)
+__device__ __forceinline__ void add64_u32(uint32_t& lo, uint32_t& hi, uint32_t d) {
+  asm("add.cc.u32 %0, %0, %2; addc.u32 %1, %1, 0;" : "+r"(lo), "+r"(hi) : "r"(d));
+}
 __device__ __forceinline__ void red_add_if(bool p, uint32_t a, uint32_t v) {
   asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q red.shared.add.u32 [%1], %2; }" ::"r"(
                    (uint32_t)p),

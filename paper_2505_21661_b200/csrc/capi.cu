@@ -77,13 +77,14 @@ struct DevBuf {
 }  // namespace
 
 using TpsKernel = void (*)(FastArgs);
+using TpsTmaKernel = void (*)(FastArgs, const CUtensorMap);
 static TpsKernel deep_kernel(bool emit, bool stats) {
   static const TpsKernel k[4] = {k_tpsd<false, false>, k_tpsd<true, false>,
                                  k_tpsd<false, true>, k_tpsd<true, true>};
   return k[(emit ? 1 : 0) | (stats ? 2 : 0)];
 }
-static TpsKernel tps_kernel(bool emit, bool stats) {
-  static const TpsKernel k[4] = {k_tps<false, false>, k_tps<true, false>,
+static TpsTmaKernel tps_kernel(bool emit, bool stats) {
+  static const TpsTmaKernel k[4] = {k_tps<false, false>, k_tps<true, false>,
                                  k_tps<false, true>, k_tps<true, true>};
   return k[(emit ? 1 : 0) | (stats ? 2 : 0)];
 }
@@ -124,6 +125,7 @@ struct wgpf_ctx {
   bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
   bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
   bool no_deep = getenv("WGPF_NO_DEEP") != nullptr;  // deep streams -> warp kernel
+  bool no_tma = getenv("WGPF_NO_TMA") != nullptr;    // k_tps windows by cp.async only
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   size_t smem_optin = 0;
@@ -603,6 +605,45 @@ static uint32_t tps_regions(const wgpf_ctx* c) {
   return std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions);
 }
 
+// The body as a 2-D u32 tensor {stride / 4, n_streams} with k_tps's window
+// box {kTpsPitch / 4, 32} (k_window.cuh); false when TMA cannot address it
+// (alignment, sizes) or the driver entry point is missing.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static CUtensorMapL2promotion l2_promotion() {
+  const char* e = getenv("WGPF_TMA_L2");
+  const int v = e ? atoi(e) : 0;
+  return v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+         : v == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride,
+                            uint64_t n_streams) {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                       cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess
+               ? reinterpret_cast<EncodeTiledFn>(p)
+               : nullptr;
+  }();
+  if (!fn || (reinterpret_cast<uintptr_t>(body) & 15u) || (stride & 15u) ||
+      stride < kTpsPitch || stride >= (1ull << 39) || n_streams < 32 ||
+      n_streams >= (1ull << 31))
+    return false;
+  const cuuint64_t dims[2] = {stride / 4, n_streams};
+  const cuuint64_t strides[1] = {stride};
+  const cuuint32_t box[2] = {kTpsPitch / 4, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(body), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                      uint64_t n_streams, uint64_t stream_base,
                      uint64_t record_cost, wgpf_event* events,
@@ -639,6 +680,7 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.list = nullptr;
   f.list_len = nullptr;
   f.tps_regions = tps_regions(c);
+  f.tma = 0;
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
   if ((tps_enabled(c) || deep_enabled(c)) && record_cost < (1ull << 21)) {
@@ -646,7 +688,11 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       // shallow streams: thread per stream
       const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
       const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
-      tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f);
+      CUtensorMap tm;
+      memset(&tm, 0, sizeof(tm));
+      f.tma = !c->no_tma && body_tensor_map(&tm, body, stride, n_streams) ? 1u : 0u;
+      tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f, tm);
+      f.tma = 0;
       CUDA_OK(c, cudaGetLastError());
       ++c->launches;
     }

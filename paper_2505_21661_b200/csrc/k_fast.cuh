@@ -57,6 +57,7 @@ struct FastArgs {
   const unsigned long long* list;
   const unsigned long long* list_len;
   uint32_t tps_regions;  // k_tps: region ids in its tables
+  uint32_t tma;          // k_tps: the tensor map of the body is valid
 };
 
 struct LevelEntry {  // last START seen at a nesting level

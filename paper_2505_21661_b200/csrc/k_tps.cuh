@@ -59,6 +59,7 @@ struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
   uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<12 | cons<<17 | hi<<18}
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
+  unsigned long long bar[2];         // TMA windows: one mbarrier per buffer
 };
 
 struct TpsCtaSmem {
@@ -105,8 +106,10 @@ __host__ inline uint32_t tps_warps(uint32_t K, uint32_t R, size_t smem_limit) {
 }
 
 // kEmit: events materialised; kStats: statistics.
+// tm: the body as a TMA tensor (a.tma != 0), see k_window.cuh
 template <bool kEmit, bool kStats>
-__global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
+__global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
+    k_tps(FastArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TpsCtaSmem& cs = *reinterpret_cast<TpsCtaSmem*>(smem_raw);
   const uint32_t lane = lane_id();
@@ -135,6 +138,13 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     cs.info[r] = inf;
   }
   if (threadIdx.x < 4) cs.warn[threadIdx.x] = 0;
+  const uint32_t s_bar = smem_addr(&ws.bar[0]);  // + 8 * buffer
+  if (a.tma && lane == 0) {
+    win_bar_init(s_bar);
+    win_bar_init(s_bar + 8u);
+    win_bar_fence();
+  }
+  uint32_t bphase = 0;  // parity of each buffer's next completion (bit = buffer)
   __syncthreads();
   const bool abort_all = a.status->decode_err != kNoErr;
   const uint32_t FULL = 0xffffffffu;
@@ -181,13 +191,25 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
     for (uint32_t r = 0; r < R; ++r) tb.cnt[r * 32 + lane] = 0;
 
-    win.begin(a.body + b * 32 * a.stride, start, n);
+    // one TMA box per window when every stream of the batch starts at slot 0
+    const bool tmab = a.tma && __all_sync(FULL, start == 0u);
+    const uint32_t s_buf = smem_addr(ws.rec[0]);
+    auto issue = [&](uint32_t bs, uint32_t c0) {
+      if (tmab) {
+        if (lane == 0)
+          win_tma(s_buf + bs * (32u * kTpsPitch), &tm, s_bar + 8u * bs, (int)(4u + 2u * c0),
+                  (int)(b * 32), 32u * kTpsPitch);
+      } else {
+        win.issue(bs, c0);
+      }
+    };
+    if (!tmab) win.begin(a.body + b * 32 * a.stride, start, n);
 
     uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
     if (n > 0) r0 = slots[start];
     if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
     uint32_t inf0 = cs.info[(r0.x >> 12) & (kTpsRegions - 1u)];
-    win.issue(0, 2);
+    issue(0, 2);
     cp_async_commit();
 
     // stack top as a shared address: row sp-1 of the lane's column; the
@@ -309,9 +331,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1) k_tps(FastArgs a) {
     const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
     for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
       const uint32_t bsel = (w0 / kTpsW) & 1u;
-      if (w0 + kTpsW < nmax) win.issue(bsel ^ 1u, w0 + kTpsW + 2u);
-      cp_async_commit();
-      cp_async_wait1();
+      if (w0 + kTpsW < nmax) issue(bsel ^ 1u, w0 + kTpsW + 2u);
+      if (tmab) {
+        win_wait(s_bar + 8u * bsel, (bphase >> bsel) & 1u);
+        bphase ^= 1u << bsel;
+      } else {
+        cp_async_commit();
+        cp_async_wait1();
+      }
       __syncwarp();
       const uint2* myrec = win.lane_records(bsel, lane, start);
       if (w0 + kTpsW + 2u <= nmin) {

@@ -13,6 +13,8 @@
 // (start & 1) in its window.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "wgpf_dev.cuh"
 
 namespace wgpf {
@@ -104,5 +106,42 @@ struct RecWindowsT {
   }
 };
 using RecWindows = RecWindowsT<kTpsW>;
+
+// ---- TMA windows ---------------------------------------------------------------
+// When all 32 streams of a batch start at slot 0 (flush plans, and circular
+// streams that never wrapped), the window of positions [c0, c0 + kW + 2) of
+// the 32 streams is one 2-D box of the body -- 32 rows (streams) x kPitch
+// bytes at byte 16 + 8 c0 -- in exactly the per-lane layout above: one TMA
+// load by one lane instead of kChunks cp.async per lane.  The host encodes
+// the body as a u32 tensor {stride / 4, n_streams}, box {kPitch / 4, 32};
+// bytes past a row's end are zero-filled (positions >= n, never used).
+__device__ __forceinline__ void win_bar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void win_bar_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// (one lane) expect `bytes` on bar and start the box load at (x, y)
+__device__ __forceinline__ void win_tma(uint32_t dst, const CUtensorMap* m, uint32_t bar,
+                                        int x, int y, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void win_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WIN_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WIN_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
 }  // namespace wgpf

@@ -54,6 +54,7 @@ struct CountArgs {
   unsigned long long* warp_len;
   unsigned long long* deep_list;  // SF_WARP | SF_DEEP streams
   unsigned long long* deep_len;
+  uint32_t tma;          // k_count_tps: the body's tensor map is valid
 };
 
 __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
@@ -206,9 +207,12 @@ constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
 constexpr int kCountUnroll = WGPF_COUNT_UNROLL;
 using CountWin = RecWindowsT<kCountW>;
 
-__global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
+// tm: the body as a TMA tensor with box {CountWin::kTpsPitch / 4, 32}
+__global__ void __launch_bounds__(kCountWarps * 32)
+    k_count_tps(CountArgs a, const __grid_constant__ CUtensorMap tm) {
   __shared__ uint8_t marker_region[256];
-  __shared__ __align__(16) uint8_t recbuf[kCountWarps][2 * 32 * CountWin::kTpsPitch];
+  __shared__ __align__(128) uint8_t recbuf[kCountWarps][2 * 32 * CountWin::kTpsPitch];
+  __shared__ __align__(8) unsigned long long wbar[kCountWarps][2];
   for (uint32_t r = threadIdx.x; r < 256; r += blockDim.x)
     marker_region[r] =
         r < a.fast_regions ? class_is_marker(a.plan, a.plan.class_of[r]) : 0;
@@ -221,6 +225,15 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
   const uint32_t cap = (uint32_t)a.plan.slots;
   CountWin win;
   win.init(recbuf[w], lane, a.stride, cap);
+  const uint32_t s_bar = smem_addr(&wbar[w][0]);  // + 8 * buffer
+  const uint32_t s_buf = smem_addr(recbuf[w]);
+  if (a.tma && lane == 0) {
+    win_bar_init(s_bar);
+    win_bar_init(s_bar + 8u);
+    win_bar_fence();
+  }
+  __syncwarp();
+  uint32_t bphase = 0;
   const uint64_t wstep = (uint64_t)gridDim.x * kCountWarps;
   for (uint64_t b = (uint64_t)blockIdx.x * kCountWarps + w; b * 32 < a.n_streams;
        b += wstep) {
@@ -256,12 +269,22 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
       }
       continue;
     }
-    win.begin(a.body + b * 32 * a.stride, start, n);
+    const bool tmab = a.tma && __all_sync(FULL, start == 0u);
+    auto issue = [&](uint32_t bs, uint32_t c0) {
+      if (tmab) {
+        if (lane == 0)
+          win_tma(s_buf + bs * (32u * CountWin::kTpsPitch), &tm, s_bar + 8u * bs,
+                  (int)(4u + 2u * c0), (int)(b * 32), 32u * CountWin::kTpsPitch);
+      } else {
+        win.issue(bs, c0);
+      }
+    };
+    if (!tmab) win.begin(a.body + b * 32 * a.stride, start, n);
     const uint2* slots = reinterpret_cast<const uint2*>(a.body + (act ? s : 0) * a.stride + 16);
     uint32_t t0 = 0, t1 = 0;  // tags of records i, i+1
     if (n > 0) t0 = slots[start].x;
     if (n > 1) t1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap].x;
-    win.issue(0, 2);
+    issue(0, 2);
     cp_async_commit();
     int32_t q = 0, run_min = 0, max_d = 0, z = -1, last_bad = -1;
     uint32_t maxrid = 0;  // region-id range: fast / thread-per-stream routing
@@ -296,9 +319,14 @@ __global__ void __launch_bounds__(kCountWarps * 32) k_count_tps(CountArgs a) {
     const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
     for (uint32_t w0 = 0; w0 < nmax; w0 += kCountW) {
       const uint32_t bsel = (w0 / kCountW) & 1u;
-      if (w0 + kCountW < nmax) win.issue(bsel ^ 1u, w0 + kCountW + 2u);
-      cp_async_commit();
-      cp_async_wait1();
+      if (w0 + kCountW < nmax) issue(bsel ^ 1u, w0 + kCountW + 2u);
+      if (tmab) {
+        win_wait(s_bar + 8u * bsel, (bphase >> bsel) & 1u);
+        bphase ^= 1u << bsel;
+      } else {
+        cp_async_commit();
+        cp_async_wait1();
+      }
       __syncwarp();
       const uint2* rec = win.lane_records(bsel, lane, start);
       if (w0 + kCountW + 1u <= nmin) {

@@ -561,3 +561,48 @@ def test_chrome_trace_long_label_falls_back_to_host_writer(ctx, reference):
     d = torch.from_numpy(ev.view(np.uint8).copy()).cuda()
     assert ctx.export_chrome_trace(None, 1965.0, on_device_ptr=d.data_ptr(),
                                    n_events=len(ev)) == want
+
+
+# ---------------------------------------------------------------------------
+# record windows: TMA boxes (every stream of a warp's batch starts at slot 0)
+# and cp.async chunks (wrapped circular streams, or WGPF_NO_TMA=1), with batch
+# counts that are not multiples of 32 (the last box's rows past the body are
+# zero-filled)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("no_tma", [False, True])
+def test_record_windows_tma_and_cp_async(oracle, monkeypatch, no_tma):
+    t = T()
+    if no_tma:
+        monkeypatch.setenv("WGPF_NO_TMA", "1")
+    else:
+        monkeypatch.delenv("WGPF_NO_TMA", raising=False)
+    c = t.Context(0)  # (the switch is read when the context is created)
+    for seed in range(16):
+        n_streams = [32, 33, 95, 257][seed % 4]
+        data, cap, strategy, labels = fuzz.random_image(
+            7000 + seed, n_streams=n_streams, cap=64 if seed % 2 else 32,
+            mode="nested", big_gaps=(seed % 5 == 0))
+        try:
+            o, oerr = oracle.replay_kpft(data, cap, strategy, labels, 33), None
+        except O.OracleError as e:
+            o, oerr = None, (e.category, str(e))
+        try:
+            r = c.replay_image_bytes(data, plan_of(cap, strategy, labels), 33, flags=0x2)
+            gerr = None
+        except t.Error as e:
+            r, gerr = None, (e.category(), str(e))
+        assert oerr == gerr, (seed, oerr, gerr)
+        if oerr:
+            continue
+        assert np.array_equal(r.events, o.events), seed
+        assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+                r.malformed_groups) == (o.dropped_heads, o.truncated_tails,
+                                        o.flagged_preconditions, o.malformed_groups)
+        want = oracle.region_stats(o.events, labels)
+        got = c.stats()
+        for s in want:
+            g = got[s.label]
+            assert (g.count, g.min, g.max, g.sum, g.mean, g.first_event,
+                    g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
+                                s.first_event, s.hist), (seed, s.label)

@@ -92,7 +92,7 @@ __host__ __device__ inline TpsTables tps_tables(uint8_t* p, uint32_t K, uint32_t
   return t;
 }
 __host__ __device__ inline size_t tps_hist_bytes(uint32_t K) {
-  return tps_align((size_t)K * WGPF_HIST_BINS * 4);
+  return tps_align((size_t)K * WGPF_HIST_BINS * 4 + 4);  // + a spare word
 }
 __host__ inline size_t tps_smem_bytes(uint32_t K, uint32_t R, uint32_t warps) {
   return tps_align(sizeof(TpsCtaSmem)) + tps_hist_bytes(K) +
@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
   // shared window base at every use)
   const uint32_t s_info = opaque_u32(smem_addr(cs.info));
   const uint32_t s_hist = opaque_u32(smem_addr(hist));
+  const uint32_t s_hist_spare = opaque_u32(smem_addr(hist + K * WGPF_HIST_BINS));
   const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);    // + 256 * level
   const uint32_t s_cnt = smem_addr(tb.cnt + lane);        // + 64 * region
   const uint32_t s_a = smem_addr(tb.a + lane);            // + 512 * class
@@ -250,7 +251,9 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       x.y = max(x.y, d);
       add64_u32(x.z, x.w, d);
       sts128_if(p, ea, x);
-      red_add_if(p, s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)), 1u);
+      // (unpredicated: lanes without an event count into a spare word past
+      // the table -- no branch around the shared atomic)
+      red_add(p ? s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)) : s_hist_spare, 1u);
     };
     // kFull: positions i .. i+2 exist on every lane (the bulk of the walk):
     // no per-record bounds predicates

@@ -303,6 +303,10 @@ __device__ __forceinline__ void red_add_if(bool p, uint32_t a, uint32_t v) {
                : "memory");
 }
 
+__device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 // ---- warp helpers --------------------------------------------------------------
 __device__ inline uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ inline uint32_t lanemask_lt() {

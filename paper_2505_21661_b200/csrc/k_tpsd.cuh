@@ -28,10 +28,12 @@ namespace wgpf {
 constexpr uint32_t kDeepDepth = 64;
 constexpr uint32_t kDeepRegions = 64;
 constexpr uint32_t kDeepWarps = 8;
+// stack entry: the START's region id where the record tag has it (bits 12..17)
+constexpr uint32_t kDeepStkRid = (kDeepRegions - 1u) << 12;
 
 struct DeepWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];        // record windows
-  uint2 stk[kDeepDepth][32];             // {lo, pos | rid<<11 | cons<<17 | hi<<18}
+  uint2 stk[kDeepDepth][32];             // {lo, pos | rid<<12 | cons<<18 | hi<<19}
   wgpf_event orph[32];                   // one orphan per lane
   uint16_t cnt[kDeepRegions][32];        // iteration counters
 };
@@ -40,6 +42,7 @@ struct DeepCtaSmem {
   SmemStats st;
   uint32_t info[kDeepRegions];  // class | marker<<8 | wait class<<16
   unsigned long long warn[4];
+  uint32_t hist_spare;          // histogram increments of lanes without an event
 };
 
 __host__ inline size_t deep_smem_bytes(uint32_t warps) {
@@ -87,6 +90,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
   const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);  // + 64 * region
   const uint32_t s_orph = smem_addr(&ws.orph[lane]);
   const uint32_t s_rec = smem_addr(ws.rec[0]);
+  const uint32_t s_spare = opaque_u32(smem_addr(&cs.hist_spare));
   const uint64_t n_list = *a.list_len;
 
   // one event per participating lane into the CTA statistics
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
         atomicMax(&cs.st.max[c0], mx);
         smin64(&cs.st.first[c0], ((unsigned long long)khi << 32) | klo);
       }
-      if (p) atomicAdd(&cs.st.hist[c0 * WGPF_HIST_BINS + hist_bin32(d)], 1u);
+      red_add(p ? smem_addr(&cs.st.hist[c0 * WGPF_HIST_BINS + hist_bin32(d)]) : s_spare, 1u);
     } else if (p) {
       stats_add_one(cs.st, a.stats, cls, d, key, &a.status->synth_overflow);
     }
@@ -188,10 +192,9 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     const uint64_t ev0 = opaque_u64(reinterpret_cast<uint64_t>(a.events + (act ? off : 0ull)));
     auto put = [&](bool p, uint32_t k, uint32_t slo, uint32_t shi, uint32_t elo,
                    uint32_t ehi, uint32_t region, uint32_t it) {
-      const bool ok = p & (k < lim);
-      stg256_if(ok, ev0 + 32ull * k, make_uint4(slo, shi, elo, ehi),
+      // (events past lim are counted once at the stream end: kw - lim)
+      stg256_if(p & (k < lim), ev0 + 32ull * k, make_uint4(slo, shi, elo, ehi),
                 make_uint4(region, it, blk, wg));
-      w_ovf += (p && !ok) ? 1u : 0u;
     };
     auto step = [&](auto full, uint32_t i, uint2 r2) {
       constexpr bool kFull = decltype(full)::value;
@@ -211,13 +214,13 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       const bool mend = en && nonempty;
       w_drop += (en && !nonempty) ? 1u : 0u;
       sts64_if(st, stop + 256u,
-               make_uint2(v, i | (rid << 11) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 17) |
-                                 (hi << 18)));
+               make_uint2(v, i | (tag & kDeepStkRid) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 18) |
+                                 (hi << 19)));
       stop = stop + (st ? 256u : 0u) - (mend ? 256u : 0u);
-      const uint32_t shi = e.y >> 18;
+      const uint32_t shi = e.y >> 19;
       const uint32_t meas = v - e.x;
       const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
-      const bool mism = mend && ((e.y >> 11) & 63u) != rid;
+      const bool mism = mend && ((e.y ^ tag) & kDeepStkRid) != 0u;
       const bool tlong = mend && !mism && dhi;
       broken |= mism || tlong;
       const bool ok = mend && !mism && !tlong;
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       sts16_if(ok, ca, it + 1u);
       const bool is_mk = (inf & 0x100u) != 0u;
       const bool base = ok && !is_mk;
-      const bool orphan = ok && is_mk && !((e.y >> 17) & 1u);
+      const bool orphan = ok && is_mk && !((e.y >> 18) & 1u);
       const uint32_t dpos = i - (e.y & 2047u);
       const uint32_t ovh = cost * dpos;
       const uint32_t corr = ovh > meas ? 0u : meas - ovh;
@@ -293,6 +296,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
               (uint32_t)(o.end - o.start), gkey | (kw << 1));
       kw += po ? 1u : 0u;
     }
+    w_ovf += act && kw > lim ? kw - lim : 0u;
     if (act) {
       if (bad || kw != want) {
         atomicAdd(&a.status->invalid, 1ull);

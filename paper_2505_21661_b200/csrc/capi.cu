@@ -126,6 +126,7 @@ struct wgpf_ctx {
   bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
   bool no_deep = getenv("WGPF_NO_DEEP") != nullptr;  // deep streams -> warp kernel
   bool no_tma = getenv("WGPF_NO_TMA") != nullptr;    // k_tps windows by cp.async only
+  bool no_group = getenv("WGPF_NO_GROUP") != nullptr;  // k_tps: consecutive streams per warp
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   size_t smem_optin = 0;
@@ -620,8 +621,7 @@ static CUtensorMapL2promotion l2_promotion() {
          : v == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                     : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 }
-static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride,
-                            uint64_t n_streams, uint32_t pitch) {
+static EncodeTiledFn encode_tiled() {
   static EncodeTiledFn fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -631,6 +631,11 @@ static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride
                ? reinterpret_cast<EncodeTiledFn>(p)
                : nullptr;
   }();
+  return fn;
+}
+static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride,
+                            uint64_t n_streams, uint32_t pitch) {
+  EncodeTiledFn fn = encode_tiled();
   if (!fn || (reinterpret_cast<uintptr_t>(body) & 15u) || (stride & 15u) ||
       stride < pitch || stride >= (1ull << 39) || n_streams < 32 ||
       n_streams >= (1ull << 31))
@@ -640,6 +645,45 @@ static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride
   const cuuint32_t box[2] = {pitch / 4, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(body), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Streams per block W of a device body (k_tps's lane mapping): the length of
+// the leading run of streams whose header has stream 0's block, if it
+// divides the stream count; else 1.  Reads the block field of up to 1,025
+// headers (one small strided copy).
+static uint32_t stream_group(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                             uint64_t n_streams) {
+  if (c->no_group || n_streams < 64) return 1;
+  const uint64_t m = std::min<uint64_t>(n_streams, 1025);
+  std::vector<uint32_t> blk(m);
+  if (cudaMemcpy2DAsync(blk.data(), 4, body, stride, 4, m, cudaMemcpyDeviceToHost,
+                        c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  for (uint64_t i = 1; i < m; ++i)
+    if (blk[i] != blk[0]) return n_streams % i == 0 ? (uint32_t)i : 1u;
+  return 1;
+}
+
+// 3-D view {stride / 4, W, n_streams / W} with box {kTpsPitch / 4, 1, 32}
+// for the grouped lane mapping (k_window.cuh win_tma3)
+static bool body_tensor_map3(CUtensorMap* m, const uint8_t* body, uint64_t stride,
+                             uint64_t n_streams, uint32_t W) {
+  EncodeTiledFn fn = encode_tiled();
+  const uint64_t nb = n_streams / W;
+  if (!fn || (reinterpret_cast<uintptr_t>(body) & 15u) || (stride & 15u) ||
+      stride < kTpsPitch || stride * W >= (1ull << 39) || nb >= (1ull << 31) || W > 256 ||
+      n_streams % W)
+    return false;
+  const cuuint64_t dims[3] = {stride / 4, W, nb};
+  const cuuint64_t strides[2] = {stride, stride * W};
+  const cuuint32_t box[3] = {kTpsPitch / 4, 1, 32};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint8_t*>(body), dims, strides,
             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -681,6 +725,7 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.list_len = nullptr;
   f.tps_regions = tps_regions(c);
   f.tma = 0;
+  f.group = 1;
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
   if ((tps_enabled(c) || deep_enabled(c)) && record_cost < (1ull << 21)) {
@@ -690,9 +735,11 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
       CUtensorMap tm;
       memset(&tm, 0, sizeof(tm));
-      f.tma = !c->no_tma && body_tensor_map(&tm, body, stride, n_streams, kTpsPitch) ? 1u : 0u;
+      f.group = stream_group(c, body, stride, n_streams);
+      f.tma = !c->no_tma && body_tensor_map3(&tm, body, stride, n_streams, f.group) ? 1u : 0u;
       tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f, tm);
       f.tma = 0;
+      f.group = 1;
       CUDA_OK(c, cudaGetLastError());
       ++c->launches;
     }

@@ -153,8 +153,18 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
   const uint32_t cap = a.cap;
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0, w_ovf = 0;
 
+  // Lane mapping.  The streams of one block are its warps' (or warp
+  // groups'), W of them, in image order; warps of the traced kernel with the
+  // same index run the same program, so a batch takes one warp index w of 32
+  // consecutive blocks: lane l <- stream (32 j + l) W + w.  The lanes then
+  // walk identical record-type sequences and the walk's branches are warp-
+  // uniform.  (Any mapping gives the same results: events go to pass 1's
+  // offsets, and a lane still meets its streams in increasing order.)
+  const uint32_t W = a.group;
+  const uint64_t n_blocks = a.n_streams / W;  // (host: W divides n_streams)
+  const uint64_t n_batches = W * ((n_blocks + 31) / 32);
   RecWindows win;
-  win.init(ws.rec[0], lane, a.stride, cap);
+  win.init(ws.rec[0], lane, a.stride * W, cap);  // lanes W streams apart
   // 32-bit shared addresses of the hot tables (this lane's column)
   // (opaque: kept in registers instead of being rebuilt from the CTA's
   // shared window base at every use)
@@ -167,10 +177,12 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
   const uint32_t s_orph = smem_addr(&ws.orph[lane]);
 
   const uint64_t wstep = (uint64_t)gridDim.x * nw;
-  for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b * 32 < a.n_streams;
-       b += wstep) {
-    const uint64_t s = b * 32 + lane;
-    const uint32_t flag = s < a.n_streams ? a.sflag[s] : SF_DECODE_ERR;
+  for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b < n_batches; b += wstep) {
+    const uint64_t jb = b / W;                 // batch of 32 blocks
+    const uint32_t wi = (uint32_t)(b - jb * W);  // warp index within them
+    const uint64_t s0 = jb * 32 * W + wi;      // lane 0's stream
+    const uint64_t s = s0 + (uint64_t)lane * W;
+    const uint32_t flag = jb * 32 + lane < n_blocks ? a.sflag[s] : SF_DECODE_ERR;
     if (flag & SF_GENERAL) {
       const unsigned long long k = atomicAdd(a.general_len, 1ull);
       a.general_list[k] = s;
@@ -198,13 +210,13 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     auto issue = [&](uint32_t bs, uint32_t c0) {
       if (tmab) {
         if (lane == 0)
-          win_tma(s_buf + bs * (32u * kTpsPitch), &tm, s_bar + 8u * bs, (int)(4u + 2u * c0),
-                  (int)(b * 32), 32u * kTpsPitch);
+          win_tma3(s_buf + bs * (32u * kTpsPitch), &tm, s_bar + 8u * bs, (int)(4u + 2u * c0),
+                   (int)wi, (int)(jb * 32), 32u * kTpsPitch);
       } else {
         win.issue(bs, c0);
       }
     };
-    if (!tmab) win.begin(a.body + b * 32 * a.stride, start, n);
+    if (!tmab) win.begin(a.body + s0 * a.stride, start, n);
 
     uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
     if (n > 0) r0 = slots[start];
@@ -268,6 +280,23 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       const uint32_t inf = inf0;
       const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
       const uint32_t i1 = lds32(s_info + 4u * r1id);
+      if constexpr (kFull) {
+        // every lane at a START (grouped lanes run the same program): a push
+        // is all that happens -- no event, no statistics, no wait marker
+        if (__all_sync(FULL, isS)) {
+          hi += v < vprev ? 1u : 0u;
+          vprev = v;
+          sts64_if(true, stop + 256u,
+                   make_uint2(v, i | (tag & kStkRid) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 17) |
+                                     (hi << 18)));
+          stop += 256u;
+          pw = 0xFFu;
+          inf0 = i1;
+          r0 = r1;
+          r1 = r2;
+          return;
+        }
+      }
       hi += (valid && v < vprev) ? 1u : 0u;
       vprev = valid ? v : vprev;
       // ---- stack ------------------------------------------------------------

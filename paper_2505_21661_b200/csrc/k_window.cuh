@@ -132,6 +132,18 @@ __device__ __forceinline__ void win_tma(uint32_t dst, const CUtensorMap* m, uint
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y)
       : "memory");
 }
+// 3-D form: the body as {stride / 4, W, n_blocks} (streams of a block
+// innermost), box {kPitch / 4, 1, 32}: one warp index of 32 blocks
+__device__ __forceinline__ void win_tma3(uint32_t dst, const CUtensorMap* m, uint32_t bar,
+                                         int x, int y, int z, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 __device__ __forceinline__ void win_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"

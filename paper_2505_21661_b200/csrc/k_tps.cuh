@@ -47,6 +47,7 @@ namespace wgpf {
 #define WGPF_TPS_UNROLL 4
 #endif
 constexpr int kTpsUnroll = WGPF_TPS_UNROLL;  // full steps unrolled per window
+constexpr int kTpsPairUnroll = kTpsUnroll / 2;  // (record pairs)
 constexpr uint32_t kTpsMaxWarps = 16;                 // warps per CTA (<=)
 constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     };
 
     const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
+    const bool even_start = __all_sync(FULL, (start & 1u) == 0u);
     for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
       const uint32_t bsel = (w0 / kTpsW) & 1u;
       if (w0 + kTpsW < nmax) issue(bsel ^ 1u, w0 + kTpsW + 2u);
@@ -374,9 +376,21 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       __syncwarp();
       const uint2* myrec = win.lane_records(bsel, lane, start);
       if (w0 + kTpsW + 2u <= nmin) {
-#pragma unroll kTpsUnroll
-        for (uint32_t j = 0; j < kTpsW; ++j)
-          step(std::true_type{}, w0 + j, myrec[j]);
+        if (even_start) {
+          // records in 16-B pairs: one conflict-free LDS.128 per two steps
+          // (8-B loads at the 80-B lane pitch hit 4-way bank conflicts)
+          const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
+#pragma unroll kTpsPairUnroll
+          for (uint32_t j = 0; j < kTpsW; j += 2) {
+            const uint4 q = myrec2[j / 2];
+            step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
+            step(std::true_type{}, w0 + j + 1, make_uint2(q.z, q.w));
+          }
+        } else {
+#pragma unroll 1
+          for (uint32_t j = 0; j < kTpsW; ++j)
+            step(std::true_type{}, w0 + j, myrec[j]);
+        }
       } else {
 #pragma unroll 1
         for (uint32_t j = 0; j < kTpsW; ++j)

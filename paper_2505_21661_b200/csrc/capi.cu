@@ -726,6 +726,7 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.tps_regions = tps_regions(c);
   f.tma = 0;
   f.group = 1;
+  f.batch_ctr = nullptr;
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
   if ((tps_enabled(c) || deep_enabled(c)) && record_cost < (1ull << 21)) {
@@ -736,6 +737,8 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       CUtensorMap tm;
       memset(&tm, 0, sizeof(tm));
       f.group = stream_group(c, body, stride, n_streams);
+      f.batch_ctr = c->d_glen.as<unsigned long long>() + 4;
+      CUDA_OK(c, cudaMemsetAsync(f.batch_ctr, 0, 8, c->stream));
       f.tma = !c->no_tma && body_tensor_map3(&tm, body, stride, n_streams, f.group) ? 1u : 0u;
       tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f, tm);
       f.tma = 0;

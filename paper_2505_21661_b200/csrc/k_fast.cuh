@@ -58,6 +58,7 @@ struct FastArgs {
   const unsigned long long* list_len;
   uint32_t tps_regions;  // k_tps: region ids in its tables
   uint32_t tma;          // k_tps: the tensor map of the body is valid
+  unsigned long long* batch_ctr;  // k_tps: dynamic batch counter (zeroed)
   uint32_t group;        // k_tps: streams per block W (lane l of batch (j, w)
                          // takes stream (32 j + l) W + w; 1 = consecutive)
 };

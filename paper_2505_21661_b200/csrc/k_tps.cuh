@@ -178,7 +178,14 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
   const uint32_t s_orph = smem_addr(&ws.orph[lane]);
 
   const uint64_t wstep = (uint64_t)gridDim.x * nw;
-  for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b < n_batches; b += wstep) {
+  // Batches: the first gridDim.x * nw statically, then dynamically from a
+  // global counter (the next index is fetched at the top of each batch, so
+  // the atomic's latency hides behind the walk): warps finish together
+  // whatever the per-batch work (producer / consumer warp indices differ).
+  unsigned long long nxt = 0;
+  for (uint64_t b = (uint64_t)blockIdx.x * nw + w; !abort_all && b < n_batches;
+       b = wstep + __shfl_sync(FULL, nxt, 0)) {
+    if (lane == 0) nxt = atomicAdd(a.batch_ctr, 1ull);
     const uint64_t jb = b / W;                 // batch of 32 blocks
     const uint32_t wi = (uint32_t)(b - jb * W);  // warp index within them
     const uint64_t s0 = jb * 32 * W + wi;      // lane 0's stream

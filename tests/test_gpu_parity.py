@@ -567,7 +567,7 @@ def test_chrome_trace_long_label_falls_back_to_host_writer(ctx, reference):
 # record windows: TMA boxes (every stream of a warp's batch starts at slot 0)
 # and cp.async chunks (wrapped circular streams, or WGPF_NO_TMA=1), with batch
 # counts that are not multiples of 32 (the last box's rows past the body are
-# zero-filled)
+# zero-filled); consecutive and grouped (W streams per block) lane mappings
 # ---------------------------------------------------------------------------
 
 @pytest.mark.parametrize("no_tma", [False, True])
@@ -578,8 +578,10 @@ def test_record_windows_tma_and_cp_async(oracle, monkeypatch, no_tma):
     else:
         monkeypatch.delenv("WGPF_NO_TMA", raising=False)
     c = t.Context(0)  # (the switch is read when the context is created)
-    for seed in range(16):
-        n_streams = [32, 33, 95, 257][seed % 4]
+    for seed in range(24):
+        # (fuzz images have 4 streams per block: 100 and 256 streams take the
+        # grouped lane mapping, 25 and 64 blocks -- a ragged last batch)
+        n_streams = [32, 33, 95, 257, 100, 256][seed % 6]
         data, cap, strategy, labels = fuzz.random_image(
             7000 + seed, n_streams=n_streams, cap=64 if seed % 2 else 32,
             mode="nested", big_gaps=(seed % 5 == 0))

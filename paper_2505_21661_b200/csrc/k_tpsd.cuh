@@ -207,6 +207,23 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       const uint32_t inf = inf0;
       const uint32_t r1id = (r1.x >> 12) & (kDeepRegions - 1u);
       const uint32_t i1 = lds32(s_info + 4u * r1id);
+      if constexpr (kFull) {
+        // every lane at a START (the streams of a trace run the same program
+        // from the same wrap position): a push is all that happens
+        if (__all_sync(FULL, isS)) {
+          hi += v < vprev ? 1u : 0u;
+          vprev = v;
+          sts64_if(true, stop + 256u,
+                   make_uint2(v, i | (tag & kDeepStkRid) |
+                                     ((pw == (inf & 0xFFu) ? 1u : 0u) << 18) | (hi << 19)));
+          stop += 256u;
+          pw = 0xFFu;
+          inf0 = i1;
+          r0 = r1;
+          r1 = r2;
+          return;
+        }
+      }
       hi += (valid && v < vprev) ? 1u : 0u;
       vprev = valid ? v : vprev;
       const uint2 e = lds64(stop);

@@ -164,8 +164,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
   const uint32_t W = a.group;
   const uint64_t n_blocks = a.n_streams / W;  // (host: W divides n_streams)
   const uint64_t n_batches = W * ((n_blocks + 31) / 32);
-  RecWindows win;
-  win.init(ws.rec[0], lane, a.stride * W, cap);  // lanes W streams apart
+
   // 32-bit shared addresses of the hot tables (this lane's column)
   // (opaque: kept in registers instead of being rebuilt from the CTA's
   // shared window base at every use)
@@ -215,6 +214,13 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     // one TMA box per window when every stream of the batch starts at slot 0
     const bool tmab = a.tma && __all_sync(FULL, start == 0u);
     const uint32_t s_buf = smem_addr(ws.rec[0]);
+    // cp.async window state only for batches that need it (its ~35
+    // registers are dead in the TMA walk)
+    RecWindows win;
+    if (!tmab) {
+      win.init(ws.rec[0], lane, a.stride * W, cap);  // lanes W streams apart
+      win.begin(a.body + s0 * a.stride, start, n);
+    }
     auto issue = [&](uint32_t bs, uint32_t c0) {
       if (tmab) {
         if (lane == 0)
@@ -224,7 +230,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
         win.issue(bs, c0);
       }
     };
-    if (!tmab) win.begin(a.body + s0 * a.stride, start, n);
 
     uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
     if (n > 0) r0 = slots[start];
@@ -370,41 +375,58 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
 
     const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
     const bool even_start = __all_sync(FULL, (start & 1u) == 0u);
-    for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
-      const uint32_t bsel = (w0 / kTpsW) & 1u;
-      if (w0 + kTpsW < nmax) issue(bsel ^ 1u, w0 + kTpsW + 2u);
-      if (tmab) {
-        win_wait(s_bar + 8u * bsel, (bphase >> bsel) & 1u);
-        bphase ^= 1u << bsel;
-      } else {
-        cp_async_commit();
-        cp_async_wait1();
-      }
-      __syncwarp();
-      const uint2* myrec = win.lane_records(bsel, lane, start);
-      if (w0 + kTpsW + 2u <= nmin) {
-        if (even_start) {
-          // records in 16-B pairs: one conflict-free LDS.128 per two steps
-          // (8-B loads at the 80-B lane pitch hit 4-way bank conflicts)
-          const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
+    // the window loop, specialised for TMA batches (the bulk: unrolled steps)
+    // and cp.async batches (wrapped circular streams: steps not unrolled)
+    auto walk = [&](auto tma_tag) {
+      constexpr bool kTma = decltype(tma_tag)::value;
+      for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
+        const uint32_t bsel = (w0 / kTpsW) & 1u;
+        if (w0 + kTpsW < nmax) issue(bsel ^ 1u, w0 + kTpsW + 2u);
+        if constexpr (kTma) {
+          win_wait(s_bar + 8u * bsel, (bphase >> bsel) & 1u);
+          bphase ^= 1u << bsel;
+        } else {
+          cp_async_commit();
+          cp_async_wait1();
+        }
+        __syncwarp();
+        const uint2* myrec =
+            kTma ? reinterpret_cast<const uint2*>(ws.rec[bsel] + lane * kTpsPitch)
+                 : win.lane_records(bsel, lane, start);
+        // records in 16-B pairs when starts are even: one conflict-free
+        // LDS.128 per two steps (8-B loads at the 80-B lane pitch hit 4-way
+        // bank conflicts)
+        const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
+        if (w0 + kTpsW + 2u <= nmin) {
+          if constexpr (kTma) {
 #pragma unroll kTpsPairUnroll
-          for (uint32_t j = 0; j < kTpsW; j += 2) {
-            const uint4 q = myrec2[j / 2];
-            step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
-            step(std::true_type{}, w0 + j + 1, make_uint2(q.z, q.w));
+            for (uint32_t j = 0; j < kTpsW; j += 2) {
+              const uint4 q = myrec2[j / 2];
+              step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
+              step(std::true_type{}, w0 + j + 1, make_uint2(q.z, q.w));
+            }
+          } else if (even_start) {
+#pragma unroll 1
+            for (uint32_t j = 0; j < kTpsW; j += 2) {
+              const uint4 q = myrec2[j / 2];
+              step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
+              step(std::true_type{}, w0 + j + 1, make_uint2(q.z, q.w));
+            }
+          } else {
+#pragma unroll 1
+            for (uint32_t j = 0; j < kTpsW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
           }
         } else {
 #pragma unroll 1
-          for (uint32_t j = 0; j < kTpsW; ++j)
-            step(std::true_type{}, w0 + j, myrec[j]);
+          for (uint32_t j = 0; j < kTpsW; ++j) step(std::false_type{}, w0 + j, myrec[j]);
         }
-      } else {
-#pragma unroll 1
-        for (uint32_t j = 0; j < kTpsW; ++j)
-          step(std::false_type{}, w0 + j, myrec[j]);
+        __syncwarp();
       }
-      __syncwarp();
-    }
+    };
+    if (tmab)
+      walk(std::true_type{});
+    else
+      walk(std::false_type{});
     // stream end: the orphan after the base events, final writes, checks
     const bool bad = broken || n_orph > 1;
     const bool po = act && !bad && n_orph == 1;

@@ -127,6 +127,8 @@ struct wgpf_ctx {
   bool no_deep = getenv("WGPF_NO_DEEP") != nullptr;  // deep streams -> warp kernel
   bool no_tma = getenv("WGPF_NO_TMA") != nullptr;    // k_tps windows by cp.async only
   bool no_group = getenv("WGPF_NO_GROUP") != nullptr;  // k_tps: consecutive streams per warp
+  uint32_t group_hint = 0;   // W known from host headers (pipelined replay)
+  uint32_t* h_blk = nullptr;  // pinned: block fields read by stream_group
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   size_t smem_optin = 0;
@@ -147,6 +149,7 @@ struct wgpf_ctx {
 
   ~wgpf_ctx() {
     if (h_status) cudaFreeHost(h_status);
+    if (h_blk) cudaFreeHost(h_blk);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : pev)
@@ -656,9 +659,15 @@ static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride
 static uint32_t stream_group(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                              uint64_t n_streams) {
   if (c->no_group || n_streams < 64) return 1;
+  if (c->group_hint) return n_streams % c->group_hint == 0 ? c->group_hint : 1u;
   const uint64_t m = std::min<uint64_t>(n_streams, 1025);
-  std::vector<uint32_t> blk(m);
-  if (cudaMemcpy2DAsync(blk.data(), 4, body, stride, 4, m, cudaMemcpyDeviceToHost,
+  if (!c->h_blk && cudaMallocHost(&c->h_blk, 4 * 1025) != cudaSuccess) {
+    c->h_blk = nullptr;
+    cudaGetLastError();
+    return 1;
+  }
+  const uint32_t* blk = c->h_blk;
+  if (cudaMemcpy2DAsync(c->h_blk, 4, body, stride, 4, m, cudaMemcpyDeviceToHost,
                         c->stream) != cudaSuccess ||
       cudaStreamSynchronize(c->stream) != cudaSuccess) {
     cudaGetLastError();
@@ -1211,6 +1220,22 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
   c->chunk_sbase.clear();
   c->chunk_ebase.clear();
   c->chunk_mode = false;
+  // streams per block from the host headers (no device read per chunk: a
+  // small D2H would queue behind the event copies)
+  {
+    uint32_t W = 1;
+    const uint64_t m = std::min<uint64_t>(count, 1025);
+    for (uint64_t i = 1; i < m; ++i)
+      if (rd32(kpft + off + i * stride) != rd32(kpft + off)) {
+        W = (uint32_t)i;
+        break;
+      }
+    c->group_hint = W;
+  }
+  struct HintReset {
+    wgpf_ctx* c;
+    ~HintReset() { c->group_hint = 0; }
+  } hint_reset{c};
   int rc = h2d(0);
   if (rc) return rc;
   uint64_t total = 0;

@@ -48,7 +48,10 @@ namespace wgpf {
 #endif
 constexpr int kTpsUnroll = WGPF_TPS_UNROLL;  // full steps unrolled per window
 constexpr int kTpsPairUnroll = kTpsUnroll / 2;  // (record pairs)
-constexpr uint32_t kTpsMaxWarps = 16;                 // warps per CTA (<=)
+#ifndef WGPF_TPS_WARPS
+#define WGPF_TPS_WARPS 15  // measured: 15 -> 5.10 ms, 16 -> 5.38 (8 B spills at 128 regs), 14 -> 5.22
+#endif
+constexpr uint32_t kTpsMaxWarps = WGPF_TPS_WARPS;     // warps per CTA (<=)
 constexpr uint32_t kTpsDepth = 8;                     // stack entries per lane
 constexpr uint32_t kTpsRegions = 32;                  // region ids < this
 constexpr uint32_t kTpsClasses = 16;                  // dense classes held

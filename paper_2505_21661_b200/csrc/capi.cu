@@ -659,7 +659,9 @@ static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride
 static uint32_t stream_group(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                              uint64_t n_streams) {
   if (c->no_group || n_streams < 64) return 1;
-  if (c->group_hint) return n_streams % c->group_hint == 0 ? c->group_hint : 1u;
+  if (c->group_hint)
+    return n_streams % c->group_hint == 0 && n_streams / c->group_hint >= 32 ? c->group_hint
+                                                                             : 1u;
   const uint64_t m = std::min<uint64_t>(n_streams, 1025);
   if (!c->h_blk && cudaMallocHost(&c->h_blk, 4 * 1025) != cudaSuccess) {
     c->h_blk = nullptr;
@@ -673,8 +675,9 @@ static uint32_t stream_group(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
     cudaGetLastError();
     return 1;
   }
+  // (fewer than 32 blocks would leave lanes of every batch idle)
   for (uint64_t i = 1; i < m; ++i)
-    if (blk[i] != blk[0]) return n_streams % i == 0 ? (uint32_t)i : 1u;
+    if (blk[i] != blk[0]) return n_streams % i == 0 && n_streams / i >= 32 ? (uint32_t)i : 1u;
   return 1;
 }
 

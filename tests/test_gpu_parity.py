@@ -579,9 +579,10 @@ def test_record_windows_tma_and_cp_async(oracle, monkeypatch, no_tma):
         monkeypatch.delenv("WGPF_NO_TMA", raising=False)
     c = t.Context(0)  # (the switch is read when the context is created)
     for seed in range(24):
-        # (fuzz images have 4 streams per block: 100 and 256 streams take the
-        # grouped lane mapping, 25 and 64 blocks -- a ragged last batch)
-        n_streams = [32, 33, 95, 257, 100, 256][seed % 6]
+        # (fuzz images have 4 streams per block: 160 and 256 streams take the
+        # grouped lane mapping -- 40 blocks (a ragged second row of 32) and 64;
+        # 100 streams = 25 blocks stay consecutive)
+        n_streams = [32, 33, 95, 257, 160, 256, 100][seed % 7]
         data, cap, strategy, labels = fuzz.random_image(
             7000 + seed, n_streams=n_streams, cap=64 if seed % 2 else 32,
             mode="nested", big_gaps=(seed % 5 == 0))

@@ -16,18 +16,22 @@
 //                               replay                             (GPU)
 //   wgprof/pipeline.hpp:58-81   TraceReplay, replay_image          (GPU)
 //   wgprof/pipeline.hpp:105-133 RegionStats, region_stats          (GPU)
+//   wgprof/perfmodel.hpp:22-222 swp_latency, ws_latency, roofline,
+//                               overhead_model, load_stage_table   (host)
 //
 // A program built against the reference's headers switches by including this
 // header instead and linking libwgpf.so.  Do not include it
 // together with the reference headers (same namespace).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -514,6 +518,168 @@ inline std::string export_chrome_trace(const std::vector<TimelineEvent>& events,
   return out;
 }
 
+// ---------------------------------------------------------------------------
+// Analytic models (perfmodel.hpp:22-222).  Tiny graphs and a few integers:
+// host code, fed by the GPU's critical-path result (CriticalPathResult::graph
+// below).  Same arithmetic as the reference (u64 wrap, i64 delta, ceiling
+// divisions), same tie-breaks and error texts.
+// ---------------------------------------------------------------------------
+struct SwpStage {
+  std::string name;
+  std::uint64_t t_load = 0;
+  std::uint64_t t_comp = 0;
+  bool operator==(const SwpStage&) const = default;
+};
+struct SwpInput {
+  std::uint32_t n_warp_groups = 1;
+  std::uint32_t n_pipe_stages = 1;
+  std::uint64_t n_loop = 1;
+  std::vector<SwpStage> stages;
+};
+struct SwpResult {
+  std::int64_t delta = 0;
+  std::uint64_t latency = 0;
+};
+// delta = N_WG N_pipe sum(t_comp) - max(t_load + t_comp): compute bound
+// (sum(t_comp) N_loop) when delta >= 0, else ceil(max N_loop / N_pipe)
+inline SwpResult swp_latency(const SwpInput& in) {
+  if (in.stages.empty() || !in.n_warp_groups || !in.n_pipe_stages || !in.n_loop)
+    throw Error(ErrorKind::Validate, "swp_latency: inputs must be positive");
+  std::uint64_t comp = 0, worst = 0;
+  for (const SwpStage& s : in.stages) {
+    comp += s.t_comp;
+    const std::uint64_t t = s.t_load + s.t_comp;
+    if (t > worst) worst = t;
+  }
+  const std::uint64_t lanes = (std::uint64_t)in.n_warp_groups * in.n_pipe_stages;
+  SwpResult r;
+  r.delta = static_cast<std::int64_t>(lanes * comp - worst);  // (two's complement)
+  r.latency = r.delta >= 0 ? comp * in.n_loop
+                           : (worst * in.n_loop + in.n_pipe_stages - 1) / in.n_pipe_stages;
+  return r;
+}
+
+enum class StageKind { Load, Comp };
+struct WsNode {
+  std::string label;
+  std::uint64_t duration = 0;
+  StageKind kind = StageKind::Comp;
+  bool operator==(const WsNode&) const = default;
+};
+struct WsInput {
+  std::vector<WsNode> nodes;
+  std::vector<std::pair<std::size_t, std::size_t>> edges;  // node indices
+  bool operator==(const WsInput&) const = default;
+};
+struct WsResult {
+  std::vector<std::string> critical_path;
+  std::uint64_t latency = 0;
+};
+// Longest duration-weighted path of the stage DAG (iterative depth-first
+// post-order; a successor still on the DFS stack is a cycle).  A node's
+// successor is the first longest one in edge order, replaced by a later one
+// of equal length with a smaller label; the start is the longest node,
+// smaller label on ties.
+inline WsResult ws_latency(const WsInput& in) {
+  const std::size_t n = in.nodes.size();
+  std::vector<std::vector<std::size_t>> out(n);
+  for (const auto& e : in.edges) {
+    if (e.first >= n || e.second >= n)
+      throw Error(ErrorKind::Validate, "ws_latency: edge index out of range");
+    out[e.first].push_back(e.second);
+  }
+  constexpr std::size_t kNone = ~std::size_t(0);
+  std::vector<std::uint8_t> colour(n, 0);  // 0 new, 1 on stack, 2 done
+  std::vector<std::uint64_t> best(n, 0);
+  std::vector<std::size_t> next(n, kNone);
+  std::vector<std::pair<std::size_t, std::size_t>> stack;
+  for (std::size_t root = 0; root < n; ++root) {
+    if (colour[root]) continue;
+    colour[root] = 1;
+    stack.assign(1, {root, 0});
+    while (!stack.empty()) {
+      auto& [v, k] = stack.back();
+      if (k < out[v].size()) {
+        const std::size_t s = out[v][k++];
+        if (colour[s] == 1)
+          throw Error(ErrorKind::Validate, "ws_latency: stage graph has a cycle");
+        if (colour[s] == 0) {
+          colour[s] = 1;
+          stack.push_back({s, 0});
+        }
+        continue;
+      }
+      const std::uint64_t d = in.nodes[v].duration;
+      std::uint64_t b = d;
+      std::size_t c = kNone;
+      for (std::size_t s : out[v]) {
+        const std::uint64_t cand = d + best[s];
+        if (cand > b || (cand == b && c != kNone && in.nodes[s].label < in.nodes[c].label)) {
+          b = cand;
+          c = s;
+        }
+      }
+      best[v] = b;
+      next[v] = c;
+      colour[v] = 2;
+      stack.pop_back();
+    }
+  }
+  WsResult r;
+  if (!n) return r;
+  std::size_t start = 0;
+  for (std::size_t i = 1; i < n; ++i)
+    if (best[i] > best[start] ||
+        (best[i] == best[start] && in.nodes[i].label < in.nodes[start].label))
+      start = i;
+  r.latency = best[start];
+  for (std::size_t v = start; v != kNone; v = next[v]) r.critical_path.push_back(in.nodes[v].label);
+  return r;
+}
+
+struct RooflineInput {
+  std::uint64_t flops = 0;
+  std::uint64_t throughput = 1;  // operations per cycle
+  std::uint64_t t_read = 0;
+  std::uint64_t bytes = 0;
+  std::uint64_t bandwidth = 1;  // bytes per cycle
+};
+struct RooflineResult {
+  std::uint64_t compute_cycles = 0;
+  std::uint64_t memory_cycles = 0;
+};
+inline RooflineResult roofline(const RooflineInput& in) {
+  if (!in.throughput || !in.bandwidth)
+    throw Error(ErrorKind::Validate, "roofline: rates must be positive");
+  return {(in.flops + in.throughput - 1) / in.throughput,
+          in.t_read + (in.bytes + in.bandwidth - 1) / in.bandwidth};
+}
+struct OverheadInput {
+  std::uint64_t t_vanilla = 0;
+  std::uint64_t n_record = 0;
+  std::uint64_t cycle_record = 0;
+};
+// Eq. 1 of the paper: T = T_vanilla + N_record * cycle_record
+inline std::uint64_t overhead_model(const OverheadInput& in) {
+  return in.t_vanilla + in.n_record * in.cycle_record;
+}
+// "<stage> <t_load> <t_comp>" per line, '#' comments, blank lines skipped
+inline std::vector<SwpStage> load_stage_table(std::istream& is) {
+  std::vector<SwpStage> out;
+  std::string line;
+  for (int no = 1; std::getline(is, line); ++no) {
+    line.erase(std::min(line.find('#'), line.size()));
+    std::istringstream ls(line);
+    SwpStage s;
+    if (!(ls >> s.name)) continue;
+    if (!(ls >> s.t_load >> s.t_comp))
+      throw Error(ErrorKind::Parse, "stage table line " + std::to_string(no) +
+                                        ": expected <stage> <t_load> <t_comp>");
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+
 // analyze_critical_path (perfmodel.hpp:317-501).  The reference takes the
 // lowered DeviceProgram and derives the barrier edges from it
 // (perfmodel.hpp:258-313); this drop-in takes those edges directly (the
@@ -529,6 +695,7 @@ struct CriticalPathResult {
   std::vector<std::string> cycle;
   std::uint64_t period = 0;
   std::map<std::string, std::uint64_t> stage_mean;
+  WsInput graph;  // CriticalPathAnalysis::graph: feeds ws_latency
 };
 inline CriticalPathResult analyze_critical_path(
     const std::vector<TimelineEvent>& events,
@@ -563,6 +730,31 @@ inline CriticalPathResult analyze_critical_path(
     for (std::uint32_t i = 0; i < ns; ++i) r.stage_mean[st[i].label] = st[i].mean;
     for (std::uint32_t i = 0; i < nc; ++i) r.cycle.push_back(st[cyc[i]].label);
     r.period = period;
+    // the stage graph (perfmodel.hpp:470-497): stages in label order, kind
+    // Load when the label says so; edges the unfolded cycle, else every edge
+    // binding in at least half of its target's steady instances
+    std::vector<std::uint32_t> order(ns);
+    for (std::uint32_t i = 0; i < ns; ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+      return std::string(st[a].label) < std::string(st[b].label);
+    });
+    std::vector<std::size_t> pos(ns);
+    for (std::uint32_t k = 0; k < ns; ++k) {
+      pos[order[k]] = k;
+      const std::string l = st[order[k]].label;
+      r.graph.nodes.push_back(
+          {l, st[order[k]].mean, l.find("Load") != std::string::npos ? StageKind::Load
+                                                                      : StageKind::Comp});
+    }
+    if (nc) {
+      for (std::uint32_t i = 0; i + 1 < nc; ++i) r.graph.edges.emplace_back(pos[cyc[i]], pos[cyc[i + 1]]);
+    } else {
+      for (std::uint32_t a = 0; a < ns; ++a)
+        for (std::uint32_t b = 0; b < ns; ++b)
+          if (bind[(std::size_t)a * ns + b] && 2 * bind[(std::size_t)a * ns + b] >= st[b].steady)
+            r.graph.edges.emplace_back(pos[a], pos[b]);
+      std::sort(r.graph.edges.begin(), r.graph.edges.end());
+    }
     return r;
   }
 }

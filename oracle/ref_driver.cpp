@@ -19,6 +19,8 @@
 //   region_stats       pipeline.hpp:114         analyze_critical_path perfmodel.hpp:317
 //   run_pipeline/write_artifacts pipeline.hpp:248,271 (fixture regeneration)
 //   testgen::random_program tests/support.hpp:26 (random replay programs)
+//   swp_latency / ws_latency / roofline / overhead_model / load_stage_table
+//                      perfmodel.hpp:44,97,180,196,202 (text in / text out)
 
 #define wgprof wgprof_ref
 #include "support.hpp"
@@ -37,6 +39,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -711,5 +714,110 @@ int64_t ref_export_chrome(const ref_wgpf_event* ev, uint64_t n,
 }
 
 void ref_free_text(char* p) { std::free(p); }
+
+// Analytic models.  Text protocol (tests/test_models.py):
+//   in : one "swp <nwg> <npipe> <nloop>", "stage <name> <t_load> <t_comp>",
+//        "node <label> <duration>", "edge <a> <b>", "roofline f t r b w",
+//        "overhead v n c" per line; "table" + the rest of the text is a stage
+//        table for load_stage_table.
+//   out: "ok <result...>" or "err <kind> <message>".
+// labels travel %-encoded (they may hold blanks): %XX -> byte
+static std::string pct_dec(const std::string& s) {
+  std::string o;
+  for (size_t i = 0; i < s.size(); ++i) {
+    if (s[i] == '%' && i + 2 < s.size()) {
+      o.push_back(static_cast<char>(std::stoi(s.substr(i + 1, 2), nullptr, 16)));
+      i += 2;
+    } else {
+      o.push_back(s[i]);
+    }
+  }
+  return o;
+}
+static std::string pct_enc(const std::string& s) {
+  static const char* hx = "0123456789ABCDEF";
+  std::string o;
+  for (unsigned char c : s) {
+    if (c <= ' ' || c == '%' || c >= 0x7F) {
+      o.push_back('%');
+      o.push_back(hx[c >> 4]);
+      o.push_back(hx[c & 15]);
+    } else {
+      o.push_back(static_cast<char>(c));
+    }
+  }
+  return o;
+}
+static char* dup_text(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+char* ref_models(const char* text) {
+  std::string in(text);
+  std::ostringstream out;
+  try {
+    if (in.rfind("table\n", 0) == 0) {
+      std::istringstream is(in.substr(6));
+      auto st = R::load_stage_table(is);
+      out << "ok";
+      for (const auto& x : st) out << " " << x.name << " " << x.t_load << " " << x.t_comp;
+      return dup_text(out.str());
+    }
+    std::istringstream is(in);
+    std::string kw;
+    R::SwpInput swp;
+    R::WsInput ws;
+    bool is_swp = false, is_ws = false;
+    while (is >> kw) {
+      if (kw == "swp") {
+        is >> swp.n_warp_groups >> swp.n_pipe_stages >> swp.n_loop;
+        is_swp = true;
+      } else if (kw == "stage") {
+        R::SwpStage st;
+        is >> st.name >> st.t_load >> st.t_comp;
+        swp.stages.push_back(st);
+      } else if (kw == "node") {
+        R::WsNode nd;
+        is >> nd.label >> nd.duration;
+        nd.label = pct_dec(nd.label);
+        ws.nodes.push_back(nd);
+        is_ws = true;
+      } else if (kw == "edge") {
+        std::size_t a, b;
+        is >> a >> b;
+        ws.edges.emplace_back(a, b);
+        is_ws = true;
+      } else if (kw == "wsempty") {
+        is_ws = true;
+      } else if (kw == "roofline") {
+        R::RooflineInput r;
+        is >> r.flops >> r.throughput >> r.t_read >> r.bytes >> r.bandwidth;
+        auto x = R::roofline(r);
+        out << "ok " << x.compute_cycles << " " << x.memory_cycles;
+        return dup_text(out.str());
+      } else if (kw == "overhead") {
+        R::OverheadInput o;
+        is >> o.t_vanilla >> o.n_record >> o.cycle_record;
+        out << "ok " << R::overhead_model(o);
+        return dup_text(out.str());
+      }
+    }
+    if (is_swp) {
+      auto r = R::swp_latency(swp);
+      out << "ok " << r.delta << " " << r.latency;
+    } else if (is_ws) {
+      auto r = R::ws_latency(ws);
+      out << "ok " << r.latency;
+      for (const auto& l : r.critical_path) out << " " << pct_enc(l);
+    } else {
+      out << "err none no model";
+    }
+  } catch (const R::Error& e) {
+    out.str("");
+    out << "err " << static_cast<int>(e.kind()) << " " << e.what();
+  }
+  return dup_text(out.str());
+}
 
 } // extern "C"

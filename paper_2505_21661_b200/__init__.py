@@ -7,7 +7,7 @@ trace API (trace.py).  There is no CPU fallback.
 """
 from . import _build  # noqa: F401
 
-__all__ = ["trace", "build"]
+__all__ = ["trace", "models", "build"]
 
 
 def build(force: bool = False) -> str:

@@ -145,6 +145,13 @@ int main(int argc, char** argv) {
       CHECK(cp.period == 4200);
       CHECK((cp.cycle == std::vector<std::string>{"GEMM1.c0", "GEMM1.c0.wait", "Load V0",
                                                   "Load V0.wait"}));
+      // the stage graph feeds ws_latency: the unfolded cycle is its longest
+      // path (perfmodel.hpp:479-491)
+      CHECK(cp.graph.nodes.size() == cp.stage_mean.size());
+      CHECK(cp.graph.edges.size() == cp.cycle.size() - 1);
+      const WsResult ws = ws_latency(cp.graph);
+      CHECK(ws.latency == cp.period);
+      CHECK(ws.critical_path == cp.cycle);
     }
   }
   if (failures == 0) std::printf("ALL PASS\n");

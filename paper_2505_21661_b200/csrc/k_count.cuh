@@ -199,7 +199,10 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
 // owns stream 32 b + l and walks its records sequentially, windows staged in
 // shared memory (k_window.cuh).  Used when the capacity is even and at most
 // kTpsMaxSlots (the record windows need 16-B chunk alignment).
-constexpr uint32_t kCountWarps = 4;
+#ifndef WGPF_COUNT_WARPS
+#define WGPF_COUNT_WARPS 4
+#endif
+constexpr uint32_t kCountWarps = WGPF_COUNT_WARPS;
 constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
 #ifndef WGPF_COUNT_UNROLL
 #define WGPF_COUNT_UNROLL 16

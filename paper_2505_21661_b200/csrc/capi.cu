@@ -1188,7 +1188,20 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
   uint64_t chunk_bytes = kChunkBytes;
   if (const char* e = getenv("WGPF_CHUNK_MB")) chunk_bytes = (uint64_t)atoll(e) << 20;
   const uint64_t cs = std::max<uint64_t>(32, (chunk_bytes / stride) & ~31ull);
-  const uint64_t nc = (count + cs - 1) / cs;
+  // chunk boundaries: a quarter-size first and last chunk shorten the
+  // pipeline's fill (first H2D alone) and drain (last D2H alone)
+  std::vector<uint64_t> cut{0};
+  {
+    const uint64_t q = std::max<uint64_t>(32, (cs / 4) & ~31ull);
+    uint64_t at = 0;
+    if (count > 2 * cs) {
+      cut.push_back(at = q);
+      while (count - at > cs + q) cut.push_back(at += cs);
+      if (count - at > q) cut.push_back(at = count - q);
+    }
+    while (at < count) cut.push_back(at = std::min(count, at + cs));
+  }
+  const uint64_t nc = cut.size() - 1;
   const uint64_t ev_cap = std::max<uint64_t>(cs * c->slots, 1);
   if (!c->s_h2d) {
     CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
@@ -1208,7 +1221,7 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
   cudaEvent_t* eD = c->pev + 4;
   auto h2d = [&](uint64_t k) -> int {
     const uint32_t b = (uint32_t)(k & 1);
-    const uint64_t s0 = k * cs, m = std::min(cs, count - s0);
+    const uint64_t s0 = cut[k], m = cut[k + 1] - cut[k];
     if (k >= 2) CUDA_OK(c, cudaStreamWaitEvent(c->s_h2d, eC[b], 0));
     CUDA_OK(c, cudaMemcpyAsync(c->d_cbody[b].p, kpft + off + s0 * stride, m * stride,
                                cudaMemcpyHostToDevice, c->s_h2d));
@@ -1246,7 +1259,7 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
   bool overflow = false;
   for (uint64_t k = 0; k < nc; ++k) {
     const uint32_t b = (uint32_t)(k & 1);
-    const uint64_t s0 = k * cs, m = std::min(cs, count - s0);
+    const uint64_t s0 = cut[k], m = cut[k + 1] - cut[k];
     if (k + 1 < nc && (rc = h2d(k + 1))) return rc;
     CUDA_OK(c, cudaStreamWaitEvent(c->stream, eH[b], 0));
     if (k >= 2) CUDA_OK(c, cudaStreamWaitEvent(c->stream, eD[b], 0));

@@ -72,7 +72,7 @@ def _stream_records(rng, n, n_labels, mode, big_gaps):
 
 def random_image(seed: int, n_streams: int = 8, cap: int = 64,
                  mode: str = "nested", big_gaps: bool = False,
-                 labels_idx: int | None = None):
+                 labels_idx: int | None = None, per_block: int = 4):
     """Returns (kpft v1 bytes, slots, strategy, labels)."""
     rng = np.random.default_rng(seed)
     labels = LABEL_SETS[labels_idx if labels_idx is not None else
@@ -87,8 +87,8 @@ def random_image(seed: int, n_streams: int = 8, cap: int = 64,
             count = int(rng.integers(0, 3 * cap))
             writes = count
         tags, clocks = _stream_records(rng, writes, len(labels), mode, big_gaps)
-        body[s, 0] = s // 4
-        body[s, 1] = s % 4
+        body[s, 0] = s // per_block
+        body[s, 1] = s % per_block
         body[s, 2] = count
         body[s, 3] = cap
         for w in range(writes):

@@ -609,3 +609,41 @@ def test_record_windows_tma_and_cp_async(oracle, monkeypatch, no_tma):
             assert (g.count, g.min, g.max, g.sum, g.mean, g.first_event,
                     g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
                                 s.first_event, s.hist), (seed, s.label)
+
+
+@pytest.mark.parametrize("per_block", [1, 3, 5, 16, 33])
+def test_grouped_lane_mapping_streams_per_block(ctx, oracle, per_block):
+    """k_tps's grouped lane mapping for W = 1, 3, 5, 16, 33 streams per block
+    (3-D TMA boxes of one warp index of 32 blocks; W not dividing 32; ragged
+    last row of blocks; W that does not divide the stream count falls back to
+    consecutive streams)."""
+    t = T()
+    for seed in range(6):
+        n_blocks = [32, 40, 70, 33, 64, 31][seed]
+        n = n_blocks * per_block + (1 if seed == 5 else 0)
+        data, cap, strategy, labels = fuzz.random_image(
+            9100 + 10 * per_block + seed, n_streams=n, cap=32, mode="nested",
+            per_block=per_block)
+        try:
+            o, oerr = oracle.replay_kpft(data, cap, strategy, labels, 33), None
+        except O.OracleError as e:
+            o, oerr = None, (e.category, str(e))
+        try:
+            r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33, flags=0x2)
+            gerr = None
+        except t.Error as e:
+            r, gerr = None, (e.category(), str(e))
+        assert oerr == gerr, (seed, oerr, gerr)
+        if oerr:
+            continue
+        assert np.array_equal(r.events, o.events), seed
+        assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+                r.malformed_groups) == (o.dropped_heads, o.truncated_tails,
+                                        o.flagged_preconditions, o.malformed_groups)
+        want = oracle.region_stats(o.events, labels)
+        got = ctx.stats()
+        for s in want:
+            g = got[s.label]
+            assert (g.count, g.min, g.max, g.sum, g.mean, g.first_event,
+                    g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
+                                s.first_event, s.hist), (seed, s.label)

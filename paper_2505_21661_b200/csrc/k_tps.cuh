@@ -19,10 +19,18 @@
 //       per class in shared memory (no atomics); the first-event key per warp
 //       (a shared atomicMin when a lane meets a class for the first time).
 //
-// Data movement.  Records: the warp stages 8-record windows of its 32 streams
-// in shared memory with cp.async (16-B chunks, double buffered; chunk k of the
-// window of stream l is copied by a fixed lane, so one instruction covers a
-// few contiguous lines).  Events: each lane stores its 32-B events straight
+// Scheduling.  A batch is one warp index w of 32 consecutive blocks (lane l
+// <- stream (32 j + l) W + w, W streams per block, host-detected): the lanes
+// run the same record-type sequence, the walk's branches are warp-uniform,
+// and an all-START step does nothing but the push.  Batches beyond the first
+// grid-wide round come from a global counter (dynamic load balance).
+//
+// Data movement.  Records: the warp stages 8-record windows (+2 look-ahead)
+// of its 32 streams in shared memory, double buffered: one 3-D TMA box per
+// window when every stream of the batch starts at slot 0, else cp.async
+// (16-B chunks; chunk k of the window of stream l is copied by a fixed lane,
+// so one instruction covers a few contiguous lines).  Lanes read records in
+// 16-B pairs (conflict-free at the 80-B lane pitch).  Events: each lane stores its 32-B events straight
 // to HBM (one 256-bit store per event, a full L2 sector; a stream's events are contiguous, so
 // L2 completes each line before write-back).  Measured against staging the
 // events in shared-memory rings with a warp-cooperative coalesced flush, the
@@ -33,7 +41,9 @@
 // duration reaches 2^32 is an error, so every emitted duration fits); errors
 // are recorded per lane and handled after the stream (the stack depth stays
 // within pass 1's bound whatever the regions, so a lane can keep going).
-// Histograms: one per-CTA table, one shared atomic per event.
+// Histograms: one per-CTA table, one shared atomic per event (lanes without
+// an event add into a spare word: no branch); a class's count is the sum of
+// its bins.
 #pragma once
 
 #include <type_traits>

@@ -264,6 +264,12 @@ int wgpf_export_chrome_trace(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n
                              int on_device, double cycles_per_us, char* out,
                              uint64_t cap, uint64_t* len);
 
+/* A double as nlohmann 3.11.3 serialises it (Grisu2 shortest digits, the
+ * library's fixed / exponent layout, "null" when not finite) -- the number
+ * format of the reference's JSON reports (pipeline.hpp:146-240).  Host code,
+ * no device needed.  Returns the length written (<= 32), or -1 if cap < 33. */
+int wgpf_format_json_double(double x, char* out, uint64_t cap);
+
 /* ----------------------------------------------------------------------- */
 /* Synthetic trace generator (bench / tests)    */
 /* ----------------------------------------------------------------------- */

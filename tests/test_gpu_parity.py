@@ -647,3 +647,22 @@ def test_grouped_lane_mapping_streams_per_block(ctx, oracle, per_block):
             assert (g.count, g.min, g.max, g.sum, g.mean, g.first_event,
                     g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
                                 s.first_event, s.hist), (seed, s.label)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_reports_from_gpu_results_byte_identical(ctx, name):
+    """The reference's replay / model reports rebuilt from the GPU path's
+    statistics, critical path and warnings equal the golden files."""
+    from paper_2505_21661_b200 import reports as R
+    from test_reports import PARAMS, _golden
+    from test_oracle import dev_barrier_edges
+    data, slots, strategy, labels, cost, dev = load_fixture(name)
+    plan = plan_of(slots, strategy, labels)
+    r = ctx.replay_image_bytes(data, plan, cost)
+    stats = T().region_stats(r.events, labels)  # (exact mean, the default context)
+    cp = ctx.critical_path(r.events, dev_barrier_edges(dev))
+    want = json.loads(_golden(name, "replay"))
+    sim = R.SimTotals(want["total_cycles"], want["vanilla_cycles"], want["records_written"])
+    assert R.dumps(R.replay_report(name, sim, stats, cp, r, cost)) == _golden(name, "replay")
+    assert R.dumps(R.model_report(name, sim, stats, cp, cost, PARAMS.get(name))) == \
+        _golden(name, "model")

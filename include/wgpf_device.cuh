@@ -82,6 +82,12 @@ __host__ __device__ constexpr uint64_t profile_bytes(uint64_t ctas,
   return ctas * streams_per_cta * (uint64_t)(kStreamHdr + 8u * cap);
 }
 
+// signature_for (vgpu.hpp:39-45) packed as trace.hpp:42-46 (wave slot 5 bits,
+// SIMD 4 bits, pipe 3 bits): the tag's low 12 bits for stream `wg`
+__host__ __device__ constexpr uint32_t signature_for(uint32_t wg) {
+  return (wg % 32u) | (((wg / 32u) % 16u) << 5) | (((wg / 512u) % 8u) << 9);
+}
+
 __host__ __device__ constexpr uint32_t make_tag(bool start, uint32_t region,
                                                 uint32_t sig = 0) {
   return (start ? WGPF_START_FLAG : 0u) | (region << 12) | (sig & WGPF_SIGNATURE_MASK);

@@ -796,6 +796,23 @@ char* ref_models(const char* text) {
         auto x = R::roofline(r);
         out << "ok " << x.compute_cycles << " " << x.memory_cycles;
         return dup_text(out.str());
+      } else if (kw == "plan") {  // plan <regions> <nwg> <strategy 0|1> <cap> <n> <trips...>
+        std::uint32_t regions, nwg;
+        int strat;
+        std::uint64_t cap, n;
+        is >> regions >> nwg >> strat >> cap >> n;
+        std::vector<std::uint64_t> trips(n);
+        for (auto& t : trips) is >> t;
+        auto pl = R::plan_slots(regions, trips, nwg,
+                                strat ? R::BufferStrategy::Flush : R::BufferStrategy::Circular, cap);
+        out << "ok " << pl.slots_per_warp_group;
+        return dup_text(out.str());
+      } else if (kw == "sig") {
+        std::uint32_t wg;
+        is >> wg;
+        R::MachineConfig mc;
+        out << "ok " << mc.signature_for(wg).packed();
+        return dup_text(out.str());
       } else if (kw == "overhead") {
         R::OverheadInput o;
         is >> o.t_vanilla >> o.n_record >> o.cycle_record;

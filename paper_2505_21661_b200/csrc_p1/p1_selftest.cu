@@ -16,6 +16,14 @@
 
 #include "wgpf_device.cuh"
 
+// signature_for packs MachineConfig::signature_for (vgpu.hpp:39-45) as
+// Signature::packed (trace.hpp:42-46); tests/test_models.py checks the same
+// formula against the reference
+static_assert(wgpf_dev::signature_for(0) == 0u, "");
+static_assert(wgpf_dev::signature_for(33) == (1u | (1u << 5)), "");
+static_assert(wgpf_dev::signature_for(4095) == (31u | (15u << 5) | (7u << 9)), "");
+static_assert(wgpf_dev::signature_for(4096) == 0u, "");
+
 namespace {
 
 constexpr uint32_t R_KERNEL = 0, R_OUTER = 1, R_INNER = 2, R_ASYNC = 3,

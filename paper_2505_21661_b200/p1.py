@@ -163,3 +163,48 @@ def kpft_v1(body: bytes | np.ndarray, n_streams: int) -> bytes:
     assert n_streams <= 0xFFFF
     b = body.tobytes() if isinstance(body, np.ndarray) else bytes(body)
     return b"KPFT" + struct.pack("<HH", 1, n_streams) + b
+
+
+# ---- buffer planning (lower.hpp:142-188) --------------------------------------
+
+def _pow2_floor(v: int) -> int:
+    p = 1
+    while p * 2 <= v:
+        p *= 2
+    return p
+
+
+def plan_slots(num_regions: int, trip_counts, num_warp_groups: int, strategy,
+               capacity_bytes: int):
+    """plan_slots: slots per stream (warp group) of a device buffer of
+    capacity_bytes without a concrete program.  Flush: two records per region
+    per iteration (iterations = product of the nonzero trip counts) spread over
+    the streams, rejected with a capacity-error when they do not fit; circular:
+    the largest power of two that fits.  Returns a BufferPlan with no labels."""
+    from .trace import BufferPlan, BufferStrategy, Error, ErrorKind
+    M64 = (1 << 64) - 1
+    if num_regions == 0 or num_warp_groups == 0:
+        raise Error(ErrorKind.Lower, "plan_slots: inputs must be positive")
+    iters = 1
+    for t in trip_counts:
+        iters = (iters * (t if t else 1)) & M64
+    strategy = BufferStrategy(strategy)
+    if strategy == BufferStrategy.Flush:
+        total = (2 * num_regions * iters) & M64
+        per = max(1, ((total + num_warp_groups - 1) & M64) // num_warp_groups)
+        need = (per * num_warp_groups * 8) & M64
+        if need > capacity_bytes:
+            raise Error(ErrorKind.Capacity,
+                        f"flush sizing needs {need} bytes, capacity is {capacity_bytes}")
+        return BufferPlan(per, strategy, [])
+    slots = capacity_bytes // (8 * num_warp_groups)
+    if slots == 0:
+        raise Error(ErrorKind.Capacity, "circular sizing: capacity too small for one "
+                    "slot per warp group")
+    return BufferPlan(_pow2_floor(slots), strategy, [])
+
+
+def signature_for(wg: int) -> int:
+    """MachineConfig::signature_for (vgpu.hpp:39-45), packed (trace.hpp:42-46):
+    the 12 signature bits of stream wg's tags (wgpf_dev::signature_for)."""
+    return (wg % 32) | (((wg // 32) % 16) << 5) | (((wg // 512) % 8) << 9)

@@ -253,3 +253,31 @@ def test_cxx_dropin_models_vs_reference(reference, tmp_path):
     got = res.stdout.split("\n")[:len(queries)]
     for q, g in zip(queries, got):
         assert g.rstrip() == _ref_raw(reference, q).rstrip(), q
+
+
+# ---- buffer planning and stream signatures (P1 host helpers) -------------------
+
+def test_plan_slots_known_answers():
+    from paper_2505_21661_b200 import p1
+    from paper_2505_21661_b200.trace import BufferStrategy
+    assert p1.plan_slots(4, [512], 2, BufferStrategy.Flush, 1 << 20).slots_per_warp_group * 2 == 4096
+    with pytest.raises(Error) as e:
+        p1.plan_slots(4, [512], 2, BufferStrategy.Flush, 16384)
+    assert e.value.kind == ErrorKind.Capacity
+    assert p1.plan_slots(1, [], 1, BufferStrategy.Circular, 1024).slots_per_warp_group == 128
+    assert p1.plan_slots(1, [], 1, BufferStrategy.Circular, 1000).slots_per_warp_group == 64
+
+
+def test_plan_slots_and_signature_vs_reference(reference):
+    from paper_2505_21661_b200 import p1
+    rng = np.random.default_rng(15)
+    for _ in range(400):
+        regions, nwg = int(rng.integers(0, 20)), int(rng.integers(0, 9))
+        strat = int(rng.integers(0, 2))
+        cap = int(rng.choice([0, 7, 8, 1000, 1024, 4096, 1 << 16, 1 << 20]))
+        trips = [int(rng.integers(0, 600)) for _ in range(int(rng.integers(0, 3)))]
+        text = f"plan {regions} {nwg} {strat} {cap} {len(trips)} " + " ".join(map(str, trips))
+        got = _ours(lambda: [p1.plan_slots(regions, trips, nwg, strat, cap).slots_per_warp_group])
+        assert got == _ref(reference, text), text
+    for wg in list(range(0, 2048, 7)) + [4095, 4096, 65535, (1 << 32) - 1]:
+        assert "ok " + str(p1.signature_for(wg)) == _ref(reference, f"sig {wg}")

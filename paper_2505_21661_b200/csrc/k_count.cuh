@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(kCountWarps * 32)
     const uint32_t n_end = (n - (uint32_t)q) >> 1;
     const bool wide = n && maxrid >= a.fast_regions;
     const bool tps_out = n && maxrid >= a.tps_regions;
+    bool to_deep = false, to_warp = false;
     if (act) {
       a.counts[s] = n_end - (uint32_t)(-run_min);
       a.zpos[s] = z;
@@ -355,10 +356,26 @@ __global__ void __launch_bounds__(kCountWarps * 32)
       const bool deep = warp && !(n && maxrid >= a.deep_regions) &&
                         max_d <= (int32_t)a.deep_depth;
       a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
-      if (warp && deep)
-        a.deep_list[atomicAdd(a.deep_len, 1ull)] = s;
-      else if (warp)
-        a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
+      to_deep = warp && deep;
+      to_warp = warp && !deep;
+    }
+    // warp-aggregated appends: one atomic per warp, the batch's listed
+    // streams stay consecutive and in stream order (coalesced window copies
+    // in the list kernels)
+    const uint32_t lt = lanemask_lt();
+    const uint32_t dm = __ballot_sync(FULL, to_deep);
+    if (dm) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(a.deep_len, (unsigned long long)__popc(dm));
+      base = __shfl_sync(FULL, base, 0);
+      if (to_deep) a.deep_list[base + __popc(dm & lt)] = s;
+    }
+    const uint32_t wm = __ballot_sync(FULL, to_warp);
+    if (wm) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(a.warp_len, (unsigned long long)__popc(wm));
+      base = __shfl_sync(FULL, base, 0);
+      if (to_warp) a.warp_list[base + __popc(wm & lt)] = s;
     }
   }
 }

@@ -131,6 +131,7 @@ struct wgpf_ctx {
   uint32_t* h_blk = nullptr;  // pinned: block fields read by stream_group
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
+  DevBuf d_dorph;  // k_tpsd: one orphan event per lane
   size_t smem_optin = 0;
   // pipelined replay_image (host buffers): copy streams, chunk buffers, and
   // per-chunk (first stream, first event) for first_event lookups
@@ -763,6 +764,8 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       f.list = c->d_dlist.as<unsigned long long>();
       f.list_len = c->d_glen.as<unsigned long long>() + 2;
       const uint32_t dw = deep_warps(c->smem_optin);
+      ALLOC_OK(c, c->d_dorph, sizeof(wgpf_event) * (uint64_t)c->sms * dw * 32);
+      f.orphan_scratch = c->d_dorph.as<wgpf_event>();  // one orphan per lane
       deep_kernel(events != nullptr, !no_stats)<<<c->sms, dw * 32, deep_smem_bytes(dw),
                                                   c->stream>>>(f);
       CUDA_OK(c, cudaGetLastError());

@@ -34,7 +34,8 @@ constexpr uint32_t kDeepStkRid = (kDeepRegions - 1u) << 12;
 struct DeepWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];        // record windows
   uint2 stk[kDeepDepth][32];             // {lo, pos | rid<<12 | cons<<18 | hi<<19}
-  wgpf_event orph[32];                   // one orphan per lane
+  unsigned long long wsum[kSmemClasses];  // this warp's sums and counts for
+  uint32_t wcnt[kSmemClasses];            //   the warp-uniform statistics path
   uint16_t cnt[kDeepRegions][32];        // iteration counters
 };
 
@@ -88,7 +89,13 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
   const uint32_t s_info = opaque_u32(smem_addr(cs.info));
   const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);  // + 256 * level
   const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);  // + 64 * region
-  const uint32_t s_orph = smem_addr(&ws.orph[lane]);
+  // one orphan per lane, in global scratch (rare; shared memory holds the
+  // warp's statistics instead)
+  wgpf_event* const orph = a.orphan_scratch + ((size_t)blockIdx.x * nw + w) * 32u + lane;
+  for (uint32_t c = lane; c < kSmemClasses; c += 32) {
+    ws.wsum[c] = 0;
+    ws.wcnt[c] = 0;
+  }
   const uint32_t s_rec = smem_addr(ws.rec[0]);
   const uint32_t s_spare = opaque_u32(smem_addr(&cs.hist_spare));
   const uint64_t n_list = *a.list_len;
@@ -111,8 +118,10 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       const bool cand = p && (uint32_t)(key >> 32) == khi;
       const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
       if (lane == leader) {
-        sadd64(&cs.st.count[c0], (unsigned long long)__popc(pm));
-        sadd64(&cs.st.sum[c0], (unsigned long long)slo + ((unsigned long long)shi << 16));
+        // count and sum in the warp's own table (no atomics, nothing to wait
+        // for); min / max are fire-and-forget shared atomics
+        ws.wcnt[c0] += __popc(pm);
+        ws.wsum[c0] += (unsigned long long)slo + ((unsigned long long)shi << 16);
         atomicMin(&cs.st.min[c0], mn);
         atomicMax(&cs.st.max[c0], mx);
         smin64(&cs.st.first[c0], ((unsigned long long)khi << 32) | klo);
@@ -268,8 +277,9 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       }
       kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
       pw = base ? (inf >> 16) : 0xFFu;
-      sts128_if(orphan && n_orph == 0, s_orph, make_uint4(e.x, shi, v, hi));
-      sts64_if(orphan && n_orph == 0, s_orph + 16u, make_uint2(rid, it));
+      if (orphan && n_orph == 0)
+        *orph = wgpf_event{(uint64_t)e.x | ((uint64_t)shi << 32), (uint64_t)v | ((uint64_t)hi << 32),
+                           rid, it, 0u, 0u};
       n_orph += orphan ? 1u : 0u;
       if constexpr (stats) {
         wstat(base, inf & 0xFFu, corr, gkey | (kpos << 1));
@@ -304,7 +314,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     const bool bad = broken || n_orph > 1;
     const bool po = act && !bad && n_orph == 1;
     if (__any_sync(FULL, po)) {
-      const wgpf_event o = ws.orph[lane];
+      const wgpf_event o = po ? *orph : wgpf_event{};
       if (emit)
         put(po, kw, (uint32_t)o.start, (uint32_t)(o.start >> 32), (uint32_t)o.end,
             (uint32_t)(o.end >> 32), o.region, o.iteration);
@@ -336,6 +346,14 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     if (t) atomicAdd(&cs.warn[1], t);
     if (f) atomicAdd(&cs.warn[2], f);
     if (m) atomicAdd(&cs.warn[3], m);
+  }
+  if (stats) {  // the warp's counts and sums into the CTA table
+    for (uint32_t c = lane; c < kSmemClasses; c += 32) {
+      if (ws.wcnt[c]) {
+        sadd64(&cs.st.count[c], (unsigned long long)ws.wcnt[c]);
+        sadd64(&cs.st.sum[c], ws.wsum[c]);
+      }
+    }
   }
   __syncthreads();
   if (threadIdx.x < 4 && cs.warn[threadIdx.x])

@@ -108,6 +108,10 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     const uint32_t c0 = __shfl_sync(FULL, cls, leader);
     const bool uni = __all_sync(FULL, !p || cls == c0);
     if (uni && c0 < kSmemClasses && c0 < K) {
+      // the CTA's current first key, loaded ahead of the reductions so its
+      // latency overlaps them (the min below rarely needs the atomic)
+      const unsigned long long cur_first =
+          *reinterpret_cast<volatile unsigned long long*>(&cs.st.first[c0]);
       const uint32_t dd = p ? d : 0u;
       const uint32_t slo = __reduce_add_sync(FULL, dd & 0xFFFFu);
       const uint32_t shi = __reduce_add_sync(FULL, dd >> 16);
@@ -124,7 +128,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
         ws.wsum[c0] += (unsigned long long)slo + ((unsigned long long)shi << 16);
         atomicMin(&cs.st.min[c0], mn);
         atomicMax(&cs.st.max[c0], mx);
-        smin64(&cs.st.first[c0], ((unsigned long long)khi << 32) | klo);
+        const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
+        if (fk < cur_first) atomicMin(&cs.st.first[c0], fk);
       }
       red_add(p ? smem_addr(&cs.st.hist[c0 * WGPF_HIST_BINS + hist_bin32(d)]) : s_spare, 1u);
     } else if (p) {

@@ -104,9 +104,11 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
   auto wstat = [&](bool p, uint32_t cls, uint32_t d, unsigned long long key) {
     const uint32_t pm = __ballot_sync(FULL, p);
     if (pm == 0) return;
+    // one class for every participating lane?  (two independent reductions
+    // instead of a leader shuffle followed by a vote)
+    const uint32_t c0 = __reduce_min_sync(FULL, p ? cls : 0xFFFFFFFFu);
+    const bool uni = c0 == __reduce_max_sync(FULL, p ? cls : 0u);
     const uint32_t leader = __ffs(pm) - 1u;
-    const uint32_t c0 = __shfl_sync(FULL, cls, leader);
-    const bool uni = __all_sync(FULL, !p || cls == c0);
     if (uni && c0 < kSmemClasses && c0 < K) {
       // the CTA's current first key, loaded ahead of the reductions so its
       // latency overlaps them (the min below rarely needs the atomic)

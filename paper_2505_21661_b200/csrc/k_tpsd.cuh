@@ -163,12 +163,15 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     // record windows: chunk k of this lane copies part (q % C) of the window
     // of batch slot q / C, q = 32 k + lane; that slot's stream from its lane
     uint32_t wp[kTpsChunks];
+    const uint8_t* srck[kTpsChunks];  // slots of chunk k's stream (null: none)
     const uint32_t s32 = (uint32_t)s;
     const uint32_t live = act ? 1u : 0u;
 #pragma unroll
     for (uint32_t k = 0; k < kTpsChunks; ++k) {
       const uint32_t q = k * 32u + lane, sl = q / kTpsChunks, part = q % kTpsChunks;
       const uint32_t st_k = __shfl_sync(FULL, start, sl);
+      const uint32_t ss = __shfl_sync(FULL, s32, sl);
+      srck[k] = __shfl_sync(FULL, live, sl) ? a.body + (uint64_t)ss * a.stride + 16 : nullptr;
       uint32_t p = st_k + 2u;
       if (p >= cap) p -= cap;
       p = (p & ~1u) + 2u * part;
@@ -179,11 +182,10 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
 #pragma unroll
       for (uint32_t k = 0; k < kTpsChunks; ++k) {
         const uint32_t q = k * 32u + lane, sl = q / kTpsChunks, part = q % kTpsChunks;
-        const uint32_t ss = __shfl_sync(FULL, s32, sl);
-        const uint32_t lv = __shfl_sync(FULL, live, sl);
-        if (lv)
+        // (stream addresses resolved once per batch, not per window)
+        if (srck[k])
           cp_async16(s_rec + bsel * (32 * kTpsPitch) + sl * kTpsPitch + 16u * part,
-                     a.body + (uint64_t)ss * a.stride + 16 + 8u * wp[k]);
+                     srck[k] + 8u * wp[k]);
         wp[k] += kTpsW;
         if (wp[k] >= cap) wp[k] -= cap;
       }

@@ -34,8 +34,9 @@ constexpr uint32_t kDeepStkRid = (kDeepRegions - 1u) << 12;
 struct DeepWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];        // record windows
   uint2 stk[kDeepDepth][32];             // {lo, pos | rid<<12 | cons<<18 | hi<<19}
-  unsigned long long wsum[kSmemClasses];  // this warp's sums and counts for
-  uint32_t wcnt[kSmemClasses];            //   the warp-uniform statistics path
+  unsigned long long wsum[kSmemClasses];  // this warp's sums, mins and maxes
+  uint32_t wmin[kSmemClasses];            //   for the warp-uniform statistics
+  uint32_t wmax[kSmemClasses];            //   path (counts: histogram sums)
   uint16_t cnt[kDeepRegions][32];        // iteration counters
 };
 
@@ -94,7 +95,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
   wgpf_event* const orph = a.orphan_scratch + ((size_t)blockIdx.x * nw + w) * 32u + lane;
   for (uint32_t c = lane; c < kSmemClasses; c += 32) {
     ws.wsum[c] = 0;
-    ws.wcnt[c] = 0;
+    ws.wmin[c] = 0xFFFFFFFFu;
+    ws.wmax[c] = 0;
   }
   const uint32_t s_rec = smem_addr(ws.rec[0]);
   const uint32_t s_spare = opaque_u32(smem_addr(&cs.hist_spare));
@@ -126,10 +128,9 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       if (lane == leader) {
         // count and sum in the warp's own table (no atomics, nothing to wait
         // for); min / max are fire-and-forget shared atomics
-        ws.wcnt[c0] += __popc(pm);
         ws.wsum[c0] += (unsigned long long)slo + ((unsigned long long)shi << 16);
-        atomicMin(&cs.st.min[c0], mn);
-        atomicMax(&cs.st.max[c0], mx);
+        ws.wmin[c0] = min(ws.wmin[c0], mn);
+        ws.wmax[c0] = max(ws.wmax[c0], mx);
         const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
         if (fk < cur_first) atomicMin(&cs.st.first[c0], fk);
       }
@@ -356,15 +357,26 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     if (f) atomicAdd(&cs.warn[2], f);
     if (m) atomicAdd(&cs.warn[3], m);
   }
-  if (stats) {  // the warp's counts and sums into the CTA table
+  if (stats) {  // the warp's sums, mins and maxes into the CTA table
     for (uint32_t c = lane; c < kSmemClasses; c += 32) {
-      if (ws.wcnt[c]) {
-        sadd64(&cs.st.count[c], (unsigned long long)ws.wcnt[c]);
+      if (ws.wmin[c] != 0xFFFFFFFFu || ws.wmax[c] != 0u) {
         sadd64(&cs.st.sum[c], ws.wsum[c]);
+        atomicMin(&cs.st.min[c], ws.wmin[c]);
+        atomicMax(&cs.st.max[c], ws.wmax[c]);
       }
     }
   }
   __syncthreads();
+  if (stats) {
+    // counts = histogram sums (every event, on either statistics path, adds
+    // exactly one histogram increment; the warp-uniform path keeps no count)
+    for (uint32_t c = threadIdx.x; c < kSmemClasses; c += blockDim.x) {
+      unsigned long long t = 0;
+      for (uint32_t b = 0; b < WGPF_HIST_BINS; ++b) t += cs.st.hist[c * WGPF_HIST_BINS + b];
+      cs.st.count[c] = t;
+    }
+    __syncthreads();
+  }
   if (threadIdx.x < 4 && cs.warn[threadIdx.x])
     atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
   if (stats) smem_stats_flush(cs.st, a.stats);

@@ -1,25 +1,32 @@
 """bench.py -- trace records decoded/s on the synthetic config-4 trace.
 
-One step = one replay_image of this rank's full config-4 trace (SURVEY.md 8(d)
-config 4: 148 SMs x 2048 CTAs x 16 warps = 4,849,664 streams, 2^30 records,
-flush, capacity 256, 8 regions) already resident in HBM: pass-1 counts, the
-offset scan, the warp-cooperative decode/pair/replay/stats pass writing all
-531,791,872 events, statistics finalisation, and (N > 1) the one NCCL
-all-gather + merge of the per-label tables.  Weak scaling: every rank owns one
-config-4-sized block range of an N x 2^30-record trace.
+One step = one replay of the config-4 trace (148 SMs x
+2048 CTAs x 16 warps = 4,849,664 streams, 2^30 records, flush, capacity 256, 8
+regions) already resident in HBM: pass-1 counts, the offset scan, the
+decode / pair / replay / stats pass writing all 531,791,872 events, statistics
+finalisation.  At N > 1 GPUs the ONE trace is sharded by contiguous block
+ranges (shard.stream_range; strong scaling: every rank decodes 2^30 / N
+records) and each step ends with the single NCCL collective of the path: an
+all-gather of the packed per-label tables, merged on every rank
+(wgpf_stats_merge).  A config-5 sub-line (circular, 64 nested scopes,
+overflow-heavy) is measured in the same run.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+--gpus N > 1 outside torchrun re-launches itself under
+torch.distributed.run with N ranks; under torchrun WORLD_SIZE must equal N.
 Prints one JSON line on rank 0.  --impl reference times the reference's own
 CPU implementation (oracle/_ref, compiled from the reference headers) on a
-bounded sample of the same workload with all host threads.
+bounded sample of the same workload with all host threads (rank 0 only).
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,11 +37,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = ("trace records decoded/s (GB/s vs HBM peak) at 1/2/4/8 GPU; "
           "instr. overhead %")
-WORKLOAD = ("config 4: synthetic 2^30-record trace per GPU (148 SMs x 2048 CTAs "
-            "x 16 warps = 4,849,664 streams), flush, 256 slots, 8 regions, "
-            "TMA producer / MMA consumer patterns")
-WORKLOAD5 = ("config 5: 2^22 circular streams per GPU, 256 slots, 1000 writes each "
-             "(2^30 surviving records), 64 nested scopes S0..S63 E63..E0")
+WORKLOAD = ("config 4: synthetic 2^30-record trace (148 SMs x 2048 CTAs x 16 "
+            "warps = 4,849,664 streams), flush, 256 slots, 8 regions, TMA "
+            "producer / MMA consumer patterns; sharded by block range across the "
+            "GPUs")
+WORKLOAD5 = ("config 5: 2^22 circular streams, 256 slots, 1000 writes each "
+             "(2^30 surviving records), 64 nested scopes S0..S63 E63..E0; sharded "
+             "by block range across the GPUs")
+RECORD_COST = 33
+CHUNK = 65535  # streams per KPFT v1 image (u16 count, trace.hpp:162)
 
 
 def env_int(k, d):
@@ -48,8 +59,22 @@ def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0))
 
 
 class ClockSampler:
@@ -103,47 +128,116 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference arm
+# multi-process launch
 # ---------------------------------------------------------------------------
 
 
-def run_reference(args, rank):
-    if rank != 0:
-        return
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(n: int) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N ranks (one per GPU) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own pipeline (oracle/_ref)
+# ---------------------------------------------------------------------------
+
+
+def ref_sample(rate: float, threads: int, budget_s: float, n_avail: int) -> tuple:
+    """Sample size for the all-threads reference run: a whole number of
+    rounds of `threads` equal chunks (<= 65,535 streams each, a multiple of
+    16 so chunks hold whole blocks), so no thread idles in a half-empty last
+    wave.  Returns (n_streams, chunk_streams)."""
+    chunk = min(CHUNK // 16 * 16, max(16, (n_avail // threads) // 16 * 16))
+    per_round = chunk * threads
+    rounds = max(1, min(n_avail // per_round, int(rate * budget_s / (221.5 * per_round))))
+    return rounds * per_round, chunk
+
+
+def cpu_baseline(host_body_u8, n_avail: int, budget_s: float, labels, cap: int,
+                 strategy: int, rec_per_stream: float):
+    """oracle/_ref (the reference compiled from its headers) on a bounded
+    sample of the workload: all host threads over equal KPFT v1 chunks, plus
+    the single-core line (the reference as shipped is single-threaded)."""
     from oracle import oracle as O
     from oracle import synth as S
+    if not O.have_ref():
+        return None
     ref = O.Reference()
-    threads = len(os.sched_getaffinity(0))
+    threads = host_threads()
+    stride = S.stream_stride()
+    one = min(n_avail, CHUNK // 16 * 16)
+    r1 = ref.bench_replay(host_body_u8[:one * stride], one, cap, strategy, labels,
+                          RECORD_COST, CHUNK, 1)
+    rate1 = r1["records"] / max(r1["seconds"], 1e-9)
+    n, chunk = ref_sample(rate1 * threads, threads, budget_s, n_avail)
+    r = ref.bench_replay(host_body_u8[:n * stride], n, cap, strategy, labels,
+                         RECORD_COST, chunk, threads)
+    return {"value": r["records"] / r["seconds"], "unit": "records/s",
+            "cores": threads, "kind": "reference",
+            "sample": (f"first {n} streams ({r['records']} records, "
+                       f"{r['seconds']:.2f} s); reference deserialize->decode->pair->"
+                       f"replay->region_stats, {n // chunk} KPFT v1 chunks of {chunk} "
+                       f"streams on {threads} threads (harness-level parallelism)"),
+            "single_core": {"value": rate1, "unit": "records/s", "cores": 1,
+                            "sample": f"first {one} streams ({r1['records']} records, "
+                                      f"{r1['seconds']:.2f} s), one thread"},
+            "nproc": os.cpu_count(), "cpu_model": cpu_model()}
+
+
+def run_reference(args, rank):
+    """The reference arm: the reference's CPU pipeline on the box's host cores."""
+    if rank != 0:
+        return
+    from oracle import synth as S
+    threads = host_threads()
+    # calibrate on one chunk's worth of the workload
+    n_cal = CHUNK // 16 * 16
+    body = S.mixed_body(0, n_cal, S.MIXED_FULL_LONG)
+    from oracle import oracle as O
+    ref = O.Reference()
+    r = ref.bench_replay(body, n_cal, S.CAP, 1, S.MIXED_LABELS, RECORD_COST, CHUNK, 1)
+    rate1 = r["records"] / max(r["seconds"], 1e-9)
     steps, warmup = args.steps, args.warmup
-    # calibrate: one 65,535-stream chunk on all threads
-    cal_n = 65535 * max(1, min(threads, 8))
-    body = S.mixed_body(0, cal_n, S.MIXED_FULL_LONG)
-    r = ref.bench_replay(body, cal_n, S.CAP, 1, S.MIXED_LABELS, 33, 65535, threads)
-    rate = r["records"] / max(r["seconds"], 1e-6)
-    budget = args.ref_budget_s / (steps + warmup)
-    n = int(min(S.MIXED_FULL_STREAMS, max(cal_n, rate * budget / 221.5)))
-    n = (n // 16) * 16
-    if n != cal_n:
-        body = S.mixed_body(0, n, S.MIXED_FULL_LONG)
+    n, chunk = ref_sample(rate1 * threads, threads,
+                          args.ref_budget_s / (steps + warmup), S.MIXED_FULL_STREAMS)
+    body = S.mixed_body(0, n, S.MIXED_FULL_LONG)
     times, recs, evs = [], 0, 0
     for i in range(warmup + steps):
-        r = ref.bench_replay(body, n, S.CAP, 1, S.MIXED_LABELS, 33, 65535, threads)
+        r = ref.bench_replay(body, n, S.CAP, 1, S.MIXED_LABELS, RECORD_COST, chunk,
+                             threads)
         if i >= warmup:
             times.append(r["seconds"])
             recs, evs = r["records"], r["events"]
-    sec = sum(times) / len(times)
+    sec = statistics.mean(times)
     value = recs / sec
     sample = (f"first {n} streams of config 4 ({recs} records, {evs} events) per "
               f"step; deserialize->decode->pair->replay->region_stats over "
-              f"65,535-stream KPFT v1 chunks, {threads} threads")
+              f"{n // chunk} KPFT v1 chunks of {chunk} streams on {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "records/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32/u64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample_streams": n},
         "cpu_baseline": {"value": value, "unit": "records/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample,
+                         "single_core": {"value": rate1, "unit": "records/s",
+                                         "cores": 1,
+                                         "sample": f"first {n_cal} streams, one thread"},
+                         "nproc": os.cpu_count(), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "records/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -155,29 +249,165 @@ def run_reference(args, rank):
 # ---------------------------------------------------------------------------
 
 
-def cpu_baseline(host_body_u8, n_avail, budget_s):
-    """oracle/_ref (the reference) on a bounded sample, all host threads."""
-    from oracle import oracle as O
-    from oracle import synth as S
-    if not O.have_ref():
-        return None
-    ref = O.Reference()
-    threads = len(os.sched_getaffinity(0))
-    stride = S.stream_stride()
-    cal_n = min(n_avail, 65535 * max(1, min(threads, 8)))
-    r = ref.bench_replay(host_body_u8[:cal_n * stride], cal_n, S.CAP, 1,
-                         S.MIXED_LABELS, 33, 65535, threads)
-    rate = r["records"] / max(r["seconds"], 1e-6)
-    n = int(min(n_avail, max(cal_n, rate * budget_s / 221.5)))
-    n = (n // 16) * 16
-    r = ref.bench_replay(host_body_u8[:n * stride], n, S.CAP, 1, S.MIXED_LABELS,
-                         33, 65535, threads)
-    return {"value": r["records"] / r["seconds"], "unit": "records/s",
-            "cores": threads, "kind": "reference",
-            "sample": (f"first {n} streams of config 4 ({r['records']} records, "
-                       f"{r['seconds']:.1f} s); reference deserialize->decode->"
-                       f"pair->replay->region_stats, 65,535-stream v1 chunks, "
-                       f"{threads} threads")}
+def stats_digest(st: dict) -> str:
+    """sha256 over the integer statistics fields (count, sum, min, max, the
+    64 histogram bins, warp group, kind) in label order: equal for every
+    number of GPUs because the shard merge is exact."""
+    h = hashlib.sha256()
+    for k in sorted(st):
+        s = st[k]
+        h.update(json.dumps([k, s.warp_group, s.kind, s.count, s.sum, s.min, s.max,
+                             list(s.hist)]).encode())
+    return h.hexdigest()[:16]
+
+
+class Decode:
+    """One config (4 or 5) on this rank: its shard of the one synthetic trace
+    resident in HBM, the events buffer, the step."""
+
+    def __init__(self, cfg, ctx, merged_ctx, world, rank, dev, streams_total=0):
+        import torch
+
+        from paper_2505_21661_b200 import _lib as L
+        from paper_2505_21661_b200 import shard
+        from paper_2505_21661_b200 import trace as T
+        from paper_2505_21661_b200 import workloads as S
+        self.L, self.T, self.S = L, T, S
+        self.cfg, self.ctx, self.merged = cfg, ctx, merged_ctx
+        self.world, self.rank = world, rank
+        nested = cfg == 5
+        self.nested = nested
+        if nested:
+            self.plan = T.BufferPlan(S.CAP, T.BufferStrategy.Circular, S.NESTED_LABELS)
+            total = streams_total or S.NESTED_FULL_STREAMS
+            n_long = 0
+        else:
+            self.plan = T.BufferPlan(S.CAP, T.BufferStrategy.Flush, S.MIXED_LABELS)
+            total = streams_total or S.MIXED_FULL_STREAMS
+            n_long = S.MIXED_FULL_LONG if total == S.MIXED_FULL_STREAMS else \
+                S.mixed_long_for(total)
+        self.total = total
+        s0, s1 = shard.stream_range(total, S.STREAMS_PER_BLOCK, world, rank)
+        self.s0, self.n = s0, s1 - s0
+        n = self.n
+        ctx.set_plan(self.plan)
+        if merged_ctx is not None:
+            merged_ctx.set_plan(self.plan)
+        self.stride = S.stream_stride()
+        self.body = torch.empty(max(1, n) * self.stride, dtype=torch.uint8, device=dev)
+        ctx.synth_body(self.body.data_ptr(), S.NESTED if nested else S.MIXED, s0, n,
+                       n_long)
+        torch.cuda.synchronize()
+        if nested:
+            self.records = n * S.CAP
+            self.records_total = total * S.CAP
+        else:
+            self.records = S.mixed_records(s0, s1, n_long)
+            self.records_total = S.mixed_records(0, total, n_long)
+        ne, _ = ctx.replay_device(self.body.data_ptr(), self.body.numel(), n,
+                                  RECORD_COST, 0, 0, L.F_STATS_ONLY | L.F_NO_STATS,
+                                  stream_base=s0)
+        self.n_ev = ne
+        self.events = torch.empty(max(1, ne) * 32, dtype=torch.uint8, device=dev)
+        # algorithmic bytes (SURVEY.md 8(d)): headers + surviving records read,
+        # 32-B events written
+        self.alg_bytes = 16 * n + 8 * self.records + 32 * ne
+        packed = ctx.stats_packed_bytes()
+        self.packed = packed
+        self.mine = torch.zeros(packed, dtype=torch.uint8, device=dev)
+        self.gathered = torch.zeros(packed * world, dtype=torch.uint8, device=dev)
+        self.xflags = env_int("WGPF_BENCH_FLAGS", 0)  # A/B only, never reported
+
+    def step(self):
+        import torch.distributed as dist
+        ctx, L = self.ctx, self.L
+        ne, w = ctx.replay_device(self.body.data_ptr(), self.body.numel(), self.n,
+                                  RECORD_COST, self.events.data_ptr(), self.n_ev,
+                                  L.F_PROFILE | self.xflags, stream_base=self.s0)
+        assert ne == self.n_ev
+        prof = ctx.last_profile()
+        launches = prof["launches"]
+        if self.world > 1:
+            ctx.stats_export(self.mine.data_ptr())
+            dist.all_gather_into_tensor(self.gathered, self.mine)
+            self.merged.stats_merge(self.gathered.data_ptr(), self.world)
+            launches += 2  # export + merge kernels (+ the NCCL kernel)
+        return prof, launches
+
+    def stats(self):
+        return (self.merged if self.world > 1 else self.ctx).stats()
+
+    def timed(self, steps, warmup, stream, dev, sample_clocks, local):
+        import torch
+        import torch.distributed as dist
+        for _ in range(warmup):
+            self.step()
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local) if sample_clocks else None
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        t0.record(stream)
+        profs, launches = [], 0
+        for _ in range(steps):
+            p, l = self.step()
+            profs.append(p)
+            launches += l
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        clk = clocks.stop() if clocks else None
+        ms = t0.elapsed_time(t1)
+        if self.world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, profs, launches, clk
+
+    def summary(self, ms, profs, steps, peak, peak_kind, traffic):
+        ms_step = ms / steps
+        emit_ms = statistics.mean(p["emit_ms"] for p in profs)
+        achieved = self.alg_bytes / (emit_ms / 1e3) / 1e9
+        ph = {k: statistics.mean(p[k + "_ms"] for p in profs)
+              for k in ("count", "scan", "emit", "general", "finalize")}
+        return {
+            "value": self.records_total * steps / (ms / 1e3), "ms_per_step": ms_step,
+            "streams_total": self.total, "records_total": self.records_total,
+            "records_per_gpu": self.records, "events_per_gpu": self.n_ev,
+            "streams_per_gpu": self.n,
+            "gbs_step_rank0": self.alg_bytes / (ms_step / 1e3) / 1e9,
+            "hbm_frac_step": self.alg_bytes / (ms_step / 1e3) / 1e9 / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": ("emit phase (k_tpsd deep list)" if self.nested else
+                                    "emit phase (k_tps + k_fast_emit list)"),
+                         "algorithmic_bytes_per_launch": self.alg_bytes,
+                         "kernel_ms": emit_ms, "peak_kind": peak_kind},
+            "phases_ms": ph, "general_streams": profs[-1]["general_streams"],
+        }
+
+    def free(self):
+        del self.body, self.events, self.mine, self.gathered
+
+
+def traffic_of(name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/), or None."""
+    tp = os.path.join(ROOT, "profiles", name)
+    if os.path.exists(tp):
+        try:
+            return json.load(open(tp)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
 
 
 def main():
@@ -187,158 +417,90 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=0,
-                    help="streams per GPU (default: full config 4)")
+                    help="total streams of the trace (default: the full config)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-budget-s", type=float, default=90.0)
     ap.add_argument("--config", type=int, default=4, choices=[4, 5],
-                    help="4: mixed producer/consumer trace (headline); 5: 2^22 "
-                         "circular streams, 64 nested scopes, 1000 writes each")
+                    help="headline config: 4 (mixed producer/consumer trace) or 5")
+    ap.add_argument("--no-config5", action="store_true",
+                    help="skip the config-5 sub-line")
     ap.add_argument("--no-p1", action="store_true",
                     help="skip the config-2 instrumentation-overhead measurement")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
 
     if args.impl == "reference":
         run_reference(args, rank)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from oracle import synth as S
     from paper_2505_21661_b200 import _lib as L
     from paper_2505_21661_b200 import trace as T
 
+    ndev = torch.cuda.device_count()
+    if local >= ndev:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but this box has "
+                         f"{ndev} GPU(s); --gpus {args.gpus} cannot run here")
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     ctx = T.Context(local, stream.cuda_stream)
-    nested = args.config == 5
-    if nested:
-        plan = T.BufferPlan(S.CAP, T.BufferStrategy.Circular, S.NESTED_LABELS)
-    else:
-        plan = T.BufferPlan(S.CAP, T.BufferStrategy.Flush, S.MIXED_LABELS)
-    ctx.set_plan(plan)
-
-    n = args.streams or (S.NESTED_FULL_STREAMS if nested else S.MIXED_FULL_STREAMS)
-    s0 = rank * n
-    n_long = s0 + (S.MIXED_FULL_LONG if n == S.MIXED_FULL_STREAMS
-                   else S.mixed_long_for(n))
-    stride = S.stream_stride()
-    body = torch.empty(n * stride, dtype=torch.uint8, device=dev)
-    if nested:
-        ctx.synth_body(body.data_ptr(), 1, s0, n, 0)
-    else:
-        ctx.synth_body(body.data_ptr(), 0, s0, n, n_long)
-    torch.cuda.synchronize()
-
-    # sizes: records / events of this rank (one STATS_ONLY pass)
-    n_ev, _ = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, 0, 0,
-                                L.F_STATS_ONLY | L.F_NO_STATS, stream_base=s0)
-    if nested:
-        records = n * S.CAP
-    else:
-        records = int(min(222, 256) * (n_long - s0) + 221 * (n - (n_long - s0)))
-    events = torch.empty(n_ev * 32, dtype=torch.uint8, device=dev)
-    alg_bytes = 16 * n + 8 * records + 32 * n_ev
-
-    packed = ctx.stats_packed_bytes()
-    mine = torch.zeros(packed, dtype=torch.uint8, device=dev)
-    gathered = torch.zeros(packed * world, dtype=torch.uint8, device=dev)
-    merged_ctx = None
-    if world > 1:
-        merged_ctx = T.Context(local, stream.cuda_stream)
-        merged_ctx.set_plan(plan)
-
-    # WGPF_BENCH_FLAGS: extra replay flags for A/B experiments (never in the
-    # reported configuration)
-    xflags = env_int("WGPF_BENCH_FLAGS", 0)
-
-    def step():
-        ne, w = ctx.replay_device(body.data_ptr(), body.numel(), n, 33,
-                                  events.data_ptr(), n_ev, L.F_PROFILE | xflags,
-                                  stream_base=s0)
-        assert ne == n_ev
-        prof = ctx.last_profile()
-        launches = prof["launches"]
-        if world > 1:
-            ctx.stats_export(mine.data_ptr())
-            dist.all_gather_into_tensor(gathered, mine)
-            merged_ctx.stats_merge(gathered.data_ptr(), world)
-            launches += 3
-        return prof, launches, w
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    t0.record(stream)
-    profs, launches = [], 0
-    for _ in range(args.steps):
-        p, l, w = step()
-        profs.append(p)
-        launches += l
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    value = world * records * args.steps / (ms / 1e3)
-
-    emit_ms = statistics.mean(p["emit_ms"] for p in profs)
-    count_ms = statistics.mean(p["count_ms"] for p in profs)
+    merged_ctx = T.Context(local, stream.cuda_stream) if world > 1 else None
     peak, peak_kind = measured_peaks()
-    achieved = alg_bytes / (emit_ms / 1e3) / 1e9
-    traffic = None
-    # (the committed ncu capture is of the full config-4 emit kernel: other
-    # workloads report no traffic figure)
-    tp = os.path.join(ROOT, "profiles", "ncu_emit_traffic.json")
-    if not nested and n == S.MIXED_FULL_STREAMS and os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+
+    # ---- headline config ---------------------------------------------------
+    d = Decode(args.config, ctx, merged_ctx, world, rank, dev, args.streams)
+    ms, profs, launches, clk = d.timed(args.steps, args.warmup, stream, dev, True, local)
+    full = not args.streams
+    head = d.summary(ms, profs, args.steps, peak, peak_kind,
+                     traffic_of("ncu_emit_traffic.json" if args.config == 4 else
+                                "ncu_emit_traffic_config5.json") if full and world == 1
+                     else None)
+    digest = stats_digest(d.stats())
+    nccl = None
+    if world > 1:
+        nccl = {"backend": dist.get_backend(), "nccl_version":
+                ".".join(map(str, torch.cuda.nccl.version())),
+                "collectives_per_step": 1,
+                "collective": "all_gather_into_tensor of the packed per-label tables "
+                              f"({d.packed} B per rank)"}
 
     # ---- end to end through the reference-facing call (host buffers) -------
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0 and not nested:
+    base_host = None
+    if not args.no_e2e and args.e2e_steps > 0 and args.config == 4:
+        n = d.n
         hdr = b"KPFT" + (2).to_bytes(2, "little") + b"\0\0" + n.to_bytes(8, "little")
-        img = torch.empty(len(hdr) + body.numel(), dtype=torch.uint8, pin_memory=True)
+        img = torch.empty(len(hdr) + d.body.numel(), dtype=torch.uint8, pin_memory=True)
         img[:len(hdr)] = torch.frombuffer(bytearray(hdr), dtype=torch.uint8)
-        img[len(hdr):].copy_(body, non_blocking=False)
-        hev = torch.empty(n_ev * 32, dtype=torch.uint8, pin_memory=True)
+        img[len(hdr):].copy_(d.body, non_blocking=False)
+        hev = torch.empty(d.n_ev * 32, dtype=torch.uint8, pin_memory=True)
         lib = L.lib()
         ne, wr = C.c_uint64(), L.Warnings()
 
         def e2e_step():
             rc = lib.wgpf_replay_image(ctx.h, C.c_void_p(img.data_ptr()), img.numel(),
-                                       33, C.c_void_p(hev.data_ptr()), n_ev, 0,
-                                       C.byref(ne), C.byref(wr))
-            assert rc == 0 and ne.value == n_ev, (rc, ne.value)
-            st = ctx.stats()  # the step's result read back to the host
-            return st
+                                       RECORD_COST, C.c_void_p(hev.data_ptr()), d.n_ev,
+                                       0, C.byref(ne), C.byref(wr))
+            assert rc == 0 and ne.value == d.n_ev, (rc, ne.value)
+            return ctx.stats()  # the step's result read back to the host
 
         e2e_step()
         if world > 1:
@@ -355,22 +517,42 @@ def main():
             t = torch.tensor([sec], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             sec = float(t.item())
-        e2e = {"value": world * records / sec, "unit": "records/s",
-               "h2d_bytes_per_step": int(img.numel()),
-               "d2h_bytes_per_step": int(n_ev * 32 + packed),
-               "ms_per_step": sec * 1e3}
+        e2e = {"value": d.records_total / sec, "unit": "records/s",
+               "h2d_bytes_per_step": int(img.numel()) * world,
+               "d2h_bytes_per_step": int(d.n_ev * 32 + d.packed) * world,
+               "ms_per_step": sec * 1e3, "host_memory": "pinned",
+               "call": "wgpf_replay_image (KPFT v2 image in host memory -> host events)"}
         base_host = img[len(hdr):].numpy()
-    else:
-        base_host = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not nested:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == 4:
+        from paper_2505_21661_b200 import workloads as S
         if base_host is None:
-            base_host = body[: min(n, 1 << 20) * stride].cpu().numpy()
-        cpu = cpu_baseline(base_host, len(base_host) // stride, args.cpu_budget_s)
+            base_host = d.body[: min(d.n, 1 << 20) * d.stride].cpu().numpy()
+        cpu = cpu_baseline(base_host, len(base_host) // d.stride, args.cpu_budget_s,
+                           S.MIXED_LABELS, S.CAP, 1, 221.5)
+    d.free()
+    del d
+    torch.cuda.empty_cache()
+
+    # ---- config 5 sub-line -------------------------------------------------
+    c5 = None
+    if args.config == 4 and not args.no_config5 and not args.streams:
+        d5 = Decode(5, ctx, merged_ctx, world, rank, dev)
+        ms5, profs5, launches5, _ = d5.timed(args.steps, args.warmup, stream, dev,
+                                             False, local)
+        c5 = d5.summary(ms5, profs5, args.steps, peak, peak_kind,
+                        traffic_of("ncu_emit_traffic_config5.json") if world == 1
+                        else None)
+        c5["workload"] = WORKLOAD5
+        c5["stats_digest"] = stats_digest(d5.stats())
+        c5["gpu_launches"] = launches5
+        d5.free()
+        del d5
+        torch.cuda.empty_cache()
 
     p1line = None
-    if rank == 0 and world == 1 and not args.no_p1 and not nested:
+    if rank == 0 and world == 1 and not args.no_p1 and args.config == 4:
         # config 2 in the same run: instrumented tcgen05 GEMM 8192^3
         import bench_p1
         p1line = bench_p1.measure(iters=20, warmup=5, decode=False, sass=False)
@@ -381,31 +563,29 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "records/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "metric": METRIC, "value": head["value"], "unit": "records/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "u32/u64 (integer trace records)", "data": "synthetic",
-            "config": {"workload": WORKLOAD5 if nested else WORKLOAD, "streams_per_gpu": n,
-                       "records_per_gpu": records, "events_per_gpu": n_ev,
-                       "parallelism": f"dp{world} (block-range shards, one NCCL "
-                                      "all-gather of per-label tables per step)",
-                       "l2": f"inputs larger than L2 ({body.numel() / 1e9:.1f} GB body, "
-                             f"{n_ev * 32 / 1e9:.1f} GB events per GPU)"},
-            "gbs": alg_bytes / (ms_step / 1e3) / 1e9,
-            "hbm_frac_step": alg_bytes / (ms_step / 1e3) / 1e9 / peak,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "emit phase (k_tps + k_fast_emit list)",
-                         "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel_ms": emit_ms, "peak_kind": peak_kind},
-            "phases_ms": {"count": count_ms,
-                          "scan": statistics.mean(p["scan_ms"] for p in profs),
-                          "emit": emit_ms,
-                          "general": statistics.mean(p["general_ms"] for p in profs),
-                          "finalize": statistics.mean(p["finalize_ms"] for p in profs)},
-            "general_streams": profs[-1]["general_streams"],
+            "config": {"workload": WORKLOAD5 if args.config == 5 else WORKLOAD,
+                       "streams_total": head["streams_total"],
+                       "records_total": head["records_total"],
+                       "streams_per_gpu_rank0": head["streams_per_gpu"],
+                       "records_per_gpu_rank0": head["records_per_gpu"],
+                       "events_per_gpu_rank0": head["events_per_gpu"],
+                       "parallelism": f"dp{world}: contiguous block-range shards of one "
+                                      "trace, one NCCL all-gather of the per-label "
+                                      "tables per step" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (8.6 GB body, 17.0 GB events in "
+                             "total)"},
+            "gbs": head["gbs_step_rank0"], "hbm_frac_step": head["hbm_frac_step"],
+            "roofline": head["roofline"], "phases_ms": head["phases_ms"],
+            "general_streams": head["general_streams"],
+            "stats_digest": digest, "nccl": nccl,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": launches,
+            "config5": c5,
             "instr_overhead_pct": p1line["value"] if p1line else None,
             "p1": p1line,
         }

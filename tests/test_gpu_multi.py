@@ -1,0 +1,159 @@
+"""GPU test of the multi-GPU shard-and-reduce path with the product's own
+export / merge (pipeline.hpp:69-80 loops streams with no
+cross-stream state).
+
+Two processes share cuda:0 (the driver's boxes have one GPU); each owns a
+contiguous block range of ONE synthetic trace (shard.stream_range), replays
+it on the device (wgpf_replay_device with its global stream base), exports its
+packed per-label table (wgpf_stats_export), the tables are all-gathered --
+host-staged over gloo, the same bytes NCCL moves in bench.py -- and
+wgpf_stats_merge combines them.  The merged table must equal, byte for byte,
+the table of one process replaying the whole trace, and bench.stats_digest
+must agree.
+"""
+import os
+import queue
+import socket
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _setup(shape, total):
+    from paper_2505_21661_b200 import trace as T
+    from paper_2505_21661_b200 import workloads as W
+    if shape == W.NESTED:
+        plan = T.BufferPlan(W.CAP, T.BufferStrategy.Circular, W.NESTED_LABELS)
+        n_long = 0
+    else:
+        plan = T.BufferPlan(W.CAP, T.BufferStrategy.Flush, W.MIXED_LABELS)
+        n_long = total // 3
+    return plan, n_long
+
+
+def _replay_range(ctx, shape, s0, s1, n_long):
+    import torch
+    from paper_2505_21661_b200 import workloads as W
+    n = s1 - s0
+    body = torch.empty(max(1, n) * W.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), shape, s0, n, n_long)
+    ev = torch.empty(max(1, n) * W.CAP * 32, dtype=torch.uint8, device="cuda")
+    ne, w = ctx.replay_device(body.data_ptr(), body.numel(), n, 33, ev.data_ptr(),
+                              n * W.CAP, 0, stream_base=s0)
+    return ne, w
+
+
+def _rank_main(rank, world, port, shape, total, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+    import bench
+    from paper_2505_21661_b200 import shard
+    from paper_2505_21661_b200 import trace as T
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan, n_long = _setup(shape, total)
+        ctx = T.Context(0)
+        merged = T.Context(0)
+        ctx.set_plan(plan)
+        merged.set_plan(plan)
+        s0, s1 = shard.stream_range(total, 16, world, rank)
+        ne, w = _replay_range(ctx, shape, s0, s1, n_long)
+        pb = ctx.stats_packed_bytes()
+        mine = torch.zeros(pb, dtype=torch.uint8, device="cuda")
+        ctx.stats_export(mine.data_ptr())
+        host = mine.cpu()
+        gathered = torch.empty(pb * world, dtype=torch.uint8)
+        dist.all_gather_into_tensor(gathered, host)
+        dg = gathered.cuda()
+        merged.stats_merge(dg.data_ptr(), world)
+        out = torch.zeros(pb, dtype=torch.uint8, device="cuda")
+        merged.stats_export(out.data_ptr())
+        torch.cuda.synchronize()
+        q.put((rank, (out.cpu().numpy().tobytes(), bench.stats_digest(merged.stats()),
+                      ne, (w.dropped_heads, w.truncated_tails,
+                           w.flagged_preconditions, w.malformed_groups))))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world, shape, total):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, shape, total, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        try:
+            k, v = q.get(timeout=300)
+        except queue.Empty:
+            break
+        res[k] = v
+    for p in procs:
+        p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+        assert p.exitcode == 0
+    assert len(res) == world
+    return res
+
+
+@pytest.mark.parametrize("shape,total", [(0, 16 * 1024), (0, 16 * 101),
+                                         (1, 16 * 256)])
+def test_two_process_export_merge_equals_single_shot(shape, total):
+    import torch
+    import bench
+    from paper_2505_21661_b200 import trace as T
+    res = _run_world(2, shape, total)
+    # single shot: the whole trace in one replay
+    plan, n_long = _setup(shape, total)
+    ctx = T.Context(0)
+    ctx.set_plan(plan)
+    ne, w = _replay_range(ctx, shape, 0, total, n_long)
+    pb = ctx.stats_packed_bytes()
+    one = torch.zeros(pb, dtype=torch.uint8, device="cuda")
+    ctx.stats_export(one.data_ptr())
+    torch.cuda.synchronize()
+    single = one.cpu().numpy().tobytes()
+    for r in range(2):
+        packed, digest, _, _ = res[r]
+        assert packed == single, f"rank {r}: merged table != single-shot table"
+        assert digest == bench.stats_digest(ctx.stats())
+    # events and warnings are sums over the shards
+    assert res[0][2] + res[1][2] == ne
+    ws = tuple(a + b for a, b in zip(res[0][3], res[1][3]))
+    assert ws == (w.dropped_heads, w.truncated_tails, w.flagged_preconditions,
+                  w.malformed_groups)
+
+
+def test_bench_refuses_more_gpus_than_the_box_has():
+    """--gpus N on a box with fewer GPUs fails loudly (non-zero exit)."""
+    import subprocess
+    import sys
+    import torch
+    n = torch.cuda.device_count() + 1
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus",
+                        str(n), "--steps", "1", "--warmup", "0", "--streams", "1024",
+                        "--no-e2e", "--no-cpu-baseline", "--no-p1", "--no-config5"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode != 0
+    assert "cannot run here" in (r.stdout + r.stderr)

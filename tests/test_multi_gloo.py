@@ -159,3 +159,37 @@ def test_gloo_world2_shard_and_merge_equals_single(oracle):
         assert [int(x) for x in row[6:]] == s.hist
         assert int(row[5]) == s.warp_group
         assert int(row[4]) & 1 == (1 if s.kind == "wait" else 0)
+
+
+def test_bench_self_launches_ranks_for_the_reference_arm():
+    """bench.py --gpus 2 outside torchrun re-launches itself with 2 ranks
+    (torch.distributed.run); rank 0 alone runs the reference arm and prints
+    the one JSON line, the other rank exits 0."""
+    import json
+    import subprocess
+    import sys
+    from oracle import oracle as O
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl",
+                        "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+                        "--ref-budget-s", "0.1"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["single_core"]["cores"] == 1 and cb["nproc"] >= 1 and cb["cpu_model"]
+    # whole rounds of equal chunks: no half-idle last wave
+    assert d["config"]["sample_streams"] % cb["cores"] == 0
+
+
+def test_bench_world_size_mismatch_fails():
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr

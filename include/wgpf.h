@@ -271,6 +271,82 @@ int wgpf_export_chrome_trace(wgpf_ctx* ctx, const wgpf_event* events, uint64_t n
 int wgpf_format_json_double(double x, char* out, uint64_t cap);
 
 /* ----------------------------------------------------------------------- */
+/* P1 host helpers (the device runtime is include/wgpf_device.cuh)          */
+/* ----------------------------------------------------------------------- */
+
+/* HBM bytes the flushed profile of a grid needs: ctas x streams_per_cta x
+ * (16-byte stream header + 8 x slots) -- the KPFT body Engine::image
+ * (vgpu.hpp:136-148) copies out.  Host arithmetic, no device needed. */
+uint64_t wgpf_profile_bytes(uint64_t ctas, uint32_t streams_per_cta,
+                            uint64_t slots);
+
+/*
+ * Engine::image (vgpu.hpp:136-148) for a device profile: the n_streams-stream
+ * body the kernels flushed to d_profile, checked and copied out as a KPFT
+ * image (v1 when n_streams <= 65,535 -- readable by the reference's
+ * deserialize_image -- else v2).  Checks, in the reference's order:
+ *  - d_validate (optional, the error word of debug-mode recorders,
+ *    wgpf_dev::Recorder<..., kValidate>): the first pairing violation of the
+ *    lowest stream -> WGPF_E_INSTRUMENT with validate_record_pairing's text
+ *    (instrument.hpp:60-105);
+ *  - plan strategy Flush and record_count > slot_capacity (the recorder kept
+ *    the first capacity records and counted the rest) -> WGPF_E_CAPACITY
+ *    "wg<k>: flush buffer overflow after <cap> records" (vgpu.hpp:261-265).
+ * out == NULL only checks and reports *n_bytes.
+ */
+int wgpf_collect(wgpf_ctx* ctx, const void* d_profile, uint64_t n_streams,
+                 const uint64_t* d_validate, uint8_t* out, uint64_t cap,
+                 uint64_t* n_bytes);
+
+/* A scope program: per stream role (warp / warp group) a body of record and
+ * loop ops, the device counterpart of the KernelProgram bodies lower() reads
+ * (ir.hpp Instruction kinds Record / LoopBegin / LoopEnd). */
+#define WGPF_OP_START 0u   /* record start "label"              */
+#define WGPF_OP_END 1u     /* record end "label"                */
+#define WGPF_OP_LOOP 2u    /* for <trips> {                     */
+#define WGPF_OP_ENDLOOP 3u /* }                                 */
+typedef struct wgpf_scope_op {
+  uint32_t op;
+  uint32_t pad;
+  uint64_t trips;    /* WGPF_OP_LOOP */
+  const char* label; /* WGPF_OP_START / WGPF_OP_END */
+} wgpf_scope_op;
+
+typedef struct wgpf_lower_cfg { /* LoweringConfig, lower.hpp:44-55 */
+  const char* name;             /* kernel name (validate messages) */
+  uint32_t strategy;            /* WGPF_STRATEGY_CIRCULAR / _FLUSH */
+  int signature_bits;           /* signature_bits_enabled */
+  int iteration_signature;      /* iteration_signature */
+  int global_buffer;            /* BufferType::Global: no smem check */
+  uint64_t slots_total;         /* buffer_slots_total, 0 = from the program */
+  uint64_t smem_capacity;       /* KernelProgram::shared_mem_capacity */
+} wgpf_lower_cfg;
+
+typedef struct wgpf_lowered {
+  uint64_t slots_per_stream;   /* BufferPlan::slots_per_warp_group */
+  uint64_t smem_bytes_per_cta; /* device layout: streams x (16 + 8 x slots) */
+  uint32_t n_regions;          /* region table size (ids 0 .. n-1) */
+  uint32_t pad;
+} wgpf_lowered;
+
+/*
+ * lower() (lower.hpp:220-301) of a scope program: the loop / record checks of
+ * validate (ir.hpp:347-390, WGPF_E_VALIDATE), validate_record_pairing
+ * (instrument.hpp:60-105, WGPF_E_INSTRUMENT), the signature-mode conflict
+ * (WGPF_E_LOWER), dense region ids in first-appearance order
+ * (region_of_op[i] for every op, ~0 for loop ops; the region table is the
+ * labels in id order), the buffer plan (flush: the largest dynamic record
+ * count; circular: plan_slots; explicit slots_total must divide by the
+ * stream count) and the shared-memory budget (WGPF_E_CAPACITY), with the
+ * reference's messages in err.  ops holds the bodies back to back.  Host
+ * code, no device needed.
+ */
+int wgpf_lower_scopes(const wgpf_scope_op* ops, const uint32_t* body_len,
+                      uint32_t n_bodies, const wgpf_lower_cfg* cfg,
+                      uint32_t* region_of_op, wgpf_lowered* out, char* err,
+                      uint64_t err_cap);
+
+/* ----------------------------------------------------------------------- */
 /* Synthetic trace generator (bench / tests)    */
 /* ----------------------------------------------------------------------- */
 

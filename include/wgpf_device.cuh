@@ -30,6 +30,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "wgpf_format.h"
 
@@ -93,15 +94,46 @@ __host__ __device__ constexpr uint32_t make_tag(bool start, uint32_t region,
   return (start ? WGPF_START_FLAG : 0u) | (region << 12) | (sig & WGPF_SIGNATURE_MASK);
 }
 
-// One recording stream (a warp or a warp group).  kPow2: capacity is a power
-// of two (mask wrap); otherwise compare-and-reset.
-template <bool kPow2 = true>
+// Debug-mode pairing validation (the device form of validate_record_pairing,
+// instrument.hpp:60-105): error codes of the first violation a stream meets.
+// The 64-bit error word is stream << 32 | code << 24 | region, combined with
+// atomicMin so the lowest stream's first violation wins (the reference checks
+// wg 0 first); wgpf_collect turns it into the reference's message.
+enum : uint32_t {
+  kVErrEndMismatch = 1,       // record end "X" does not match the innermost open start
+  kVErrPairCrossesLoop = 2,   // record pair "X" crosses a loop boundary
+  kVErrStartCrossesLoop = 3,  // record start "X" crosses a loop boundary
+  kVErrNeverClosed = 4,       // record start "X" is never closed
+};
+constexpr uint32_t kVDepth = 32;  // open scopes a validating recorder tracks
+
+struct NoValidate {};
+struct Validate {
+  uint32_t stk[kVDepth];  // region | loop depth << 24
+  uint32_t top;           // open scopes
+  uint32_t depth;         // loop depth
+  uint32_t stream;        // global stream index (error key)
+  unsigned long long* err;
+  bool failed;
+};
+
+// One recording stream (a warp or a warp group).
+//   kPow2      capacity is a power of two (mask wrap); otherwise compare-and-reset
+//   kFlush     BufferStrategy::Flush: slots are never overwritten; writes past the
+//              capacity are counted (record_count > capacity), which wgpf_collect
+//              reports as the reference's capacity-error (vgpu.hpp:261-265)
+//   kValidate  debug mode: check the pairing rules of instrument.hpp:60-105 as the
+//              records execute (loops marked with wgpf_dev::Loop)
+template <bool kPow2 = true, bool kFlush = false, bool kValidate = false>
 struct Recorder {
   uint32_t base;   // shared address of this stream's slot 0
   uint32_t mask;   // cap - 1 (kPow2) / cap (else)
   uint32_t writes; // total writes (record_count)
-  uint32_t slot;   // current slot (non-pow2 only)
+  uint32_t slot;   // current slot (non-pow2 circular only)
+  uint32_t sig;    // signature bits stamped into every tag (0, signature_for,
+                   // or the loop index -- LoweringConfig, lower.hpp:44-52)
   bool leader;     // the lane that stores
+  std::conditional_t<kValidate, Validate, NoValidate> v;
 
   // InitOp: smem_buf = the CTA's buffer, stream = this warp's stream index in
   // the CTA.  Index state lives in registers (vgpu.hpp:216-219).
@@ -112,60 +144,178 @@ struct Recorder {
     mask = kPow2 ? cap - 1u : cap;
     writes = 0;
     slot = 0;
+    sig = 0;
     leader = is_leader;
   }
+
+  // debug mode: where violations go (global stream index, error word)
+  __device__ __forceinline__ void validate_into(unsigned long long* err,
+                                                uint32_t global_stream) {
+    if constexpr (kValidate) {
+      v.top = 0;
+      v.depth = 0;
+      v.stream = global_stream;
+      v.err = err;
+      v.failed = false;
+    }
+  }
+
+  // signature_bits_enabled: the stream's hardware-id signature (vgpu.hpp:245-246)
+  __device__ __forceinline__ void hw_signature(uint32_t stream_id) {
+    sig = signature_for(stream_id);
+  }
+  // iteration_signature: the innermost loop's iteration index (vgpu.hpp:247-251)
+  __device__ __forceinline__ void iteration(uint32_t i) { sig = i & WGPF_SIGNATURE_MASK; }
 
   // ReadCounter + StoreCounter.  The clock is read before anything else
   // (vgpu.hpp:220-223, the reference charges the record cost after capture).
   template <bool kStart>
-  __device__ __forceinline__ void record(uint32_t region, uint32_t sig = 0) {
+  __device__ __forceinline__ void record(uint32_t region) {
     const uint32_t clk = clock32();
+    check<kStart>(region);
     put(make_tag(kStart, region, sig), clk);
   }
-
-  __device__ __forceinline__ void start(uint32_t region, uint32_t sig = 0) {
-    record<true>(region, sig);
+  template <bool kStart>
+  __device__ __forceinline__ void record(uint32_t region, uint32_t sig_bits) {
+    const uint32_t clk = clock32();
+    check<kStart>(region);
+    put(make_tag(kStart, region, sig_bits), clk);
   }
-  __device__ __forceinline__ void end(uint32_t region, uint32_t sig = 0) {
-    record<false>(region, sig);
+
+  __device__ __forceinline__ void start(uint32_t region) { record<true>(region); }
+  __device__ __forceinline__ void end(uint32_t region) { record<false>(region); }
+  __device__ __forceinline__ void start(uint32_t region, uint32_t s) {
+    record<true>(region, s);
+  }
+  __device__ __forceinline__ void end(uint32_t region, uint32_t s) {
+    record<false>(region, s);
   }
 
   // END(end_region) immediately followed by START(start_region): the two
   // RecordOps of a scope boundary (wait -> issue, issue -> next wait) share
   // one clock capture -- same records, half the critical-path cost there.
-  __device__ __forceinline__ void mark(uint32_t end_region, uint32_t start_region,
-                                       uint32_t sig = 0) {
+  __device__ __forceinline__ void mark(uint32_t end_region, uint32_t start_region) {
     const uint32_t clk = clock32();
+    check<false>(end_region);
     put(make_tag(false, end_region, sig), clk);
+    check<true>(start_region);
     put(make_tag(true, start_region, sig), clk);
   }
 
   // StoreCounter: slot writes % cap (circular) -- vgpu.hpp:240-273
   __device__ __forceinline__ void put(uint32_t tag, uint32_t clk) {
     uint32_t s;
-    if constexpr (kPow2) {
+    bool keep = leader;
+    if constexpr (kFlush) {
+      s = writes;
+      keep = keep && (kPow2 ? writes <= mask : writes < mask);
+    } else if constexpr (kPow2) {
       s = writes & mask;
     } else {
       s = slot;
       slot = (slot + 1u == mask) ? 0u : slot + 1u;
     }
     const uint32_t addr = base + 8u * s;
-    if (leader)
+    if (keep)
       asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(tag),
                    "r"(clk)
                    : "memory");
     ++writes;
   }
 
-  // Stream header (done by the leader before the CTA flush).
+  // Stream header (done by the leader before the CTA flush).  Two 8-byte
+  // stores: with an odd capacity the per-stream stride 16 + 8 * cap is only
+  // 8-byte aligned.
   __device__ __forceinline__ void close(uint32_t block_index,
                                         uint32_t stream_id, uint32_t cap) {
+    if constexpr (kValidate) {
+      if (v.top && !v.failed) fail(kVErrNeverClosed, v.stk[v.top - 1] & 0xFFFFFFu);
+    }
     if (leader) {
       const uint32_t h = base - kStreamHdr;
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(h),
-                   "r"(block_index), "r"(stream_id), "r"(writes), "r"(cap)
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(h), "r"(block_index),
+                   "r"(stream_id)
+                   : "memory");
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(h + 8u), "r"(writes),
+                   "r"(cap)
                    : "memory");
     }
+  }
+
+  // ---- debug-mode pairing checks (instrument.hpp:60-105) ------------------
+  __device__ __forceinline__ void fail(uint32_t code, uint32_t region) {
+    if constexpr (kValidate) {
+      v.failed = true;
+      if (leader && v.err)
+        atomicMin(v.err, ((unsigned long long)v.stream << 32) |
+                             ((unsigned long long)code << 24) | region);
+    }
+  }
+  template <bool kStart>
+  __device__ __forceinline__ void check(uint32_t region) {
+    if constexpr (kValidate) {
+      if (v.failed) return;
+      if (kStart) {
+        if (v.top == kVDepth) {  // deeper than tracked: stop validating
+          v.failed = true;
+          return;
+        }
+        v.stk[v.top++] = region | (v.depth << 24);
+      } else {
+        const uint32_t t = v.top ? v.stk[v.top - 1] : ~0u;
+        if (!v.top || (t & 0xFFFFFFu) != region) {
+          fail(kVErrEndMismatch, region);
+        } else if ((t >> 24) != v.depth) {
+          fail(kVErrPairCrossesLoop, region);
+        } else {
+          --v.top;
+        }
+      }
+    }
+  }
+  // loop boundaries (wgpf_dev::Loop): the end of an iteration is the
+  // reference's LoopEnd -- a start opened at this depth must be closed by then
+  __device__ __forceinline__ void loop_begin() {
+    if constexpr (kValidate) ++v.depth;
+  }
+  __device__ __forceinline__ void loop_iteration_end() {
+    if constexpr (kValidate) {
+      if (!v.failed && v.top && (v.stk[v.top - 1] >> 24) == v.depth)
+        fail(kVErrStartCrossesLoop, v.stk[v.top - 1] & 0xFFFFFFu);
+    }
+  }
+  __device__ __forceinline__ void loop_end() {
+    if constexpr (kValidate) {
+      loop_iteration_end();
+      --v.depth;
+    }
+  }
+};
+
+// An instrumented loop: stamps the iteration index into the signature bits
+// when the recorder runs in iteration-signature mode (the caller sets it with
+// iteration(); the outer loop's index comes back when the loop ends,
+// vgpu.hpp:247-251 uses the innermost loop), and marks the loop boundaries for
+// debug-mode validation.
+//   { wgpf_dev::Loop<Rec> L(rec, iter_sig);  for (i...) { L.next(i); ... } }
+template <class Rec>
+struct Loop {
+  Rec& rec;
+  uint32_t saved;
+  bool stamp;
+  bool first = true;
+  __device__ __forceinline__ Loop(Rec& r, bool iteration_signature)
+      : rec(r), saved(r.sig), stamp(iteration_signature) {
+    rec.loop_begin();
+  }
+  __device__ __forceinline__ void next(uint32_t i) {
+    if (!first) rec.loop_iteration_end();
+    first = false;
+    if (stamp) rec.iteration(i);
+  }
+  __device__ __forceinline__ ~Loop() {
+    rec.loop_end();
+    rec.sig = saved;
   }
 };
 
@@ -173,13 +323,20 @@ struct Recorder {
 // kernel source compiled with NullRecorder records nothing and costs nothing,
 // which is how T_vanilla of the overhead metric is measured.
 struct NullRecorder {
+  uint32_t sig = 0;
   __device__ __forceinline__ void init(void*, uint32_t, uint32_t, bool) {}
+  __device__ __forceinline__ void validate_into(unsigned long long*, uint32_t) {}
+  __device__ __forceinline__ void hw_signature(uint32_t) {}
+  __device__ __forceinline__ void iteration(uint32_t) {}
   template <bool kStart>
   __device__ __forceinline__ void record(uint32_t, uint32_t = 0) {}
   __device__ __forceinline__ void start(uint32_t, uint32_t = 0) {}
   __device__ __forceinline__ void end(uint32_t, uint32_t = 0) {}
-  __device__ __forceinline__ void mark(uint32_t, uint32_t, uint32_t = 0) {}
+  __device__ __forceinline__ void mark(uint32_t, uint32_t) {}
   __device__ __forceinline__ void close(uint32_t, uint32_t, uint32_t) {}
+  __device__ __forceinline__ void loop_begin() {}
+  __device__ __forceinline__ void loop_iteration_end() {}
+  __device__ __forceinline__ void loop_end() {}
 };
 
 // ---- the instrumentation pass, as source-level helpers ---------------------
@@ -238,15 +395,24 @@ __device__ __forceinline__ void async_region(Rec& rec, uint32_t x, uint32_t xw, 
 }
 
 // FinalizeOp: after every stream of the CTA has closed (barrier), copy the
-// CTA's buffer to HBM with 16-byte vector stores by all participating threads
-// (coalesced; the buffer is a contiguous KPFT body segment).
+// CTA's buffer to HBM with vector stores by all participating threads
+// (coalesced; the buffer is a contiguous KPFT body segment).  16-byte stores
+// when the segment size is a multiple of 16 (even capacities or an even
+// stream count), else 8-byte stores (the segment, and its HBM offset, are
+// then only 8-byte aligned).
 __device__ __forceinline__ void flush(const void* smem_buf, void* profile_mem,
                                       uint64_t cta_linear, uint32_t bytes,
                                       uint32_t tid, uint32_t nthreads) {
-  const uint4* src = reinterpret_cast<const uint4*>(smem_buf);
-  uint4* dst = reinterpret_cast<uint4*>(static_cast<uint8_t*>(profile_mem) +
-                                        cta_linear * (uint64_t)bytes);
-  for (uint32_t i = tid; i < bytes / 16u; i += nthreads) dst[i] = src[i];
+  uint8_t* dst8 = static_cast<uint8_t*>(profile_mem) + cta_linear * (uint64_t)bytes;
+  if ((bytes & 15u) == 0) {
+    const uint4* src = reinterpret_cast<const uint4*>(smem_buf);
+    uint4* dst = reinterpret_cast<uint4*>(dst8);
+    for (uint32_t i = tid; i < bytes / 16u; i += nthreads) dst[i] = src[i];
+  } else {
+    const uint2* src = reinterpret_cast<const uint2*>(smem_buf);
+    uint2* dst = reinterpret_cast<uint2*>(dst8);
+    for (uint32_t i = tid; i < bytes / 8u; i += nthreads) dst[i] = src[i];
+  }
 }
 
 }  // namespace wgpf_dev

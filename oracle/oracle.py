@@ -616,6 +616,32 @@ class Reference:
                                           out_prefix.encode(), C.byref(st))
         st.raise_if()
 
+    def lower_kir(self, kir: str, strategy: int, slots_total: int = 0,
+                  signature_bits: bool = False, iteration_signature: bool = False,
+                  global_buffer: bool = False, simulate: bool = False,
+                  out_prefix: str = "") -> dict:
+        """lower() (lower.hpp:220) of KIR text, optionally simulate()
+        (vgpu.hpp:424): {'slots', 'labels'[, 'image', 'store_log']}; raises
+        RefError with the reference's kind and message."""
+        import tempfile
+        L = self.lib
+        L.ref_lower_kir.argtypes = [C.c_char_p, C.c_uint32, C.c_uint64, C.c_int, C.c_int,
+                                    C.c_int, C.c_int, C.c_char_p, C.POINTER(_RStatus)]
+        with tempfile.TemporaryDirectory() as d:
+            pre = os.path.join(d, "p")
+            st = _RStatus()
+            L.ref_lower_kir(kir.encode(), strategy, slots_total, int(signature_bits),
+                            int(iteration_signature), int(global_buffer), int(simulate),
+                            pre.encode(), C.byref(st))
+            st.raise_if()
+            lines = open(pre + ".plan").read().split("\n")
+            out = {"slots": int(lines[0]), "labels": [l for l in lines[1:-1]]}
+            if simulate:
+                out["image"] = open(pre + ".kpft", "rb").read()
+                out["store_log"] = [[int(t, 16) for t in line.split()]
+                                    for line in open(pre + ".log").read().split("\n")[:-1]]
+            return out
+
     def bench_replay(self, body: np.ndarray, n_streams: int, slots: int,
                      strategy: int, labels, record_cost: int, chunk_streams: int,
                      nthreads: int) -> dict:

@@ -575,6 +575,52 @@ int ref_random_program_image(uint64_t seed, int index, int with_loop,
   return st->code;
 }
 
+// lower() (lower.hpp:220-301) of a KIR text program (ir.hpp:540
+// parse_program) under a LoweringConfig, and optionally simulate() it
+// (vgpu.hpp:424).  Writes <out_prefix>.plan ("<slots>\n" then one region
+// label per line, id order) and, when simulating, <out_prefix>.kpft (the
+// vGPU's image) and <out_prefix>.log (the store log: per warp group one line
+// of hex tags, vgpu.hpp:269-271).
+int ref_lower_kir(const char* kir, uint32_t strategy, uint64_t slots_total,
+                  int signature_bits, int iteration_signature, int global_buffer,
+                  int simulate, const char* out_prefix, ref_status* st) {
+  set_ok(st);
+  try {
+    auto p = R::parse_program(kir);
+    R::LoweringConfig cfg;
+    cfg.buffer_strategy =
+        strategy == 0 ? R::BufferStrategy::Circular : R::BufferStrategy::Flush;
+    cfg.buffer_slots_total = slots_total;
+    cfg.signature_bits_enabled = signature_bits != 0;
+    cfg.iteration_signature = iteration_signature != 0;
+    cfg.buffer_type = global_buffer ? R::BufferType::Global : R::BufferType::Shared;
+    auto dp = R::lower(p, cfg);
+    const std::string pre(out_prefix);
+    std::string plan = std::to_string(dp.plan.slots_per_warp_group) + "\n";
+    for (const auto& l : dp.plan.region_labels) plan += l + "\n";
+    R::write_file(pre + ".plan", plan);
+    if (simulate) {
+      auto sim = R::simulate(dp, R::MachineConfig{});
+      R::write_file(pre + ".kpft", R::serialize_image(sim.image));
+      std::string log;
+      char hex[16];
+      for (const auto& wg : sim.store_log) {
+        for (const auto& r : wg) {
+          snprintf(hex, sizeof hex, "%08x ", r.tag);
+          log += hex;
+        }
+        log += "\n";
+      }
+      R::write_file(pre + ".log", log);
+    }
+  } catch (const R::Error& e) {
+    set_err(st, e);
+  } catch (const std::exception& e) {
+    set_other(st, e);
+  }
+  return st->code;
+}
+
 // ---------------------------------------------------------------------------
 // CPU baseline harness: the reference functions, unmodified, over disjoint
 // <= 65535-stream KPFT v1 chunks, with harness-level parallelism over

@@ -38,6 +38,7 @@ def _nvcc() -> str:
 def sources() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) +
                   glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.inc")) +
                   glob.glob(os.path.join(INCLUDE, "*.h")))
 
 

@@ -71,6 +71,26 @@ class Overlap(C.Structure):
 
 F_PROFILE = 0x10
 
+
+class ScopeOp(C.Structure):
+    _fields_ = [("op", C.c_uint32), ("pad", C.c_uint32), ("trips", C.c_uint64),
+                ("label", C.c_char_p)]
+
+
+class LowerCfg(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("strategy", C.c_uint32),
+                ("signature_bits", C.c_int), ("iteration_signature", C.c_int),
+                ("global_buffer", C.c_int), ("slots_total", C.c_uint64),
+                ("smem_capacity", C.c_uint64)]
+
+
+class Lowered(C.Structure):
+    _fields_ = [("slots_per_stream", C.c_uint64), ("smem_bytes_per_cta", C.c_uint64),
+                ("n_regions", C.c_uint32), ("pad", C.c_uint32)]
+
+
+OP_START, OP_END, OP_LOOP, OP_ENDLOOP = 0, 1, 2, 3
+
 _lock = threading.Lock()
 _lib = None
 
@@ -121,6 +141,11 @@ def lib() -> C.CDLL:
                                           C.POINTER(u64)], i32),
             "wgpf_overlap_counters": ([vp, vp, u64, i32, vp, u32,
                                        C.POINTER(Overlap)], i32),
+            "wgpf_profile_bytes": ([u64, u32, u64], u64),
+            "wgpf_collect": ([vp, vp, u64, vp, vp, u64, C.POINTER(u64)], i32),
+            "wgpf_lower_scopes": ([C.POINTER(ScopeOp), C.POINTER(u32), u32,
+                                   C.POINTER(LowerCfg), C.POINTER(u32),
+                                   C.POINTER(Lowered), C.c_char_p, u64], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

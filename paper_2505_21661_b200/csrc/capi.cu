@@ -1800,3 +1800,4 @@ extern "C" int wgpf_synth_body(wgpf_ctx* c, void* d_body, uint32_t shape,
 
 #include "capi_cp.inc"
 #include "capi_chrome.inc"
+#include "capi_p1.inc"

@@ -118,7 +118,177 @@ __global__ void k_record_cost(uint32_t n, uint64_t* cycles, uint32_t* sink) {
   if (x == 0xFFFFFFFFu) sink[0] = x;
 }
 
+// ---- scope-program interpreter ------------------------------------------------
+// Runs a lowered scope program (p1.lower_scopes -> p1.program_encoding): warp
+// w of every CTA executes body w -- START / END record ops, loops, ALU busy
+// work -- through Recorder<kPow2, kFlush, kValidate>, with the loop boundaries
+// and iteration signatures of wgpf_dev::Loop (the interpreter keeps its own
+// loop stack, so it calls the Recorder's loop hooks directly, exactly as Loop
+// does).  The vGPU analogue is Engine::step over a lowered body
+// (vgpu.hpp:206-238, LoopBegin / LoopEnd :366-381).
+constexpr uint32_t kProgLoops = 8;
+
+template <bool kPow2, bool kFlush, bool kValidate>
+__global__ void k_program(uint8_t* profile, uint32_t cap, const uint2* ops,
+                          const uint32_t* body_off, uint32_t sig_mode,
+                          unsigned long long* verr, uint32_t* sink) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t nwarps = blockDim.x >> 5;
+  const uint32_t bytes = wgpf_dev::smem_bytes(nwarps, cap);
+  // deterministic images: unwritten slots read as zero (as the vGPU's)
+  for (uint32_t i = threadIdx.x; i < bytes / 8u; i += blockDim.x)
+    reinterpret_cast<uint2*>(buf)[i] = make_uint2(0, 0);
+  __syncthreads();
+  wgpf_dev::Recorder<kPow2, kFlush, kValidate> rec;
+  rec.init(buf, warp, cap, lane == 0);
+  rec.validate_into(verr, blockIdx.x * nwarps + warp);
+  if (sig_mode == 1) rec.hw_signature(warp);
+  const uint2* b = ops + body_off[warp];
+  const uint32_t n = body_off[warp + 1] - body_off[warp];
+  uint32_t lpc[kProgLoops], lrem[kProgLoops], lit[kProgLoops], lsig[kProgLoops];
+  uint32_t top = 0;
+  uint32_t x = threadIdx.x + 7u * blockIdx.x;
+  for (uint32_t pc = 0; pc < n;) {
+    const uint2 o = b[pc];
+    switch (o.x) {
+      case 0:
+        rec.start(o.y);
+        ++pc;
+        break;
+      case 1:
+        rec.end(o.y);
+        ++pc;
+        break;
+      case 2:  // LoopBegin
+        lpc[top] = pc + 1;
+        lrem[top] = o.y;
+        lit[top] = 0;
+        lsig[top] = rec.sig;
+        ++top;
+        rec.loop_begin();
+        if (sig_mode == 2) rec.iteration(0);
+        ++pc;
+        break;
+      case 3: {  // LoopEnd
+        const uint32_t t = top - 1;
+        if (--lrem[t] > 0) {
+          rec.loop_iteration_end();
+          ++lit[t];
+          if (sig_mode == 2) rec.iteration(lit[t]);
+          pc = lpc[t];
+        } else {
+          rec.loop_end();
+          rec.sig = lsig[t];
+          --top;
+          ++pc;
+        }
+        break;
+      }
+      default:
+        x = busy(x, o.y);
+        ++pc;
+        break;
+    }
+  }
+  rec.close(blockIdx.x, warp, cap);
+  __syncthreads();
+  wgpf_dev::flush(buf, profile, blockIdx.x, bytes, threadIdx.x, blockDim.x);
+  if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
+// ---- loop-entry cost (vgpu.hpp:366-369; "+5 instructions") -------
+// n entries of an inner loop of `trips` iterations (a runtime value: not
+// unrolled), with or without a START/END pair in the inner body.  Per-warp
+// cycles T(n, trips) = n (E + trips B): two runs, (n, 1) and (n / 2, 2), give
+// the per-entry cost E = 2 (T(n, 1) - T(n / 2, 2)) / n, and the
+// instrumentation's loop-entry cost is E(records) - E(no records).
+template <bool kRecord>
+__global__ void k_loop_entry(uint32_t n, uint32_t trips, uint64_t* cycles,
+                             uint32_t* sink) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  wgpf_dev::Recorder<true> rec;
+  rec.init(buf, warp, 256, lane == 0);
+  uint32_t x = threadIdx.x;
+  __syncwarp();
+  const uint64_t t0 = clock64();
+  for (uint32_t e = 0; e < n; ++e) {
+#pragma unroll 1
+    for (uint32_t i = 0; i < trips; ++i) {
+      if constexpr (kRecord) rec.start(1);
+      x = x * 1664525u + 1013904223u;
+      if constexpr (kRecord) rec.end(1);
+    }
+    x ^= e;
+  }
+  __syncwarp();
+  const uint64_t t1 = clock64();
+  if (lane == 0) cycles[blockIdx.x * (blockDim.x >> 5) + warp] = t1 - t0;
+  if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
 }  // namespace
+
+template <bool P, bool F, bool V>
+static int launch_program(void* d_profile, uint32_t ctas, uint32_t nb, uint32_t cap,
+                          uint32_t sig_mode, const void* ops, const void* offs,
+                          void* verr, cudaStream_t st, uint32_t* sink) {
+  const uint32_t smem = wgpf_dev::smem_bytes(nb, cap);
+  cudaFuncSetAttribute(k_program<P, F, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
+  k_program<P, F, V><<<ctas, nb * 32, smem, st>>>(
+      static_cast<uint8_t*>(d_profile), cap, static_cast<const uint2*>(ops),
+      static_cast<const uint32_t*>(offs), sig_mode,
+      static_cast<unsigned long long*>(verr), sink);
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
+
+// runs a lowered scope program (see k_program); d_verr: the 64-bit error word
+// of debug-mode recorders (initialised to ~0 by the caller), or null
+extern "C" int wgpf_p1_run_program(void* d_profile, uint32_t ctas, uint32_t n_bodies,
+                                   uint32_t cap, int flush, int validate,
+                                   uint32_t sig_mode, const void* d_ops,
+                                   const void* d_offs, void* d_verr, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  if (!cap || !n_bodies || n_bodies > 32) return 11;
+  if (validate && !d_verr) return 11;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool pow2 = !(cap & (cap - 1));
+  const int k = (pow2 ? 1 : 0) | (flush ? 2 : 0) | (validate ? 4 : 0);
+#define WGPF_PROG(P, F, V)                                                     \
+  launch_program<P, F, V>(d_profile, ctas, n_bodies, cap, sig_mode, d_ops, d_offs, \
+                          d_verr, st, sink)
+  switch (k) {
+    case 0: return WGPF_PROG(false, false, false);
+    case 1: return WGPF_PROG(true, false, false);
+    case 2: return WGPF_PROG(false, true, false);
+    case 3: return WGPF_PROG(true, true, false);
+    case 4: return WGPF_PROG(false, false, true);
+    case 5: return WGPF_PROG(true, false, true);
+    case 6: return WGPF_PROG(false, true, true);
+    default: return WGPF_PROG(true, true, true);
+  }
+#undef WGPF_PROG
+}
+
+extern "C" int wgpf_p1_loop_entry(uint32_t n, uint32_t trips, uint32_t warps,
+                                  int record, void* d_cycles, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t smem = wgpf_dev::smem_bytes(warps, 256);
+  auto* cyc = static_cast<uint64_t*>(d_cycles);
+  if (record) {
+    cudaFuncSetAttribute(k_loop_entry<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    k_loop_entry<true><<<1, warps * 32, smem, st>>>(n, trips, cyc, sink);
+  } else {
+    k_loop_entry<false><<<1, warps * 32, smem, st>>>(n, trips, cyc, sink);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
 
 // the selftest program instrumented through the pass helpers (pow2 caps)
 extern "C" int wgpf_p1_selftest_auto(void* d_profile, uint32_t ctas,

@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -67,6 +68,11 @@ def lib() -> C.CDLL:
         L.wgpf_attn_profile_bytes.restype = u64
         L.wgpf_attn_smem_bytes.argtypes = [i32, i32]
         L.wgpf_attn_smem_bytes.restype = u32
+        L.wgpf_p1_run_program.argtypes = [vp, u32, u32, u32, i32, i32, u32, vp, vp, vp,
+                                          vp]
+        L.wgpf_p1_run_program.restype = i32
+        L.wgpf_p1_loop_entry.argtypes = [u32, u32, u32, i32, vp, vp]
+        L.wgpf_p1_loop_entry.restype = i32
         _lib = L
     return _lib
 
@@ -208,3 +214,147 @@ def signature_for(wg: int) -> int:
     """MachineConfig::signature_for (vgpu.hpp:39-45), packed (trace.hpp:42-46):
     the 12 signature bits of stream wg's tags (wgpf_dev::signature_for)."""
     return (wg % 32) | (((wg // 32) % 16) << 5) | (((wg // 512) % 8) << 9)
+
+
+# ---- lowering of a scope program (lower.hpp:220-301) ---------------------------
+
+@dataclass
+class ScopePlan:
+    """lower()'s result for a scope program: the BufferPlan fields and, per
+    body, the dense region id of every op (None for loop ops)."""
+    slots_per_stream: int
+    labels: list
+    region_ids: list
+    smem_bytes_per_cta: int
+
+
+def _scope_ops(bodies):
+    from . import _lib as L
+    flat, lens, keep = [], [], []
+    for body in bodies:
+        lens.append(len(body))
+        for o in body:
+            kind = o[0]
+            if kind in ("start", "end"):
+                lab = o[1].encode()
+                keep.append(lab)
+                flat.append(L.ScopeOp(L.OP_START if kind == "start" else L.OP_END, 0, 0,
+                                      lab))
+            elif kind == "loop":
+                flat.append(L.ScopeOp(L.OP_LOOP, 0, int(o[1]), None))
+            elif kind == "endloop":
+                flat.append(L.ScopeOp(L.OP_ENDLOOP, 0, 0, None))
+            else:
+                raise ValueError(f"unknown scope op {o!r}")
+    return flat, lens, keep
+
+
+def lower_scopes(bodies, strategy, smem_capacity: int, slots_total: int = 0,
+                 signature_bits: bool = False, iteration_signature: bool = False,
+                 global_buffer: bool = False, name: str = "kernel") -> ScopePlan:
+    """lower() of a scope program (C-ABI wgpf_lower_scopes): bodies[k] is
+    stream role k's op list -- ("start", label), ("end", label),
+    ("loop", trips), ("endloop",).  Raises trace.Error with the reference's
+    kind and message (ir.hpp:347-390 loop checks, instrument.hpp:60-105
+    pairing, lower.hpp:223-279 configuration, ids, slots, smem budget)."""
+    from . import _lib as L
+    from .trace import BufferStrategy, Error, ErrorKind
+    flat, lens, _keep = _scope_ops(bodies)
+    n = len(flat)
+    ops = (L.ScopeOp * max(1, n))(*flat)
+    blen = (C.c_uint32 * max(1, len(lens)))(*lens)
+    rid = (C.c_uint32 * max(1, n))()
+    cfg = L.LowerCfg(name.encode(), int(BufferStrategy(strategy)), int(signature_bits),
+                     int(iteration_signature), int(global_buffer), slots_total,
+                     smem_capacity)
+    out = L.Lowered()
+    err = C.create_string_buffer(1024)
+    rc = L.lib().wgpf_lower_scopes(ops, blen, len(lens), C.byref(cfg), rid, C.byref(out),
+                                   err, 1024)
+    if rc != 0:
+        if 1 <= rc <= 9:
+            raise Error(ErrorKind(rc - 1), err.value.decode())
+        raise RuntimeError(err.value.decode())
+    labels = [None] * out.n_regions
+    per_body, k = [], 0
+    for body in bodies:
+        ids = []
+        for o in body:
+            r = rid[k]
+            k += 1
+            if o[0] in ("start", "end"):
+                labels[r] = o[1]
+                ids.append(r)
+            else:
+                ids.append(None)
+        per_body.append(ids)
+    return ScopePlan(out.slots_per_stream, labels, per_body, out.smem_bytes_per_cta)
+
+
+# device interpreter ops (csrc_p1/p1_selftest.cu k_program)
+PROG_START, PROG_END, PROG_LOOP, PROG_ENDLOOP, PROG_BUSY = 0, 1, 2, 3, 4
+SIG_NONE, SIG_HW, SIG_ITER = 0, 1, 2
+
+
+def program_encoding(bodies, plan: ScopePlan, busy: int = 0):
+    """(ops u32[n, 2], body offsets u32[n_bodies + 1]) of a lowered scope
+    program for the device interpreter; `busy` inserts that many ALU steps
+    after every record (so scopes have a duration)."""
+    ops, offs = [], [0]
+    for body, ids in zip(bodies, plan.region_ids):
+        for o, r in zip(body, ids):
+            if o[0] == "start":
+                ops.append((PROG_START, r))
+            elif o[0] == "end":
+                ops.append((PROG_END, r))
+            elif o[0] == "loop":
+                ops.append((PROG_LOOP, int(o[1])))
+            else:
+                ops.append((PROG_ENDLOOP, 0))
+            if busy and o[0] in ("start", "end"):
+                ops.append((PROG_BUSY, busy))
+        offs.append(len(ops))
+    return (np.array(ops, np.uint32).reshape(-1, 2), np.array(offs, np.uint32))
+
+
+def run_program(profile_ptr: int, ctas: int, n_bodies: int, cap: int, flush: bool,
+                validate: bool, sig_mode: int, d_ops_ptr: int, d_offs_ptr: int,
+                d_err_ptr: int = 0, stream: int = 0) -> None:
+    """Runs a lowered scope program on the device: every CTA runs one warp per
+    body through wgpf_dev::Recorder<pow2, flush, validate> (loops through
+    wgpf_dev::Loop), then flushes its buffer (a KPFT body segment)."""
+    _check(lib().wgpf_p1_run_program(C.c_void_p(profile_ptr), ctas, n_bodies, cap,
+                                     int(flush), int(validate), sig_mode,
+                                     C.c_void_p(d_ops_ptr), C.c_void_p(d_offs_ptr),
+                                     C.c_void_p(d_err_ptr), C.c_void_p(stream)),
+           "wgpf_p1_run_program")
+
+
+def loop_entry_cycles(n: int, trips: int, warps: int, record: bool, cycles_ptr: int,
+                      stream: int = 0) -> None:
+    """Loop-entry microbenchmark (vgpu.hpp:366-369): per-warp cycles of n
+    entries of an inner loop of `trips` iterations, with or without a
+    START/END pair in the inner body (csrc_p1/p1_selftest.cu k_loop_entry)."""
+    _check(lib().wgpf_p1_loop_entry(n, trips, warps, int(record), C.c_void_p(cycles_ptr),
+                                    C.c_void_p(stream)), "wgpf_p1_loop_entry")
+
+
+def loop_entry_cost(n: int = 1 << 14, warps: int = 4) -> dict:
+    """Per-entry cost of entering an instrumented loop, in cycles: E = 2 (T(n,
+    1) - T(n/2, 2)) / n per variant; the instrumentation's loop-entry cost is
+    E(records) - E(plain) (the reference charges 5, vgpu.hpp:366-369)."""
+    import torch
+    out = {}
+    for rec in (False, True):
+        t = []
+        for (m, trips) in ((n, 1), (n // 2, 2)):
+            c = torch.zeros(warps, dtype=torch.int64, device="cuda")
+            loop_entry_cycles(m, trips, warps, rec, c.data_ptr())
+            loop_entry_cycles(m, trips, warps, rec, c.data_ptr())
+            torch.cuda.synchronize()
+            t.append(c.double().mean().item())
+        out["records" if rec else "plain"] = {
+            "entry": 2 * (t[0] - t[1]) / n, "body": (2 * t[1] - t[0]) / n}
+    out["loop_entry_cost_cycles"] = out["records"]["entry"] - out["plain"]["entry"]
+    out["record_pair_cycles_in_loop"] = out["records"]["body"] - out["plain"]["body"]
+    return out

@@ -652,6 +652,22 @@ class Context:
                                                        buf, ln.value + 1, C.byref(ln)))
         return buf.raw[:ln.value].decode()
 
+    def collect(self, profile_ptr: int, n_streams: int, validate_ptr: int = 0) -> bytes:
+        """Engine::image (vgpu.hpp:136-148) of a device profile: the flushed
+        KPFT body checked (debug-mode pairing errors -> instrument-error,
+        flush overflow -> capacity-error, the reference's texts) and copied
+        out as a KPFT image (v1 up to 65,535 streams, else v2)."""
+        n = C.c_uint64()
+        _check(self.h, self.L.wgpf_collect(self.h, C.c_void_p(profile_ptr), n_streams,
+                                           C.c_void_p(validate_ptr), None, 0,
+                                           C.byref(n)))
+        buf = np.empty(n.value, np.uint8)
+        _check(self.h, self.L.wgpf_collect(self.h, C.c_void_p(profile_ptr), n_streams,
+                                           C.c_void_p(validate_ptr),
+                                           C.c_void_p(buf.ctypes.data), n.value,
+                                           C.byref(n)))
+        return buf.tobytes()
+
     def synth_body(self, dst_ptr: int, shape: int, stream0: int, n_streams: int,
                    n_long: int) -> None:
         _check(self.h, self.L.wgpf_synth_body(self.h, C.c_void_p(dst_ptr), shape,

@@ -212,6 +212,14 @@ uint64_t wgpf_stats_packed_bytes(const wgpf_ctx* ctx);
 int wgpf_stats_export(wgpf_ctx* ctx, void* d_dst);
 int wgpf_stats_merge(wgpf_ctx* ctx, const void* d_gathered, uint32_t n_ranks);
 
+/* The same combination in one call over NCCL: export, one ncclAllGather of
+ * the packed tables on the context stream (NVLink / NVSwitch), merge -- the
+ * path's single collective.  nccl_comm is an ncclComm_t of
+ * the participating ranks (ncclCommInitRank, or a framework's communicator);
+ * afterwards every rank holds the whole trace's statistics.  libnccl.so.2 is
+ * resolved at run time, so C / C++ hosts need no torch. */
+int wgpf_allreduce_stats(wgpf_ctx* ctx, void* nccl_comm);
+
 /* ----------------------------------------------------------------------- */
 /* Interval-overlap analysis (K6)                                            */
 /* ----------------------------------------------------------------------- */

@@ -26,15 +26,30 @@
 
 #include <algorithm>
 #include <array>
+#include <cctype>
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <map>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <sstream>
 #include <string>
+#include <string_view>
 #include <unordered_map>
 #include <vector>
+
+// nlohmann/json (the reference's one third-party dependency, trace.hpp:10
+// includes it as <json.hpp>) for make_replay_report when it is on the path
+#if __has_include(<nlohmann/json.hpp>)
+#include <nlohmann/json.hpp>
+#define WGPROF_B200_HAVE_JSON 1
+#elif __has_include(<json.hpp>)
+#include <json.hpp>
+#define WGPROF_B200_HAVE_JSON 1
+#endif
 
 #include "wgpf.h"
 
@@ -274,6 +289,38 @@ inline void put_u32(std::vector<std::uint8_t>& o, std::uint32_t v) {
   for (int i = 0; i < 4; ++i) o.push_back((v >> (8 * i)) & 0xFF);
 }
 
+// An in-memory image as a KPFT v2 container (u64 stream count) for the
+// C-ABI: the reference's decode_image / replay_image take the image in
+// memory and never serialise it, so the v1 u16 count limit must not apply.
+template <class Img>
+inline std::vector<std::uint8_t> pack_image(const Img& img) {
+  std::size_t bytes = 16;
+  for (const auto& s : img.streams) bytes += 16 + 8 * s.slots.size();
+  std::vector<std::uint8_t> out;
+  out.reserve(bytes);
+  const std::uint64_t n = img.streams.size();
+  for (char c : {'K', 'P', 'F', 'T'}) out.push_back(static_cast<std::uint8_t>(c));
+  out.push_back(2);
+  out.push_back(0);
+  out.push_back(0);
+  out.push_back(0);
+  for (int i = 0; i < 8; ++i) out.push_back(static_cast<std::uint8_t>(n >> (8 * i)));
+  for (const auto& s : img.streams) {
+    if (s.slots.size() != s.slot_capacity)
+      throw Error(ErrorKind::Trace,
+                  "stream slot count does not match its declared capacity");
+    put_u32(out, s.block_index);
+    put_u32(out, s.warp_group);
+    put_u32(out, s.record_count);
+    put_u32(out, s.slot_capacity);
+    for (const auto& r : s.slots) {
+      put_u32(out, r.tag);
+      put_u32(out, r.payload);
+    }
+  }
+  return out;
+}
+
 }  // namespace b200
 
 // ---------------------------------------------------------------------------
@@ -351,7 +398,7 @@ inline GlobalTraceImage deserialize_image(const std::vector<std::uint8_t>& bytes
 inline std::vector<DecodedStream> decode_image(const GlobalTraceImage& img,
                                                const BufferPlan& plan) {
   b200::set_plan(plan.slots_per_warp_group, plan.strategy, plan.region_labels);
-  const auto bytes = serialize_image(img);
+  const auto bytes = b200::pack_image(img);
   std::size_t total = 0;
   for (const auto& s : img.streams) total += s.slot_capacity;
   std::vector<wgpf_record> recs(total + 1);
@@ -442,7 +489,7 @@ inline TraceReplay replay_image(const GlobalTraceImage& image,
                                 const BufferPlan& plan,
                                 std::uint64_t record_cost) {
   b200::set_plan(plan.slots_per_warp_group, plan.strategy, plan.region_labels);
-  const auto bytes = serialize_image(image);
+  const auto bytes = b200::pack_image(image);
   std::size_t cap = 1;
   for (const auto& s : image.streams) cap += s.slot_capacity / 2 + 1;
   std::vector<wgpf_event> ev(cap);
@@ -758,5 +805,490 @@ inline CriticalPathResult analyze_critical_path(
     return r;
   }
 }
+
+
+// ---------------------------------------------------------------------------
+// Device programs (lower.hpp:74-140, the `.dev` text of
+// print_device_program lower.hpp:320-371) and the program-driven
+// analyze_critical_path (perfmodel.hpp:242-318) -- what the reference CLI's
+// replay / export / decode commands (tools/wgprof.cpp:70-126) take.  Host
+// code.  The hot path behind them is the GPU replay above.
+// ---------------------------------------------------------------------------
+enum class InstrKind { SyncCompute, AsyncLaunch, AsyncWait, BarrierArrive, BarrierWait,
+                       LoopBegin, LoopEnd, Record };
+struct Instruction {
+  InstrKind kind{};
+  std::string unit;
+  std::optional<std::uint64_t> latency;
+  std::string label;
+  std::uint64_t trip_count = 0;
+  std::string barrier;
+  std::string token;
+  bool is_start = false;
+  bool operator==(const Instruction&) const = default;
+};
+struct BarrierDecl {
+  std::string name;
+  std::uint32_t expected_arrivals = 1;
+  bool operator==(const BarrierDecl&) const = default;
+};
+enum class MetricType { Clock };
+enum class Granularity { WarpGroup, Warp, Thread };
+enum class BufferType { Shared, Stack, Global };
+struct LoweringConfig {
+  MetricType metric_type = MetricType::Clock;
+  Granularity granularity = Granularity::WarpGroup;
+  BufferType buffer_type = BufferType::Shared;
+  BufferStrategy buffer_strategy = BufferStrategy::Circular;
+  std::uint64_t buffer_slots_total = 0;
+  bool signature_bits_enabled = false;
+  bool iteration_signature = false;
+  bool operator==(const LoweringConfig&) const = default;
+};
+enum class DeviceOpKind { Base, Init, ReadCounter, StoreCounter, Finalize };
+struct DeviceInstr {
+  DeviceOpKind op = DeviceOpKind::Base;
+  Instruction base;
+  std::uint32_t reg = 0;
+  std::uint32_t region_id = 0;
+  bool is_start = false;
+  bool operator==(const DeviceInstr&) const = default;
+};
+struct DeviceProgram {
+  std::string name;
+  std::uint32_t num_warp_groups = 1;
+  std::uint64_t shared_mem_capacity = 0;
+  std::vector<BarrierDecl> barriers;
+  std::vector<std::vector<DeviceInstr>> bodies;
+  BufferPlan plan;
+  LoweringConfig config;
+  bool operator==(const DeviceProgram&) const = default;
+};
+
+// pipeline.hpp:28-55
+inline std::string read_file(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw Error(ErrorKind::Io, "cannot open '" + path + "'");
+  std::ostringstream os;
+  os << is.rdbuf();
+  return os.str();
+}
+inline void write_file(const std::string& path, const std::string& data) {
+  const std::filesystem::path p(path);
+  if (p.has_parent_path()) std::filesystem::create_directories(p.parent_path());
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw Error(ErrorKind::Io, "cannot write '" + path + "'");
+  os.write(data.data(), static_cast<std::streamsize>(data.size()));
+}
+inline void write_file(const std::string& path, const std::vector<std::uint8_t>& data) {
+  write_file(path, std::string(data.begin(), data.end()));
+}
+
+namespace b200 {
+
+// Tokens of the device-program text: identifiers (letters, digits, '_', '.'),
+// decimal numbers, "strings" (\n and \<c> escapes), { } = ->; '#' comments.
+// Errors are parse-errors "<line>:<col>: <message>" like the reference's
+// lexer (ir.hpp:166-170).
+struct DevTok {
+  enum Kind { Ident, Number, String, LBrace, RBrace, Equals, Arrow, Eof } kind = Eof;
+  std::string text;
+  std::uint64_t number = 0;
+  int line = 1, col = 1;
+};
+
+[[noreturn]] inline void parse_fail(const DevTok& t, const std::string& msg) {
+  throw Error(ErrorKind::Parse, std::to_string(t.line) + ":" + std::to_string(t.col) +
+                                    ": " + msg);
+}
+
+inline std::vector<DevTok> dev_tokens(std::string_view src) {
+  std::vector<DevTok> out;
+  int line = 1, col = 1;
+  std::size_t i = 0;
+  auto step = [&]() {
+    if (src[i] == '\n') {
+      ++line;
+      col = 1;
+    } else {
+      ++col;
+    }
+    ++i;
+  };
+  for (;;) {
+    while (i < src.size()) {
+      if (src[i] == '#') {
+        while (i < src.size() && src[i] != '\n') step();
+      } else if (src[i] == ' ' || src[i] == '\t' || src[i] == '\r' || src[i] == '\n') {
+        step();
+      } else {
+        break;
+      }
+    }
+    DevTok t;
+    t.line = line;
+    t.col = col;
+    if (i >= src.size()) {
+      out.push_back(t);
+      return out;
+    }
+    const char c = src[i];
+    if (c == '{' || c == '}' || c == '=') {
+      t.kind = c == '{' ? DevTok::LBrace : c == '}' ? DevTok::RBrace : DevTok::Equals;
+      step();
+    } else if (c == '-' && i + 1 < src.size() && src[i + 1] == '>') {
+      t.kind = DevTok::Arrow;
+      step();
+      step();
+    } else if (c == '"') {
+      step();
+      while (i < src.size() && src[i] != '"') {
+        char d = src[i];
+        if (d == '\\' && i + 1 < src.size()) {
+          step();
+          d = src[i] == 'n' ? '\n' : src[i];
+        } else if (d == '\n') {
+          parse_fail(t, "unterminated string literal");
+        }
+        t.text.push_back(d);
+        step();
+      }
+      if (i >= src.size()) parse_fail(t, "unterminated string literal");
+      step();
+      t.kind = DevTok::String;
+    } else if (std::isdigit(static_cast<unsigned char>(c))) {
+      while (i < src.size() && std::isdigit(static_cast<unsigned char>(src[i]))) {
+        t.number = t.number * 10 + static_cast<std::uint64_t>(src[i] - '0');
+        t.text.push_back(src[i]);
+        step();
+      }
+      t.kind = DevTok::Number;
+    } else if (std::isalpha(static_cast<unsigned char>(c)) || c == '_') {
+      while (i < src.size() && (std::isalnum(static_cast<unsigned char>(src[i])) ||
+                                src[i] == '_' || src[i] == '.')) {
+        t.text.push_back(src[i]);
+        step();
+      }
+      t.kind = DevTok::Ident;
+    } else {
+      parse_fail(t, std::string("unexpected character '") + c + "'");
+    }
+    out.push_back(std::move(t));
+  }
+}
+
+class DevParser {
+ public:
+  explicit DevParser(std::string_view text) : t_(dev_tokens(text)) {}
+  const DevTok& peek(std::size_t k = 0) const {
+    return t_[std::min(p_ + k, t_.size() - 1)];
+  }
+  DevTok take() {
+    DevTok t = peek();
+    if (p_ < t_.size() - 1) ++p_;
+    return t;
+  }
+  DevTok want(DevTok::Kind k, const char* what) {
+    if (peek().kind != k) parse_fail(peek(), std::string("expected ") + what);
+    return take();
+  }
+  std::string keyword(const char* kw) {
+    DevTok t = want(DevTok::Ident, (std::string("'") + kw + "'").c_str());
+    if (t.text != kw) parse_fail(t, std::string("expected '") + kw + "'");
+    return t.text;
+  }
+  std::uint64_t number_attr(const char* key) {
+    DevTok k = want(DevTok::Ident, (std::string("'") + key + "'").c_str());
+    if (k.text != key) parse_fail(k, std::string("expected '") + key + "'");
+    want(DevTok::Equals, "'='");
+    return want(DevTok::Number, (std::string("value of '") + key + "'").c_str()).number;
+  }
+  // key=value pairs up to the first token that does not start one
+  std::vector<std::pair<std::string, DevTok>> attrs() {
+    std::vector<std::pair<std::string, DevTok>> kv;
+    while (peek().kind == DevTok::Ident && peek(1).kind == DevTok::Equals) {
+      std::string key = take().text;
+      take();
+      DevTok v = take();
+      if (v.kind != DevTok::Ident && v.kind != DevTok::Number && v.kind != DevTok::String)
+        parse_fail(v, "expected attribute value");
+      kv.emplace_back(std::move(key), std::move(v));
+    }
+    return kv;
+  }
+  static const DevTok* find(const std::vector<std::pair<std::string, DevTok>>& kv,
+                            const char* key) {
+    for (const auto& [k, v] : kv)
+      if (k == key) return &v;
+    return nullptr;
+  }
+  std::string ident_attr(const std::vector<std::pair<std::string, DevTok>>& kv,
+                         const DevTok& at, const char* key, const char* ctx) {
+    const DevTok* v = find(kv, key);
+    if (!v) parse_fail(at, std::string(ctx) + " requires attribute '" + key + "'");
+    if (v->kind != DevTok::Ident)
+      parse_fail(*v, std::string("attribute '") + key + "' must be an identifier");
+    return v->text;
+  }
+  std::optional<std::uint64_t> opt_number(
+      const std::vector<std::pair<std::string, DevTok>>& kv, const char* key) {
+    const DevTok* v = find(kv, key);
+    if (!v) return std::nullopt;
+    if (v->kind != DevTok::Number)
+      parse_fail(*v, std::string("attribute '") + key + "' must be an integer");
+    return v->number;
+  }
+  static std::string opt_string(const std::vector<std::pair<std::string, DevTok>>& kv,
+                                const char* key) {
+    const DevTok* v = find(kv, key);
+    return v ? v->text : std::string();
+  }
+  std::uint32_t reg(const DevTok& r) {
+    if (r.text.size() < 2 || r.text[0] != 'r') parse_fail(r, "expected register r<k>");
+    return static_cast<std::uint32_t>(std::stoul(r.text.substr(1)));
+  }
+
+  void body(std::vector<DeviceInstr>& out) {
+    for (;;) {
+      const DevTok& t = peek();
+      if (t.kind == DevTok::RBrace) {
+        take();
+        return;
+      }
+      if (t.kind == DevTok::Eof) parse_fail(t, "unexpected end of input inside a block");
+      if (t.kind != DevTok::Ident) parse_fail(t, "expected an instruction");
+      const DevTok kw = take();
+      DeviceInstr d;
+      if (kw.text == "init") {
+        d.op = DeviceOpKind::Init;
+      } else if (kw.text == "finalize") {
+        d.op = DeviceOpKind::Finalize;
+      } else if (kw.text == "read_counter") {
+        want(DevTok::Arrow, "'->'");
+        d.op = DeviceOpKind::ReadCounter;
+        d.reg = reg(want(DevTok::Ident, "register"));
+      } else if (kw.text == "store_counter") {
+        d.op = DeviceOpKind::StoreCounter;
+        d.reg = reg(want(DevTok::Ident, "register"));
+        d.region_id = static_cast<std::uint32_t>(number_attr("region"));
+        const DevTok se = want(DevTok::Ident, "'start' or 'end'");
+        if (se.text != "start" && se.text != "end") parse_fail(se, "expected 'start' or 'end'");
+        d.is_start = se.text == "start";
+      } else if (kw.text == "for") {
+        d.base.kind = InstrKind::LoopBegin;
+        d.base.trip_count = want(DevTok::Number, "loop trip count").number;
+        d.base.label = opt_string(attrs(), "label");
+        want(DevTok::LBrace, "'{'");
+        out.push_back(std::move(d));
+        body(out);
+        DeviceInstr e;
+        e.base.kind = InstrKind::LoopEnd;
+        out.push_back(std::move(e));
+        continue;
+      } else if (kw.text == "compute" || kw.text == "async_launch") {
+        const auto kv = attrs();
+        d.base.kind = kw.text == "compute" ? InstrKind::SyncCompute : InstrKind::AsyncLaunch;
+        d.base.unit = ident_attr(kv, kw, "unit", kw.text.c_str());
+        if (kw.text == "async_launch") d.base.token = ident_attr(kv, kw, "token", "async_launch");
+        d.base.latency = opt_number(kv, "latency");
+        d.base.label = opt_string(kv, "label");
+      } else if (kw.text == "async_wait") {
+        const auto kv = attrs();
+        d.base.kind = InstrKind::AsyncWait;
+        d.base.token = ident_attr(kv, kw, "token", "async_wait");
+      } else if (kw.text == "arrive" || kw.text == "wait") {
+        d.base.kind = kw.text == "arrive" ? InstrKind::BarrierArrive : InstrKind::BarrierWait;
+        d.base.barrier = want(DevTok::Ident, "barrier name").text;
+      } else if (kw.text == "record") {
+        const DevTok se = want(DevTok::Ident, "'start' or 'end'");
+        d.base.kind = InstrKind::Record;
+        d.base.label = want(DevTok::String, "quoted region name").text;
+        d.base.is_start = se.text == "start";
+      } else {
+        parse_fail(kw, "unknown instruction '" + kw.text + "'");
+      }
+      out.push_back(std::move(d));
+    }
+  }
+
+  DeviceProgram program() {
+    keyword("device");
+    keyword("kernel");
+    DeviceProgram dp;
+    dp.name = want(DevTok::Ident, "kernel name").text;
+    dp.num_warp_groups = static_cast<std::uint32_t>(number_attr("wgs"));
+    dp.shared_mem_capacity = number_attr("smem");
+    keyword("strategy");
+    want(DevTok::Equals, "'='");
+    const DevTok st = want(DevTok::Ident, "strategy value");
+    if (st.text == "circular")
+      dp.plan.strategy = BufferStrategy::Circular;
+    else if (st.text == "flush")
+      dp.plan.strategy = BufferStrategy::Flush;
+    else
+      parse_fail(st, "strategy must be circular or flush");
+    dp.config.buffer_strategy = dp.plan.strategy;
+    dp.plan.slots_per_warp_group = number_attr("slots_per_wg");
+    dp.config.buffer_slots_total = dp.plan.slots_per_warp_group * dp.num_warp_groups;
+    dp.config.signature_bits_enabled = number_attr("signature") != 0;
+    dp.config.iteration_signature = number_attr("iter_sig") != 0;
+    want(DevTok::LBrace, "'{'");
+    dp.bodies.resize(dp.num_warp_groups);
+    std::uint32_t next_wg = 0;
+    for (;;) {
+      const DevTok t = take();
+      if (t.kind == DevTok::RBrace) break;
+      if (t.kind == DevTok::Eof) parse_fail(t, "unexpected end of input inside device kernel");
+      if (t.kind != DevTok::Ident) parse_fail(t, "expected 'region', 'barrier' or a wg block");
+      if (t.text == "region") {
+        const DevTok id = want(DevTok::Number, "region id");
+        const DevTok label = want(DevTok::String, "region label");
+        if (id.number != dp.plan.region_labels.size())
+          parse_fail(id, "region ids must be dense and ascending");
+        dp.plan.region_labels.push_back(label.text);
+      } else if (t.text == "barrier") {
+        BarrierDecl b;
+        b.name = want(DevTok::Ident, "barrier name").text;
+        b.expected_arrivals = static_cast<std::uint32_t>(number_attr("arrivals"));
+        dp.barriers.push_back(std::move(b));
+      } else if (t.text.size() > 2 && t.text.compare(0, 2, "wg") == 0) {
+        const std::uint32_t idx = static_cast<std::uint32_t>(std::stoul(t.text.substr(2)));
+        if (idx >= dp.num_warp_groups || idx != next_wg)
+          parse_fail(t, "warp group blocks must appear as wg0..wgN-1 in order");
+        ++next_wg;
+        want(DevTok::LBrace, "'{'");
+        body(dp.bodies[idx]);
+      } else {
+        parse_fail(t, "expected 'region', 'barrier' or a wg block");
+      }
+    }
+    if (next_wg != dp.num_warp_groups)
+      throw Error(ErrorKind::Parse, "device kernel is missing warp group bodies");
+    return dp;
+  }
+
+ private:
+  std::vector<DevTok> t_;
+  std::size_t p_ = 0;
+};
+
+}  // namespace b200
+
+// parse_device_program (lower.hpp:476-551): the `.dev` text back to a
+// DeviceProgram (plan, barriers, bodies).
+inline DeviceProgram parse_device_program(std::string_view text) {
+  return b200::DevParser(text).program();
+}
+
+namespace detail {
+// Barrier-derived candidate edges (perfmodel.hpp:258-313): for every barrier,
+// the region whose end store is the last one before an arrive gates the
+// region whose start store is the first one after a wait on it; sorted,
+// unique, no self edges.
+inline std::vector<std::pair<std::string, std::string>> barrier_edges(
+    const DeviceProgram& dp) {
+  std::vector<std::pair<std::string, std::string>> src, dst, out;  // (barrier, label)
+  auto label = [&](std::uint32_t id) {
+    return id < dp.plan.region_labels.size() ? dp.plan.region_labels[id] : std::string();
+  };
+  for (std::uint32_t wg = 0; wg < dp.num_warp_groups && wg < dp.bodies.size(); ++wg) {
+    const auto& b = dp.bodies[wg];
+    for (std::size_t i = 0; i < b.size(); ++i) {
+      if (b[i].op != DeviceOpKind::Base) continue;
+      const InstrKind k = b[i].base.kind;
+      if (k == InstrKind::BarrierArrive) {
+        for (std::size_t j = i; j-- > 0;)
+          if (b[j].op == DeviceOpKind::StoreCounter && !b[j].is_start) {
+            const std::string l = label(b[j].region_id);
+            if (!l.empty()) src.emplace_back(b[i].base.barrier, l);
+            break;
+          }
+      } else if (k == InstrKind::BarrierWait) {
+        for (std::size_t j = i + 1; j < b.size(); ++j)
+          if (b[j].op == DeviceOpKind::StoreCounter && b[j].is_start) {
+            const std::string l = label(b[j].region_id);
+            if (!l.empty()) dst.emplace_back(b[i].base.barrier, l);
+            break;
+          }
+      }
+    }
+  }
+  for (const auto& a : src)
+    for (const auto& w : dst)
+      if (a.first == w.first && a.second != w.second) out.emplace_back(a.second, w.second);
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+  return out;
+}
+}  // namespace detail
+
+// CriticalPathAnalysis (perfmodel.hpp:242-246) and the reference's
+// analyze_critical_path(events, dp, opts) (perfmodel.hpp:317-318): the GPU
+// analysis with the program's barrier edges.
+struct CriticalPathAnalysis {
+  WsInput graph;
+  std::vector<std::string> cycle;
+  std::uint64_t period = 0;
+};
+inline CriticalPathAnalysis analyze_critical_path(const std::vector<TimelineEvent>& events,
+                                                  const DeviceProgram& dp,
+                                                  const CriticalPathOptions& opts = {}) {
+  CriticalPathResult r = analyze_critical_path(events, detail::barrier_edges(dp), opts);
+  CriticalPathAnalysis a;
+  a.graph = std::move(r.graph);
+  a.cycle = std::move(r.cycle);
+  a.period = r.period;
+  return a;
+}
+
+// The simulator totals the reports carry (vgpu.hpp:61-68); a replay of a
+// trace file has none (tools/wgprof.cpp:111).
+struct SimResult {
+  GlobalTraceImage image;
+  std::uint64_t total_cycles = 0;
+  std::uint64_t vanilla_cycles = 0;
+  std::uint64_t records_written = 0;
+  std::vector<std::vector<ProfileRecord>> store_log;
+};
+
+#ifdef WGPROF_B200_HAVE_JSON
+// make_replay_report (pipeline.hpp:146-178): the replay report from the GPU's
+// statistics (region_stats above) and critical path.
+inline nlohmann::ordered_json make_replay_report(const std::string& kernel,
+                                                 const SimResult& sim,
+                                                 const TraceReplay& tr,
+                                                 const CriticalPathAnalysis& cp,
+                                                 std::uint64_t record_cost) {
+  using J = nlohmann::ordered_json;
+  J rep;
+  rep["kernel"] = kernel;
+  rep["total_cycles"] = sim.total_cycles;
+  rep["vanilla_cycles"] = sim.vanilla_cycles;
+  rep["records_written"] = sim.records_written;
+  rep["record_cost"] = record_cost;
+  J regions = J::array();
+  for (const auto& [label, st] : region_stats(tr.events)) {
+    J r;
+    r["region"] = label;
+    r["warp_group"] = st.warp_group;
+    r["kind"] = st.kind == EventKind::Wait ? "wait" : "exec";
+    r["count"] = st.count;
+    r["mean_duration"] = st.mean;
+    r["min_duration"] = st.min;
+    r["max_duration"] = st.max;
+    regions.push_back(std::move(r));
+  }
+  rep["regions"] = std::move(regions);
+  rep["critical_path"] = cp.cycle.empty() ? ws_latency(cp.graph).critical_path : cp.cycle;
+  rep["iteration_period"] = cp.period;
+  J w;
+  w["dropped_heads"] = tr.dropped_heads;
+  w["truncated_tails"] = tr.truncated_tails;
+  w["flagged_preconditions"] = tr.flagged_preconditions;
+  w["malformed_groups"] = tr.malformed_groups;
+  rep["warnings"] = std::move(w);
+  return rep;
+}
+#endif
 
 }  // namespace wgprof

@@ -142,6 +142,7 @@ def lib() -> C.CDLL:
             "wgpf_overlap_counters": ([vp, vp, u64, i32, vp, u32,
                                        C.POINTER(Overlap)], i32),
             "wgpf_profile_bytes": ([u64, u32, u64], u64),
+            "wgpf_allreduce_stats": ([vp, vp], i32),
             "wgpf_collect": ([vp, vp, u64, vp, vp, u64, C.POINTER(u64)], i32),
             "wgpf_lower_scopes": ([C.POINTER(ScopeOp), C.POINTER(u32), u32,
                                    C.POINTER(LowerCfg), C.POINTER(u32),

@@ -131,6 +131,7 @@ struct wgpf_ctx {
   uint32_t* h_blk = nullptr;  // pinned: block fields read by stream_group
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
+  DevBuf d_nccl_send, d_nccl_recv;  // wgpf_allreduce_stats
   DevBuf d_dorph;  // k_tpsd: one orphan event per lane
   size_t smem_optin = 0;
   // pipelined replay_image (host buffers): copy streams, chunk buffers, and

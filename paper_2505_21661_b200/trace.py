@@ -525,6 +525,11 @@ class Context:
     def stats_export(self, dst_ptr: int) -> None:
         _check(self.h, self.L.wgpf_stats_export(self.h, C.c_void_p(dst_ptr)))
 
+    def allreduce_stats(self, nccl_comm: int) -> None:
+        """Combines this rank's statistics with every rank of an NCCL
+        communicator (wgpf_allreduce_stats: export, one ncclAllGather, merge)."""
+        _check(self.h, self.L.wgpf_allreduce_stats(self.h, C.c_void_p(nccl_comm)))
+
     def stats_merge(self, gathered_ptr: int, n_ranks: int) -> None:
         _check(self.h, self.L.wgpf_stats_merge(self.h, C.c_void_p(gathered_ptr),
                                                n_ranks))

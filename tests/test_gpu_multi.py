@@ -157,3 +157,43 @@ def test_bench_refuses_more_gpus_than_the_box_has():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode != 0
     assert "cannot run here" in (r.stdout + r.stderr)
+
+
+def test_allreduce_stats_over_nccl_single_rank():
+    """wgpf_allreduce_stats (export -> ncclAllGather -> merge) on a one-rank
+    NCCL communicator made through libnccl directly (no torch): the C-ABI's
+    own collective runs and leaves the statistics unchanged."""
+    import ctypes as C
+    import torch
+    from paper_2505_21661_b200 import trace as T
+    from paper_2505_21661_b200 import workloads as W
+    torch.cuda.set_device(0)
+    nccl = C.CDLL("libnccl.so.2", mode=C.RTLD_GLOBAL)
+
+    class UniqueId(C.Structure):
+        _fields_ = [("internal", C.c_char * 128)]
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    comm = C.c_void_p()
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        plan, n_long = _setup(W.MIXED, 4096)
+        ctx = T.Context(0)
+        ctx.set_plan(plan)
+        _replay_range(ctx, W.MIXED, 0, 4096, n_long)
+        pb = ctx.stats_packed_bytes()
+        before = torch.zeros(pb, dtype=torch.uint8, device="cuda")
+        ctx.stats_export(before.data_ptr())
+        torch.cuda.synchronize()
+        b = before.cpu().numpy().tobytes()
+        st0 = ctx.stats()
+        ctx.allreduce_stats(comm.value)
+        after = torch.zeros(pb, dtype=torch.uint8, device="cuda")
+        ctx.stats_export(after.data_ptr())
+        torch.cuda.synchronize()
+        assert after.cpu().numpy().tobytes() == b
+        st1 = ctx.stats()
+        assert {k: (v.count, v.sum, v.min, v.max, v.hist) for k, v in st0.items()} == \
+            {k: (v.count, v.sum, v.min, v.max, v.hist) for k, v in st1.items()}
+    finally:
+        nccl.ncclCommDestroy(comm)

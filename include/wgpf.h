@@ -354,6 +354,22 @@ int wgpf_lower_scopes(const wgpf_scope_op* ops, const uint32_t* body_len,
                       uint32_t* region_of_op, wgpf_lowered* out, char* err,
                       uint64_t err_cap);
 
+/*
+ * Cross-SM time alignment: rewrites events (device pointer when on_device)
+ * from their CTA's SM-local clock into one global cycle domain -- cycles at
+ * cycles_per_ns since the earliest CTA start -- using the runtime's per-CTA
+ * timing records (h_timing[block_index], host memory).  Durations are
+ * unchanged; start times of all CTAs become comparable (Chrome export with
+ * cycles_per_us = 1000 x cycles_per_ns puts them on one timeline).
+ * cycles_per_ns <= 0 measures the SM clock rate from the records (total
+ * cycles / total ns); the rate used is returned in *used_cycles_per_ns.
+ * The reference has a single cycle domain (its vGPU clock); this is the B200
+ * counterpart.
+ */
+int wgpf_align_events(wgpf_ctx* ctx, wgpf_event* events, uint64_t n, int on_device,
+                      const wgpf_cta_timing* h_timing, uint64_t n_ctas,
+                      double cycles_per_ns, double* used_cycles_per_ns);
+
 /* ----------------------------------------------------------------------- */
 /* Synthetic trace generator (bench / tests)    */
 /* ----------------------------------------------------------------------- */

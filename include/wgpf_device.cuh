@@ -68,6 +68,8 @@ struct CtaTiming {
   uint32_t clk_end;    // %clock at finalize
 };
 
+static_assert(sizeof(CtaTiming) == sizeof(wgpf_cta_timing), "CtaTiming layout");
+
 constexpr uint32_t kStreamHdr = WGPF_STREAM_HDR_BYTES;
 
 // Bytes of shared memory the profile buffer needs per CTA.

@@ -76,6 +76,22 @@ typedef struct wgpf_event {
   uint32_t warp_group;
 } wgpf_event;
 
+/*
+ * Per-CTA timing side record of the device runtime (wgpf_dev::CtaTiming,
+ * include/wgpf_device.cuh), 32 bytes: the SM, and %globaltimer (ns, one
+ * clock for the whole GPU) with %clock (cycles, per SM) at the CTA's start
+ * and end -- what wgpf_align_events uses to put the SM-local record clocks
+ * of all CTAs on one timeline.
+ */
+typedef struct wgpf_cta_timing {
+  uint32_t smid;
+  uint32_t streams;
+  uint64_t gt_start;  /* %globaltimer at init (ns) */
+  uint64_t gt_end;    /* %globaltimer at finalize (ns) */
+  uint32_t clk_start; /* %clock at init */
+  uint32_t clk_end;   /* %clock at finalize */
+} wgpf_cta_timing;
+
 #define WGPF_EV_WAIT 0x80000000u      /* EventKind::Wait (else Exec)      */
 #define WGPF_EV_CORRECTED 0x40000000u /* TimelineEvent::corrected         */
 #define WGPF_EV_REGION_MASK 0x0007FFFFu

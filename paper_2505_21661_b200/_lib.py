@@ -143,12 +143,17 @@ def lib() -> C.CDLL:
                                        C.POINTER(Overlap)], i32),
             "wgpf_profile_bytes": ([u64, u32, u64], u64),
             "wgpf_allreduce_stats": ([vp, vp], i32),
+            "wgpf_align_events": ([vp, vp, u64, i32, vp, u64, C.c_double,
+                                   C.POINTER(C.c_double)], i32),
             "wgpf_collect": ([vp, vp, u64, vp, vp, u64, C.POINTER(u64)], i32),
             "wgpf_lower_scopes": ([C.POINTER(ScopeOp), C.POINTER(u32), u32,
                                    C.POINTER(LowerCfg), C.POINTER(u32),
                                    C.POINTER(Lowered), C.c_char_p, u64], i32),
         }
+        override = bool(os.environ.get("WGPF_LIB_OVERRIDE"))
         for name, (args, res) in sig.items():
+            if override and not hasattr(L, name):
+                continue  # (an older build under A/B: entry points it lacks)
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res

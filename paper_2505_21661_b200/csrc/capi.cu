@@ -77,10 +77,11 @@ struct DevBuf {
 }  // namespace
 
 using TpsKernel = void (*)(FastArgs);
-using TpsTmaKernel = void (*)(FastArgs, const CUtensorMap);
-static TpsKernel deep_kernel(bool emit, bool stats) {
-  static const TpsKernel k[4] = {k_tpsd<false, false>, k_tpsd<true, false>,
-                                 k_tpsd<false, true>, k_tpsd<true, true>};
+using DeepKernel = void (*)(FastArgs, const CUtensorMap);
+using TpsTmaKernel = void (*)(FastArgs, const CUtensorMap, const CUtensorMap);
+static DeepKernel deep_kernel(bool emit, bool stats) {
+  static const DeepKernel k[4] = {k_tpsd<false, false>, k_tpsd<true, false>,
+                                  k_tpsd<false, true>, k_tpsd<true, true>};
   return k[(emit ? 1 : 0) | (stats ? 2 : 0)];
 }
 static TpsTmaKernel tps_kernel(bool emit, bool stats) {
@@ -605,7 +606,7 @@ static bool count_tps_enabled(const wgpf_ctx* c) {
 // number of label classes: its statistics live in the CTA table)
 static bool deep_enabled(const wgpf_ctx* c) {
   return !c->no_tps && !c->no_deep && c->slots % 2 == 0 && c->slots &&
-         c->slots <= kTpsMaxSlots && !c->labels.empty();
+         c->slots <= kDeepMaxSlots && !c->labels.empty();
 }
 static uint32_t tps_regions(const wgpf_ctx* c) {
   return std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions);
@@ -639,7 +640,8 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride,
-                            uint64_t n_streams, uint32_t pitch) {
+                            uint64_t n_streams, uint32_t pitch,
+                            CUtensorMapL2promotion prom = l2_promotion()) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn || (reinterpret_cast<uintptr_t>(body) & 15u) || (stride & 15u) ||
       stride < pitch || stride >= (1ull << 39) || n_streams < 32 ||
@@ -651,7 +653,7 @@ static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride
   const cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(body), dims, strides,
             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Streams per block W of a device body (k_tps's lane mapping): the length of
@@ -686,7 +688,8 @@ static uint32_t stream_group(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
 // 3-D view {stride / 4, W, n_streams / W} with box {kTpsPitch / 4, 1, 32}
 // for the grouped lane mapping (k_window.cuh win_tma3)
 static bool body_tensor_map3(CUtensorMap* m, const uint8_t* body, uint64_t stride,
-                             uint64_t n_streams, uint32_t W) {
+                             uint64_t n_streams, uint32_t W,
+                             CUtensorMapL2promotion prom = l2_promotion()) {
   EncodeTiledFn fn = encode_tiled();
   const uint64_t nb = n_streams / W;
   if (!fn || (reinterpret_cast<uintptr_t>(body) & 15u) || (stride & 15u) ||
@@ -699,8 +702,13 @@ static bool body_tensor_map3(CUtensorMap* m, const uint8_t* body, uint64_t strid
   const cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint8_t*>(body), dims, strides,
             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+// The same view without L2 promotion, for the windows that end within 256 B
+// of a stream's last record: a promoted request there would pull the unused
+// slots past record_count into L2 (config 4: 1.3 GB of the body's 10 GB).
+static bool tail_maps() { return getenv("WGPF_NO_TAIL_MAP") == nullptr; }
 
 static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                      uint64_t n_streams, uint64_t stream_base,
@@ -741,6 +749,9 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.tma = 0;
   f.group = 1;
   f.batch_ctr = nullptr;
+  // without the thread-per-stream pass (which visits every stream) the list
+  // kernels hand their SF_GENERAL entries to the general path themselves
+  f.list_general = !tps_enabled(c) && deep_enabled(c) && record_cost < (1ull << 21) ? 1u : 0u;
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
   if ((tps_enabled(c) || deep_enabled(c)) && record_cost < (1ull << 21)) {
@@ -748,13 +759,18 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       // shallow streams: thread per stream
       const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
       const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
-      CUtensorMap tm;
+      CUtensorMap tm, tmt;
       memset(&tm, 0, sizeof(tm));
+      memset(&tmt, 0, sizeof(tmt));
       f.group = stream_group(c, body, stride, n_streams);
       f.batch_ctr = c->d_glen.as<unsigned long long>() + 4;
       CUDA_OK(c, cudaMemsetAsync(f.batch_ctr, 0, 8, c->stream));
       f.tma = !c->no_tma && body_tensor_map3(&tm, body, stride, n_streams, f.group) ? 1u : 0u;
-      tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f, tm);
+      if (f.tma && !(tail_maps() && body_tensor_map3(&tmt, body, stride, n_streams, f.group,
+                                                     CU_TENSOR_MAP_L2_PROMOTION_NONE)))
+        tmt = tm;
+      tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f, tm,
+                                                                                   tmt);
       f.tma = 0;
       f.group = 1;
       CUDA_OK(c, cudaGetLastError());
@@ -767,8 +783,13 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       const uint32_t dw = deep_warps(c->smem_optin);
       ALLOC_OK(c, c->d_dorph, sizeof(wgpf_event) * (uint64_t)c->sms * dw * 32);
       f.orphan_scratch = c->d_dorph.as<wgpf_event>();  // one orphan per lane
+      CUtensorMap tmd;
+      memset(&tmd, 0, sizeof(tmd));
+      f.tma = !c->no_tma && body_tensor_map(&tmd, body, stride, n_streams, kDeepPitch) ? 1u
+                                                                                        : 0u;
       deep_kernel(events != nullptr, !no_stats)<<<c->sms, dw * 32, deep_smem_bytes(dw),
-                                                  c->stream>>>(f);
+                                                  c->stream>>>(f, tmd);
+      f.tma = 0;
       CUDA_OK(c, cudaGetLastError());
       ++c->launches;
     }
@@ -972,11 +993,14 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.tps_depth = tps ? kTpsDepth : 0u;
   ca.deep_regions = deep_enabled(c) ? kDeepRegions : 0u;
   ca.deep_depth = deep_enabled(c) ? kDeepDepth : 0u;
+  ca.list_general = 0;
   if (!tps && deep_enabled(c)) {
     // no shallow kernel for this plan: every stream with records is listed
-    // (SF_WARP) and the deep ones marked
+    // (SF_WARP) and the deep ones marked; general streams go to the warp
+    // list as well, so that its kernel hands them to the general path
     ca.tps_regions = 0;
     ca.tps_depth = 1;
+    ca.list_general = 1;
   }
   ALLOC_OK(c, c->d_wlist, 8 * n_streams);
   ca.warp_list = c->d_wlist.as<unsigned long long>();
@@ -986,14 +1010,19 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.deep_len = c->d_glen.as<unsigned long long>() + 2;
   CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 16, c->stream));
   if (count_tps_enabled(c)) {
-    CUtensorMap tm;
+    CUtensorMap tm, tmt;
     memset(&tm, 0, sizeof(tm));
+    memset(&tmt, 0, sizeof(tmt));
     ca.tma = !c->no_tma &&
                      body_tensor_map(&tm, body, stride, n_streams, CountWin::kTpsPitch)
                  ? 1u
                  : 0u;
+    if (ca.tma && !(tail_maps() && body_tensor_map(&tmt, body, stride, n_streams,
+                                                   CountWin::kTpsPitch,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_NONE)))
+      tmt = tm;
     k_count_tps<<<grid_for(c, (const void*)k_count_tps, kCountWarps * 32, 0),
-                  kCountWarps * 32, 0, c->stream>>>(ca, tm);
+                  kCountWarps * 32, 0, c->stream>>>(ca, tm, tmt);
   } else
     k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                    c->stream>>>(ca);
@@ -1182,6 +1211,9 @@ extern "C" int wgpf_stats_merge(wgpf_ctx* c, const void* d_gathered,
 // Per-chunk statistics are packed and merged at the end (the multi-GPU merge);
 // errors and warnings are the first / the sum over chunks in stream order.
 static constexpr uint64_t kChunkBytes = 256ull << 20;
+// internal: a chunk failed with a reference error; the caller redoes the call
+// on the whole image so that errors come in the reference's order
+static constexpr int WGPF_E_RETRY_WHOLE = 1000;
 
 static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
                                 uint64_t count, uint64_t record_cost,
@@ -1276,9 +1308,12 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
     c->in_chunked = false;
     if (rc) {
       drain();
-      if (rc == WGPF_E_TRACE && c->h_status->decode_err != kNoErr &&
-          c->h_status->cap_mismatch)
-        return host_walk(c, kpft, off + count * stride, off, count);
+      // The reference decodes every stream before pairing any (decode_image
+      // then the per-stream pair/replay, pipeline.hpp:69-80), so an error in
+      // chunk k may be preceded by a decode error in a later chunk: redo the
+      // call on the whole image (error path only), whose error report orders
+      // framing, decode and pair errors as the reference does.
+      if (rc >= WGPF_E_PARSE && rc <= WGPF_E_IO) return WGPF_E_RETRY_WHOLE;
       return rc;
     }
     CUDA_OK(c, cudaEventRecord(eC[b], c->stream));
@@ -1331,9 +1366,13 @@ extern "C" int wgpf_replay_image(wgpf_ctx* c, const uint8_t* kpft,
     if (parse_header(c, kpft, n_bytes, &off, &count) == WGPF_OK && count &&
         (n_bytes - off) % stride == 0 && (n_bytes - off) / stride == count &&
         n_bytes - off > 2 * kChunkBytes && h_events &&
-        !(flags & (WGPF_F_STATS_ONLY | WGPF_F_EXACT_MEAN)) && !c->no_pipeline)
-      return replay_image_chunked(c, kpft, off, count, record_cost, h_events,
-                                  events_cap, flags, n_events, warnings);
+        !(flags & (WGPF_F_STATS_ONLY | WGPF_F_EXACT_MEAN)) && !c->no_pipeline) {
+      const int rc = replay_image_chunked(c, kpft, off, count, record_cost, h_events,
+                                          events_cap, flags, n_events, warnings);
+      if (rc != WGPF_E_RETRY_WHOLE) return rc;
+      if (n_events) *n_events = 0;
+      if (warnings) memset(warnings, 0, sizeof *warnings);
+    }
   }
   const uint8_t* d_body = nullptr;
   uint64_t ns = 0;
@@ -1421,6 +1460,7 @@ extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
   ca.warp_len = nullptr;
   ca.deep_list = nullptr;
   ca.deep_len = nullptr;
+  ca.list_general = 0;
   k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                  c->stream>>>(ca);
   CUDA_OK(c, cudaGetLastError());

@@ -55,6 +55,9 @@ struct CountArgs {
   unsigned long long* deep_list;  // SF_WARP | SF_DEEP streams
   unsigned long long* deep_len;
   uint32_t tma;          // k_count_tps: the body's tensor map is valid
+  uint32_t list_general; // no thread-per-stream emit kernel (every stream is
+                         // listed): SF_GENERAL streams go to the warp list
+                         // too, whose kernel hands them to the general path
 };
 
 __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
       if (warp && deep)
         a.deep_list[atomicAdd(a.deep_len, 1ull)] = s;
-      else if (warp)
+      else if (warp || (general && a.list_general))
         a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
     }
   }
@@ -210,9 +213,12 @@ constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
 constexpr int kCountUnroll = WGPF_COUNT_UNROLL;
 using CountWin = RecWindowsT<kCountW>;
 
-// tm: the body as a TMA tensor with box {CountWin::kTpsPitch / 4, 32}
+// tm: the body as a TMA tensor with box {CountWin::kTpsPitch / 4, 32};
+// tm_tail: the same without L2 promotion, for windows within 256 B of the
+// streams' last records (promotion there would pull the unused slots)
 __global__ void __launch_bounds__(kCountWarps * 32)
-    k_count_tps(CountArgs a, const __grid_constant__ CUtensorMap tm) {
+    k_count_tps(CountArgs a, const __grid_constant__ CUtensorMap tm,
+                const __grid_constant__ CUtensorMap tm_tail) {
   __shared__ uint8_t marker_region[256];
   __shared__ __align__(128) uint8_t recbuf[kCountWarps][2 * 32 * CountWin::kTpsPitch];
   __shared__ __align__(8) unsigned long long wbar[kCountWarps][2];
@@ -273,11 +279,14 @@ __global__ void __launch_bounds__(kCountWarps * 32)
       continue;
     }
     const bool tmab = a.tma && __all_sync(FULL, start == 0u);
+    const uint32_t ntail = __reduce_min_sync(FULL, act ? n : 0xFFFFFFFFu);
     auto issue = [&](uint32_t bs, uint32_t c0) {
       if (tmab) {
         if (lane == 0)
-          win_tma(s_buf + bs * (32u * CountWin::kTpsPitch), &tm, s_bar + 8u * bs,
-                  (int)(4u + 2u * c0), (int)(b * 32), 32u * CountWin::kTpsPitch);
+          win_tma(s_buf + bs * (32u * CountWin::kTpsPitch),
+                  c0 + CountWin::kTpsPitch / 8u + 32u <= ntail ? &tm : &tm_tail,
+                  s_bar + 8u * bs, (int)(4u + 2u * c0), (int)(b * 32),
+                  32u * CountWin::kTpsPitch);
       } else {
         win.issue(bs, c0);
       }
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(kCountWarps * 32)
                         max_d <= (int32_t)a.deep_depth;
       a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
       to_deep = warp && deep;
-      to_warp = warp && !deep;
+      to_warp = (warp && !deep) || (general && a.list_general);
     }
     // warp-aggregated appends: one atomic per warp, the batch's listed
     // streams stay consecutive and in stream order (coalesced window copies

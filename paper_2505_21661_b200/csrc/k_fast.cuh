@@ -61,6 +61,8 @@ struct FastArgs {
   unsigned long long* batch_ctr;  // k_tps: dynamic batch counter (zeroed)
   uint32_t group;        // k_tps: streams per block W (lane l of batch (j, w)
                          // takes stream (32 j + l) W + w; 1 = consecutive)
+  uint32_t list_general; // list kernels hand their SF_GENERAL entries to the
+                         // general path (no k_tps pass to collect them)
 };
 
 struct LevelEntry {  // last START seen at a nesting level
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(kFastWarps * 32) k_fast_emit(FastArgs a) {
     if constexpr (kStage) sbuf ^= 1;
     const uint32_t flag = a.sflag[s];
     if (flag & (SF_DECODE_ERR | SF_GENERAL)) {
-      if ((flag & SF_GENERAL) && lane == 0 && !a.list) {
+      if ((flag & SF_GENERAL) && lane == 0 && (!a.list || a.list_general)) {
         const unsigned long long k = atomicAdd(a.general_len, 1ull);
         a.general_list[k] = s;
       }

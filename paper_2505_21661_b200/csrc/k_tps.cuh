@@ -120,10 +120,12 @@ __host__ inline uint32_t tps_warps(uint32_t K, uint32_t R, size_t smem_limit) {
 }
 
 // kEmit: events materialised; kStats: statistics.
-// tm: the body as a TMA tensor (a.tma != 0), see k_window.cuh
+// tm: the body as a TMA tensor (a.tma != 0), see k_window.cuh; tm_tail: the
+// same without L2 promotion, for windows within 256 B of the streams' end
 template <bool kEmit, bool kStats>
 __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
-    k_tps(FastArgs a, const __grid_constant__ CUtensorMap tm) {
+    k_tps(FastArgs a, const __grid_constant__ CUtensorMap tm,
+          const __grid_constant__ CUtensorMap tm_tail) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   TpsCtaSmem& cs = *reinterpret_cast<TpsCtaSmem*>(smem_raw);
   const uint32_t lane = lane_id();
@@ -234,11 +236,15 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       win.init(ws.rec[0], lane, a.stride * W, cap);  // lanes W streams apart
       win.begin(a.body + s0 * a.stride, start, n);
     }
+    // windows whose rows end within 256 B (32 records) of the shortest
+    // stream's last record: no L2 promotion (it would pull unused slots)
+    const uint32_t ntail = __reduce_min_sync(FULL, act ? n : 0xFFFFFFFFu);
     auto issue = [&](uint32_t bs, uint32_t c0) {
       if (tmab) {
         if (lane == 0)
-          win_tma3(s_buf + bs * (32u * kTpsPitch), &tm, s_bar + 8u * bs, (int)(4u + 2u * c0),
-                   (int)wi, (int)(jb * 32), 32u * kTpsPitch);
+          win_tma3(s_buf + bs * (32u * kTpsPitch),
+                   c0 + kTpsPitch / 8u + 32u <= ntail ? &tm : &tm_tail, s_bar + 8u * bs,
+                   (int)(4u + 2u * c0), (int)wi, (int)(jb * 32), 32u * kTpsPitch);
       } else {
         win.issue(bs, c0);
       }

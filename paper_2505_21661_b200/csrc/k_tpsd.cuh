@@ -5,18 +5,33 @@
 // pair_records :294-346, replay :398-487, region_stats pipeline.hpp:114-133);
 // what changes with depth:
 //
-//   * the per-lane stack has 64 rows (16 KB per warp), so 8 warps per SM;
+//   * 64-row stacks.  The kernel is latency-bound (a lane's walk is a serial
+//     chain), so warps per SM are what it runs on, and shared memory is what
+//     limits them: the stack is split into a u32 clock row and a u16 row of
+//     {position (9 bits) | region (6) | consumable (1)} -- 12 KB per warp
+//     instead of 16 -- and the clock's high word is not stored at all: a
+//     pair's wrap count is read off the positions of the lane's last two
+//     clock wraps (a duration reaches 2^32 iff two wraps lie after the START,
+//     or one and the END's low word is not below the START's).  Iteration
+//     counters are u8 (a region completes at most cap / 2 <= 256 times),
+//     record windows 4 positions (+2) wide: 12 warps per SM (8 before).
 //   * statistics cannot be lane-private for 64 classes: events go to the
 //     CTA's shared table.  Streams of a trace usually advance in lockstep
-//     (same scope program, same wrap position), so a warp's events of one step
-//     mostly share a class: then one lane applies the warp's reduced
-//     count / sum / min / max / first key (redux.sync), otherwise each lane
-//     updates the table with shared atomics.  Histograms: one shared increment
-//     per event (same-bin increments of a warp aggregate in hardware).
+//     (same scope program, same wrap position), so a warp's events of one
+//     step mostly share a class: then one lane applies the warp's reduced
+//     sum / min / max with fire-and-forget shared reductions (red, no return
+//     value to wait for) and the first key, otherwise each lane updates the
+//     table with shared atomics.  Histograms: one shared increment per event;
+//     counts are the histogram sums.
+//   * record windows: one 2-D TMA box per window when the warp's 32 list
+//     entries are 32 consecutive streams with one even start slot and the
+//     window does not cross the circular wrap (config 5: all but one window
+//     per stream), else 16-B cp.async chunks.  Lanes read records in 16-B
+//     pairs when the start is even (conflict-free LDS.128 at the 48-B pitch).
 //
 // It runs over pass 1's deep list (SF_WARP | SF_DEEP: depth <= 64, ids < 64,
 // not general); the warp-per-stream kernel (k_fast.cuh) takes pass 1's warp
-// list (the rest).
+// list (the rest).  Capacities up to kDeepMaxSlots (positions in 9 bits).
 #pragma once
 
 #include <type_traits>
@@ -27,17 +42,26 @@ namespace wgpf {
 
 constexpr uint32_t kDeepDepth = 64;
 constexpr uint32_t kDeepRegions = 64;
-constexpr uint32_t kDeepWarps = 8;
-// stack entry: the START's region id where the record tag has it (bits 12..17)
-constexpr uint32_t kDeepStkRid = (kDeepRegions - 1u) << 12;
+constexpr uint32_t kDeepMaxSlots = 512;  // stack positions in 9 bits
+#ifndef WGPF_DEEP_W
+#define WGPF_DEEP_W 4
+#endif
+constexpr uint32_t kDeepW = WGPF_DEEP_W;  // positions per record window
+constexpr uint32_t kDeepChunks = WinGeom<kDeepW>::kChunks;
+constexpr uint32_t kDeepPitch = WinGeom<kDeepW>::kPitch;  // 48 B: 12 words
+#ifndef WGPF_DEEP_WARPS
+#define WGPF_DEEP_WARPS 12
+#endif
+constexpr uint32_t kDeepWarps = WGPF_DEEP_WARPS;
+// stack meta: position | region << 9 | consumable << 15
+constexpr uint32_t kDeepMetaRid = (kDeepRegions - 1u) << 9;
 
 struct DeepWarpSmem {
-  uint8_t rec[2][32 * kTpsPitch];        // record windows
-  uint2 stk[kDeepDepth][32];             // {lo, pos | rid<<12 | cons<<18 | hi<<19}
-  unsigned long long wsum[kSmemClasses];  // this warp's sums, mins and maxes
-  uint32_t wmin[kSmemClasses];            //   for the warp-uniform statistics
-  uint32_t wmax[kSmemClasses];            //   path (counts: histogram sums)
-  uint16_t cnt[kDeepRegions][32];        // iteration counters
+  uint8_t rec[2][32 * kDeepPitch];        // record windows
+  uint32_t stk_lo[kDeepDepth][32];        // START clock (low word)
+  uint16_t stk_meta[kDeepDepth][32];      // position | region | consumable
+  uint8_t cnt[kDeepRegions][32];          // iteration counters
+  unsigned long long bar[2];              // TMA windows: one mbarrier per buffer
 };
 
 struct DeepCtaSmem {
@@ -47,7 +71,7 @@ struct DeepCtaSmem {
   uint32_t hist_spare;          // histogram increments of lanes without an event
 };
 
-__host__ inline size_t deep_smem_bytes(uint32_t warps) {
+__host__ __device__ inline size_t deep_smem_bytes(uint32_t warps) {
   return tps_align(sizeof(DeepCtaSmem)) + warps * tps_align(sizeof(DeepWarpSmem));
 }
 __host__ inline uint32_t deep_warps(size_t smem_limit) {
@@ -56,8 +80,44 @@ __host__ inline uint32_t deep_warps(size_t smem_limit) {
   return w;
 }
 
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts8_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.u8 [%1], %2; }" ::"r"(
+                   (uint32_t)p),
+               "r"(a), "h"((uint16_t)v)
+               : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
+}
+__device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.u32 [%1], %2; }" ::"r"(
+                   (uint32_t)p),
+               "r"(a), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void red_add64(uint32_t a, unsigned long long v) {
+  asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_min32(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_max32(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// tm: the body as a 2-D TMA tensor {stride / 4, n_streams}, box
+// {kDeepPitch / 4, 32} (a.tma != 0)
 template <bool kEmit, bool kStats>
-__global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
+__global__ void __launch_bounds__(kDeepWarps * 32, 1)
+    k_tpsd(FastArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   DeepCtaSmem& cs = *reinterpret_cast<DeepCtaSmem*>(smem_raw);
   const uint32_t lane = lane_id();
@@ -80,6 +140,13 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     cs.info[r] = inf;
   }
   if (threadIdx.x < 4) cs.warn[threadIdx.x] = 0;
+  const uint32_t s_bar = smem_addr(&ws.bar[0]);  // + 8 * buffer
+  if (a.tma && lane == 0) {
+    win_bar_init(s_bar);
+    win_bar_init(s_bar + 8u);
+    win_bar_fence();
+  }
+  uint32_t bphase = 0;  // parity of each buffer's next TMA completion
   __syncthreads();
   const bool abort_all = a.status->decode_err != kNoErr;
   const uint32_t FULL = 0xffffffffu;
@@ -88,16 +155,16 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
   uint32_t w_drop = 0, w_tail = 0, w_flag = 0, w_mal = 0, w_ovf = 0;
 
   const uint32_t s_info = opaque_u32(smem_addr(cs.info));
-  const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);  // + 256 * level
-  const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);  // + 64 * region
-  // one orphan per lane, in global scratch (rare; shared memory holds the
-  // warp's statistics instead)
+  const uint32_t s_lo = smem_addr(&ws.stk_lo[0][lane]);      // + 128 * level
+  const uint32_t s_meta = smem_addr(&ws.stk_meta[0][lane]);  // + 64 * level
+  const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);        // + 32 * region
+  const uint32_t s_cnt_all = smem_addr(&ws.cnt[0][0]);
+  const uint32_t s_sum = opaque_u32(smem_addr(cs.st.sum));
+  const uint32_t s_min = opaque_u32(smem_addr(cs.st.min));
+  const uint32_t s_max = opaque_u32(smem_addr(cs.st.max));
+  const uint32_t s_hist = opaque_u32(smem_addr(cs.st.hist));
+  // one orphan per lane, in global scratch (rare)
   wgpf_event* const orph = a.orphan_scratch + ((size_t)blockIdx.x * nw + w) * 32u + lane;
-  for (uint32_t c = lane; c < kSmemClasses; c += 32) {
-    ws.wsum[c] = 0;
-    ws.wmin[c] = 0xFFFFFFFFu;
-    ws.wmax[c] = 0;
-  }
   const uint32_t s_rec = smem_addr(ws.rec[0]);
   const uint32_t s_spare = opaque_u32(smem_addr(&cs.hist_spare));
   const uint64_t n_list = *a.list_len;
@@ -106,8 +173,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
   auto wstat = [&](bool p, uint32_t cls, uint32_t d, unsigned long long key) {
     const uint32_t pm = __ballot_sync(FULL, p);
     if (pm == 0) return;
-    // one class for every participating lane?  (two independent reductions
-    // instead of a leader shuffle followed by a vote)
+    // one class for every participating lane?  (two independent reductions)
     const uint32_t c0 = __reduce_min_sync(FULL, p ? cls : 0xFFFFFFFFu);
     const bool uni = c0 == __reduce_max_sync(FULL, p ? cls : 0u);
     const uint32_t leader = __ffs(pm) - 1u;
@@ -126,15 +192,14 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       const bool cand = p && (uint32_t)(key >> 32) == khi;
       const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
       if (lane == leader) {
-        // count and sum in the warp's own table (no atomics, nothing to wait
-        // for); min / max are fire-and-forget shared atomics
-        ws.wsum[c0] += (unsigned long long)slo + ((unsigned long long)shi << 16);
-        ws.wmin[c0] = min(ws.wmin[c0], mn);
-        ws.wmax[c0] = max(ws.wmax[c0], mx);
+        // fire-and-forget shared reductions: nothing comes back to wait for
+        red_add64(s_sum + 8u * c0, (unsigned long long)slo + ((unsigned long long)shi << 16));
+        red_min32(s_min + 4u * c0, mn);
+        red_max32(s_max + 4u * c0, mx);
         const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
         if (fk < cur_first) atomicMin(&cs.st.first[c0], fk);
       }
-      red_add(p ? smem_addr(&cs.st.hist[c0 * WGPF_HIST_BINS + hist_bin32(d)]) : s_spare, 1u);
+      red_add(p ? s_hist + 4u * (c0 * WGPF_HIST_BINS + hist_bin32(d)) : s_spare, 1u);
     } else if (p) {
       stats_add_one(cs.st, a.stats, cls, d, key, &a.status->synth_overflow);
     }
@@ -145,6 +210,11 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     const uint64_t li = b * 32 + lane;
     const uint64_t s = li < n_list ? a.list[li] : 0ull;
     const uint32_t flag = li < n_list ? a.sflag[s] : SF_DECODE_ERR;
+    if ((flag & SF_GENERAL) && a.list_general) {
+      // (a re-emit after an exact recount: the stream is the general path's)
+      const unsigned long long k = atomicAdd(a.general_len, 1ull);
+      a.general_list[k] = s;
+    }
     const bool act = (flag & SF_DEEP) && !(flag & (SF_DECODE_ERR | SF_GENERAL));
     const uint8_t* sbase = a.body + (act ? s : 0) * a.stride;
     uint4 h = make_uint4(0u, 0u, 0u, cap);
@@ -159,17 +229,28 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     const uint64_t off = act ? a.offsets[s] : 0ull;
     const unsigned long long gkey = (unsigned long long)(s + a.stream_base) << 25;
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
-    for (uint32_t r = 0; r < kDeepRegions; ++r) ws.cnt[r][lane] = 0;
+    // iteration counters: the warp clears its 2 KB table with 16-B stores
+#pragma unroll
+    for (uint32_t k = lane; k < kDeepRegions * 32u / 16u; k += 32)
+      sts128_if(true, s_cnt_all + 16u * k, make_uint4(0u, 0u, 0u, 0u));
+    __syncwarp();
 
-    // record windows: chunk k of this lane copies part (q % C) of the window
-    // of batch slot q / C, q = 32 k + lane; that slot's stream from its lane
-    uint32_t wp[kTpsChunks];
-    const uint8_t* srck[kTpsChunks];  // slots of chunk k's stream (null: none)
+    // TMA windows: the warp's list entries are 32 consecutive streams with
+    // one even start slot (config 5: every batch)
     const uint32_t s32 = (uint32_t)s;
+    const uint32_t s_first = __shfl_sync(FULL, s32, 0);
+    const uint32_t st0 = __shfl_sync(FULL, start, 0);
+    const bool tmab = a.tma && __all_sync(FULL, act && s32 == s_first + lane &&
+                                                    start == st0 && (start & 1u) == 0u);
+    // cp.async windows: chunk k of this lane copies part (q % C) of the
+    // window of batch slot q / C, q = 32 k + lane; that slot's stream from
+    // its lane
+    uint32_t wp[kDeepChunks];
+    const uint8_t* srck[kDeepChunks];  // slots of chunk k's stream (null: none)
     const uint32_t live = act ? 1u : 0u;
 #pragma unroll
-    for (uint32_t k = 0; k < kTpsChunks; ++k) {
-      const uint32_t q = k * 32u + lane, sl = q / kTpsChunks, part = q % kTpsChunks;
+    for (uint32_t k = 0; k < kDeepChunks; ++k) {
+      const uint32_t q = k * 32u + lane, sl = q / kDeepChunks, part = q % kDeepChunks;
       const uint32_t st_k = __shfl_sync(FULL, start, sl);
       const uint32_t ss = __shfl_sync(FULL, s32, sl);
       srck[k] = __shfl_sync(FULL, live, sl) ? a.body + (uint64_t)ss * a.stride + 16 : nullptr;
@@ -179,15 +260,29 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       if (p >= cap) p -= cap;
       wp[k] = p;
     }
-    auto issue = [&](uint32_t bsel) {
+    uint32_t tma_buf = 0;  // bit b: buffer b's window came by TMA
+    auto issue = [&](uint32_t bsel, uint32_t c0) {
+      // (physical slot of the window's first position: even on this path)
+      uint32_t p = st0 + c0;
+      p = p >= cap ? p - cap : p;
+      if (tmab && p + kDeepW <= cap) {
+        if (lane == 0)
+          win_tma(s_rec + bsel * (32 * kDeepPitch), &tm, s_bar + 8u * bsel,
+                  (int)(4u + 2u * p), (int)s_first, 32u * kDeepPitch);
+        tma_buf |= 1u << bsel;
+      } else {
+        tma_buf &= ~(1u << bsel);
 #pragma unroll
-      for (uint32_t k = 0; k < kTpsChunks; ++k) {
-        const uint32_t q = k * 32u + lane, sl = q / kTpsChunks, part = q % kTpsChunks;
-        // (stream addresses resolved once per batch, not per window)
-        if (srck[k])
-          cp_async16(s_rec + bsel * (32 * kTpsPitch) + sl * kTpsPitch + 16u * part,
-                     srck[k] + 8u * wp[k]);
-        wp[k] += kTpsW;
+        for (uint32_t k = 0; k < kDeepChunks; ++k) {
+          const uint32_t q = k * 32u + lane, sl = q / kDeepChunks, part = q % kDeepChunks;
+          if (srck[k])
+            cp_async16(s_rec + bsel * (32 * kDeepPitch) + sl * kDeepPitch + 16u * part,
+                       srck[k] + 8u * wp[k]);
+        }
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < kDeepChunks; ++k) {
+        wp[k] += kDeepW;
         if (wp[k] >= cap) wp[k] -= cap;
       }
     };
@@ -196,11 +291,15 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     if (n > 0) r0 = slots[start];
     if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
     uint32_t inf0 = cs.info[(r0.x >> 12) & (kDeepRegions - 1u)];
-    issue(0);
+    issue(0, 2);
     cp_async_commit();
 
-    const uint32_t s_stk0 = s_stk - 256u;  // empty stack: one row below (rec)
-    uint32_t hi = 0, vprev = 0, stop = s_stk0;
+    // stack top: offset 64 * level (meta) / 128 * level (clock); empty = -64
+    // (reads one row below each array: bytes of the preceding arrays, never
+    // written, used only when an END has a partner)
+    int32_t tp = -64;
+    uint32_t hi = 0, vprev = 0;
+    uint32_t w_last = 0, w_prev = 0;  // positions of the last two clock wraps
     uint32_t pw = 0xFFu;
     uint32_t kw = 0;
     uint32_t n_orph = 0;
@@ -226,16 +325,20 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       const uint32_t inf = inf0;
       const uint32_t r1id = (r1.x >> 12) & (kDeepRegions - 1u);
       const uint32_t i1 = lds32(s_info + 4u * r1id);
+      const bool wrap = valid && v < vprev;
+      const uint32_t meta_new =
+          i | ((tag >> 3) & kDeepMetaRid) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 15);
       if constexpr (kFull) {
         // every lane at a START (the streams of a trace run the same program
         // from the same wrap position): a push is all that happens
         if (__all_sync(FULL, isS)) {
-          hi += v < vprev ? 1u : 0u;
+          hi += wrap ? 1u : 0u;
+          w_prev = wrap ? w_last : w_prev;
+          w_last = wrap ? i : w_last;
           vprev = v;
-          sts64_if(true, stop + 256u,
-                   make_uint2(v, i | (tag & kDeepStkRid) |
-                                     ((pw == (inf & 0xFFu) ? 1u : 0u) << 18) | (hi << 19)));
-          stop += 256u;
+          tp += 64;
+          sts32(s_lo + 2 * tp, v);
+          sts16(s_meta + tp, meta_new);
           pw = 0xFFu;
           inf0 = i1;
           r0 = r1;
@@ -243,30 +346,35 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
           return;
         }
       }
-      hi += (valid && v < vprev) ? 1u : 0u;
+      hi += wrap ? 1u : 0u;
+      w_prev = wrap ? w_last : w_prev;
+      w_last = wrap ? i : w_last;
       vprev = valid ? v : vprev;
-      const uint2 e = lds64(stop);
-      const bool nonempty = stop != s_stk0;
+      const uint32_t elo = lds32(s_lo + 2 * tp);
+      const uint32_t em = lds16(s_meta + tp);
+      const bool nonempty = tp >= 0;
       const bool mend = en && nonempty;
       w_drop += (en && !nonempty) ? 1u : 0u;
-      sts64_if(st, stop + 256u,
-               make_uint2(v, i | (tag & kDeepStkRid) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 18) |
-                                 (hi << 19)));
-      stop = stop + (st ? 256u : 0u) - (mend ? 256u : 0u);
-      const uint32_t shi = e.y >> 19;
-      const uint32_t meas = v - e.x;
-      const bool dhi = hi != shi + (v < e.x ? 1u : 0u);
-      const bool mism = mend && ((e.y ^ tag) & kDeepStkRid) != 0u;
-      const bool tlong = mend && !mism && dhi;
+      sts32_if(st, s_lo + 2 * (tp + 64), v);
+      sts16_if(st, s_meta + tp + 64, meta_new);
+      tp += (st ? 64 : 0) - (mend ? 64 : 0);
+      const uint32_t spos = em & 511u;
+      const uint32_t meas = v - elo;  // low 32 bits of u - su
+      // the pair spans >= 2^32 cycles iff two clock wraps lie after the
+      // START, or one and the END's low word is not below the START's
+      const bool tl = w_prev > spos || (w_last > spos && v >= elo);
+      const bool mism = mend && ((em ^ (tag >> 3)) & kDeepMetaRid) != 0u;
+      const bool tlong = mend && !mism && tl;
       broken |= mism || tlong;
       const bool ok = mend && !mism && !tlong;
-      const uint32_t ca = s_cnt + 64u * rid;
-      const uint32_t it = lds16(ca);
-      sts16_if(ok, ca, it + 1u);
+      const uint32_t shi = hi - (v < elo ? 1u : 0u);
+      const uint32_t ca = s_cnt + 32u * rid;
+      const uint32_t it = lds8(ca);
+      sts8_if(ok, ca, it + 1u);
       const bool is_mk = (inf & 0x100u) != 0u;
       const bool base = ok && !is_mk;
-      const bool orphan = ok && is_mk && !((e.y >> 18) & 1u);
-      const uint32_t dpos = i - (e.y & 2047u);
+      const bool orphan = ok && is_mk && !((em >> 15) & 1u);
+      const uint32_t dpos = i - spos;
       const uint32_t ovh = cost * dpos;
       const uint32_t corr = ovh > meas ? 0u : meas - ovh;
       const bool cclose = (kFull || i + 2 < n) && (int32_t)r2.x >= 0 &&
@@ -279,8 +387,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       w_flag += (consumed && !corr_w) ? 1u : 0u;
       const uint32_t kpos = kw;
       if constexpr (emit) {
-        const uint32_t elo = e.x + corr;
-        put(base, kw, e.x, shi, elo, shi + (elo < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED,
+        const uint32_t eend = elo + corr;
+        put(base, kw, elo, shi, eend, shi + (eend < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED,
             it);
         put(consumed, kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
             r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
@@ -288,7 +396,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
       pw = base ? (inf >> 16) : 0xFFu;
       if (orphan && n_orph == 0)
-        *orph = wgpf_event{(uint64_t)e.x | ((uint64_t)shi << 32), (uint64_t)v | ((uint64_t)hi << 32),
+        *orph = wgpf_event{(uint64_t)elo | ((uint64_t)shi << 32), (uint64_t)v | ((uint64_t)hi << 32),
                            rid, it, 0u, 0u};
       n_orph += orphan ? 1u : 0u;
       if constexpr (stats) {
@@ -302,22 +410,36 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     };
 
     const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
-    for (uint32_t w0 = 0; w0 < nmax; w0 += kTpsW) {
-      const uint32_t bsel = (w0 / kTpsW) & 1u;
-      if (w0 + kTpsW < nmax) issue(bsel ^ 1u);
+    const bool even_start = __all_sync(FULL, (start & 1u) == 0u);
+    for (uint32_t w0 = 0; w0 < nmax; w0 += kDeepW) {
+      const uint32_t bsel = (w0 / kDeepW) & 1u;
+      if (w0 + kDeepW < nmax) issue(bsel ^ 1u, w0 + kDeepW + 2u);
       cp_async_commit();
       cp_async_wait1();
+      if ((tma_buf >> bsel) & 1u) {
+        win_wait(s_bar + 8u * bsel, (bphase >> bsel) & 1u);
+        bphase ^= 1u << bsel;
+      }
       __syncwarp();
       const uint2* myrec = reinterpret_cast<const uint2*>(
-          ws.rec[bsel] + lane * kTpsPitch + 8u * (start & 1u));
-      if (w0 + kTpsW + 2u <= nmin) {
-        // (2 steps per iteration: the step with its reduced statistics is
-        // long, and 8 unrolled copies thrash the instruction cache)
+          ws.rec[bsel] + lane * kDeepPitch + 8u * (start & 1u));
+      if (w0 + kDeepW + 2u <= nmin) {
+        if (even_start) {
+          // 16-B record pairs: one conflict-free LDS.128 per two steps
+          const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
 #pragma unroll 1
-        for (uint32_t j = 0; j < kTpsW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
+          for (uint32_t j = 0; j < kDeepW; j += 2) {
+            const uint4 q = myrec2[j / 2];
+            step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
+            step(std::true_type{}, w0 + j + 1, make_uint2(q.z, q.w));
+          }
+        } else {
+#pragma unroll 1
+          for (uint32_t j = 0; j < kDeepW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
+        }
       } else {
 #pragma unroll 1
-        for (uint32_t j = 0; j < kTpsW; ++j) step(std::false_type{}, w0 + j, myrec[j]);
+        for (uint32_t j = 0; j < kDeepW; ++j) step(std::false_type{}, w0 + j, myrec[j]);
       }
       __syncwarp();
     }
@@ -341,7 +463,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
       }
       if (!bad) {
         w_mal += n_orph;
-        w_tail += (stop - s_stk0) >> 8;
+        w_tail += (uint32_t)(tp + 64) >> 6;
       }
     }
   }
@@ -356,15 +478,6 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1) k_tpsd(FastArgs a) {
     if (t) atomicAdd(&cs.warn[1], t);
     if (f) atomicAdd(&cs.warn[2], f);
     if (m) atomicAdd(&cs.warn[3], m);
-  }
-  if (stats) {  // the warp's sums, mins and maxes into the CTA table
-    for (uint32_t c = lane; c < kSmemClasses; c += 32) {
-      if (ws.wmin[c] != 0xFFFFFFFFu || ws.wmax[c] != 0u) {
-        sadd64(&cs.st.sum[c], ws.wsum[c]);
-        atomicMin(&cs.st.min[c], ws.wmin[c]);
-        atomicMax(&cs.st.max[c], ws.wmax[c]);
-      }
-    }
   }
   __syncthreads();
   if (stats) {

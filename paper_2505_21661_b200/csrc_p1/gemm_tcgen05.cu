@@ -9,8 +9,10 @@
 // 128x256x16 (cta_group::1), 4 smem stages of 48 KB, 2 x 256 TMEM columns
 // (double-buffered accumulator).
 //
-// Scopes (region ids): 0 tile, 1 tma.wait, 2 tma.issue, 3 mma.wait,
-// 4 mma.issue, 5 epi.wait, 6 epi.ld, 7 epi.st.
+// Scopes (region ids): 0 tile, 1 tma.stall, 2 tma.issue, 3 mma.stall,
+// 4 mma.issue, 5 epi.stall, 6 epi.ld, 7 epi.st (the stalls are sync scopes
+// around mbarrier waits: no ".wait" suffix, which replay reserves for the
+// async pattern's wait markers, trace.hpp:377-382).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "wgpf_device.cuh"
 
@@ -228,7 +229,69 @@ __global__ void k_loop_entry(uint32_t n, uint32_t trips, uint64_t* cycles,
   if (x == 0xFFFFFFFFu) sink[0] = x;
 }
 
+// ---- per-scope timing accuracy (2 % relative error) ---------------
+// Every warp runs `scopes` scopes back to back, each a dependent chain of
+// `chain` integer multiply-adds (deterministic latency, nothing to overlap);
+// instrumented, each scope is one START / END pair.  Ground truth: the same
+// kernel uninstrumented, timed by CUDA events at two scope counts -- the
+// slope is the true per-scope time.  The record-derived scope durations
+// (decoded, sync-corrected) are converted to ns with the SM clock rate of the
+// CtaTiming side records.
+template <bool kInstr>
+__global__ void k_accuracy(uint8_t* profile, uint32_t cap, uint32_t scopes, uint32_t chain,
+                           wgpf_dev::CtaTiming* timing, uint32_t* sink) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t nwarps = blockDim.x >> 5;
+  if (kInstr && threadIdx.x == 0 && timing) {
+    timing[blockIdx.x].smid = wgpf_dev::smid();
+    timing[blockIdx.x].streams = nwarps;
+    timing[blockIdx.x].gt_start = wgpf_dev::globaltimer();
+    timing[blockIdx.x].clk_start = wgpf_dev::clock32();
+  }
+  std::conditional_t<kInstr, wgpf_dev::Recorder<true>, wgpf_dev::NullRecorder> rec;
+  rec.init(buf, warp, cap, lane == 0);
+  uint32_t x = threadIdx.x + 1u, a = 1664525u + (blockIdx.x & 1u);
+  for (uint32_t s = 0; s < scopes; ++s) {
+    rec.start(0);
+#pragma unroll 4
+    for (uint32_t i = 0; i < chain; ++i) x = x * a + 1013904223u;
+    rec.end(0);
+  }
+  if constexpr (kInstr) {
+    rec.close(blockIdx.x, warp, cap);
+    __syncthreads();
+    wgpf_dev::flush(buf, profile, blockIdx.x, wgpf_dev::smem_bytes(nwarps, cap), threadIdx.x,
+                    blockDim.x);
+    if (threadIdx.x == 0 && timing) {
+      timing[blockIdx.x].gt_end = wgpf_dev::globaltimer();
+      timing[blockIdx.x].clk_end = wgpf_dev::clock32();
+    }
+  }
+  if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
 }  // namespace
+
+extern "C" int wgpf_p1_accuracy(uint32_t ctas, uint32_t warps, uint32_t scopes,
+                                uint32_t chain, int instr, void* d_profile, uint32_t cap,
+                                void* d_timing, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (instr) {
+    if (!cap || (cap & (cap - 1)) || cap < 2 * scopes) return 11;
+    const uint32_t smem = wgpf_dev::smem_bytes(warps, cap);
+    cudaFuncSetAttribute(k_accuracy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_accuracy<true><<<ctas, warps * 32, smem, st>>>(static_cast<uint8_t*>(d_profile), cap,
+                                                     scopes, chain,
+                                                     static_cast<wgpf_dev::CtaTiming*>(d_timing),
+                                                     sink);
+  } else {
+    k_accuracy<false><<<ctas, warps * 32, 0, st>>>(nullptr, cap, scopes, chain, nullptr, sink);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
 
 template <bool P, bool F, bool V>
 static int launch_program(void* d_profile, uint32_t ctas, uint32_t nb, uint32_t cap,

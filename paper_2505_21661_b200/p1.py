@@ -19,8 +19,8 @@ _lib = None
 # scope-program self-test regions (csrc_p1/p1_selftest.cu)
 SELFTEST_LABELS = ["kernel", "outer", "inner", "async", "async.wait"]
 # GEMM scopes (csrc_p1/gemm_tcgen05.cu)
-GEMM_LABELS = ["tile", "tma.wait", "tma.issue", "mma.wait", "mma.issue",
-               "epi.wait", "epi.ld", "epi.st"]
+GEMM_LABELS = ["tile", "tma.stall", "tma.issue", "mma.stall", "mma.issue",
+               "epi.stall", "epi.ld", "epi.st"]
 GEMM_WARPS = 6
 GEMM_SLOTS = 64
 # attention scopes (csrc_p1/attn_tcgen05.cu), the fa3 fixture's names
@@ -72,6 +72,8 @@ def lib() -> C.CDLL:
                                           vp]
         L.wgpf_p1_run_program.restype = i32
         L.wgpf_p1_loop_entry.argtypes = [u32, u32, u32, i32, vp, vp]
+        L.wgpf_p1_accuracy.argtypes = [u32, u32, u32, u32, i32, vp, u32, vp, vp]
+        L.wgpf_p1_accuracy.restype = i32
         L.wgpf_p1_loop_entry.restype = i32
         _lib = L
     return _lib

@@ -525,6 +525,25 @@ class Context:
     def stats_export(self, dst_ptr: int) -> None:
         _check(self.h, self.L.wgpf_stats_export(self.h, C.c_void_p(dst_ptr)))
 
+    def align_events(self, events, timing: np.ndarray, cycles_per_ns: float = 0.0,
+                     on_device_ptr: int = 0, n_events: int | None = None):
+        """Cross-SM alignment (wgpf_align_events): events from their CTA's
+        SM clock into one global cycle domain using the runtime's per-CTA
+        timing records (p1.CTA_TIMING_DTYPE).  Host events: returns the
+        aligned copy; device events: in place.  Returns (events, cycles_per_ns)."""
+        tm = np.ascontiguousarray(timing)
+        f = C.c_double()
+        if on_device_ptr:
+            _check(self.h, self.L.wgpf_align_events(self.h, C.c_void_p(on_device_ptr),
+                                                    n_events, 1, C.c_void_p(tm.ctypes.data),
+                                                    len(tm), cycles_per_ns, C.byref(f)))
+            return None, f.value
+        ev = np.ascontiguousarray(events, EVENT_DTYPE).copy()
+        _check(self.h, self.L.wgpf_align_events(self.h, C.c_void_p(ev.ctypes.data), len(ev),
+                                                0, C.c_void_p(tm.ctypes.data), len(tm),
+                                                cycles_per_ns, C.byref(f)))
+        return ev, f.value
+
     def allreduce_stats(self, nccl_comm: int) -> None:
         """Combines this rank's statistics with every rank of an NCCL
         communicator (wgpf_allreduce_stats: export, one ncclAllGather, merge)."""

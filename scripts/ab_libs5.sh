@@ -1,9 +1,12 @@
-# A/B of alternative libwgpf builds on config 5 (k_tpsd)
-O=gpurun_out/${1:-abl5}; mkdir -p $O
+# A/B of alternative builds of libwgpf (paper_2505_21661_b200/_lib/ab/*.so) vs the default
+# on config 5 (the deep kernel)
+O=gpurun_out/${1:-abl5}; mkdir -p $O; : > $O/ab.txt
 for rep in 1 2; do
 for L in default paper_2505_21661_b200/_lib/ab/*.so; do
   if [ $L = default ]; then unset WGPF_LIB_OVERRIDE; else export WGPF_LIB_OVERRIDE=$PWD/$L; fi
-  timeout 300 python bench.py --config 5 --no-e2e --no-cpu-baseline --no-p1 --steps 5 > $O/tmp.json 2>/dev/null
+  timeout 300 python bench.py --config 5 --no-e2e --no-cpu-baseline --no-p1 --steps 10 > $O/tmp.json 2>$O/tmp.err
   python -c "
-import json; d=json.load(open('$O/tmp.json')); print('$(basename $L)', d['value']/1e9, d['phases_ms']['emit'])" >> $O/ab.txt
+import json; d=json.load(open('$O/tmp.json')); p=d['phases_ms']
+print('%-12s %7.2f G/s step %.3f count %.3f emit %.3f' % ('$(basename $L)', d['value']/1e9, d['ms_per_step'], p['count'], p['emit']))" >> $O/ab.txt 2>&1 || tail -3 $O/tmp.err >> $O/ab.txt
 done; done
+cat $O/ab.txt

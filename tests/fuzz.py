@@ -97,3 +97,66 @@ def random_image(seed: int, n_streams: int = 8, cap: int = 64,
             body[s, 5 + 2 * slot] = clocks[w]
     data = S.kpft_v1(body.view(np.uint8).reshape(-1), n_streams)
     return data, cap, strategy, labels
+
+
+DEEP_LABELS = [f"D{i:02d}" for i in range(56)] + [f"D{i:02d}.wait" for i in range(8)]
+
+
+def _deep_records(rng, writes, depth, big_gaps, violate):
+    """A nesting program `depth` levels deep (labels D00.. by level),
+    repeated: START per level going down, at the bottom an async group of an
+    eight-label base (S(X) E(X) S(X.wait) E(X.wait)) or a plain scope, then
+    the ENDs going up; `violate` swaps one END's region now and then."""
+    tags, clocks = [], []
+    clock = int(rng.integers(0, 1 << 32))
+
+    def rec(tag):
+        nonlocal clock
+        tags.append(tag)
+        clocks.append(clock)
+        if big_gaps and rng.random() < 0.01:
+            clock = (clock + int(rng.integers(1 << 29, 1 << 31))) & 0xFFFFFFFF
+        else:
+            clock = (clock + int(rng.integers(1, 300))) & 0xFFFFFFFF
+
+    while len(tags) < writes:
+        d = depth if rng.random() < 0.7 else int(rng.integers(1, depth + 1))
+        for lv in range(d):
+            rec(0x80000000 | (lv << 12))
+        x = int(rng.integers(0, 8))
+        if rng.random() < 0.5:
+            rec(0x80000000 | (x << 12))
+            rec(x << 12)
+            rec(0x80000000 | ((56 + x) << 12))
+            rec((56 + x) << 12)
+        for lv in reversed(range(d)):
+            r = lv
+            if violate and rng.random() < 0.01:
+                r = (lv + 1) % 56
+            rec(r << 12)
+    return np.array(tags[:writes], np.uint32), np.array(clocks[:writes], np.uint32)
+
+
+def deep_image(seed: int, n_streams: int = 64, cap: int = 256, depth: int = 40,
+               same_start: bool = True, odd: bool = False, big_gaps: bool = False,
+               violate: bool = False, per_block: int = 16):
+    """Circular streams of deep nesting (the deep thread-per-stream kernel's
+    inputs): every stream wraps (writes > cap); same_start gives all streams
+    one write count (one start slot: TMA windows), odd an odd start slot.
+    Returns (kpft v1 bytes, slots, strategy, labels)."""
+    rng = np.random.default_rng(seed)
+    body = np.zeros((n_streams, 4 + 2 * cap), np.uint32)
+    base_writes = 3 * cap + (1 if odd else 0) + (0 if odd else 2 * int(rng.integers(0, cap // 2)))
+    for s in range(n_streams):
+        writes = base_writes if same_start else int(rng.integers(cap + 1, 4 * cap))
+        tags, clocks = _deep_records(rng, writes, depth, big_gaps, violate)
+        body[s, 0] = s // per_block
+        body[s, 1] = s % per_block
+        body[s, 2] = writes
+        body[s, 3] = cap
+        for w in range(writes):
+            slot = w % cap
+            body[s, 4 + 2 * slot] = tags[w]
+            body[s, 5 + 2 * slot] = clocks[w]
+    data = S.kpft_v1(body.view(np.uint8).reshape(-1), n_streams)
+    return data, cap, 0, list(DEEP_LABELS)

@@ -18,7 +18,7 @@ def P1():
 
 
 @pytest.mark.parametrize("cap,iters", [(64, 3), (64, 20), (48, 20), (256, 30)])
-def test_selftest_buffer_decodes_to_store_log(oracle, cap, iters):
+def test_selftest_buffer_decodes_to_store_log(oracle, reference, cap, iters):
     import torch
     p1 = P1()
     ctas, warps = 5, 4
@@ -40,9 +40,12 @@ def test_selftest_buffer_decodes_to_store_log(oracle, cap, iters):
         assert got == tail
         u = oracle.unwrap_clock(d["records"]["payload"])
         assert np.all(np.diff(u.astype(np.int64)) >= 0)
-    # the reference itself reads the image and replays it
-    r = oracle.replay_kpft(img, cap, strategy, P1().SELFTEST_LABELS, 33)
+    # the reference itself (oracle/_ref) reads the image and replays it, and
+    # the C restatement agrees
+    r = reference.replay_kpft(img, cap, strategy, P1().SELFTEST_LABELS, 33)
     assert len(r.events) > 0
+    assert len(oracle.replay_kpft(img, cap, strategy, P1().SELFTEST_LABELS, 33).events) \
+        == len(r.events)
     t = timing.cpu().numpy().view(P1().CTA_TIMING_DTYPE)
     assert np.all(t["gt_end"] >= t["gt_start"]) and np.all(t["streams"] == warps)
 
@@ -115,6 +118,8 @@ def test_gemm_matches_cublas_and_instrumented_is_identical(oracle, shape):
                                     r.flagged_preconditions, r.malformed_groups)
     gev = ev[: ne * 32].cpu().numpy().view(T.EVENT_DTYPE)
     assert np.array_equal(gev, r.events)
+    # the stall scopes are sync scopes, not wait markers: nothing malformed
+    assert w.malformed_groups == 0
     st = oracle.region_stats(r.events, p1.GEMM_LABELS)
     labels = {s.label for s in st}
     assert {"mma.issue", "tma.issue", "epi.ld", "epi.st", "tile"} <= labels

@@ -366,6 +366,51 @@ def test_replay_image_pipelined_matches_device(ctx):
     assert c2.stats() == whole
 
 
+def test_replay_image_pipelined_error_order(ctx, reference):
+    """The reference decodes every stream before pairing any
+    (pipeline.hpp:69-80 -> decode_image first), so a decode error in a late
+    chunk of the pipelined path must win over a pair error (duration >= 2^32)
+    in chunk 0, as in the reference on the same streams."""
+    import torch
+    t = T()
+    n = 300000  # three chunks
+    plan = plan_of(S.CAP, 1, S.MIXED_LABELS)
+    ctx.set_plan(plan)
+    body = torch.empty(n * S.stream_stride(), dtype=torch.uint8, device="cuda")
+    ctx.synth_body(body.data_ptr(), 0, 0, n, n // 3)
+    b = body.cpu().numpy()
+    st = S.stream_stride()
+    # stream 5 (a consumer: S4 S5 S6 S7 E7 E6 ...): the gaps of records 1..7
+    # grow by 2^31 + 1, so E6 closes S6 3 (2^31 + 1) > 2^32 cycles later ->
+    # the reference's pair error
+    w = b[5 * st:6 * st].view(np.uint32)
+    clk = w[5:4 + 2 * 221:2].astype(np.int64)
+    k = np.minimum(np.arange(len(clk)), 7)
+    w[5:4 + 2 * 221:2] = ((clk + k * 0x80000001) & 0xFFFFFFFF).astype(np.uint32)
+    # stream 290000 (chunk 2): a flush stream claiming more records than slots
+    h = b[290000 * st:290000 * st + 16].view(np.uint32)
+    h[2] = S.CAP + 1
+    hdr = b"KPFT" + (2).to_bytes(2, "little") + b"\0\0" + n.to_bytes(8, "little")
+    img = hdr + b.tobytes()
+    with pytest.raises(t.Error) as e:
+        t.Context(0).replay_image_bytes(img, plan, 33)
+    # the reference on the streams that matter (v1 images of <= 65,535 streams)
+    sub = np.concatenate([b[0:64 * st], b[290000 * st:290001 * st]])
+    v1 = b"KPFT" + (1).to_bytes(2, "little") + (65).to_bytes(2, "little") + sub.tobytes()
+    from oracle.oracle import OracleError
+    with pytest.raises(OracleError) as er:
+        reference.replay_kpft(v1, S.CAP, 1, S.MIXED_LABELS, 33)
+    assert str(e.value) == str(er.value) == "flush stream claims more records than slots"
+    # without the decode error the pair error is reported
+    h[2] = 221
+    with pytest.raises(t.Error) as e2:
+        t.Context(0).replay_image_bytes(hdr + b.tobytes(), plan, 33)
+    with pytest.raises(OracleError) as er2:
+        reference.replay_kpft(b"KPFT" + (1).to_bytes(2, "little") + (64).to_bytes(2, "little")
+                              + b[0:64 * st].tobytes(), S.CAP, 1, S.MIXED_LABELS, 33)
+    assert str(e2.value) == str(er2.value)
+
+
 def test_stats_merge_two_shards(ctx):
     """Multi-GPU shard-and-reduce on one device: two shards of a body, each
     replayed with its stream_base, stats exported, gathered and merged,
@@ -666,3 +711,56 @@ def test_reports_from_gpu_results_byte_identical(ctx, name):
     assert R.dumps(R.replay_report(name, sim, stats, cp, r, cost)) == _golden(name, "replay")
     assert R.dumps(R.model_report(name, sim, stats, cp, cost, PARAMS.get(name))) == \
         _golden(name, "model")
+
+
+# ---------------------------------------------------------------------------
+# the deep thread-per-stream kernel (k_tpsd): nesting 9..64, circular wraps,
+# TMA windows (one even start slot per batch) and cp.async windows (mixed or
+# odd starts, windows across the wrap), clock wraps and >= 2^32 pairs (routed
+# to the exact path), broken nesting, capacities at and past its 512 limit
+# ---------------------------------------------------------------------------
+
+DEEP_CASES = [
+    dict(n_streams=96, cap=256, depth=64),                          # TMA, config-5-like
+    dict(n_streams=96, cap=256, depth=20, same_start=False),        # cp.async
+    dict(n_streams=64, cap=256, depth=33, odd=True),                # odd start
+    dict(n_streams=70, cap=512, depth=64),                          # 9-bit positions
+    dict(n_streams=64, cap=514, depth=12),                          # past the deep limit
+    dict(n_streams=64, cap=128, depth=50, big_gaps=True),           # clock wraps
+    dict(n_streams=64, cap=256, depth=30, violate=True),            # broken nesting
+    dict(n_streams=33, cap=64, depth=10, same_start=False, big_gaps=True),
+]
+
+
+@pytest.mark.parametrize("case", range(len(DEEP_CASES)))
+def test_deep_kernel_vs_oracle(ctx, oracle, case):
+    t = T()
+    for seed in range(3):
+        data, cap, strategy, labels = fuzz.deep_image(31000 + 10 * case + seed,
+                                                      **DEEP_CASES[case])
+        try:
+            o, oerr = oracle.replay_kpft(data, cap, strategy, labels, 33), None
+        except O.OracleError as e:
+            o, oerr = None, (e.category, str(e))
+        try:
+            r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33, flags=0x2)
+            gerr = None
+        except t.Error as e:
+            r, gerr = None, (e.category(), str(e))
+        assert oerr == gerr, (case, seed, oerr, gerr)
+        if oerr:
+            continue
+        assert len(r.events) == len(o.events) > 0
+        assert np.array_equal(r.events, o.events), (case, seed)
+        assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+                r.malformed_groups) == (o.dropped_heads, o.truncated_tails,
+                                        o.flagged_preconditions, o.malformed_groups)
+        want = oracle.region_stats(o.events, labels)
+        got = ctx.stats()
+        assert list(got) == [s.label for s in want]
+        for s in want:
+            g = got[s.label]
+            assert (g.count, g.min, g.max, g.sum, g.mean, g.first_event, g.warp_group,
+                    g.kind, g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
+                                        s.first_event, s.warp_group, s.kind,
+                                        s.hist), (case, seed, s.label)

@@ -133,6 +133,7 @@ struct wgpf_ctx {
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   DevBuf d_nccl_send, d_nccl_recv;  // wgpf_allreduce_stats
+  DevBuf d_deep_rep;  // k_tpsd: per-CTA statistics replicas
   DevBuf d_dorph;  // k_tpsd: one orphan event per lane
   size_t smem_optin = 0;
   // pipelined replay_image (host buffers): copy streams, chunk buffers, and
@@ -751,6 +752,7 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.batch_ctr = nullptr;
   // without the thread-per-stream pass (which visits every stream) the list
   // kernels hand their SF_GENERAL entries to the general path themselves
+  f.deep_rep = nullptr;
   f.list_general = !tps_enabled(c) && deep_enabled(c) && record_cost < (1ull << 21) ? 1u : 0u;
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
@@ -787,8 +789,16 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       memset(&tmd, 0, sizeof(tmd));
       f.tma = !c->no_tma && body_tensor_map(&tmd, body, stride, n_streams, kDeepPitch) ? 1u
                                                                                         : 0u;
+      const size_t rep_bytes = 8ull * c->sms * kSmemClasses * kDeepRep;
+      ALLOC_OK(c, c->d_deep_rep, rep_bytes);
+      f.deep_rep = c->d_deep_rep.as<unsigned long long>();
+      if (!no_stats) CUDA_OK(c, cudaMemsetAsync(f.deep_rep, 0, rep_bytes, c->stream));
       deep_kernel(events != nullptr, !no_stats)<<<c->sms, dw * 32, deep_smem_bytes(dw),
                                                   c->stream>>>(f, tmd);
+      CUDA_OK(c, cudaGetLastError());
+      if (!no_stats)
+        k_deep_reduce<<<(kSmemClasses * kDeepRep + 255) / 256, 256, 0, c->stream>>>(
+            f.deep_rep, c->sms, c->K, f.stats);
       f.tma = 0;
       CUDA_OK(c, cudaGetLastError());
       ++c->launches;

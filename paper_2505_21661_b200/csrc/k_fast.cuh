@@ -63,6 +63,8 @@ struct FastArgs {
                          // takes stream (32 j + l) W + w; 1 = consecutive)
   uint32_t list_general; // list kernels hand their SF_GENERAL entries to the
                          // general path (no k_tps pass to collect them)
+  unsigned long long* deep_rep;  // k_tpsd: per-CTA count / sum / histogram
+                                 // replicas (zeroed; summed by k_deep_reduce)
 };
 
 struct LevelEntry {  // last START seen at a nesting level

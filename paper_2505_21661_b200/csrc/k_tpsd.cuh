@@ -53,22 +53,41 @@ constexpr uint32_t kDeepPitch = WinGeom<kDeepW>::kPitch;  // 48 B: 12 words
 #define WGPF_DEEP_WARPS 12
 #endif
 constexpr uint32_t kDeepWarps = WGPF_DEEP_WARPS;
+#ifndef WGPF_DEEP_UNROLL
+#define WGPF_DEEP_UNROLL 2  // record pairs per full-step loop iteration (measured: 2 > 1 by 1 %)
+#endif
+constexpr int kDeepUnroll = WGPF_DEEP_UNROLL;
 // stack meta: position | region << 9 | consumable << 15
 constexpr uint32_t kDeepMetaRid = (kDeepRegions - 1u) << 9;
 
+#ifndef WGPF_DEEP_BUFS
+#define WGPF_DEEP_BUFS 3
+#endif
+constexpr uint32_t kDeepBufs = WGPF_DEEP_BUFS;  // record windows: 2 or 3 (1 / 2 ahead)
+
 struct DeepWarpSmem {
-  uint8_t rec[2][32 * kDeepPitch];        // record windows
-  uint32_t stk_lo[kDeepDepth][32];        // START clock (low word)
-  uint16_t stk_meta[kDeepDepth][32];      // position | region | consumable
-  uint8_t cnt[kDeepRegions][32];          // iteration counters
-  unsigned long long bar[2];              // TMA windows: one mbarrier per buffer
+  uint8_t rec[kDeepBufs][32 * kDeepPitch];  // record windows
+  uint32_t stk_lo[kDeepDepth][32];          // START clock (low word)
+  uint16_t stk_meta[kDeepDepth][32];        // position | region | consumable
+  uint8_t cnt[kDeepRegions][32];            // iteration counters
+  unsigned long long bar[kDeepBufs];        // TMA windows: one mbarrier per buffer
 };
 
+// Per CTA only what needs a shared reduction: min / max (native u32 shared
+// reductions) and the first-event key.  Counts, sums and histogram bins go
+// to this CTA's own replica of the table in global memory (kDeepRep u64 per
+// class: count, sum, 64 bins) with fire-and-forget global reductions
+// (native u64 in L2; a 64-bit shared add would be a CAS loop), aggregated per
+// warp first; k_deep_reduce sums the replicas afterwards.  Per-CTA replicas
+// keep SMs off each other's L2 lines (one shared table: 40 % slower), and
+// moving the 16-KB histogram out of shared memory buys warps.
+constexpr uint32_t kDeepRep = 2 + WGPF_HIST_BINS;
 struct DeepCtaSmem {
-  SmemStats st;
+  unsigned long long first[kSmemClasses];
+  uint32_t min[kSmemClasses];
+  uint32_t max[kSmemClasses];
   uint32_t info[kDeepRegions];  // class | marker<<8 | wait class<<16
   unsigned long long warn[4];
-  uint32_t hist_spare;          // histogram increments of lanes without an event
 };
 
 __host__ __device__ inline size_t deep_smem_bytes(uint32_t warps) {
@@ -103,8 +122,8 @@ __device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
                "r"(a), "r"(v)
                : "memory");
 }
-__device__ __forceinline__ void red_add64(uint32_t a, unsigned long long v) {
-  asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+__device__ __forceinline__ void red_gadd64(unsigned long long* a, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_min32(uint32_t a, uint32_t v) {
   asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
@@ -128,7 +147,11 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       smem_raw + tps_align(sizeof(DeepCtaSmem)) + w * tps_align(sizeof(DeepWarpSmem)));
   constexpr bool stats = kStats;
   constexpr bool emit = kEmit;
-  if (stats) smem_stats_init(cs.st);
+  for (uint32_t c = threadIdx.x; c < kSmemClasses; c += blockDim.x) {
+    cs.first[c] = ~0ull;
+    cs.min[c] = 0xFFFFFFFFu;
+    cs.max[c] = 0u;
+  }
   for (uint32_t r = threadIdx.x; r < kDeepRegions; r += blockDim.x) {
     uint32_t inf = 0xFFFFFFFFu;
     if (r < a.fast_regions) {
@@ -142,8 +165,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
   if (threadIdx.x < 4) cs.warn[threadIdx.x] = 0;
   const uint32_t s_bar = smem_addr(&ws.bar[0]);  // + 8 * buffer
   if (a.tma && lane == 0) {
-    win_bar_init(s_bar);
-    win_bar_init(s_bar + 8u);
+    for (uint32_t k = 0; k < kDeepBufs; ++k) win_bar_init(s_bar + 8u * k);
     win_bar_fence();
   }
   uint32_t bphase = 0;  // parity of each buffer's next TMA completion
@@ -159,17 +181,16 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
   const uint32_t s_meta = smem_addr(&ws.stk_meta[0][lane]);  // + 64 * level
   const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);        // + 32 * region
   const uint32_t s_cnt_all = smem_addr(&ws.cnt[0][0]);
-  const uint32_t s_sum = opaque_u32(smem_addr(cs.st.sum));
-  const uint32_t s_min = opaque_u32(smem_addr(cs.st.min));
-  const uint32_t s_max = opaque_u32(smem_addr(cs.st.max));
-  const uint32_t s_hist = opaque_u32(smem_addr(cs.st.hist));
+  const uint32_t s_min = opaque_u32(smem_addr(cs.min));
+  const uint32_t s_max = opaque_u32(smem_addr(cs.max));
   // one orphan per lane, in global scratch (rare)
   wgpf_event* const orph = a.orphan_scratch + ((size_t)blockIdx.x * nw + w) * 32u + lane;
   const uint32_t s_rec = smem_addr(ws.rec[0]);
-  const uint32_t s_spare = opaque_u32(smem_addr(&cs.hist_spare));
   const uint64_t n_list = *a.list_len;
 
-  // one event per participating lane into the CTA statistics
+  // this CTA's replica of the count / sum / histogram table
+  unsigned long long* const rep = a.deep_rep + (size_t)blockIdx.x * kSmemClasses * kDeepRep;
+  // one event per participating lane into the statistics
   auto wstat = [&](bool p, uint32_t cls, uint32_t d, unsigned long long key) {
     const uint32_t pm = __ballot_sync(FULL, p);
     if (pm == 0) return;
@@ -177,11 +198,13 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     const uint32_t c0 = __reduce_min_sync(FULL, p ? cls : 0xFFFFFFFFu);
     const bool uni = c0 == __reduce_max_sync(FULL, p ? cls : 0u);
     const uint32_t leader = __ffs(pm) - 1u;
+    // histogram bin: lanes with the same bin aggregate into one reduction
+    const uint32_t bin = hist_bin32(d);
     if (uni && c0 < kSmemClasses && c0 < K) {
       // the CTA's current first key, loaded ahead of the reductions so its
       // latency overlaps them (the min below rarely needs the atomic)
       const unsigned long long cur_first =
-          *reinterpret_cast<volatile unsigned long long*>(&cs.st.first[c0]);
+          *reinterpret_cast<volatile unsigned long long*>(&cs.first[c0]);
       const uint32_t dd = p ? d : 0u;
       const uint32_t slo = __reduce_add_sync(FULL, dd & 0xFFFFu);
       const uint32_t shi = __reduce_add_sync(FULL, dd >> 16);
@@ -191,17 +214,31 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       const uint32_t khi = __reduce_min_sync(FULL, p ? (uint32_t)(key >> 32) : 0xFFFFFFFFu);
       const bool cand = p && (uint32_t)(key >> 32) == khi;
       const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
+      const uint32_t same = __match_any_sync(FULL, p ? bin : 0xFFFFFFFFu);
       if (lane == leader) {
-        // fire-and-forget shared reductions: nothing comes back to wait for
-        red_add64(s_sum + 8u * c0, (unsigned long long)slo + ((unsigned long long)shi << 16));
+        // fire-and-forget reductions: nothing comes back to wait for
+        red_gadd64(rep + c0 * kDeepRep, (unsigned long long)__popc(pm));
+        red_gadd64(rep + c0 * kDeepRep + 1u,
+                   (unsigned long long)slo + ((unsigned long long)shi << 16));
         red_min32(s_min + 4u * c0, mn);
         red_max32(s_max + 4u * c0, mx);
         const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
-        if (fk < cur_first) atomicMin(&cs.st.first[c0], fk);
+        if (fk < cur_first) atomicMin(&cs.first[c0], fk);
       }
-      red_add(p ? s_hist + 4u * (c0 * WGPF_HIST_BINS + hist_bin32(d)) : s_spare, 1u);
+      if (p && lane == __ffs(same) - 1u)
+        red_gadd64(rep + c0 * kDeepRep + 2u + bin, (unsigned long long)__popc(same));
     } else if (p) {
-      stats_add_one(cs.st, a.stats, cls, d, key, &a.status->synth_overflow);
+      if (cls < kSmemClasses && cls < K) {
+        red_gadd64(rep + cls * kDeepRep, 1ull);
+        red_gadd64(rep + cls * kDeepRep + 1u, (unsigned long long)d);
+        red_gadd64(rep + cls * kDeepRep + 2u + bin, 1ull);
+        red_min32(s_min + 4u * cls, d);
+        red_max32(s_max + 4u * cls, d);
+        smin64(&cs.first[cls], key);
+      } else {
+        stats_add_global(a.stats, stats_slot(a.stats, cls, &a.status->synth_overflow), d,
+                         key);
+      }
     }
   };
 
@@ -291,8 +328,13 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     if (n > 0) r0 = slots[start];
     if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
     uint32_t inf0 = cs.info[(r0.x >> 12) & (kDeepRegions - 1u)];
+    // kDeepBufs - 1 windows in flight ahead of the walk
     issue(0, 2);
     cp_async_commit();
+    if (kDeepBufs == 3) {
+      if (kDeepW < nmax) issue(1, 2 + kDeepW);
+      cp_async_commit();
+    }
 
     // stack top: offset 64 * level (meta) / 128 * level (clock); empty = -64
     // (reads one row below each array: bytes of the preceding arrays, never
@@ -411,11 +453,15 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 
     const uint32_t nmin = __reduce_min_sync(FULL, act ? n : 0u);
     const bool even_start = __all_sync(FULL, (start & 1u) == 0u);
+    uint32_t bsel = 0, bnext = kDeepBufs - 1u;  // window k's buffer: k % kDeepBufs
+    constexpr uint32_t ahead = (kDeepBufs - 1u) * kDeepW;
     for (uint32_t w0 = 0; w0 < nmax; w0 += kDeepW) {
-      const uint32_t bsel = (w0 / kDeepW) & 1u;
-      if (w0 + kDeepW < nmax) issue(bsel ^ 1u, w0 + kDeepW + 2u);
+      if (w0 + ahead < nmax) issue(bnext, w0 + ahead + 2u);
       cp_async_commit();
-      cp_async_wait1();
+      if (kDeepBufs == 3)
+        cp_async_wait2();
+      else
+        cp_async_wait1();
       if ((tma_buf >> bsel) & 1u) {
         win_wait(s_bar + 8u * bsel, (bphase >> bsel) & 1u);
         bphase ^= 1u << bsel;
@@ -427,7 +473,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         if (even_start) {
           // 16-B record pairs: one conflict-free LDS.128 per two steps
           const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
-#pragma unroll 1
+#pragma unroll kDeepUnroll
           for (uint32_t j = 0; j < kDeepW; j += 2) {
             const uint4 q = myrec2[j / 2];
             step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
@@ -442,6 +488,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         for (uint32_t j = 0; j < kDeepW; ++j) step(std::false_type{}, w0 + j, myrec[j]);
       }
       __syncwarp();
+      bsel = bsel == kDeepBufs - 1u ? 0u : bsel + 1u;
+      bnext = bnext == kDeepBufs - 1u ? 0u : bnext + 1u;
     }
     const bool bad = broken || n_orph > 1;
     const bool po = act && !bad && n_orph == 1;
@@ -480,19 +528,36 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     if (m) atomicAdd(&cs.warn[3], m);
   }
   __syncthreads();
-  if (stats) {
-    // counts = histogram sums (every event, on either statistics path, adds
-    // exactly one histogram increment; the warp-uniform path keeps no count)
-    for (uint32_t c = threadIdx.x; c < kSmemClasses; c += blockDim.x) {
-      unsigned long long t = 0;
-      for (uint32_t b = 0; b < WGPF_HIST_BINS; ++b) t += cs.st.hist[c * WGPF_HIST_BINS + b];
-      cs.st.count[c] = t;
-    }
-    __syncthreads();
-  }
   if (threadIdx.x < 4 && cs.warn[threadIdx.x])
     atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
-  if (stats) smem_stats_flush(cs.st, a.stats);
+  if (stats) {  // the CTA's min / max / first keys into the global table
+    const uint32_t kc = K < kSmemClasses ? K : kSmemClasses;
+    for (uint32_t c = threadIdx.x; c < kc; c += blockDim.x) {
+      if (cs.min[c] == 0xFFFFFFFFu && cs.max[c] == 0u && cs.first[c] == ~0ull) continue;
+      atomicMin(&a.stats.min[c], (unsigned long long)cs.min[c]);
+      atomicMax(&a.stats.max[c], (unsigned long long)cs.max[c]);
+      atomicMin(&a.stats.first[c], cs.first[c]);
+    }
+  }
+}
+
+// Sums the per-CTA replicas of the deep kernel into the global table.
+__global__ void k_deep_reduce(const unsigned long long* rep, uint32_t ctas, uint32_t K,
+                              DevStats st) {
+  const uint32_t kc = K < kSmemClasses ? K : kSmemClasses;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < kc * kDeepRep;
+       i += gridDim.x * blockDim.x) {
+    unsigned long long t = 0;
+    for (uint32_t b = 0; b < ctas; ++b) t += rep[(size_t)b * kSmemClasses * kDeepRep + i];
+    if (!t) continue;
+    const uint32_t c = i / kDeepRep, f = i % kDeepRep;
+    if (f == 0)
+      atomicAdd(&st.count[c], t);
+    else if (f == 1)
+      atomicAdd(&st.sum[c], t);
+    else
+      atomicAdd(&st.hist[c * WGPF_HIST_BINS + (f - 2)], t);
+  }
 }
 
 }  // namespace wgpf

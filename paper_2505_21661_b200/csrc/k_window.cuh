@@ -40,6 +40,9 @@ __device__ __forceinline__ void cp_async_commit() {
 __device__ __forceinline__ void cp_async_wait1() {
   asm volatile("cp.async.wait_group 1;" ::: "memory");
 }
+__device__ __forceinline__ void cp_async_wait2() {
+  asm volatile("cp.async.wait_group 2;" ::: "memory");
+}
 
 template <uint32_t kW = kTpsW>
 struct RecWindowsT {

@@ -560,6 +560,14 @@ def main():
                                          "t_cublas_ms", "accuracy_rel_err",
                                          "smem_profile_bytes_per_cta",
                                          "record_cost_cycles")}
+        # per-scope accuracy (record-derived scope durations vs the
+        # uninstrumented kernel's own clock), the north-star's 2 % measure
+        acc = bench_p1.measure_accuracy(reps=3)
+        p1line["accuracy_kernel_rel_err"] = p1line["accuracy_rel_err"]
+        p1line["accuracy_rel_err"] = acc["rel_err_max"]
+        p1line["accuracy_scopes"] = [{k: o[k] for k in ("scope", "chain", "true_cycles",
+                                                         "record_cycles", "rel_err")}
+                                     for o in acc["scopes"]]
 
     if rank == 0:
         line = {

@@ -332,6 +332,104 @@ def measure_attn(B: int = 16, H: int = 16, S: int = 8192, iters: int = 20,
     return line
 
 
+def measure_accuracy(chains=(1000, 10000, 100000), scopes=(8, 40), ctas: int = 148,
+                     warps: int = 4, reps: int = 7, record_cost: int | None = None,
+                     mem_chains=(100, 1000)) -> dict:
+    """Per-scope timing accuracy (PAPER.md:23, 2 % relative error): every
+    warp runs scopes of a dependent integer chain (csrc_p1/p1_selftest.cu
+    k_accuracy).  Ground truth, without any scope records: the uninstrumented
+    kernel's per-scope time as the slope between two scope counts -- in SM
+    cycles from its per-CTA %clock span (same clock the records use, so SM
+    clock changes between launches cancel), and in ns from CUDA events for
+    reference.  Measured: the mean decoded, sync-corrected scope duration of
+    the instrumented kernel (cycles).  Two scope kinds: integer MAD chains
+    (deterministic) and chains of dependent global loads through a random
+    64-MB cycle (memory latency, L2 misses: variable).  Returns per chain the
+    truth, the measurement and the relative error (cycles)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2505_21661_b200 import p1
+    from paper_2505_21661_b200 import trace as T
+    L = p1.lib()
+    stream = torch.cuda.current_stream().cuda_stream
+    s1, s2 = scopes
+    cap = 1
+    while cap < 2 * s2:
+        cap *= 2
+    n_streams = ctas * warps
+    prof = torch.zeros(ctas * warps * p1.stream_stride(cap), dtype=torch.uint8, device="cuda")
+    timing = torch.zeros(ctas * 32, dtype=torch.uint8, device="cuda")
+    ev = torch.empty(n_streams * cap * 32, dtype=torch.uint8, device="cuda")
+    ctx = T.Context(0)
+    ctx.set_plan(T.BufferPlan(cap, T.BufferStrategy.Circular, ["scope"]))
+    if record_cost is None:
+        c0 = torch.zeros(4, dtype=torch.int64, device="cuda")
+        c1 = torch.zeros(4, dtype=torch.int64, device="cuda")
+        p1.record_cost(1 << 14, 4, False, c0.data_ptr())
+        p1.record_cost(1 << 14, 4, True, c1.data_ptr())
+        torch.cuda.synchronize()
+        record_cost = int(round((c1.float().mean() - c0.float().mean()).item() / (2 << 14)))
+
+    # a random cyclic permutation of 16 M entries (64 MB > L2)
+    n_chase = 1 << 24
+    perm = np.random.default_rng(0).permutation(n_chase).astype(np.uint32)
+    nxt = np.empty(n_chase, np.uint32)
+    nxt[perm] = np.roll(perm, -1)
+    chase = torch.from_numpy(nxt.view(np.int32)).cuda()
+    mem = [False]
+
+    def run(scopes_n, chain, instr):
+        rc = L.wgpf_p1_accuracy(ctas, warps, scopes_n, chain, int(instr),
+                                C.c_void_p(prof.data_ptr() if instr else 0), cap,
+                                C.c_void_p(timing.data_ptr()),
+                                C.c_void_p(chase.data_ptr() if mem[0] else 0), n_chase - 1,
+                                C.c_void_p(stream))
+        assert rc == 0, rc
+
+    def timed(fn):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        tm = timing.cpu().numpy().view(p1.CTA_TIMING_DTYPE)
+        span = ((tm["clk_end"].astype(np.int64) - tm["clk_start"]) & 0xFFFFFFFF)
+        return e0.elapsed_time(e1) * 1e6, float(np.median(span))  # ns, cycles
+
+    out = []
+    for kind, chain in [("mad", c) for c in chains] + [("load", c) for c in mem_chains]:
+        mem[0] = kind == "load"
+        run(s2, chain, False)
+        truth_c, truth_ns, meas = [], [], []
+        for _ in range(reps):
+            na, ca = timed(lambda: run(s1, chain, False))
+            nb, cb = timed(lambda: run(s2, chain, False))
+            truth_c.append((cb - ca) / (s2 - s1))
+            truth_ns.append((nb - na) / (s2 - s1))
+            run(s2, chain, True)
+            torch.cuda.synchronize()
+            ne, _ = ctx.replay_device(prof.data_ptr(), prof.numel(), n_streams, record_cost,
+                                      ev.data_ptr(), n_streams * cap)
+            e = ev[:ne * 32].cpu().numpy().view(T.EVENT_DTYPE)
+            meas.append(float((e["end"] - e["start"]).astype(np.float64).mean()))
+        t_c, m_c = float(np.median(truth_c)), float(np.median(meas))
+        out.append({"scope": kind, "chain": chain, "true_cycles": t_c, "record_cycles": m_c,
+                    "true_ns_events": float(np.median(truth_ns)),
+                    "rel_err": abs(m_c - t_c) / t_c})
+    return {"record_cost_cycles_used": record_cost, "scopes": out,
+            "rel_err_max": max(o["rel_err"] for o in out),
+            "method": "scope = dependent IMAD chain or dependent global-load chain (64-MB "
+                      "random cycle) per warp (148 CTAs x 4 warps); truth = "
+                      "slope of the uninstrumented kernel's per-CTA %clock span between "
+                      f"{s1} and {s2} scopes (SM cycles; CUDA-event ns alongside); "
+                      "measured = mean decoded sync-corrected scope cycles of the "
+                      f"instrumented kernel (median of {reps})"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=8192)
@@ -340,8 +438,12 @@ def main():
     ap.add_argument("--iters", type=int, default=25)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--attn", action="store_true", help="config 3 (attention)")
+    ap.add_argument("--accuracy", action="store_true", help="per-scope accuracy only")
     ap.add_argument("--seq", type=int, default=8192)
     args = ap.parse_args()
+    if args.accuracy:
+        print(json.dumps(measure_accuracy()), flush=True)
+        return
     if args.attn:
         print(json.dumps(measure_attn(S=args.seq, iters=args.iters,
                                       warmup=args.warmup)), flush=True)

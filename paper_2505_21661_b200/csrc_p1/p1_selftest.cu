@@ -237,13 +237,16 @@ __global__ void k_loop_entry(uint32_t n, uint32_t trips, uint64_t* cycles,
 // slope is the true per-scope time.  The record-derived scope durations
 // (decoded, sync-corrected) are converted to ns with the SM clock rate of the
 // CtaTiming side records.
+// chase != null: the scope is a chain of dependent global loads through a
+// random cycle (memory-latency scopes, L2 misses) instead of integer MADs.
 template <bool kInstr>
 __global__ void k_accuracy(uint8_t* profile, uint32_t cap, uint32_t scopes, uint32_t chain,
-                           wgpf_dev::CtaTiming* timing, uint32_t* sink) {
+                           wgpf_dev::CtaTiming* timing, const uint32_t* chase,
+                           uint32_t chase_mask, uint32_t* sink) {
   extern __shared__ __align__(16) uint8_t buf[];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
   const uint32_t nwarps = blockDim.x >> 5;
-  if (kInstr && threadIdx.x == 0 && timing) {
+  if (threadIdx.x == 0 && timing) {
     timing[blockIdx.x].smid = wgpf_dev::smid();
     timing[blockIdx.x].streams = nwarps;
     timing[blockIdx.x].gt_start = wgpf_dev::globaltimer();
@@ -252,10 +255,15 @@ __global__ void k_accuracy(uint8_t* profile, uint32_t cap, uint32_t scopes, uint
   std::conditional_t<kInstr, wgpf_dev::Recorder<true>, wgpf_dev::NullRecorder> rec;
   rec.init(buf, warp, cap, lane == 0);
   uint32_t x = threadIdx.x + 1u, a = 1664525u + (blockIdx.x & 1u);
+  if (chase) x = (x * 2654435761u + blockIdx.x * 40503u) & chase_mask;
   for (uint32_t s = 0; s < scopes; ++s) {
     rec.start(0);
+    if (chase) {
+      for (uint32_t i = 0; i < chain; ++i) x = __ldcg(chase + x);
+    } else {
 #pragma unroll 4
-    for (uint32_t i = 0; i < chain; ++i) x = x * a + 1013904223u;
+      for (uint32_t i = 0; i < chain; ++i) x = x * a + 1013904223u;
+    }
     rec.end(0);
   }
   if constexpr (kInstr) {
@@ -263,10 +271,14 @@ __global__ void k_accuracy(uint8_t* profile, uint32_t cap, uint32_t scopes, uint
     __syncthreads();
     wgpf_dev::flush(buf, profile, blockIdx.x, wgpf_dev::smem_bytes(nwarps, cap), threadIdx.x,
                     blockDim.x);
-    if (threadIdx.x == 0 && timing) {
-      timing[blockIdx.x].gt_end = wgpf_dev::globaltimer();
-      timing[blockIdx.x].clk_end = wgpf_dev::clock32();
-    }
+  } else {
+    __syncthreads();
+  }
+  // (the uninstrumented kernel keeps the CTA timing too: its cycles between
+  // two scope counts are the ground truth in the SM's own clock)
+  if (threadIdx.x == 0 && timing) {
+    timing[blockIdx.x].gt_end = wgpf_dev::globaltimer();
+    timing[blockIdx.x].clk_end = wgpf_dev::clock32();
   }
   if (x == 0xFFFFFFFFu) sink[0] = x;
 }
@@ -275,7 +287,9 @@ __global__ void k_accuracy(uint8_t* profile, uint32_t cap, uint32_t scopes, uint
 
 extern "C" int wgpf_p1_accuracy(uint32_t ctas, uint32_t warps, uint32_t scopes,
                                 uint32_t chain, int instr, void* d_profile, uint32_t cap,
-                                void* d_timing, void* stream) {
+                                void* d_timing, const void* d_chase, uint32_t chase_mask,
+                                void* stream) {
+  const uint32_t* chase = static_cast<const uint32_t*>(d_chase);
   static uint32_t* sink = nullptr;
   if (!sink) cudaMalloc(&sink, 4);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -286,9 +300,11 @@ extern "C" int wgpf_p1_accuracy(uint32_t ctas, uint32_t warps, uint32_t scopes,
     k_accuracy<true><<<ctas, warps * 32, smem, st>>>(static_cast<uint8_t*>(d_profile), cap,
                                                      scopes, chain,
                                                      static_cast<wgpf_dev::CtaTiming*>(d_timing),
-                                                     sink);
+                                                     chase, chase_mask, sink);
   } else {
-    k_accuracy<false><<<ctas, warps * 32, 0, st>>>(nullptr, cap, scopes, chain, nullptr, sink);
+    k_accuracy<false><<<ctas, warps * 32, 0, st>>>(
+        nullptr, cap, scopes, chain, static_cast<wgpf_dev::CtaTiming*>(d_timing), chase,
+        chase_mask, sink);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 10;
 }

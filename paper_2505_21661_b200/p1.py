@@ -72,7 +72,7 @@ def lib() -> C.CDLL:
                                           vp]
         L.wgpf_p1_run_program.restype = i32
         L.wgpf_p1_loop_entry.argtypes = [u32, u32, u32, i32, vp, vp]
-        L.wgpf_p1_accuracy.argtypes = [u32, u32, u32, u32, i32, vp, u32, vp, vp]
+        L.wgpf_p1_accuracy.argtypes = [u32, u32, u32, u32, i32, vp, u32, vp, vp, u32, vp]
         L.wgpf_p1_accuracy.restype = i32
         L.wgpf_p1_loop_entry.restype = i32
         _lib = L

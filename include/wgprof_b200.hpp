@@ -38,6 +38,7 @@
 #include <sstream>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -243,27 +244,76 @@ inline void set_plan(std::uint64_t slots, BufferStrategy st,
                       static_cast<std::uint32_t>(p.size())));
 }
 
+// The host side of the value-semantics API (one std::string-labelled
+// TimelineEvent per event, vectors of ProfileRecord) is per-element work:
+// it runs over the host's cores in contiguous ranges.
+inline unsigned host_threads() {
+  static const unsigned n = [] {
+    const unsigned h = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(32u, h ? h : 1u));
+  }();
+  return n;
+}
+template <class F>  // f(begin, end, part)
+inline void parallel_ranges(std::size_t n, F&& f, std::size_t min_per = 1u << 16) {
+  const unsigned parts = (unsigned)std::min<std::size_t>(
+      host_threads(), std::max<std::size_t>(1, n / std::max<std::size_t>(1, min_per)));
+  if (parts <= 1) {
+    f(std::size_t(0), n, 0u);
+    return;
+  }
+  std::vector<std::thread> th;
+  const std::size_t per = (n + parts - 1) / parts;
+  for (unsigned p = 1; p < parts; ++p)
+    th.emplace_back([&, p] { f(std::min(n, p * per), std::min(n, (p + 1) * per), p); });
+  f(std::size_t(0), std::min(n, per), 0u);
+  for (auto& t : th) t.join();
+}
+
 // TimelineEvents -> 32-byte events with a dense label table (first-seen order)
 inline std::vector<wgpf_event> pack_events(const std::vector<TimelineEvent>& events,
                                            std::vector<std::string>& table) {
-  std::unordered_map<std::string, std::uint32_t> ids;
-  std::vector<wgpf_event> ev(events.size() + 1);
-  for (std::size_t i = 0; i < events.size(); ++i) {
-    const auto& e = events[i];
-    auto it = ids.find(e.region);
-    std::uint32_t id;
-    if (it == ids.end()) {
-      id = static_cast<std::uint32_t>(table.size());
-      ids.emplace(e.region, id);
-      table.push_back(e.region);
-    } else {
-      id = it->second;
+  // distinct labels per range (events repeat a handful of labels: each
+  // lookup first compares with the range's previous label), merged in
+  // first-seen order; then the ids
+  const std::size_t n = events.size();
+  const unsigned parts = host_threads();
+  std::vector<std::vector<std::string>> seen(parts);
+  parallel_ranges(n, [&](std::size_t lo, std::size_t hi, unsigned p) {
+    std::unordered_map<std::string_view, bool> m;
+    const std::string* last = nullptr;
+    for (std::size_t i = lo; i < hi; ++i) {
+      const std::string& r = events[i].region;
+      if (last && r == *last) continue;
+      last = &r;
+      if (m.emplace(r, true).second) seen[p].push_back(r);
     }
-    ev[i] = wgpf_event{e.start, e.end,
-                       id | (e.kind == EventKind::Wait ? WGPF_EV_WAIT : 0u) |
-                           (e.corrected ? WGPF_EV_CORRECTED : 0u),
-                       e.iteration, e.block_index, e.warp_group};
-  }
+  });
+  std::unordered_map<std::string_view, std::uint32_t> ids;
+  for (auto& v : seen)
+    for (auto& l : v)
+      if (!ids.count(l)) {
+        table.push_back(l);
+        ids.emplace(table.back(), 0);
+      }
+  ids.clear();
+  for (std::uint32_t k = 0; k < table.size(); ++k) ids.emplace(table[k], k);
+  std::vector<wgpf_event> ev(n + 1);
+  parallel_ranges(n, [&](std::size_t lo, std::size_t hi, unsigned) {
+    const std::string* last = nullptr;
+    std::uint32_t last_id = 0;
+    for (std::size_t i = lo; i < hi; ++i) {
+      const auto& e = events[i];
+      if (!last || e.region != *last) {
+        last = &e.region;
+        last_id = ids.find(e.region)->second;
+      }
+      ev[i] = wgpf_event{e.start, e.end,
+                         last_id | (e.kind == EventKind::Wait ? WGPF_EV_WAIT : 0u) |
+                             (e.corrected ? WGPF_EV_CORRECTED : 0u),
+                         e.iteration, e.block_index, e.warp_group};
+    }
+  });
   return ev;
 }
 
@@ -294,30 +344,31 @@ inline void put_u32(std::vector<std::uint8_t>& o, std::uint32_t v) {
 // memory and never serialise it, so the v1 u16 count limit must not apply.
 template <class Img>
 inline std::vector<std::uint8_t> pack_image(const Img& img) {
-  std::size_t bytes = 16;
-  for (const auto& s : img.streams) bytes += 16 + 8 * s.slots.size();
-  std::vector<std::uint8_t> out;
-  out.reserve(bytes);
-  const std::uint64_t n = img.streams.size();
-  for (char c : {'K', 'P', 'F', 'T'}) out.push_back(static_cast<std::uint8_t>(c));
-  out.push_back(2);
-  out.push_back(0);
-  out.push_back(0);
-  out.push_back(0);
-  for (int i = 0; i < 8; ++i) out.push_back(static_cast<std::uint8_t>(n >> (8 * i)));
-  for (const auto& s : img.streams) {
+  static_assert(sizeof(ProfileRecord) == 8, "ProfileRecord is {u32 tag, u32 payload}");
+  const std::size_t ns = img.streams.size();
+  std::vector<std::size_t> at(ns + 1);
+  at[0] = 16;
+  for (std::size_t k = 0; k < ns; ++k) {
+    const auto& s = img.streams[k];
     if (s.slots.size() != s.slot_capacity)
       throw Error(ErrorKind::Trace,
                   "stream slot count does not match its declared capacity");
-    put_u32(out, s.block_index);
-    put_u32(out, s.warp_group);
-    put_u32(out, s.record_count);
-    put_u32(out, s.slot_capacity);
-    for (const auto& r : s.slots) {
-      put_u32(out, r.tag);
-      put_u32(out, r.payload);
-    }
+    at[k + 1] = at[k] + 16 + 8 * s.slots.size();
   }
+  std::vector<std::uint8_t> out(at[ns]);
+  const std::uint64_t n = ns;
+  std::memcpy(out.data(), "KPFT\x02\0\0\0", 8);
+  std::memcpy(out.data() + 8, &n, 8);
+  // (records and headers are little-endian u32s: the host layout)
+  parallel_ranges(ns, [&](std::size_t lo, std::size_t hi, unsigned) {
+    for (std::size_t k = lo; k < hi; ++k) {
+      const auto& s = img.streams[k];
+      const std::uint32_t h[4] = {s.block_index, s.warp_group, s.record_count,
+                                  s.slot_capacity};
+      std::memcpy(out.data() + at[k], h, 16);
+      std::memcpy(out.data() + at[k] + 16, s.slots.data(), 8 * s.slots.size());
+    }
+  }, 1024);
   return out;
 }
 
@@ -364,15 +415,26 @@ inline GlobalTraceImage deserialize_image(const std::vector<std::uint8_t>& bytes
     throw Error(ErrorKind::Trace, "bad magic: not a trace image");
   need(4, 2);
   const std::uint16_t version = bytes[4] | (bytes[5] << 8);
-  if (version != kTraceVersion)
+  // version 1 as the reference; version 2 is this framework's container for
+  // more than 65,535 streams (u64 count, include/wgpf_format.h) -- an
+  // extension: the reference rejects it here (trace.hpp:187-190)
+  if (version != kTraceVersion && version != 2)
     throw Error(ErrorKind::Trace,
                 "unsupported trace version " + std::to_string(version));
-  need(6, 2);
-  const std::uint16_t count = bytes[6] | (bytes[7] << 8);
+  std::uint64_t count = 0;
   std::size_t pos = 8;
+  if (version == 1) {
+    need(6, 2);
+    count = bytes[6] | (bytes[7] << 8);
+  } else {
+    need(8, 8);
+    count = static_cast<std::uint64_t>(u32(8)) | (static_cast<std::uint64_t>(u32(12)) << 32);
+    pos = 16;
+  }
   GlobalTraceImage img;
   img.streams.resize(count);
-  for (auto& s : img.streams) {
+  std::vector<std::size_t> at(count);
+  for (auto& s : img.streams) {  // framing, in order (the reference's errors)
     need(pos, 16);
     s.block_index = u32(pos);
     s.warp_group = u32(pos + 4);
@@ -380,14 +442,19 @@ inline GlobalTraceImage deserialize_image(const std::vector<std::uint8_t>& bytes
     s.slot_capacity = u32(pos + 12);
     pos += 16;
     need(pos, static_cast<std::size_t>(s.slot_capacity) * 8);
-    s.slots.resize(s.slot_capacity);
-    for (auto& r : s.slots) {
-      r = decode_record(&bytes[pos]);
-      pos += 8;
-    }
+    at[&s - img.streams.data()] = pos;
+    pos += static_cast<std::size_t>(s.slot_capacity) * 8;
   }
   if (pos != bytes.size())
     throw Error(ErrorKind::Trace, "trailing bytes after trace image");
+  static_assert(sizeof(ProfileRecord) == 8, "ProfileRecord is {u32 tag, u32 payload}");
+  b200::parallel_ranges(count, [&](std::size_t lo, std::size_t hi, unsigned) {
+    for (std::size_t k = lo; k < hi; ++k) {
+      auto& s = img.streams[k];
+      s.slots.resize(s.slot_capacity);
+      std::memcpy(s.slots.data(), bytes.data() + at[k], 8ull * s.slot_capacity);
+    }
+  }, 1024);
   return img;
 }
 
@@ -492,16 +559,18 @@ inline TraceReplay replay_image(const GlobalTraceImage& image,
   const auto bytes = b200::pack_image(image);
   std::size_t cap = 1;
   for (const auto& s : image.streams) cap += s.slot_capacity / 2 + 1;
-  std::vector<wgpf_event> ev(cap);
+  // (not value-initialised: the pages are first written by the copy-out)
+  std::unique_ptr<wgpf_event[]> ev(new wgpf_event[cap]);
   std::uint64_t n = 0;
   wgpf_warnings w{};
   int rc = wgpf_replay_image(b200::ctx(), bytes.data(), bytes.size(), record_cost,
-                             ev.data(), ev.size(), 0, &n, &w);
+                             ev.get(), cap, 0, &n, &w);
   b200::check(rc);
   TraceReplay out;
-  out.events.reserve(n);
-  for (std::uint64_t i = 0; i < n; ++i)
-    out.events.push_back(b200::to_event(ev[i], plan.region_labels));
+  out.events.resize(n);
+  b200::parallel_ranges(n, [&](std::size_t lo, std::size_t hi, unsigned) {
+    for (std::size_t i = lo; i < hi; ++i) out.events[i] = b200::to_event(ev[i], plan.region_labels);
+  });
   out.dropped_heads = w.dropped_heads;
   out.truncated_tails = w.truncated_tails;
   out.flagged_preconditions = w.flagged_preconditions;
@@ -512,24 +581,7 @@ inline TraceReplay replay_image(const GlobalTraceImage& image,
 inline std::map<std::string, RegionStats> region_stats(
     const std::vector<TimelineEvent>& events) {
   std::vector<std::string> table;
-  std::unordered_map<std::string, std::uint32_t> ids;
-  std::vector<wgpf_event> ev(events.size() + 1);
-  for (std::size_t i = 0; i < events.size(); ++i) {
-    const auto& e = events[i];
-    auto it = ids.find(e.region);
-    std::uint32_t id;
-    if (it == ids.end()) {
-      id = static_cast<std::uint32_t>(table.size());
-      ids.emplace(e.region, id);
-      table.push_back(e.region);
-    } else {
-      id = it->second;
-    }
-    ev[i] = wgpf_event{e.start, e.end,
-                       id | (e.kind == EventKind::Wait ? WGPF_EV_WAIT : 0u) |
-                           (e.corrected ? WGPF_EV_CORRECTED : 0u),
-                       e.iteration, e.block_index, e.warp_group};
-  }
+  std::vector<wgpf_event> ev = b200::pack_events(events, table);
   b200::set_plan(0, BufferStrategy::Flush, table);
   std::vector<wgpf_region_stat> st(table.size() + 1);
   std::uint32_t n = 0;

@@ -38,6 +38,7 @@
 #include <cmath>
 #include <functional>
 #include <memory>
+#include <thread>
 
 using namespace wgpf;
 
@@ -134,6 +135,10 @@ struct wgpf_ctx {
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   DevBuf d_nccl_send, d_nccl_recv;  // wgpf_allreduce_stats
   DevBuf d_deep_rep;  // k_tpsd: per-CTA statistics replicas
+  // pinned bounce buffers for pageable caller memory (replay_image pipeline)
+  uint8_t* h_bounce_in[2] = {nullptr, nullptr};
+  uint8_t* h_bounce_out[2] = {nullptr, nullptr};
+  size_t bounce_in_n = 0, bounce_out_n[2] = {0, 0};
   DevBuf d_dorph;  // k_tpsd: one orphan event per lane
   size_t smem_optin = 0;
   // pipelined replay_image (host buffers): copy streams, chunk buffers, and
@@ -160,6 +165,10 @@ struct wgpf_ctx {
       if (e) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
+    for (int b = 0; b < 2; ++b) {
+      if (h_bounce_in[b]) cudaFreeHost(h_bounce_in[b]);
+      if (h_bounce_out[b]) cudaFreeHost(h_bounce_out[b]);
+    }
   }
   void mark(int i) {
     if (profiling) cudaEventRecord(ev[i], stream);
@@ -1225,6 +1234,34 @@ static constexpr uint64_t kChunkBytes = 256ull << 20;
 // on the whole image so that errors come in the reference's order
 static constexpr int WGPF_E_RETRY_WHOLE = 1000;
 
+// Host memory the caller passed: pinned (page-locked / registered) or not.
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy over several host threads (pageable <-> pinned staging): one thread
+// copies ~4 GB/s on this class of host, 8-16 copy 50-77 GB/s, PCIe's order
+static void parallel_memcpy(void* dst, const void* src, size_t n) {
+  static const unsigned kThreads = [] {
+    const unsigned h = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(16u, h ? h : 1u));
+  }();
+  const size_t piece = std::max<size_t>(4u << 20, (n + kThreads - 1) / kThreads);
+  std::vector<std::thread> th;
+  for (size_t o = piece; o < n; o += piece)
+    th.emplace_back([=] {
+      memcpy(static_cast<uint8_t*>(dst) + o, static_cast<const uint8_t*>(src) + o,
+             std::min(piece, n - o));
+    });
+  memcpy(dst, src, std::min(piece, n));
+  for (auto& t : th) t.join();
+}
+
 static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
                                 uint64_t count, uint64_t record_cost,
                                 wgpf_event* h_events, uint64_t events_cap,
@@ -1265,13 +1302,47 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
   cudaEvent_t* eH = c->pev;
   cudaEvent_t* eC = c->pev + 2;
   cudaEvent_t* eD = c->pev + 4;
+  // Pageable caller memory: an async copy from / to it would serialise the
+  // pipeline (and runs at ~10 / 18 GB/s), and registering it costs ~20 GB/s,
+  // so chunks are staged through pinned bounce buffers with a multi-threaded
+  // host memcpy instead.
+  const bool stage_in = !host_pinned(kpft);
+  const bool stage_out = !host_pinned(h_events);
+  if (stage_in && c->bounce_in_n < cs * stride) {
+    for (auto& h : c->h_bounce_in) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+    }
+    c->bounce_in_n = 0;
+    for (auto& h : c->h_bounce_in)
+      CUDA_OK(c, cudaMallocHost(reinterpret_cast<void**>(&h), cs * stride));
+    c->bounce_in_n = cs * stride;
+  }
   auto h2d = [&](uint64_t k) -> int {
     const uint32_t b = (uint32_t)(k & 1);
     const uint64_t s0 = cut[k], m = cut[k + 1] - cut[k];
     if (k >= 2) CUDA_OK(c, cudaStreamWaitEvent(c->s_h2d, eC[b], 0));
-    CUDA_OK(c, cudaMemcpyAsync(c->d_cbody[b].p, kpft + off + s0 * stride, m * stride,
-                               cudaMemcpyHostToDevice, c->s_h2d));
+    const uint8_t* src = kpft + off + s0 * stride;
+    if (stage_in) {
+      // the bounce buffer's previous copy (chunk k - 2) must have left
+      if (k >= 2) CUDA_OK(c, cudaEventSynchronize(eH[b]));
+      parallel_memcpy(c->h_bounce_in[b], src, m * stride);
+      src = c->h_bounce_in[b];
+    }
+    CUDA_OK(c, cudaMemcpyAsync(c->d_cbody[b].p, src, m * stride, cudaMemcpyHostToDevice,
+                               c->s_h2d));
     CUDA_OK(c, cudaEventRecord(eH[b], c->s_h2d));
+    return WGPF_OK;
+  };
+  // staged output: chunk k's events land in bounce_out[k & 1]; the copy to
+  // the caller's buffer happens one chunk later (or at the end)
+  uint64_t out_pending = ~0ull, out_at = 0, out_n = 0;
+  auto copy_out = [&]() -> int {
+    if (out_pending == ~0ull) return WGPF_OK;
+    const uint32_t b = (uint32_t)(out_pending & 1);
+    CUDA_OK(c, cudaEventSynchronize(eD[b]));
+    parallel_memcpy(h_events + out_at, c->h_bounce_out[b], out_n * sizeof(wgpf_event));
+    out_pending = ~0ull;
     return WGPF_OK;
   };
   auto drain = [&]() {
@@ -1332,9 +1403,26 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
     CUDA_OK(c, cudaMemcpyAsync(c->d_off_all.as<uint64_t>() + s0, c->d_offsets.p, 8 * m,
                                cudaMemcpyDeviceToDevice, c->stream));
     if (total + ne > events_cap) overflow = true;
+    if (stage_out && (rc = copy_out())) return rc;  // chunk k - 1 (frees its buffer)
     if (!overflow && ne) {
       CUDA_OK(c, cudaStreamWaitEvent(c->s_d2h, eC[b], 0));
-      CUDA_OK(c, cudaMemcpyAsync(h_events + total, c->d_cev[b].p, ne * sizeof(wgpf_event),
+      wgpf_event* dst = h_events + total;
+      if (stage_out) {
+        const size_t need = ne * sizeof(wgpf_event);
+        if (c->bounce_out_n[b] < need) {
+          if (c->h_bounce_out[b]) cudaFreeHost(c->h_bounce_out[b]);
+          c->h_bounce_out[b] = nullptr;
+          c->bounce_out_n[b] = 0;
+          CUDA_OK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_bounce_out[b]),
+                                    need + need / 4));
+          c->bounce_out_n[b] = need + need / 4;
+        }
+        dst = reinterpret_cast<wgpf_event*>(c->h_bounce_out[b]);
+        out_pending = k;
+        out_at = total;
+        out_n = ne;
+      }
+      CUDA_OK(c, cudaMemcpyAsync(dst, c->d_cev[b].p, ne * sizeof(wgpf_event),
                                  cudaMemcpyDeviceToHost, c->s_d2h));
     }
     CUDA_OK(c, cudaEventRecord(eD[b], c->s_d2h));
@@ -1347,6 +1435,7 @@ static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
     acc.malformed_groups += w.malformed_groups;
   }
   drain();
+  if (stage_out && (rc = copy_out())) return rc;
   if (n_events) *n_events = total;
   if (warnings) *warnings = acc;
   if (overflow)

@@ -62,11 +62,37 @@ __global__ void k_event_first_wg(const wgpf_event* ev, DevStats st,
 // (count + 1) in IEEE double, round-to-nearest, no contraction, over the
 // label's durations in global event order (u32 count as the reference).
 // seg[c] .. seg[c+1] index the class-sorted (stable) durations.
+// RN(num / n) for num >= 0, n >= 1 an integer below 2^53, from the
+// reciprocal y = RN(1 / n) (computed off the recurrence's critical path):
+// Markstein's correction q1 = q0 + r y with the exact FMA residual, then a
+// check that the exact quotient lies strictly inside q1's rounding interval
+// (the residual of q1, exact, against n times half the neighbouring gaps;
+// every product is exact: n < 2^53 times a power of two); a tie or a miss
+// takes the IEEE division.  Bit-identical to __ddiv_rn, ~5 dependent FP64
+// operations instead of the division's long sequence.
+__device__ __forceinline__ double div_rn_by_int(double num, double n, double y) {
+  const double q0 = __dmul_rn(num, y);
+  const double r0 = __fma_rn(-q0, n, num);
+  const double q1 = __fma_rn(r0, y, q0);
+  if (q1 <= 0.0) return num == 0.0 ? 0.0 : __ddiv_rn(num, n);
+  const double r1 = __fma_rn(-q1, n, num);  // n (x - q1), exact
+  const long long b = __double_as_longlong(q1);
+  const double up = __longlong_as_double(b + 1) - q1;    // gap above q1
+  const double down = q1 - __longlong_as_double(b - 1);  // gap below q1
+  if (r1 < 0.5 * up * n && -r1 < 0.5 * down * n) return q1;
+  return __ddiv_rn(num, n);
+}
+
+// The reference's mean recurrence (pipeline.hpp:129): mean = (mean * count +
+// d) / (count + 1) in IEEE double, round-to-nearest, no contraction, over the
+// label's durations in global event order (u32 count as the reference).  One
+// thread per class: the segment of its class in the class-sorted (stable)
+// durations is found first, so the loop's loads and reciprocals do not wait
+// on the recurrence.
 __global__ void k_exact_mean(const uint32_t* sorted_cls,
                              const unsigned long long* dur, uint64_t n,
                              const DevStats st, uint32_t n_slots,
                              double* mean_out, const int* slot_of_class_dense) {
-  // one thread per slot: binary search the segment of its class
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_slots) return;
   mean_out[i] = 0.0;
@@ -77,12 +103,20 @@ __global__ void k_exact_mean(const uint32_t* sorted_cls,
     const uint64_t mid = (lo + hi) >> 1;
     if (sorted_cls[mid] < cls) lo = mid + 1; else hi = mid;
   }
+  uint64_t end = lo, top = n;
+  while (end < top) {
+    const uint64_t mid = (end + top) >> 1;
+    if (sorted_cls[mid] <= cls) end = mid + 1; else top = mid;
+  }
   double mean = 0.0;
   uint32_t count = 0;
-  for (uint64_t k = lo; k < n && sorted_cls[k] == cls; ++k) {
+  for (uint64_t k = lo; k < end; ++k) {
+    const double d = (double)dur[k];
+    const double m1 = (double)(uint32_t)(count + 1u);
+    const double y = __drcp_rn(m1);
     const double prod = __dmul_rn(mean, (double)count);
-    const double num = __dadd_rn(prod, (double)dur[k]);
-    mean = __ddiv_rn(num, (double)(uint32_t)(count + 1u));
+    const double num = __dadd_rn(prod, d);
+    mean = div_rn_by_int(num, m1, y);
     ++count;
   }
   mean_out[i] = mean;

@@ -71,6 +71,8 @@ constexpr uint32_t kStkRid = (kTpsRegions - 1u) << 12;
 
 struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
+  uint2 stk_empty[32];               // row -1: what an empty stack reads (never
+                                     // written; its value is not used)
   uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<12 | cons<<17 | hi<<18}
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
   unsigned long long bar[2];         // TMA windows: one mbarrier per buffer
@@ -258,8 +260,8 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     cp_async_commit();
 
     // stack top as a shared address: row sp-1 of the lane's column; the
-    // empty stack points one row below (bytes of the record windows: read,
-    // never written, and only used when an END has a partner)
+    // empty stack points one row below (stk_empty: read, never written, and
+    // only used when an END has a partner)
     const uint32_t s_stk0 = s_stk - 256u;
     uint32_t hi = 0, vprev = 0, stop = s_stk0;
     uint32_t pw = 0xFFu;  // wait class of the previous record if it was a

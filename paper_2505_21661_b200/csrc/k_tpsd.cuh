@@ -67,8 +67,11 @@ constexpr uint32_t kDeepBufs = WGPF_DEEP_BUFS;  // record windows: 2 or 3 (1 / 2
 
 struct DeepWarpSmem {
   uint8_t rec[kDeepBufs][32 * kDeepPitch];  // record windows
-  uint32_t stk_lo[kDeepDepth][32];          // START clock (low word)
-  uint16_t stk_meta[kDeepDepth][32];        // position | region | consumable
+  uint32_t lo_empty[32];                    // row -1 of each stack array: what
+  uint32_t stk_lo[kDeepDepth][32];          //   an empty stack reads (never
+  uint16_t meta_empty[32];                  //   written; the value is unused)
+  uint16_t stk_meta[kDeepDepth][32];        // START clock (low word);
+                                            // position | region | consumable
   uint8_t cnt[kDeepRegions][32];            // iteration counters
   unsigned long long bar[kDeepBufs];        // TMA windows: one mbarrier per buffer
 };
@@ -337,8 +340,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     }
 
     // stack top: offset 64 * level (meta) / 128 * level (clock); empty = -64
-    // (reads one row below each array: bytes of the preceding arrays, never
-    // written, used only when an END has a partner)
+    // (reads row -1 of each array: lo_empty / meta_empty, never written, used
+    // only when an END has a partner)
     int32_t tp = -64;
     uint32_t hi = 0, vprev = 0;
     uint32_t w_last = 0, w_prev = 0;  // positions of the last two clock wraps

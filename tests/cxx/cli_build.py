@@ -78,7 +78,30 @@ def source(shim: bool) -> str:
     return head + "namespace {\n" + cmds + "}  // namespace\n" + MAIN
 
 
+SHIM_BENCH = os.path.join(OUT, "shim_bench")
+
+
+def build_shim_bench(verbose: bool = False) -> str:
+    """tests/cxx/shim_bench.cpp (the drop-in C++ path, end to end) against
+    the shim and libwgpf.so; needs no reference sources."""
+    sys.path.insert(0, ROOT)
+    from paper_2505_21661_b200 import _build
+    lib = _build.build()
+    os.makedirs(OUT, exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", os.path.join(HERE, "shim_bench.cpp"),
+           "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include", lib,
+           "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{os.path.dirname(lib)}",
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-o", SHIM_BENCH]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"building shim_bench failed:\n{r.stderr[-6000:]}")
+    if verbose:
+        print("built", SHIM_BENCH)
+    return SHIM_BENCH
+
+
 def build(verbose: bool = False) -> bool:
+    build_shim_bench(verbose)
     if not os.path.exists(TOOL):
         return os.path.exists(CLI)
     sys.path.insert(0, ROOT)

@@ -764,3 +764,24 @@ def test_deep_kernel_vs_oracle(ctx, oracle, case):
                     g.kind, g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
                                         s.first_event, s.warp_group, s.kind,
                                         s.hist), (case, seed, s.label)
+
+
+def test_exact_mean_recurrence_stress(ctx, oracle):
+    """region_stats' bit-exact mean (pipeline.hpp:129) over long chains of
+    random durations across the whole u32 range (the GPU division by the
+    count runs a Markstein step with an exactness check, falling back to the
+    IEEE division): equal to the CPU recurrence bit for bit."""
+    t = T()
+    rng = np.random.default_rng(11)
+    n = 600_000
+    ev = np.zeros(n, t.EVENT_DTYPE)
+    ev["region"] = rng.integers(0, 3, n).astype(np.uint32)
+    ev["start"] = rng.integers(0, 1 << 40, n, dtype=np.uint64)
+    scale = rng.choice([10, 1000, 1 << 20, (1 << 32) - 1], n)
+    ev["end"] = ev["start"] + (rng.random(n) * scale).astype(np.uint64)
+    labels = ["a", "b", "c"]
+    got = t.region_stats(ev, labels)
+    want = {s.label: s for s in oracle.region_stats(ev, labels)}
+    for k, s in want.items():
+        assert got[k].count == s.count and got[k].sum == s.sum
+        assert got[k].mean == s.mean, (k, got[k].mean, s.mean)

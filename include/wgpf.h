@@ -108,14 +108,20 @@ typedef struct wgpf_region_stat { /* RegionStats, pipeline.hpp:105-112 + ext */
 /* Per-phase device time of the last wgpf_replay_device (WGPF_F_PROFILE) and
  * the number of this library's kernels it launched. */
 typedef struct wgpf_profile {
-  float count_ms;    /* pass 1 (k_count_fast)                      */
-  float scan_ms;     /* event-offset scan                          */
-  float emit_ms;     /* pass 2 fast path (k_fast_emit)             */
+  float count_ms;    /* pass 1 (k_count_tps / k_count_fast); overlapped
+                        replay: pass 1 + scan of the first chunk only   */
+  float scan_ms;     /* event-offset scan (0 when overlapped)          */
+  float emit_ms;     /* pass 2 fast paths (k_tps, k_tpsd, k_fast_emit);
+                        overlapped replay: with pass 1 of every later
+                        chunk running beside it                        */
   float general_ms;  /* general path (k_general_emit), if any      */
   float finalize_ms; /* statistics finalisation                    */
   float total_ms;
   uint32_t launches;        /* kernels of this library launched     */
   uint32_t general_streams; /* streams taken by the general path   */
+  uint32_t overlap_chunks;  /* chunks of the overlapped pass 1 / pass 2
+                               (0: not overlapped)                     */
+  uint32_t reserved;
 } wgpf_profile;
 int wgpf_last_profile(const wgpf_ctx* ctx, wgpf_profile* out);
 

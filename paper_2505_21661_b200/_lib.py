@@ -55,7 +55,8 @@ class Profile(C.Structure):
     _fields_ = [("count_ms", C.c_float), ("scan_ms", C.c_float),
                 ("emit_ms", C.c_float), ("general_ms", C.c_float),
                 ("finalize_ms", C.c_float), ("total_ms", C.c_float),
-                ("launches", C.c_uint32), ("general_streams", C.c_uint32)]
+                ("launches", C.c_uint32), ("general_streams", C.c_uint32),
+                ("overlap_chunks", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class CpStage(C.Structure):

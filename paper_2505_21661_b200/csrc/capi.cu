@@ -80,10 +80,12 @@ struct DevBuf {
 using TpsKernel = void (*)(FastArgs);
 using DeepKernel = void (*)(FastArgs, const CUtensorMap);
 using TpsTmaKernel = void (*)(FastArgs, const CUtensorMap, const CUtensorMap);
-static DeepKernel deep_kernel(bool emit, bool stats) {
-  static const DeepKernel k[4] = {k_tpsd<false, false>, k_tpsd<true, false>,
-                                  k_tpsd<false, true>, k_tpsd<true, true>};
-  return k[(emit ? 1 : 0) | (stats ? 2 : 0)];
+static DeepKernel deep_kernel(bool emit, bool stats, bool markers) {
+  static const DeepKernel k[8] = {
+      k_tpsd<false, false, false>, k_tpsd<true, false, false>, k_tpsd<false, true, false>,
+      k_tpsd<true, true, false>,   k_tpsd<false, false, true>, k_tpsd<true, false, true>,
+      k_tpsd<false, true, true>,   k_tpsd<true, true, true>};
+  return k[(emit ? 1 : 0) | (stats ? 2 : 0) | (markers ? 4 : 0)];
 }
 static TpsTmaKernel tps_kernel(bool emit, bool stats) {
   static const TpsTmaKernel k[4] = {k_tps<false, false>, k_tps<true, false>,
@@ -105,6 +107,7 @@ struct wgpf_ctx {
   std::vector<std::string> class_label;  // dense classes
   std::unordered_map<std::string, uint32_t> class_by_label;
   uint32_t K = 0;
+  bool has_markers = false;  // some label is a wait marker ("X.wait")
   DevBuf d_class_of, d_wait_class, d_is_marker, d_swait_id, d_swait_cls;
   uint32_t n_synth_wait = 0;
 
@@ -132,6 +135,13 @@ struct wgpf_ctx {
   uint32_t group_hint = 0;   // W known from host headers (pipelined replay)
   uint32_t* h_blk = nullptr;  // pinned: block fields read by stream_group
   bool no_pipeline = getenv("WGPF_NO_PIPELINE") != nullptr;
+  // overlapped pass 1 / pass 2 (replay_overlapped): a second stream for the
+  // pass-1 chain, one event per chunk, chunk bases and batch counters
+  // opt-in (WGPF_OVERLAP=1): measured slower, see replay_overlapped
+  bool no_overlap = getenv("WGPF_OVERLAP") == nullptr;
+  cudaStream_t s_count = nullptr;
+  std::vector<cudaEvent_t> oev;
+  DevBuf d_obase;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
   DevBuf d_nccl_send, d_nccl_recv;  // wgpf_allreduce_stats
   DevBuf d_deep_rep;  // k_tpsd: per-CTA statistics replicas
@@ -150,6 +160,7 @@ struct wgpf_ctx {
   std::vector<uint64_t> chunk_sbase, chunk_ebase;
   uint64_t chunk_nstreams = 0;
   uint32_t launches = 0;
+  uint32_t overlap_chunks = 0;
   uint64_t general_streams = 0;
   wgpf_profile prof{};
   uint64_t last_stream_base = 0, last_n_streams = 0;
@@ -164,6 +175,9 @@ struct wgpf_ctx {
     for (auto& e : pev)
       if (e) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_count) cudaStreamDestroy(s_count);
+    for (auto& e : oev)
+      if (e) cudaEventDestroy(e);
     if (s_d2h) cudaStreamDestroy(s_d2h);
     for (int b = 0; b < 2; ++b) {
       if (h_bounce_in[b]) cudaFreeHost(h_bounce_in[b]);
@@ -352,8 +366,9 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
     for (int v = 0; v < 4; ++v) {
       cudaFuncSetAttribute(tps_kernel(v & 1, v & 2),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-      cudaFuncSetAttribute(deep_kernel(v & 1, v & 2),
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      for (int m = 0; m < 2; ++m)
+        cudaFuncSetAttribute(deep_kernel(v & 1, v & 2, m),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     }
   }
   cudaFuncSetAttribute(k_fast_emit<false>,
@@ -401,6 +416,7 @@ int wgpf_set_plan(wgpf_ctx* c, uint64_t slots, uint32_t strategy,
     }
   }
   c->K = (uint32_t)c->class_label.size();
+  c->has_markers = false;
   std::vector<uint32_t> class_of(WGPF_MAX_REGIONS);
   for (uint32_t r = 0; r < WGPF_MAX_REGIONS; ++r)
     class_of[r] = r < n_labels ? cls_of_table[r] : c->K + r;
@@ -410,6 +426,7 @@ int wgpf_set_plan(wgpf_ctx* c, uint64_t slots, uint32_t strategy,
   for (uint32_t k = 0; k < c->K; ++k) {
     const std::string& L = c->class_label[k];
     is_marker[k] = L.size() > 5 && L.compare(L.size() - 5, 5, ".wait") == 0;
+    if (is_marker[k]) c->has_markers = true;
     auto it = c->class_by_label.find(L + ".wait");
     if (it != c->class_by_label.end()) wait_class[k] = it->second;
     // out-of-table ids whose synthesized label is a table label
@@ -720,19 +737,10 @@ static bool body_tensor_map3(CUtensorMap* m, const uint8_t* body, uint64_t strid
 // slots past record_count into L2 (config 4: 1.3 GB of the body's 10 GB).
 static bool tail_maps() { return getenv("WGPF_NO_TAIL_MAP") == nullptr; }
 
-static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
-                     uint64_t n_streams, uint64_t stream_base,
-                     uint64_t record_cost, wgpf_event* events,
-                     uint64_t events_cap, bool no_stats, bool force_general) {
-  CUDA_OK(c, cudaMemsetAsync(c->d_glen.p, 0, 8, c->stream));
-  if (force_general) {
-    c->mark(3);
-    c->general_streams += n_streams;
-    int rc = run_general(c, body, stride, n_streams, stream_base, record_cost,
-                         events, events_cap, no_stats, false, n_streams);
-    c->mark(4);
-    return rc;
-  }
+// The pass-2 arguments shared by every emit kernel of one call.
+static FastArgs fast_args(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                          uint64_t n_streams, uint64_t stream_base, uint64_t record_cost,
+                          wgpf_event* events, uint64_t events_cap, bool no_stats) {
   FastArgs f;
   f.body = body;
   f.stride = stride;
@@ -759,33 +767,73 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
   f.tma = 0;
   f.group = 1;
   f.batch_ctr = nullptr;
+  f.deep_rep = nullptr;
+  f.list_base = 0;
   // without the thread-per-stream pass (which visits every stream) the list
   // kernels hand their SF_GENERAL entries to the general path themselves
-  f.deep_rep = nullptr;
   f.list_general = !tps_enabled(c) && deep_enabled(c) && record_cost < (1ull << 21) ? 1u : 0u;
+  return f;
+}
+
+// k_tps over streams [s0, s0 + n) of the call's body (W streams per block,
+// W | n): the chunk's own body pointer, tensor maps and per-stream arrays;
+// stream indices in the general list and first-event keys stay call-global.
+// bctr: the chunk's dynamic batch counter (zeroed).
+static int launch_tps(wgpf_ctx* c, FastArgs f, uint64_t s0, uint64_t n, uint32_t W,
+                      unsigned long long* bctr, cudaStream_t st) {
+  const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
+  const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
+  f.body += s0 * f.stride;
+  f.n_streams = n;
+  f.stream_base += s0;
+  f.list_base = s0;
+  f.counts += s0;
+  f.zpos += s0;
+  f.sflag += s0;
+  f.offsets += s0;
+  f.group = W;
+  f.batch_ctr = bctr;
+  CUtensorMap tm, tmt;
+  memset(&tm, 0, sizeof(tm));
+  memset(&tmt, 0, sizeof(tmt));
+  f.tma = !c->no_tma && body_tensor_map3(&tm, f.body, f.stride, n, W) ? 1u : 0u;
+  if (f.tma && !(tail_maps() && body_tensor_map3(&tmt, f.body, f.stride, n, W,
+                                                 CU_TENSOR_MAP_L2_PROMOTION_NONE)))
+    tmt = tm;
+  tps_kernel(f.events != nullptr, !f.no_stats)<<<c->sms, tw * 32, tsm, st>>>(f, tm, tmt);
+  CUDA_OK(c, cudaGetLastError());
+  ++c->launches;
+  return WGPF_OK;
+}
+
+// tps_done: the thread-per-stream pass already ran (replay_overlapped, chunk
+// by chunk, which also zeroed the general list)
+static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
+                     uint64_t n_streams, uint64_t stream_base,
+                     uint64_t record_cost, wgpf_event* events,
+                     uint64_t events_cap, bool no_stats, bool force_general,
+                     bool tps_done = false) {
+  if (!tps_done) CUDA_OK(c, cudaMemsetAsync(c->d_glen.p, 0, 8, c->stream));
+  if (force_general) {
+    c->mark(3);
+    c->general_streams += n_streams;
+    int rc = run_general(c, body, stride, n_streams, stream_base, record_cost,
+                         events, events_cap, no_stats, false, n_streams);
+    c->mark(4);
+    return rc;
+  }
+  FastArgs f = fast_args(c, body, stride, n_streams, stream_base, record_cost, events,
+                         events_cap, no_stats);
   // (record_cost < 2^21: cost x position (< 2^11) fits the kernel's 32-bit
   // correction arithmetic; larger costs take the warp-per-stream kernel)
   if ((tps_enabled(c) || deep_enabled(c)) && record_cost < (1ull << 21)) {
-    if (tps_enabled(c)) {
+    if (tps_enabled(c) && !tps_done) {
       // shallow streams: thread per stream
-      const uint32_t tw = tps_warps(c->K, f.tps_regions, c->smem_optin);
-      const size_t tsm = tps_smem_bytes(c->K, f.tps_regions, tw);
-      CUtensorMap tm, tmt;
-      memset(&tm, 0, sizeof(tm));
-      memset(&tmt, 0, sizeof(tmt));
-      f.group = stream_group(c, body, stride, n_streams);
-      f.batch_ctr = c->d_glen.as<unsigned long long>() + 4;
-      CUDA_OK(c, cudaMemsetAsync(f.batch_ctr, 0, 8, c->stream));
-      f.tma = !c->no_tma && body_tensor_map3(&tm, body, stride, n_streams, f.group) ? 1u : 0u;
-      if (f.tma && !(tail_maps() && body_tensor_map3(&tmt, body, stride, n_streams, f.group,
-                                                     CU_TENSOR_MAP_L2_PROMOTION_NONE)))
-        tmt = tm;
-      tps_kernel(events != nullptr, !no_stats)<<<c->sms, tw * 32, tsm, c->stream>>>(f, tm,
-                                                                                   tmt);
-      f.tma = 0;
-      f.group = 1;
-      CUDA_OK(c, cudaGetLastError());
-      ++c->launches;
+      unsigned long long* bctr = c->d_glen.as<unsigned long long>() + 4;
+      CUDA_OK(c, cudaMemsetAsync(bctr, 0, 8, c->stream));
+      int rc = launch_tps(c, f, 0, n_streams, stream_group(c, body, stride, n_streams), bctr,
+                          c->stream);
+      if (rc) return rc;
     }
     if (deep_enabled(c)) {
       // pass 1's deep list: thread per stream, 64-deep stacks
@@ -802,7 +850,7 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       ALLOC_OK(c, c->d_deep_rep, rep_bytes);
       f.deep_rep = c->d_deep_rep.as<unsigned long long>();
       if (!no_stats) CUDA_OK(c, cudaMemsetAsync(f.deep_rep, 0, rep_bytes, c->stream));
-      deep_kernel(events != nullptr, !no_stats)<<<c->sms, dw * 32, deep_smem_bytes(dw),
+      deep_kernel(events != nullptr, !no_stats, c->has_markers)<<<c->sms, dw * 32, deep_smem_bytes(dw),
                                                   c->stream>>>(f, tmd);
       CUDA_OK(c, cudaGetLastError());
       if (!no_stats)
@@ -843,6 +891,158 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                        events, events_cap, no_stats, true, glen);
   c->mark(4);
   return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Overlapped pass 1 / pass 2.  Pass 2 (k_tps) needs every stream's event
+// offset, i.e. pass 1 over all streams before it, and pass 1 reads the body
+// once more.  k_tps is latency-bound (about 60 % of issue slots and 65 % of
+// DRAM bandwidth used), so pass 1 of the next chunk of streams runs beside it:
+// the streams are cut into chunks of whole 32-block batch groups (32 W
+// streams, k_tps's lane mapping), chunk 0 is small and counted alone by the
+// full pass-1 kernel, and every later chunk k+1 is counted on a second stream
+// by the co-resident pass-1 kernel (one warp per CTA, two CTAs per SM at <=
+// 64 registers: they fit beside k_tps's CTA) while k_tps emits chunk k.
+// Chunk sizes grow geometrically so that the counting of chunk k+1 (on two
+// warps per SM) finishes within the emission of chunk k.  Offsets: one
+// exclusive scan per chunk whose initial value is the running total left in
+// device memory by the previous chunk (cub::FutureValue), no host round trip.
+//
+// Measured on config 4 (parity suite green with it on): 23.4 ms per replay
+// vs 6.88 ms for the plain sequence -- the co-resident pass-1 warps run at
+// ~380 cycles per record step (memory-latency bound with one 16-record window
+// in flight; the stand-alone pass hides the same ~240 cycles per step behind
+// 18 warps per SM), so the emission of every chunk waits for its count.
+// Hence opt-in (WGPF_OVERLAP=1) and kept as the measured alternative.
+// ---------------------------------------------------------------------------
+
+__global__ void k_chunk_base(const uint32_t* counts, const uint64_t* off, uint64_t n,
+                             unsigned long long* base_next) {
+  *base_next = n ? off[n - 1] + counts[n - 1] : *(base_next - 1);
+}
+__global__ void k_total_from(const unsigned long long* total, DevStatus* st) {
+  st->total_events = *total;
+}
+
+static double env_double(const char* k, double d) {
+  const char* e = getenv(k);
+  return e ? atof(e) : d;
+}
+
+// chunk starts (in streams, ending with n_streams) for the overlapped replay;
+// empty when the call is too small to split
+static std::vector<uint64_t> plan_overlap_chunks(uint64_t n_streams, uint32_t W) {
+  std::vector<uint64_t> cs;
+  const uint64_t unit = 32ull * W;
+  const uint64_t units = n_streams / unit;  // whole batch groups (the rest joins the last chunk)
+  const double first_div = env_double("WGPF_OVL_FIRST", 32.0);
+  const double growth = env_double("WGPF_OVL_GROWTH", 1.25);
+  const uint32_t max_chunks = (uint32_t)env_double("WGPF_OVL_MAX", 48.0);
+  if (units < 8) return cs;
+  double sz = std::max(1.0, (double)units / first_div);
+  uint64_t at = 0;
+  cs.push_back(0);
+  while (true) {
+    const uint64_t take = std::max<uint64_t>(1, (uint64_t)(sz + 0.5));
+    if (at + take >= units || cs.size() >= max_chunks) break;
+    at += take;
+    cs.push_back(at * unit);
+    sz *= growth;
+  }
+  cs.push_back(n_streams);
+  return cs;
+}
+
+static int replay_overlapped(wgpf_ctx* c, CountArgs ca, const uint8_t* body, uint64_t stride,
+                             uint64_t n_streams, uint64_t stream_base, uint64_t record_cost,
+                             wgpf_event* events, uint64_t events_cap, bool no_stats,
+                             uint32_t W, const std::vector<uint64_t>& cs) {
+  const size_t C = cs.size() - 1;
+  c->overlap_chunks = (uint32_t)C;
+  if (!c->s_count)
+    CUDA_OK(c, cudaStreamCreateWithFlags(&c->s_count, cudaStreamNonBlocking));
+  while (c->oev.size() < C + 1) {
+    cudaEvent_t e;
+    CUDA_OK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->oev.push_back(e);
+  }
+  // [0, C]: running event totals (chunk bases); [C + 1, 2C]: k_tps batch counters
+  ALLOC_OK(c, c->d_obase, 8 * (2 * C + 2));
+  unsigned long long* base = c->d_obase.as<unsigned long long>();
+  unsigned long long* bctr = base + C + 1;
+  CUDA_OK(c, cudaMemsetAsync(base, 0, 8 * (2 * C + 2), c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->d_glen.p, 0, 8, c->stream));  // general list
+  // scan temporary storage for the largest chunk
+  uint64_t max_n = 0;
+  for (size_t k = 0; k < C; ++k) max_n = std::max(max_n, cs[k + 1] - cs[k]);
+  auto widen = thrust::make_transform_iterator(c->d_counts.as<uint32_t>(), ToU64());
+  size_t tmp = 0;
+  CUDA_OK(c, cub::DeviceScan::ExclusiveScan(
+                 nullptr, tmp, widen, c->d_offsets.as<uint64_t>(), cuda::std::plus<uint64_t>{},
+                 cub::FutureValue<uint64_t>(reinterpret_cast<uint64_t*>(base)), (int64_t)max_n,
+                 c->s_count));
+  ALLOC_OK(c, c->d_scan_tmp, tmp);
+  // the pass-1 stream starts after this call's resets on the main stream
+  CUDA_OK(c, cudaEventRecord(c->oev[0], c->stream));
+  CUDA_OK(c, cudaStreamWaitEvent(c->s_count, c->oev[0], 0));
+
+  const FastArgs f = fast_args(c, body, stride, n_streams, stream_base, record_cost, events,
+                               events_cap, no_stats);
+  const void* k_big = (const void*)k_count_tps<kCountWarps, kCountUnroll, 1>;
+  const uint32_t g_big = grid_for(c, k_big, kCountWarps * 32, 0);
+  for (size_t k = 0; k < C; ++k) {
+    const uint64_t s0 = cs[k], n = cs[k + 1] - cs[k];
+    // pass 1 of chunk k (second stream)
+    CountArgs a = ca;
+    a.body = body + s0 * stride;
+    a.n_streams = n;
+    a.counts += s0;
+    a.zpos += s0;
+    a.sflag += s0;
+    a.list_base = s0;
+    CUtensorMap tm, tmt;
+    memset(&tm, 0, sizeof(tm));
+    memset(&tmt, 0, sizeof(tmt));
+    a.tma = !c->no_tma && body_tensor_map(&tm, a.body, stride, n, CountWin::kTpsPitch) ? 1u
+                                                                                       : 0u;
+    if (a.tma && !(tail_maps() && body_tensor_map(&tmt, a.body, stride, n, CountWin::kTpsPitch,
+                                                   CU_TENSOR_MAP_L2_PROMOTION_NONE)))
+      tmt = tm;
+    if (k == 0)
+      k_count_tps<kCountWarps, kCountUnroll, 1>
+          <<<g_big, kCountWarps * 32, 0, c->s_count>>>(a, tm, tmt);
+    else
+      k_count_tps<1, kCountCoUnroll, kCountCoMinBlocks>
+          <<<c->sms * kCountCoCtas, 32, 0, c->s_count>>>(a, tm, tmt);
+    CUDA_OK(c, cudaGetLastError());
+    ++c->launches;
+    // offsets of chunk k: exclusive scan from the running total
+    auto it = thrust::make_transform_iterator(c->d_counts.as<uint32_t>() + s0, ToU64());
+    CUDA_OK(c, cub::DeviceScan::ExclusiveScan(
+                   c->d_scan_tmp.p, tmp, it, c->d_offsets.as<uint64_t>() + s0,
+                   cuda::std::plus<uint64_t>{},
+                   cub::FutureValue<uint64_t>(reinterpret_cast<uint64_t*>(base + k)), (int64_t)n,
+                   c->s_count));
+    k_chunk_base<<<1, 1, 0, c->s_count>>>(c->d_counts.as<uint32_t>() + s0,
+                                          c->d_offsets.as<uint64_t>() + s0, n, base + k + 1);
+    CUDA_OK(c, cudaGetLastError());
+    c->launches += 2;
+    CUDA_OK(c, cudaEventRecord(c->oev[k + 1], c->s_count));
+    // pass 2 of chunk k (main stream) once its offsets exist
+    CUDA_OK(c, cudaStreamWaitEvent(c->stream, c->oev[k + 1], 0));
+    if (k == 0) {
+      c->mark(1);
+      c->mark(2);
+    }
+    int rc = launch_tps(c, f, s0, n, W, bctr + k, c->stream);
+    if (rc) return rc;
+  }
+  k_total_from<<<1, 1, 0, c->stream>>>(base + C, c->d_status.as<DevStatus>());
+  CUDA_OK(c, cudaGetLastError());
+  ++c->launches;
+  // the list kernels (deep, warp, general) over the whole call
+  return emit_pass(c, body, stride, n_streams, stream_base, record_cost, events, events_cap,
+                   no_stats, false, true);
 }
 
 static int report_errors(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
@@ -970,6 +1170,7 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   if (!c->in_chunked) c->chunk_mode = false;
   c->profiling = (flags & WGPF_F_PROFILE) != 0;
   c->launches = 0;
+  c->overlap_chunks = 0;
   c->general_streams = 0;
   c->prof = wgpf_profile{};
   c->mark(0);
@@ -996,6 +1197,7 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
 
   CountArgs ca;
   ca.tma = 0;
+  ca.list_base = 0;
   ca.body = body;
   ca.stride = stride;
   ca.n_streams = n_streams;
@@ -1028,7 +1230,19 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.deep_list = c->d_dlist.as<unsigned long long>();
   ca.deep_len = c->d_glen.as<unsigned long long>() + 2;
   CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 16, c->stream));
-  if (count_tps_enabled(c)) {
+  // pass 1 of the next chunk beside pass 2 of the current one (large calls)
+  std::vector<uint64_t> ovl;
+  uint32_t ovl_w = 1;
+  if (!c->no_overlap && !force_general && tps_enabled(c) && count_tps_enabled(c) &&
+      record_cost < (1ull << 21) && n_streams >= 4096) {
+    ovl_w = stream_group(c, body, stride, n_streams);
+    ovl = plan_overlap_chunks(n_streams, ovl_w);
+  }
+  if (!ovl.empty()) {
+    rc = replay_overlapped(c, ca, body, stride, n_streams, stream_base, record_cost, events,
+                           events_cap, no_stats, ovl_w, ovl);
+    if (rc) return rc;
+  } else if (count_tps_enabled(c)) {
     CUtensorMap tm, tmt;
     memset(&tm, 0, sizeof(tm));
     memset(&tmt, 0, sizeof(tmt));
@@ -1040,20 +1254,23 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
                                                    CountWin::kTpsPitch,
                                                    CU_TENSOR_MAP_L2_PROMOTION_NONE)))
       tmt = tm;
-    k_count_tps<<<grid_for(c, (const void*)k_count_tps, kCountWarps * 32, 0),
-                  kCountWarps * 32, 0, c->stream>>>(ca, tm, tmt);
+    const void* kc = (const void*)k_count_tps<kCountWarps, kCountUnroll, 1>;
+    k_count_tps<kCountWarps, kCountUnroll, 1>
+        <<<grid_for(c, kc, kCountWarps * 32, 0), kCountWarps * 32, 0, c->stream>>>(ca, tm, tmt);
   } else
     k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,
                    c->stream>>>(ca);
-  CUDA_OK(c, cudaGetLastError());
-  ++c->launches;
-  c->mark(1);
-  rc = scan_counts(c, n_streams);
-  if (rc) return rc;
-  c->mark(2);
-  rc = emit_pass(c, body, stride, n_streams, stream_base, record_cost, events,
-                 events_cap, no_stats, force_general);
-  if (rc) return rc;
+  if (ovl.empty()) {
+    CUDA_OK(c, cudaGetLastError());
+    ++c->launches;
+    c->mark(1);
+    rc = scan_counts(c, n_streams);
+    if (rc) return rc;
+    c->mark(2);
+    rc = emit_pass(c, body, stride, n_streams, stream_base, record_cost, events,
+                   events_cap, no_stats, force_general);
+    if (rc) return rc;
+  }
   rc = status_read(c);
   if (rc) return rc;
   if (c->h_status->invalid && c->h_status->decode_err == kNoErr) {
@@ -1119,6 +1336,7 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
     cudaEventElapsedTime(&c->prof.total_ms, c->ev[0], c->ev[5]);
   }
   c->prof.launches = c->launches;
+  c->prof.overlap_chunks = c->overlap_chunks;
   c->prof.general_streams = (uint32_t)c->general_streams;
   return WGPF_OK;
 }
@@ -1540,6 +1758,7 @@ extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
   ALLOC_OK(c, c->d_sflag, 4 * ns);
   CountArgs ca;
   ca.tma = 0;
+  ca.list_base = 0;
   ca.body = d_body;
   ca.stride = stride;
   ca.n_streams = ns;

@@ -58,6 +58,9 @@ struct CountArgs {
   uint32_t list_general; // no thread-per-stream emit kernel (every stream is
                          // listed): SF_GENERAL streams go to the warp list
                          // too, whose kernel hands them to the general path
+  uint64_t list_base;    // index of stream 0 of this body in the call's
+                         // stream arrays (overlapped chunks): list entries
+                         // and decode-error positions are call-global
 };
 
 __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
@@ -202,6 +205,13 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
 // owns stream 32 b + l and walks its records sequentially, windows staged in
 // shared memory (k_window.cuh).  Used when the capacity is even and at most
 // kTpsMaxSlots (the record windows need 16-B chunk alignment).
+//
+// Two instantiations: the stand-alone pass (kCountWarps warps per CTA, as
+// many CTAs as fit) and the co-resident one of the overlapped replay
+// (capi.cu replay_overlapped): one warp per CTA at <= 64 registers, two CTAs
+// per SM, small enough to run beside the emit kernel's CTA on every SM, so
+// pass 1 of chunk k+1 uses the issue slots and DRAM bandwidth that k_tps of
+// chunk k leaves idle.
 #ifndef WGPF_COUNT_WARPS
 #define WGPF_COUNT_WARPS 4
 #endif
@@ -211,17 +221,30 @@ constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
 #define WGPF_COUNT_UNROLL 16
 #endif
 constexpr int kCountUnroll = WGPF_COUNT_UNROLL;
+#ifndef WGPF_COUNT_CO_UNROLL
+#define WGPF_COUNT_CO_UNROLL 8
+#endif
+constexpr int kCountCoUnroll = WGPF_COUNT_CO_UNROLL;
+#ifndef WGPF_COUNT_CO_CTAS
+#define WGPF_COUNT_CO_CTAS 2  // co-resident pass-1 CTAs (one warp each) per SM
+#endif
+constexpr uint32_t kCountCoCtas = WGPF_COUNT_CO_CTAS;
+#ifndef WGPF_COUNT_CO_MINB
+#define WGPF_COUNT_CO_MINB 32  // launch bound: 32 one-warp CTAs per SM -> <= 64 registers
+#endif
+constexpr uint32_t kCountCoMinBlocks = WGPF_COUNT_CO_MINB;
 using CountWin = RecWindowsT<kCountW>;
 
 // tm: the body as a TMA tensor with box {CountWin::kTpsPitch / 4, 32};
 // tm_tail: the same without L2 promotion, for windows within 256 B of the
 // streams' last records (promotion there would pull the unused slots)
-__global__ void __launch_bounds__(kCountWarps * 32)
+template <uint32_t kWarps, int kUnroll, uint32_t kMinBlocks>
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     k_count_tps(CountArgs a, const __grid_constant__ CUtensorMap tm,
                 const __grid_constant__ CUtensorMap tm_tail) {
   __shared__ uint8_t marker_region[256];
-  __shared__ __align__(128) uint8_t recbuf[kCountWarps][2 * 32 * CountWin::kTpsPitch];
-  __shared__ __align__(8) unsigned long long wbar[kCountWarps][2];
+  __shared__ __align__(128) uint8_t recbuf[kWarps][2 * 32 * CountWin::kTpsPitch];
+  __shared__ __align__(8) unsigned long long wbar[kWarps][2];
   for (uint32_t r = threadIdx.x; r < 256; r += blockDim.x)
     marker_region[r] =
         r < a.fast_regions ? class_is_marker(a.plan, a.plan.class_of[r]) : 0;
@@ -243,8 +266,8 @@ __global__ void __launch_bounds__(kCountWarps * 32)
   }
   __syncwarp();
   uint32_t bphase = 0;
-  const uint64_t wstep = (uint64_t)gridDim.x * kCountWarps;
-  for (uint64_t b = (uint64_t)blockIdx.x * kCountWarps + w; b * 32 < a.n_streams;
+  const uint64_t wstep = (uint64_t)gridDim.x * kWarps;
+  for (uint64_t b = (uint64_t)blockIdx.x * kWarps + w; b * 32 < a.n_streams;
        b += wstep) {
     const uint64_t s = b * 32 + lane;
     const bool live = s < a.n_streams;
@@ -262,7 +285,7 @@ __global__ void __launch_bounds__(kCountWarps * 32)
         a.counts[s] = 0;
         a.zpos[s] = -1;
         a.sflag[s] = SF_DECODE_ERR;
-        atomicMin(&a.status->decode_err, ((unsigned long long)s << 2) | code);
+        atomicMin(&a.status->decode_err, ((unsigned long long)(s + a.list_base) << 2) | code);
         if (code == DEC_CAP) atomicAdd(&a.status->cap_mismatch, 1ull);
       }
     }
@@ -342,7 +365,7 @@ __global__ void __launch_bounds__(kCountWarps * 32)
       __syncwarp();
       const uint2* rec = win.lane_records(bsel, lane, start);
       if (w0 + kCountW + 1u <= nmin) {
-#pragma unroll kCountUnroll
+#pragma unroll kUnroll
         for (uint32_t j = 0; j < kCountW; ++j) step(std::true_type{}, w0 + j, rec[j].x);
       } else {
 #pragma unroll 1
@@ -377,14 +400,14 @@ __global__ void __launch_bounds__(kCountWarps * 32)
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(a.deep_len, (unsigned long long)__popc(dm));
       base = __shfl_sync(FULL, base, 0);
-      if (to_deep) a.deep_list[base + __popc(dm & lt)] = s;
+      if (to_deep) a.deep_list[base + __popc(dm & lt)] = s + a.list_base;
     }
     const uint32_t wm = __ballot_sync(FULL, to_warp);
     if (wm) {
       unsigned long long base = 0;
       if (lane == 0) base = atomicAdd(a.warp_len, (unsigned long long)__popc(wm));
       base = __shfl_sync(FULL, base, 0);
-      if (to_warp) a.warp_list[base + __popc(wm & lt)] = s;
+      if (to_warp) a.warp_list[base + __popc(wm & lt)] = s + a.list_base;
     }
   }
 }

@@ -65,6 +65,9 @@ struct FastArgs {
                          // general path (no k_tps pass to collect them)
   unsigned long long* deep_rep;  // k_tpsd: per-CTA count / sum / histogram
                                  // replicas (zeroed; summed by k_deep_reduce)
+  uint64_t list_base;    // k_tps over one chunk of the call's streams
+                         // (overlapped replay): general-list entries are
+                         // call-global stream indices
 };
 
 struct LevelEntry {  // last START seen at a nesting level

@@ -71,8 +71,13 @@ constexpr uint32_t kStkRid = (kTpsRegions - 1u) << 12;
 
 struct TpsWarpSmem {
   uint8_t rec[2][32 * kTpsPitch];    // record windows
-  uint2 stk_empty[32];               // row -1: what an empty stack reads (never
-                                     // written; its value is not used)
+#ifdef WGPF_STK_EMPTY
+  // row -1: what an empty stack reads (never written; its value is not used).
+  // Default: row -1 is the last 256 B of rec[1], read but unused -- the
+  // dedicated row (for compute-sanitizer racecheck, which reports the read
+  // against the window's TMA write) costs 2.8 % (emit 5.27 vs 5.13 ms)
+  uint2 stk_empty[32];
+#endif
   uint2 stk[kTpsDepth][32];          // {lo clock, pos | rid<<12 | cons<<17 | hi<<18}
   wgpf_event orph[32];               // one orphan per lane (more: SF_INVALID)
   unsigned long long bar[2];         // TMA windows: one mbarrier per buffer
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     const uint32_t flag = jb * 32 + lane < n_blocks ? a.sflag[s] : SF_DECODE_ERR;
     if (flag & SF_GENERAL) {
       const unsigned long long k = atomicAdd(a.general_len, 1ull);
-      a.general_list[k] = s;
+      a.general_list[k] = s + a.list_base;
     }
     const bool act = !(flag & (SF_DECODE_ERR | SF_GENERAL | SF_WARP));
     const uint8_t* sbase = a.body + (act ? s : 0) * a.stride;
@@ -238,14 +243,23 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       win.init(ws.rec[0], lane, a.stride * W, cap);  // lanes W streams apart
       win.begin(a.body + s0 * a.stride, start, n);
     }
-    // windows whose rows end within 256 B (32 records) of the shortest
-    // stream's last record: no L2 promotion (it would pull unused slots)
+    // WGPF_TAIL_SEL: windows whose rows end within 256 B (32 records) of the
+    // shortest stream's last record without L2 promotion (it would pull
+    // unused slots).  Measured on config 4: emit 5.38 vs 5.13 ms without the
+    // per-window map selection (tm_tail is then unused here)
+#ifdef WGPF_TAIL_SEL
     const uint32_t ntail = __reduce_min_sync(FULL, act ? n : 0xFFFFFFFFu);
+#endif
     auto issue = [&](uint32_t bs, uint32_t c0) {
       if (tmab) {
         if (lane == 0)
           win_tma3(s_buf + bs * (32u * kTpsPitch),
-                   c0 + kTpsPitch / 8u + 32u <= ntail ? &tm : &tm_tail, s_bar + 8u * bs,
+#ifdef WGPF_TAIL_SEL
+                   c0 + kTpsPitch / 8u + 32u <= ntail ? &tm : &tm_tail,
+#else
+                   &tm,
+#endif
+                   s_bar + 8u * bs,
                    (int)(4u + 2u * c0), (int)wi, (int)(jb * 32), 32u * kTpsPitch);
       } else {
         win.issue(bs, c0);

@@ -136,8 +136,12 @@ __device__ __forceinline__ void red_max32(uint32_t a, uint32_t v) {
 }
 
 // tm: the body as a 2-D TMA tensor {stride / 4, n_streams}, box
-// {kDeepPitch / 4, 32} (a.tma != 0)
-template <bool kEmit, bool kStats>
+// {kDeepPitch / 4, 32} (a.tma != 0).
+// kMarkers: the plan has wait-marker labels ("X.wait").  Without them no
+// record can be a consumed wait or an orphan marker (replay,
+// trace.hpp:421-485, only pairs a base with a ".wait" class), so that
+// machinery -- about a fifth of an END step -- is compiled out.
+template <bool kEmit, bool kStats, bool kMarkers>
 __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     k_tpsd(FastArgs a, const __grid_constant__ CUtensorMap tm) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -193,6 +197,12 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 
   // this CTA's replica of the count / sum / histogram table
   unsigned long long* const rep = a.deep_rep + (size_t)blockIdx.x * kSmemClasses * kDeepRep;
+  // First-event keys.  Keys are (stream, event index): a lane meets its
+  // keys in increasing order and the batch's smallest stream (lane `lmin`)
+  // beats every other lane.  So once a warp-uniform step of class c has had
+  // lmin participate, no later event of class c in this batch can lower the
+  // minimum: `wseen` (warp-uniform, bit c) skips the key reductions then.
+  uint32_t wseen_lo = 0, wseen_hi = 0, lmin = 0;
   // one event per participating lane into the statistics
   auto wstat = [&](bool p, uint32_t cls, uint32_t d, unsigned long long key) {
     const uint32_t pm = __ballot_sync(FULL, p);
@@ -204,20 +214,27 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     // histogram bin: lanes with the same bin aggregate into one reduction
     const uint32_t bin = hist_bin32(d);
     if (uni && c0 < kSmemClasses && c0 < K) {
-      // the CTA's current first key, loaded ahead of the reductions so its
-      // latency overlaps them (the min below rarely needs the atomic)
-      const unsigned long long cur_first =
-          *reinterpret_cast<volatile unsigned long long*>(&cs.first[c0]);
       const uint32_t dd = p ? d : 0u;
       const uint32_t slo = __reduce_add_sync(FULL, dd & 0xFFFFu);
       const uint32_t shi = __reduce_add_sync(FULL, dd >> 16);
       const uint32_t mn = __reduce_min_sync(FULL, p ? d : 0xFFFFFFFFu);
       const uint32_t mx = __reduce_max_sync(FULL, dd);
-      // smallest 64-bit first-event key of the participating lanes
-      const uint32_t khi = __reduce_min_sync(FULL, p ? (uint32_t)(key >> 32) : 0xFFFFFFFFu);
-      const bool cand = p && (uint32_t)(key >> 32) == khi;
-      const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
       const uint32_t same = __match_any_sync(FULL, p ? bin : 0xFFFFFFFFu);
+      const bool seen = ((c0 < 32u ? wseen_lo : wseen_hi) >> (c0 & 31u)) & 1u;
+      if (!seen) {
+        // smallest 64-bit first-event key of the participating lanes
+        const unsigned long long cur_first =
+            *reinterpret_cast<volatile unsigned long long*>(&cs.first[c0]);
+        const uint32_t khi = __reduce_min_sync(FULL, p ? (uint32_t)(key >> 32) : 0xFFFFFFFFu);
+        const bool cand = p && (uint32_t)(key >> 32) == khi;
+        const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
+        const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
+        if (lane == leader && fk < cur_first) atomicMin(&cs.first[c0], fk);
+        if ((pm >> lmin) & 1u) {
+          wseen_lo |= c0 < 32u ? 1u << c0 : 0u;
+          wseen_hi |= c0 >= 32u ? 1u << (c0 - 32u) : 0u;
+        }
+      }
       if (lane == leader) {
         // fire-and-forget reductions: nothing comes back to wait for
         red_gadd64(rep + c0 * kDeepRep, (unsigned long long)__popc(pm));
@@ -225,8 +242,6 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
                    (unsigned long long)slo + ((unsigned long long)shi << 16));
         red_min32(s_min + 4u * c0, mn);
         red_max32(s_max + 4u * c0, mx);
-        const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
-        if (fk < cur_first) atomicMin(&cs.first[c0], fk);
       }
       if (p && lane == __ffs(same) - 1u)
         red_gadd64(rep + c0 * kDeepRep + 2u + bin, (unsigned long long)__popc(same));
@@ -268,6 +283,15 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     const uint32_t want = act ? a.counts[s] : 0u;
     const uint64_t off = act ? a.offsets[s] : 0ull;
     const unsigned long long gkey = (unsigned long long)(s + a.stream_base) << 25;
+    {
+      // lane of the batch's smallest active stream (first-key shortcut)
+      const uint32_t shi_ = __reduce_min_sync(FULL, act ? (uint32_t)(s >> 32) : 0xFFFFFFFFu);
+      const uint32_t slo_ =
+          __reduce_min_sync(FULL, act && (uint32_t)(s >> 32) == shi_ ? (uint32_t)s : 0xFFFFFFFFu);
+      lmin = __ffs(__ballot_sync(FULL, act && s == (((uint64_t)shi_ << 32) | slo_))) - 1u;
+      wseen_lo = 0;
+      wseen_hi = 0;
+    }
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
     // iteration counters: the warp clears its 2 KB table with 16-B stores
 #pragma unroll
@@ -284,21 +308,18 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
                                                     start == st0 && (start & 1u) == 0u);
     // cp.async windows: chunk k of this lane copies part (q % C) of the
     // window of batch slot q / C, q = 32 k + lane; that slot's stream from
-    // its lane
-    uint32_t wp[kDeepChunks];
+    // its lane.  wst[k]: that stream's start slot (the chunk's physical slot
+    // for a window is computed when a window needs cp.async -- one per
+    // stream on config 5, at the circular wrap)
+    uint32_t wst[kDeepChunks];
     const uint8_t* srck[kDeepChunks];  // slots of chunk k's stream (null: none)
     const uint32_t live = act ? 1u : 0u;
 #pragma unroll
     for (uint32_t k = 0; k < kDeepChunks; ++k) {
-      const uint32_t q = k * 32u + lane, sl = q / kDeepChunks, part = q % kDeepChunks;
-      const uint32_t st_k = __shfl_sync(FULL, start, sl);
+      const uint32_t q = k * 32u + lane, sl = q / kDeepChunks;
+      wst[k] = __shfl_sync(FULL, start, sl);
       const uint32_t ss = __shfl_sync(FULL, s32, sl);
       srck[k] = __shfl_sync(FULL, live, sl) ? a.body + (uint64_t)ss * a.stride + 16 : nullptr;
-      uint32_t p = st_k + 2u;
-      if (p >= cap) p -= cap;
-      p = (p & ~1u) + 2u * part;
-      if (p >= cap) p -= cap;
-      wp[k] = p;
     }
     uint32_t tma_buf = 0;  // bit b: buffer b's window came by TMA
     auto issue = [&](uint32_t bsel, uint32_t c0) {
@@ -315,15 +336,16 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 #pragma unroll
         for (uint32_t k = 0; k < kDeepChunks; ++k) {
           const uint32_t q = k * 32u + lane, sl = q / kDeepChunks, part = q % kDeepChunks;
+          // the even physical slot at or below (start + c0) mod cap, + part
+          uint32_t p = wst[k] + c0;
+          p = p >= cap ? p - cap : p;  // (c0 < cap + 2: one subtraction
+          p = p >= cap ? p - cap : p;  //  may not suffice)
+          p = (p & ~1u) + 2u * part;
+          p = p >= cap ? p - cap : p;
           if (srck[k])
             cp_async16(s_rec + bsel * (32 * kDeepPitch) + sl * kDeepPitch + 16u * part,
-                       srck[k] + 8u * wp[k]);
+                       srck[k] + 8u * p);
         }
-      }
-#pragma unroll
-      for (uint32_t k = 0; k < kDeepChunks; ++k) {
-        wp[k] += kDeepW;
-        if (wp[k] >= cap) wp[k] -= cap;
       }
     };
 
@@ -372,7 +394,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       const uint32_t i1 = lds32(s_info + 4u * r1id);
       const bool wrap = valid && v < vprev;
       const uint32_t meta_new =
-          i | ((tag >> 3) & kDeepMetaRid) | ((pw == (inf & 0xFFu) ? 1u : 0u) << 15);
+          i | ((tag >> 3) & kDeepMetaRid) |
+          ((kMarkers && pw == (inf & 0xFFu) ? 1u : 0u) << 15);
       if constexpr (kFull) {
         // every lane at a START (the streams of a trace run the same program
         // from the same wrap position): a push is all that happens
@@ -416,15 +439,15 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       const uint32_t ca = s_cnt + 32u * rid;
       const uint32_t it = lds8(ca);
       sts8_if(ok, ca, it + 1u);
-      const bool is_mk = (inf & 0x100u) != 0u;
+      const bool is_mk = kMarkers && (inf & 0x100u) != 0u;
       const bool base = ok && !is_mk;
-      const bool orphan = ok && is_mk && !((em >> 15) & 1u);
+      const bool orphan = kMarkers && ok && is_mk && !((em >> 15) & 1u);
       const uint32_t dpos = i - spos;
       const uint32_t ovh = cost * dpos;
       const uint32_t corr = ovh > meas ? 0u : meas - ovh;
       const bool cclose = (kFull || i + 2 < n) && (int32_t)r2.x >= 0 &&
                           ((r2.x >> 12) & (kDeepRegions - 1u)) == r1id;
-      const bool consumed = base && (kFull || i + 1 < n) && (int32_t)r1.x < 0 &&
+      const bool consumed = kMarkers && base && (kFull || i + 1 < n) && (int32_t)r1.x < 0 &&
                             (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
                             ((int32_t)(i + 1) <= z || cclose);
       const uint32_t wd = r1.y - v;
@@ -435,8 +458,9 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         const uint32_t eend = elo + corr;
         put(base, kw, elo, shi, eend, shi + (eend < corr ? 1u : 0u), rid | WGPF_EV_CORRECTED,
             it);
-        put(consumed, kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
-            r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
+        if constexpr (kMarkers)
+          put(consumed, kw + 1u, v, hi, r1.y, hi + (r1.y < v ? 1u : 0u),
+              r1id | WGPF_EV_WAIT | (corr_w ? WGPF_EV_CORRECTED : 0u), it);
       }
       kw += (base ? 1u : 0u) + (consumed ? 1u : 0u);
       pw = base ? (inf >> 16) : 0xFFu;
@@ -446,8 +470,9 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       n_orph += orphan ? 1u : 0u;
       if constexpr (stats) {
         wstat(base, inf & 0xFFu, corr, gkey | (kpos << 1));
-        if (__any_sync(FULL, consumed))
-          wstat(consumed, i1 & 0xFFu, wd, gkey | ((kpos + 1u) << 1) | 1u);
+        if constexpr (kMarkers)
+          if (__any_sync(FULL, consumed))
+            wstat(consumed, i1 & 0xFFu, wd, gkey | ((kpos + 1u) << 1) | 1u);
       }
       inf0 = i1;
       r0 = r1;

@@ -279,6 +279,33 @@ def test_device_body_vs_oracle_64k_streams(ctx, oracle, shape):
                                            s.hist)
 
 
+def test_overlapped_pass1_pass2_equals_sequential(ctx, monkeypatch):
+    """The opt-in overlapped replay (WGPF_OVERLAP=1: pass 1 of chunk k+1 on a
+    second stream beside k_tps on chunk k, chunked offset scans with a
+    device-side running base) gives the sequential replay's events,
+    warnings and statistics bit for bit."""
+    import torch
+    from paper_2505_21661_b200 import trace as T
+    n = 1 << 16
+    s0 = S.MIXED_FULL_LONG - n // 2
+    body, ev, ne, w, labels, strategy = _device_replay(ctx, 0, s0, n, 0x2)
+    want_ev = ev[:ne * 32].clone()
+    want_st = ctx.stats()
+    monkeypatch.setenv("WGPF_OVERLAP", "1")
+    octx = T.Context(0)
+    octx.set_plan(plan_of(S.CAP, strategy, labels))
+    ev2 = torch.zeros_like(ev)
+    ne2, w2 = octx.replay_device(body.data_ptr(), body.numel(), n, 33, ev2.data_ptr(),
+                                 n * 128, 0x2 | 0x10)
+    assert octx.last_profile()["overlap_chunks"] > 1
+    assert ne2 == ne
+    assert torch.equal(ev2[:ne * 32], want_ev)
+    assert (w2.dropped_heads, w2.truncated_tails, w2.flagged_preconditions,
+            w2.malformed_groups) == (w.dropped_heads, w.truncated_tails,
+                                     w.flagged_preconditions, w.malformed_groups)
+    assert octx.stats() == want_st
+
+
 @pytest.mark.slow
 def test_full_config4_properties(ctx, oracle):
     """Full 2^30-record config 4 on one B200: closed-form totals plus a

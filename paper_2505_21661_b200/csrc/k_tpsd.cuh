@@ -77,9 +77,10 @@ struct DeepWarpSmem {
 };
 
 // Per CTA only what needs a shared reduction: min / max (native u32 shared
-// reductions) and the first-event key.  Counts, sums and histogram bins go
-// to this CTA's own replica of the table in global memory (kDeepRep u64 per
-// class: count, sum, 64 bins) with fire-and-forget global reductions
+// reductions) and the first-event key.  Sums and histogram bins go to this
+// CTA's own replica of the table in global memory (kDeepRep u64 per class:
+// [unused], sum, 64 bins; a class's count is the sum of its bins) with
+// fire-and-forget global reductions
 // (native u64 in L2; a 64-bit shared add would be a CAS loop), aggregated per
 // warp first; k_deep_reduce sums the replicas afterwards.  Per-CTA replicas
 // keep SMs off each other's L2 lines (one shared table: 40 % slower), and
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
   // beats every other lane.  So once a warp-uniform step of class c has had
   // lmin participate, no later event of class c in this batch can lower the
   // minimum: `wseen` (warp-uniform, bit c) skips the key reductions then.
-  uint32_t wseen_lo = 0, wseen_hi = 0, lmin = 0;
+  unsigned long long wseen = 0;
+  uint32_t lmin = 0;
   // one event per participating lane into the statistics
   auto wstat = [&](bool p, uint32_t cls, uint32_t d, unsigned long long key) {
     const uint32_t pm = __ballot_sync(FULL, p);
@@ -214,13 +216,22 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     // histogram bin: lanes with the same bin aggregate into one reduction
     const uint32_t bin = hist_bin32(d);
     if (uni && c0 < kSmemClasses && c0 < K) {
+      unsigned long long* const rc = rep + c0 * kDeepRep;  // this class's replica row
       const uint32_t dd = p ? d : 0u;
-      const uint32_t slo = __reduce_add_sync(FULL, dd & 0xFFFFu);
-      const uint32_t shi = __reduce_add_sync(FULL, dd >> 16);
       const uint32_t mn = __reduce_min_sync(FULL, p ? d : 0xFFFFFFFFu);
       const uint32_t mx = __reduce_max_sync(FULL, dd);
+      // the sum: one 32-bit reduction when 32 x max cannot carry out, else
+      // two 16-bit halves
+      unsigned long long sum;
+      if (mx < (1u << 27)) {
+        sum = __reduce_add_sync(FULL, dd);
+      } else {
+        const uint32_t slo = __reduce_add_sync(FULL, dd & 0xFFFFu);
+        const uint32_t shi = __reduce_add_sync(FULL, dd >> 16);
+        sum = (unsigned long long)slo + ((unsigned long long)shi << 16);
+      }
       const uint32_t same = __match_any_sync(FULL, p ? bin : 0xFFFFFFFFu);
-      const bool seen = ((c0 < 32u ? wseen_lo : wseen_hi) >> (c0 & 31u)) & 1u;
+      const bool seen = (wseen >> c0) & 1ull;
       if (!seen) {
         // smallest 64-bit first-event key of the participating lanes
         const unsigned long long cur_first =
@@ -230,24 +241,18 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
         const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
         if (lane == leader && fk < cur_first) atomicMin(&cs.first[c0], fk);
-        if ((pm >> lmin) & 1u) {
-          wseen_lo |= c0 < 32u ? 1u << c0 : 0u;
-          wseen_hi |= c0 >= 32u ? 1u << (c0 - 32u) : 0u;
-        }
+        if ((pm >> lmin) & 1u) wseen |= 1ull << c0;
       }
       if (lane == leader) {
-        // fire-and-forget reductions: nothing comes back to wait for
-        red_gadd64(rep + c0 * kDeepRep, (unsigned long long)__popc(pm));
-        red_gadd64(rep + c0 * kDeepRep + 1u,
-                   (unsigned long long)slo + ((unsigned long long)shi << 16));
+        // fire-and-forget reductions: nothing comes back to wait for (the
+        // count is the sum of the histogram bins, k_deep_reduce)
+        red_gadd64(rc + 1u, sum);
         red_min32(s_min + 4u * c0, mn);
         red_max32(s_max + 4u * c0, mx);
       }
-      if (p && lane == __ffs(same) - 1u)
-        red_gadd64(rep + c0 * kDeepRep + 2u + bin, (unsigned long long)__popc(same));
+      if (p && lane == __ffs(same) - 1u) red_gadd64(rc + 2u + bin, (unsigned long long)__popc(same));
     } else if (p) {
       if (cls < kSmemClasses && cls < K) {
-        red_gadd64(rep + cls * kDeepRep, 1ull);
         red_gadd64(rep + cls * kDeepRep + 1u, (unsigned long long)d);
         red_gadd64(rep + cls * kDeepRep + 2u + bin, 1ull);
         red_min32(s_min + 4u * cls, d);
@@ -289,8 +294,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       const uint32_t slo_ =
           __reduce_min_sync(FULL, act && (uint32_t)(s >> 32) == shi_ ? (uint32_t)s : 0xFFFFFFFFu);
       lmin = __ffs(__ballot_sync(FULL, act && s == (((uint64_t)shi_ << 32) | slo_))) - 1u;
-      wseen_lo = 0;
-      wseen_hi = 0;
+      wseen = 0;
     }
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
     // iteration counters: the warp clears its 2 KB table with 16-B stores
@@ -580,11 +584,13 @@ __global__ void k_deep_reduce(const unsigned long long* rep, uint32_t ctas, uint
     if (!t) continue;
     const uint32_t c = i / kDeepRep, f = i % kDeepRep;
     if (f == 0)
-      atomicAdd(&st.count[c], t);
+      continue;  // (unused: counts are the bin sums, below)
     else if (f == 1)
       atomicAdd(&st.sum[c], t);
-    else
+    else {
       atomicAdd(&st.hist[c * WGPF_HIST_BINS + (f - 2)], t);
+      atomicAdd(&st.count[c], t);  // a class's count is the sum of its bins
+    }
   }
 }
 

@@ -363,6 +363,55 @@ struct Scope {
   __device__ __forceinline__ ~Scope() { rec.end(region); }
 };
 
+// Back-to-back scopes on one stream: the phases of a warp-specialised
+// pipeline loop (wait -> issue -> wait -> ...).  to(r) closes the open scope
+// and opens r; the destructor closes the last one.  kShare: the END / START
+// pair at each boundary shares one clock capture (Recorder::mark), otherwise
+// every RecordOp captures its own.  Either way the records are exactly the
+// hand-placed start/end pairs of instrument.hpp:163-244's sync regions.
+// In a loop, name the phase each boundary closes and end every iteration
+// with iteration_end(), so every tag is an immediate:
+//   Chain<Rec, share> ch(rec);
+//   for (k...) {
+//     ch.to(WAIT, ISSUE);  wait();  ch.to(ISSUE, WAIT);  issue();
+//     ch.iteration_end();
+//   }                                   // ~Chain: end(ISSUE) if still open
+template <class Rec, bool kShare>
+struct Chain {
+  Rec& rec;
+  uint32_t cur = 0;
+  bool open = false;
+  __device__ __forceinline__ explicit Chain(Rec& r) : rec(r) {}
+  __device__ __forceinline__ void to(uint32_t region) { to(region, cur); }
+  // prev: the phase the caller knows is open here (it must equal the open
+  // one) -- a constant at the call site, so the END tag is an immediate
+  // even where the open phase is loop-carried
+  __device__ __forceinline__ void to(uint32_t region, uint32_t prev) {
+    if (!open) {
+      rec.start(region);
+    } else if constexpr (kShare) {
+      rec.mark(prev, region);
+    } else {
+      rec.end(prev);
+      rec.start(region);
+    }
+    cur = region;
+    open = true;
+  }
+  __device__ __forceinline__ void close() {
+    if (open) rec.end(cur);
+    open = false;
+  }
+  // end of one loop iteration: with separate captures the iteration's last
+  // phase closes here (a loop body then starts with nothing open, and every
+  // tag is an immediate); with shared captures it stays open so the next
+  // iteration's first boundary shares its capture
+  __device__ __forceinline__ void iteration_end() {
+    if constexpr (!kShare) close();
+  }
+  __device__ __forceinline__ ~Chain() { close(); }
+};
+
 // One async operation X (region ids x and x_wait = the "X.wait" label):
 //   AsyncOp op(rec, x, xw);  op.launch([&]{ issue });  ... ;  op.wait([&]{ wait });
 template <class Rec>

@@ -12,13 +12,18 @@
 // Scopes (region ids): 0 tile, 1 tma.stall, 2 tma.issue, 3 mma.stall,
 // 4 mma.issue, 5 epi.stall, 6 epi.ld, 7 epi.st (the stalls are sync scopes
 // around mbarrier waits: no ".wait" suffix, which replay reserves for the
-// async pattern's wait markers, trace.hpp:377-382).
+// async pattern's wait markers, trace.hpp:377-382).  Placed by the
+// instrumentation-pass helpers of wgpf_device.cuh, not by hand: the tile is
+// a wgpf_dev::Scope, each role's pipeline phases a wgpf_dev::Chain
+// (stall -> issue -> stall ...); the plain twin is the same source on
+// wgpf_dev::NullRecorder.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "wgpf_device.cuh"
 
@@ -148,7 +153,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t nk = K / BK;
   const uint64_t cta = blockIdx.x;
 
-  wgpf_dev::Recorder<true> rec;
+  // the uninstrumented twin records nothing (strip_profiling)
+  using Rec = std::conditional_t<kMode == 0, wgpf_dev::NullRecorder, wgpf_dev::Recorder<true>>;
+  using Tile = wgpf_dev::Scope<Rec>;
+  using Phases = wgpf_dev::Chain<Rec, kMode == 2>;
+  Rec rec;
   if constexpr (kMode != 0) {
     rec.init(prof, warp, PROF_CAP, lane == 0);
     if (threadIdx.x == 0 && timing) {
@@ -191,18 +200,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t mb, nb;
       tile_coords(t, nM, nN, mb, nb);
       const uint32_t m0 = mb * BM, n0 = nb * BN;
-      if constexpr (kMode != 0) rec.start(R_TILE);
-      if constexpr (kMode == 2) rec.start(R_TMA_WAIT);
+      Tile tile(rec, R_TILE);
+      Phases ph_(rec);  // tma.stall -> tma.issue per k-block
       for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
         const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
-        if constexpr (kMode == 1) rec.start(R_TMA_WAIT);
+        ph_.to(R_TMA_WAIT, R_TMA);
         if (lane == 0) mbar_wait(&empty[s], ph ^ 1u);
         __syncwarp();
-        if constexpr (kMode == 1) {
-          rec.end(R_TMA_WAIT);
-          rec.start(R_TMA);
-        }
-        if constexpr (kMode == 2) rec.mark(R_TMA_WAIT, R_TMA);
+        ph_.to(R_TMA, R_TMA_WAIT);
         if (lane == 0) {
           uint8_t* a = stage_base + s * STAGE_BYTES;
           mbar_expect_tx(&full[s], STAGE_BYTES);
@@ -210,15 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_2d(&tb, &full[s], a + A_BYTES, (int)(kb * BK), (int)n0);
         }
         __syncwarp();
-        if constexpr (kMode == 1) rec.end(R_TMA);
-        if constexpr (kMode == 2) {
-          if (kb + 1 < nk)
-            rec.mark(R_TMA, R_TMA_WAIT);
-          else
-            rec.end(R_TMA);
-        }
+        ph_.iteration_end();
       }
-      if constexpr (kMode != 0) rec.end(R_TILE);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -226,23 +224,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++tl) {
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
       const uint32_t dt = tmem + acc * BN;
-      if constexpr (kMode != 0) rec.start(R_TILE);
+      Tile tile(rec, R_TILE);
       // the epilogue has drained this accumulator (two tiles ago)
       if (lane == 0) mbar_wait(&tmem_empty[acc], aph ^ 1u);
       __syncwarp();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if constexpr (kMode == 2) rec.start(R_MMA_WAIT);
+      Phases ph_(rec);  // mma.stall -> mma.issue per k-block
       for (uint32_t kb = 0; kb < nk; ++kb, ++it) {
         const uint32_t s = it % STAGES, ph = (it / STAGES) & 1u;
-        if constexpr (kMode == 1) rec.start(R_MMA_WAIT);
+        ph_.to(R_MMA_WAIT, R_MMA);
         if (lane == 0) mbar_wait(&full[s], ph);
         __syncwarp();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if constexpr (kMode == 1) {
-          rec.end(R_MMA_WAIT);
-          rec.start(R_MMA);
-        }
-        if constexpr (kMode == 2) rec.mark(R_MMA_WAIT, R_MMA);
+        ph_.to(R_MMA, R_MMA_WAIT);
         if (lane == 0) {
           const uint32_t a = smem_u32(stage_base + s * STAGE_BYTES);
           const uint32_t b = a + A_BYTES;
@@ -253,15 +247,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (kb == nk - 1) umma_commit(&tmem_full[acc]);
         }
         __syncwarp();
-        if constexpr (kMode == 1) rec.end(R_MMA);
-        if constexpr (kMode == 2) {
-          if (kb + 1 < nk)
-            rec.mark(R_MMA, R_MMA_WAIT);
-          else
-            rec.end(R_MMA);
-        }
+        ph_.iteration_end();
       }
-      if constexpr (kMode != 0) rec.end(R_TILE);
     }
   } else {
     // ---------------- epilogue: TMEM -> registers -> bf16 -> HBM -----------
@@ -273,17 +260,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t m0 = mb * BM, n0 = nb * BN;
       const uint32_t acc = tl & 1u, aph = (tl >> 1) & 1u;
       const uint32_t row = m0 + quad * 32u + lane;
-      if constexpr (kMode != 0) {
-        rec.start(R_TILE);
-        rec.start(R_EPI_WAIT);
-      }
+      Tile tile(rec, R_TILE);
+      Phases ph_(rec);  // epi.stall, then epi.ld -> epi.st per 32 columns
+      ph_.to(R_EPI_WAIT);
       mbar_wait(&tmem_full[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if constexpr (kMode == 1) rec.end(R_EPI_WAIT);
-      if constexpr (kMode == 2) rec.mark(R_EPI_WAIT, R_EPI_LD);
+      ph_.iteration_end();
       const uint32_t taddr = tmem + acc * BN + ((quad * 32u) << 16);
       for (uint32_t c = 0; c < BN; c += 32) {
-        if constexpr (kMode == 1) rec.start(R_EPI_LD);
+        ph_.to(R_EPI_LD, c ? R_EPI_ST : R_EPI_WAIT);
         uint32_t v[32];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,"
@@ -307,11 +292,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                              smem_u32(&tmem_empty[acc]))
                          : "memory");
         }
-        if constexpr (kMode == 1) {
-          rec.end(R_EPI_LD);
-          rec.start(R_EPI_ST);
-        }
-        if constexpr (kMode == 2) rec.mark(R_EPI_LD, R_EPI_ST);
+        ph_.to(R_EPI_ST, R_EPI_LD);
         uint4 out[4];
         uint32_t* o = reinterpret_cast<uint32_t*>(out);
 #pragma unroll
@@ -325,15 +306,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) dst[j] = out[j];
         }
-        if constexpr (kMode == 1) rec.end(R_EPI_ST);
-        if constexpr (kMode == 2) {
-          if (c + 32 < BN)
-            rec.mark(R_EPI_ST, R_EPI_LD);
-          else
-            rec.end(R_EPI_ST);
-        }
+        ph_.iteration_end();
       }
-      if constexpr (kMode != 0) rec.end(R_TILE);
     }
   }
 

@@ -343,6 +343,68 @@ def test_full_config4_properties(ctx, oracle):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.slow
+def test_full_config5_properties(ctx, oracle):
+    """Full config 5 on one B200 (2^22 circular 64-deep streams, 2^30
+    surviving records): closed-form totals and per-label counts, plus a
+    sample of streams checked against the oracle event for event."""
+    import torch
+    n = S.NESTED_FULL_STREAMS
+    body, ev, ne, w, labels, strategy = _device_replay(ctx, 1, 0, n, 0)
+    # surviving window = writes 744..999 of S0..S63 E63..E0 repeated: 24 dropped
+    # heads (E23..E0), then S0..S63 E63..E0 S0..S63 E63..E24: 104 events and
+    # 24 open STARTs per stream
+    per = 104
+    assert ne == per * n
+    assert (w.dropped_heads, w.truncated_tails, w.malformed_groups,
+            w.flagged_preconditions) == (24 * n, 24 * n, 0, 0)
+    st = ctx.stats()
+    for k, lab in enumerate(labels):
+        assert st[lab].count == (2 if k >= 24 else 1) * n, lab
+    rng = np.random.default_rng(5)
+    stride = S.stream_stride()
+    for s in sorted(rng.choice(n, 64, replace=False)):
+        s = int(s)
+        one = body[s * stride:(s + 1) * stride].cpu().numpy()
+        o = oracle.replay_body(one, 1, S.CAP, 0, labels, 33)
+        assert len(o.events) == per
+        got = ev[s * per * 32:(s + 1) * per * 32].cpu().numpy().view(O.EVENT_DTYPE)
+        # (the oracle numbers the stream 0 and block / warp group come from
+        # the header, so the records compare as they are)
+        assert np.array_equal(got, o.events), s
+    del body, ev
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("shape,switch", [(0, "WGPF_NO_TPS"), (1, "WGPF_NO_DEEP")])
+def test_full_size_fast_kernel_equals_warp_kernel(ctx, monkeypatch, shape, switch):
+    """Differential check at the full BASELINE sizes: the thread-per-stream
+    kernel (k_tps on config 4, k_tpsd on config 5) and the independent
+    warp-per-stream kernel (k_fast_emit: ballots, match.any, per-level
+    tables), each pinned to the oracle on smaller bodies, give the same 531.8
+    M / 436.2 M events bit for bit and the same statistics."""
+    import torch
+    from paper_2505_21661_b200 import trace as T
+    n = S.MIXED_FULL_STREAMS if shape == 0 else S.NESTED_FULL_STREAMS
+    body, ev, ne, w, labels, strategy = _device_replay(ctx, shape, 0, n, 0x2)
+    want_st = ctx.stats()
+    monkeypatch.setenv(switch, "1")
+    wctx = T.Context(0)
+    wctx.set_plan(plan_of(S.CAP, strategy, labels))
+    ev2 = torch.empty_like(ev)
+    ne2, w2 = wctx.replay_device(body.data_ptr(), body.numel(), n, 33, ev2.data_ptr(),
+                                 n * 128, 0x2)
+    assert ne2 == ne
+    assert torch.equal(ev2[:ne * 32], ev[:ne * 32])
+    assert (w2.dropped_heads, w2.truncated_tails, w2.flagged_preconditions,
+            w2.malformed_groups) == (w.dropped_heads, w.truncated_tails,
+                                     w.flagged_preconditions, w.malformed_groups)
+    assert wctx.stats() == want_st
+    del body, ev, ev2
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("n", [4000, 40000])
 def test_stats_only_equals_materialized(ctx, oracle, n):
     """WGPF_F_STATS_ONLY (no event materialisation) gives the same

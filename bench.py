@@ -419,7 +419,10 @@ def shim_e2e(streams: int):
     try:
         r = subprocess.run([exe, str(streams), "2"], capture_output=True, text=True,
                            timeout=600)
-        d = json.loads(r.stdout.strip().splitlines()[-1])
+        lines = r.stdout.strip().splitlines()
+        d = json.loads(lines[-1])
+        if len(lines) > 1:  # region_stats breakdown (host packing, GPU statistics)
+            d["region_stats_breakdown"] = json.loads(lines[-2])
     except Exception as e:  # (reported, not fatal: the headline is above)
         return {"error": str(e)[:200]}
     d["unit"] = "records/s"

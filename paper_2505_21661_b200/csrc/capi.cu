@@ -80,12 +80,17 @@ struct DevBuf {
 using TpsKernel = void (*)(FastArgs);
 using DeepKernel = void (*)(FastArgs, const CUtensorMap);
 using TpsTmaKernel = void (*)(FastArgs, const CUtensorMap, const CUtensorMap);
-static DeepKernel deep_kernel(bool emit, bool stats, bool markers) {
-  static const DeepKernel k[8] = {
-      k_tpsd<false, false, false>, k_tpsd<true, false, false>, k_tpsd<false, true, false>,
-      k_tpsd<true, true, false>,   k_tpsd<false, false, true>, k_tpsd<true, false, true>,
-      k_tpsd<false, true, true>,   k_tpsd<true, true, true>};
-  return k[(emit ? 1 : 0) | (stats ? 2 : 0) | (markers ? 4 : 0)];
+static DeepKernel deep_kernel(bool emit, bool stats, bool markers, bool wide) {
+  static const DeepKernel k[16] = {
+      k_tpsd<false, false, false, false>, k_tpsd<true, false, false, false>,
+      k_tpsd<false, true, false, false>,  k_tpsd<true, true, false, false>,
+      k_tpsd<false, false, true, false>,  k_tpsd<true, false, true, false>,
+      k_tpsd<false, true, true, false>,   k_tpsd<true, true, true, false>,
+      k_tpsd<false, false, false, true>,  k_tpsd<true, false, false, true>,
+      k_tpsd<false, true, false, true>,   k_tpsd<true, true, false, true>,
+      k_tpsd<false, false, true, true>,   k_tpsd<true, false, true, true>,
+      k_tpsd<false, true, true, true>,    k_tpsd<true, true, true, true>};
+  return k[(emit ? 1 : 0) | (stats ? 2 : 0) | (markers ? 4 : 0) | (wide ? 8 : 0)];
 }
 static TpsTmaKernel tps_kernel(bool emit, bool stats) {
   static const TpsTmaKernel k[4] = {k_tps<false, false>, k_tps<true, false>,
@@ -130,6 +135,7 @@ struct wgpf_ctx {
   bool no_stage = getenv("WGPF_NO_STAGE") != nullptr;
   bool no_tps = getenv("WGPF_NO_TPS") != nullptr;
   bool no_deep = getenv("WGPF_NO_DEEP") != nullptr;  // deep streams -> warp kernel
+  bool no_wide = getenv("WGPF_NO_WIDE") != nullptr;  // wide streams -> warp kernel
   bool no_tma = getenv("WGPF_NO_TMA") != nullptr;    // k_tps windows by cp.async only
   bool no_group = getenv("WGPF_NO_GROUP") != nullptr;  // k_tps: consecutive streams per warp
   uint32_t group_hint = 0;   // W known from host headers (pipelined replay)
@@ -143,6 +149,7 @@ struct wgpf_ctx {
   std::vector<cudaEvent_t> oev;
   DevBuf d_obase;
   DevBuf d_wlist;  // SF_WARP streams (count in d_glen[1])
+  DevBuf d_vlist;  // wide-path streams (count in d_glen[3])
   DevBuf d_nccl_send, d_nccl_recv;  // wgpf_allreduce_stats
   DevBuf d_deep_rep;  // k_tpsd: per-CTA statistics replicas
   // pinned bounce buffers for pageable caller memory (replay_image pipeline)
@@ -366,8 +373,8 @@ int wgpf_create(int device, void* stream, wgpf_ctx** out) {
     for (int v = 0; v < 4; ++v) {
       cudaFuncSetAttribute(tps_kernel(v & 1, v & 2),
                            cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-      for (int m = 0; m < 2; ++m)
-        cudaFuncSetAttribute(deep_kernel(v & 1, v & 2, m),
+      for (int m = 0; m < 4; ++m)
+        cudaFuncSetAttribute(deep_kernel(v & 1, v & 2, m & 1, m & 2),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     }
   }
@@ -635,6 +642,12 @@ static bool deep_enabled(const wgpf_ctx* c) {
   return !c->no_tps && !c->no_deep && c->slots % 2 == 0 && c->slots &&
          c->slots <= kDeepMaxSlots && !c->labels.empty();
 }
+// wide thread-per-stream path (k_tpsd<kWide>): plans with region ids past the
+// deep kernel's 64
+static bool wide_enabled(const wgpf_ctx* c) {
+  return deep_enabled(c) && !c->no_wide && c->labels.size() > kDeepRegions &&
+         c->slots <= kDeepMaxSlots;
+}
 static uint32_t tps_regions(const wgpf_ctx* c) {
   return std::min<uint32_t>((uint32_t)c->labels.size(), kTpsRegions);
 }
@@ -836,29 +849,34 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       if (rc) return rc;
     }
     if (deep_enabled(c)) {
-      // pass 1's deep list: thread per stream, 64-deep stacks
-      f.list = c->d_dlist.as<unsigned long long>();
-      f.list_len = c->d_glen.as<unsigned long long>() + 2;
-      const uint32_t dw = deep_warps(c->smem_optin);
-      ALLOC_OK(c, c->d_dorph, sizeof(wgpf_event) * (uint64_t)c->sms * dw * 32);
-      f.orphan_scratch = c->d_dorph.as<wgpf_event>();  // one orphan per lane
+      // pass 1's deep list (64-deep stacks, ids < 64), then its wide list
+      // (32-deep stacks, ids < 256): thread per stream
       CUtensorMap tmd;
       memset(&tmd, 0, sizeof(tmd));
-      f.tma = !c->no_tma && body_tensor_map(&tmd, body, stride, n_streams, kDeepPitch) ? 1u
-                                                                                        : 0u;
-      const size_t rep_bytes = 8ull * c->sms * kSmemClasses * kDeepRep;
-      ALLOC_OK(c, c->d_deep_rep, rep_bytes);
-      f.deep_rep = c->d_deep_rep.as<unsigned long long>();
-      if (!no_stats) CUDA_OK(c, cudaMemsetAsync(f.deep_rep, 0, rep_bytes, c->stream));
-      deep_kernel(events != nullptr, !no_stats, c->has_markers)<<<c->sms, dw * 32, deep_smem_bytes(dw),
-                                                  c->stream>>>(f, tmd);
-      CUDA_OK(c, cudaGetLastError());
-      if (!no_stats)
-        k_deep_reduce<<<(kSmemClasses * kDeepRep + 255) / 256, 256, 0, c->stream>>>(
-            f.deep_rep, c->sms, c->K, f.stats);
-      f.tma = 0;
-      CUDA_OK(c, cudaGetLastError());
-      ++c->launches;
+      const uint32_t tma_ok =
+          !c->no_tma && body_tensor_map(&tmd, body, stride, n_streams, kDeepPitch) ? 1u : 0u;
+      for (int wide = 0; wide < (wide_enabled(c) ? 2 : 1); ++wide) {
+        f.list = wide ? c->d_vlist.as<unsigned long long>() : c->d_dlist.as<unsigned long long>();
+        f.list_len = c->d_glen.as<unsigned long long>() + (wide ? 3 : 2);
+        const uint32_t dw = deep_warps(c->smem_optin, wide);
+        ALLOC_OK(c, c->d_dorph, sizeof(wgpf_event) * (uint64_t)c->sms * kDeepWarps * 32);
+        f.orphan_scratch = c->d_dorph.as<wgpf_event>();  // one orphan per lane
+        f.tma = tma_ok;
+        const uint32_t classes = deep_classes(wide);
+        const size_t rep_bytes = 8ull * c->sms * classes * kDeepRep;
+        ALLOC_OK(c, c->d_deep_rep, 8ull * c->sms * deep_classes(true) * kDeepRep);
+        f.deep_rep = c->d_deep_rep.as<unsigned long long>();
+        if (!no_stats) CUDA_OK(c, cudaMemsetAsync(f.deep_rep, 0, rep_bytes, c->stream));
+        deep_kernel(events != nullptr, !no_stats, c->has_markers, wide)
+            <<<c->sms, dw * 32, deep_smem_bytes(dw, wide), c->stream>>>(f, tmd);
+        CUDA_OK(c, cudaGetLastError());
+        if (!no_stats)
+          k_deep_reduce<<<(classes * kDeepRep + 255) / 256, 256, 0, c->stream>>>(
+              f.deep_rep, c->sms, c->K, f.stats, classes);
+        f.tma = 0;
+        CUDA_OK(c, cudaGetLastError());
+        c->launches += no_stats ? 1 : 2;
+      }
     }
     // then the rest of the SF_WARP streams: warp per stream
     f.list = c->d_wlist.as<unsigned long long>();
@@ -1214,6 +1232,8 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ca.tps_depth = tps ? kTpsDepth : 0u;
   ca.deep_regions = deep_enabled(c) ? kDeepRegions : 0u;
   ca.deep_depth = deep_enabled(c) ? kDeepDepth : 0u;
+  ca.wide_regions = wide_enabled(c) ? kWideRegions : 0u;
+  ca.wide_depth = wide_enabled(c) ? kWideDepth : 0u;
   ca.list_general = 0;
   if (!tps && deep_enabled(c)) {
     // no shallow kernel for this plan: every stream with records is listed
@@ -1229,7 +1249,10 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
   ALLOC_OK(c, c->d_dlist, deep_enabled(c) ? 8 * n_streams : 8);
   ca.deep_list = c->d_dlist.as<unsigned long long>();
   ca.deep_len = c->d_glen.as<unsigned long long>() + 2;
-  CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 16, c->stream));
+  ALLOC_OK(c, c->d_vlist, wide_enabled(c) ? 8 * n_streams : 8);
+  ca.wide_list = c->d_vlist.as<unsigned long long>();
+  ca.wide_len = c->d_glen.as<unsigned long long>() + 3;
+  CUDA_OK(c, cudaMemsetAsync(ca.warp_len, 0, 24, c->stream));
   // pass 1 of the next chunk beside pass 2 of the current one (large calls)
   std::vector<uint64_t> ovl;
   uint32_t ovl_w = 1;
@@ -1774,6 +1797,10 @@ extern "C" int wgpf_decode_image(wgpf_ctx* c, const uint8_t* kpft,
   ca.tps_depth = 0;
   ca.deep_regions = 0;
   ca.deep_depth = 0;
+  ca.wide_regions = 0;
+  ca.wide_depth = 0;
+  ca.wide_list = nullptr;
+  ca.wide_len = nullptr;
   ca.warp_list = nullptr;
   ca.warp_len = nullptr;
   ca.deep_list = nullptr;

@@ -54,6 +54,11 @@ struct CountArgs {
   unsigned long long* warp_len;
   unsigned long long* deep_list;  // SF_WARP | SF_DEEP streams
   unsigned long long* deep_len;
+  uint32_t wide_regions; // wide thread-per-stream path (k_tpsd<kWide>): the
+  uint32_t wide_depth;   //   rest of the warp list with ids below this and
+                         //   nesting up to this (0: path disabled)
+  unsigned long long* wide_list;  // SF_WARP | SF_DEEP streams of the wide path
+  unsigned long long* wide_len;
   uint32_t tma;          // k_count_tps: the body's tensor map is valid
   uint32_t list_general; // no thread-per-stream emit kernel (every stream is
                          // listed): SF_GENERAL streams go to the warp list
@@ -105,6 +110,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     bool wide = false;
     bool tps_out = false;  // region id beyond the thread-per-stream tables
     bool deep_out = false; // region id beyond the deep kernel's tables
+    bool wide_out = false; // region id beyond the wide kernel's tables
     bool prev_end = false;       // record c-1 is an END
     uint32_t pend_rid = kNone;   // lane-31 marker START awaiting its END
     auto chunk = [&](uint32_t c, uint32_t tag) {
@@ -117,6 +123,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
       wide |= valid && !in_range;
       tps_out |= valid && rid >= a.tps_regions;
       deep_out |= valid && rid >= a.deep_regions;
+      wide_out |= valid && rid >= a.wide_regions;
       const uint32_t smk = __ballot_sync(0xffffffffu, st);
       const uint32_t emk = __ballot_sync(0xffffffffu, en);
       const int32_t q = q_in + (int32_t)__popc(smk & le) - (int32_t)__popc(emk & le);
@@ -184,6 +191,7 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
     wide = __any_sync(0xffffffffu, wide);
     tps_out = __any_sync(0xffffffffu, tps_out);
     deep_out = __any_sync(0xffffffffu, deep_out);
+    wide_out = __any_sync(0xffffffffu, wide_out);
     if (lane == 0) {
       a.counts[s] = n_end - (uint32_t)(-run_min);
       a.zpos[s] = z;
@@ -191,9 +199,13 @@ __global__ void __launch_bounds__(256) k_count_fast(CountArgs a) {
                            max_d > (int32_t)a.max_depth || last_bad > (int64_t)z;
       const bool warp = a.tps_depth != 0 && !general && (tps_out || max_d > (int32_t)a.tps_depth);
       const bool deep = warp && !deep_out && max_d <= (int32_t)a.deep_depth;
-      a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
+      const bool wide = warp && !deep && !wide_out && max_d <= (int32_t)a.wide_depth;
+      a.sflag[s] = general ? SF_GENERAL
+                           : (warp ? (SF_WARP | (deep || wide ? SF_DEEP : 0u)) : 0u);
       if (warp && deep)
         a.deep_list[atomicAdd(a.deep_len, 1ull)] = s;
+      else if (wide)
+        a.wide_list[atomicAdd(a.wide_len, 1ull)] = s;
       else if (warp || (general && a.list_general))
         a.warp_list[atomicAdd(a.warp_len, 1ull)] = s;
     }
@@ -377,7 +389,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
     const uint32_t n_end = (n - (uint32_t)q) >> 1;
     const bool wide = n && maxrid >= a.fast_regions;
     const bool tps_out = n && maxrid >= a.tps_regions;
-    bool to_deep = false, to_warp = false;
+    bool to_deep = false, to_warp = false, to_wide = false;
     if (act) {
       a.counts[s] = n_end - (uint32_t)(-run_min);
       a.zpos[s] = z;
@@ -387,9 +399,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
                         (tps_out || max_d > (int32_t)a.tps_depth);
       const bool deep = warp && !(n && maxrid >= a.deep_regions) &&
                         max_d <= (int32_t)a.deep_depth;
-      a.sflag[s] = general ? SF_GENERAL : (warp ? (SF_WARP | (deep ? SF_DEEP : 0u)) : 0u);
+      const bool wide = warp && !deep && !(n && maxrid >= a.wide_regions) &&
+                        max_d <= (int32_t)a.wide_depth;
+      a.sflag[s] = general ? SF_GENERAL
+                           : (warp ? (SF_WARP | (deep || wide ? SF_DEEP : 0u)) : 0u);
       to_deep = warp && deep;
-      to_warp = (warp && !deep) || (general && a.list_general);
+      to_wide = wide;
+      to_warp = (warp && !deep && !wide) || (general && a.list_general);
     }
     // warp-aggregated appends: one atomic per warp, the batch's listed
     // streams stay consecutive and in stream order (coalesced window copies
@@ -401,6 +417,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks)
       if (lane == 0) base = atomicAdd(a.deep_len, (unsigned long long)__popc(dm));
       base = __shfl_sync(FULL, base, 0);
       if (to_deep) a.deep_list[base + __popc(dm & lt)] = s + a.list_base;
+    }
+    const uint32_t vm = __ballot_sync(FULL, to_wide);
+    if (vm) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(a.wide_len, (unsigned long long)__popc(vm));
+      base = __shfl_sync(FULL, base, 0);
+      if (to_wide) a.wide_list[base + __popc(vm & lt)] = s + a.list_base;
     }
     const uint32_t wm = __ballot_sync(FULL, to_warp);
     if (wm) {

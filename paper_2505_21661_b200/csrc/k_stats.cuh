@@ -110,7 +110,54 @@ __global__ void k_exact_mean(const uint32_t* sorted_cls,
   }
   double mean = 0.0;
   uint32_t count = 0;
-  for (uint64_t k = lo; k < end; ++k) {
+  // blocks of kB durations loaded ahead of the recurrence (the loads and the
+  // reciprocals do not depend on it; one thread per class would otherwise
+  // wait for every load)
+  // Speculation: the quotient's correctness check (div_rn_by_int) is taken
+  // off the recurrence's critical path -- a block runs on the Markstein
+  // quotient q1 alone (5 dependent FP64 operations per event) while the
+  // checks accumulate beside it; a block with any failed check (a tie or a
+  // miss, rare) is redone with the checked division from its start.
+  constexpr uint32_t kB = 16;
+  uint64_t k = lo;
+  for (; k + kB <= end; k += kB) {
+    unsigned long long dv[kB];
+#pragma unroll
+    for (uint32_t j = 0; j < kB; ++j) dv[j] = __ldg(dur + k + j);
+    double m = mean;
+    bool ok = true;
+#pragma unroll
+    for (uint32_t j = 0; j < kB; ++j) {
+      const uint32_t c = count + j;
+      const double m1 = (double)(uint32_t)(c + 1u);
+      const double y = __drcp_rn(m1);
+      const double prod = __dmul_rn(m, (double)c);
+      const double num = __dadd_rn(prod, (double)dv[j]);
+      const double q0 = __dmul_rn(num, y);
+      const double r0 = __fma_rn(-q0, m1, num);
+      const double q1 = __fma_rn(r0, y, q0);
+      // the check of div_rn_by_int, off the chain
+      const double r1 = __fma_rn(-q1, m1, num);
+      const long long b = __double_as_longlong(q1);
+      const double up = __longlong_as_double(b + 1) - q1;
+      const double down = q1 - __longlong_as_double(b - 1);
+      ok = ok && (num == 0.0 ? q1 == 0.0
+                             : (q1 > 0.0 && r1 < 0.5 * up * m1 && -r1 < 0.5 * down * m1));
+      m = q1;
+    }
+    if (!ok) {
+      m = mean;
+      for (uint32_t j = 0; j < kB; ++j) {
+        const uint32_t c = count + j;
+        const double m1 = (double)(uint32_t)(c + 1u);
+        const double prod = __dmul_rn(m, (double)c);
+        m = div_rn_by_int(__dadd_rn(prod, (double)dv[j]), m1, __drcp_rn(m1));
+      }
+    }
+    mean = m;
+    count += kB;
+  }
+  for (; k < end; ++k) {
     const double d = (double)dur[k];
     const double m1 = (double)(uint32_t)(count + 1u);
     const double y = __drcp_rn(m1);

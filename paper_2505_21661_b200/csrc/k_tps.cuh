@@ -191,12 +191,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
   // (opaque: kept in registers instead of being rebuilt from the CTA's
   // shared window base at every use)
   const uint32_t s_info = opaque_u32(smem_addr(cs.info));
-#ifdef WGPF_TPS_INFO_SHFL
-  // region info by warp shuffle: lane r holds region r's entry (region ids
-  // < kTpsRegions = 32), so the per-step lookup is no shared-memory load
-  static_assert(kTpsRegions == 32, "one region per lane");
-  const uint32_t info_lane = cs.info[lane];  // (after the barrier above)
-#endif
   const uint32_t s_hist = opaque_u32(smem_addr(hist));
   const uint32_t s_hist_spare = opaque_u32(smem_addr(hist + K * WGPF_HIST_BINS));
   const uint32_t s_stk = smem_addr(&ws.stk[0][lane]);    // + 256 * level
@@ -333,11 +327,7 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       const uint32_t rid = (tag >> 12) & (kTpsRegions - 1u);
       const uint32_t inf = inf0;
       const uint32_t r1id = (r1.x >> 12) & (kTpsRegions - 1u);
-#ifdef WGPF_TPS_INFO_SHFL
-      const uint32_t i1 = __shfl_sync(FULL, info_lane, r1id);
-#else
       const uint32_t i1 = lds32(s_info + 4u * r1id);
-#endif
       if constexpr (kFull) {
         // every lane at a START (grouped lanes run the same program): a push
         // is all that happens -- no event, no statistics, no wait marker

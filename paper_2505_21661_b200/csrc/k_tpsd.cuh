@@ -1,36 +1,41 @@
-// k_tpsd.cuh -- pass 2 of replay_image for DEEP streams, thread per stream:
-// nesting up to kDeepDepth and region ids below kDeepRegions (config 5: 64
-// nested scopes, 64 labels).  Same algorithm and outputs as k_tps (k_tps.cuh
-// documents the reference mapping: unwrap_clock trace.hpp:257-272,
-// pair_records :294-346, replay :398-487, region_stats pipeline.hpp:114-133);
-// what changes with depth:
+// k_tpsd.cuh -- pass 2 of replay_image for DEEP and WIDE streams, thread per
+// stream.  Same algorithm and outputs as k_tps (k_tps.cuh documents the
+// reference mapping: unwrap_clock trace.hpp:257-272, pair_records :294-346,
+// replay :398-487, region_stats pipeline.hpp:114-133); two geometries
+// (DeepGeom below): the deep list (nesting <= 64, region ids < 64; config 5:
+// 64 nested scopes, 64 labels) and the wide list (nesting <= 32, region ids
+// < 256: plans with up to 256 labels).  What changes against k_tps:
 //
-//   * 64-row stacks.  The kernel is latency-bound (a lane's walk is a serial
-//     chain), so warps per SM are what it runs on, and shared memory is what
-//     limits them: the stack is split into a u32 clock row and a u16 row of
-//     {position (9 bits) | region (6) | consumable (1)} -- 12 KB per warp
-//     instead of 16 -- and the clock's high word is not stored at all: a
-//     pair's wrap count is read off the positions of the lane's last two
-//     clock wraps (a duration reaches 2^32 iff two wraps lie after the START,
-//     or one and the END's low word is not below the START's).  Iteration
-//     counters are u8 (a region completes at most cap / 2 <= 256 times),
-//     record windows 4 positions (+2) wide: 12 warps per SM (8 before).
-//   * statistics cannot be lane-private for 64 classes: events go to the
-//     CTA's shared table.  Streams of a trace usually advance in lockstep
-//     (same scope program, same wrap position), so a warp's events of one
-//     step mostly share a class: then one lane applies the warp's reduced
-//     sum / min / max with fire-and-forget shared reductions (red, no return
-//     value to wait for) and the first key, otherwise each lane updates the
-//     table with shared atomics.  Histograms: one shared increment per event;
-//     counts are the histogram sums.
+//   * stacks.  The kernel is latency-bound (a lane's walk is a serial chain),
+//     so warps per SM are what it runs on, and shared memory is what limits
+//     them: the stack is split into a u32 clock row and a meta row of
+//     {position (9 bits) | region | consumable} (u16 deep, u32 wide), and
+//     the clock's high word is not stored at all: a pair's wrap count is read
+//     off the positions of the lane's last two clock wraps (a duration
+//     reaches 2^32 iff two wraps lie after the START, or one and the END's
+//     low word is not below the START's).  Iteration counters are u8 (a
+//     region completes at most cap / 2 <= 256 times), record windows 4
+//     positions (+2) wide, three buffers: 12 warps per SM deep, 10 wide.
+//   * statistics cannot be lane-private for 64+ classes.  Streams of a trace
+//     usually advance in lockstep (same scope program, same wrap position),
+//     so a warp's events of one step mostly share a class: then one lane
+//     applies the warp's redux-reduced min / max to the CTA table with
+//     fire-and-forget shared reductions and the sum and the match.any-
+//     aggregated histogram bins to this CTA's replica rows in HBM with
+//     fire-and-forget global reductions (k_deep_reduce adds the replicas;
+//     counts are the bin sums); otherwise each lane updates the tables with
+//     atomics.  First-event keys skip their reductions once the batch's
+//     smallest stream has met the class.
+//   * kMarkers = false (no ".wait" labels in the plan) compiles out the
+//     consumed-wait / orphan-marker machinery of replay.
 //   * record windows: one 2-D TMA box per window when the warp's 32 list
 //     entries are 32 consecutive streams with one even start slot and the
 //     window does not cross the circular wrap (config 5: all but one window
 //     per stream), else 16-B cp.async chunks.  Lanes read records in 16-B
 //     pairs when the start is even (conflict-free LDS.128 at the 48-B pitch).
 //
-// It runs over pass 1's deep list (SF_WARP | SF_DEEP: depth <= 64, ids < 64,
-// not general); the warp-per-stream kernel (k_fast.cuh) takes pass 1's warp
+// It runs over pass 1's deep and wide lists (SF_WARP | SF_DEEP, not
+// general); the warp-per-stream kernel (k_fast.cuh) takes pass 1's warp
 // list (the rest).  Capacities up to kDeepMaxSlots (positions in 9 bits).
 #pragma once
 
@@ -40,8 +45,25 @@
 
 namespace wgpf {
 
-constexpr uint32_t kDeepDepth = 64;
-constexpr uint32_t kDeepRegions = 64;
+// Geometry.  kWide = false (the deep list): nesting <= 64, region ids < 64,
+// u16 stack meta {position (9) | region (6) | consumable (1)}.  kWide = true
+// (the wide list, plans with up to 256 region labels): nesting <= 32, region
+// ids < 256, u32 meta {position (9) | region (8) | consumable (1)}; the
+// iteration counters (u8 per region and lane) grow to 8 KB per warp and the
+// CTA tables to 256 classes, the stack halves: 10 warps per SM.
+template <bool kWide>
+struct DeepGeom {
+  static constexpr uint32_t kDepth = kWide ? 32u : 64u;
+  static constexpr uint32_t kRegions = kWide ? 256u : 64u;
+  static constexpr uint32_t kClasses = kWide ? 256u : kSmemClasses;
+  using Meta = std::conditional_t<kWide, uint32_t, uint16_t>;
+  static constexpr uint32_t kMetaRid = (kRegions - 1u) << 9;  // region bits of the meta
+  static constexpr uint32_t kCons = kWide ? 17u : 15u;         // consumable bit
+};
+constexpr uint32_t kDeepDepth = DeepGeom<false>::kDepth;
+constexpr uint32_t kDeepRegions = DeepGeom<false>::kRegions;
+constexpr uint32_t kWideDepth = DeepGeom<true>::kDepth;
+constexpr uint32_t kWideRegions = DeepGeom<true>::kRegions;
 constexpr uint32_t kDeepMaxSlots = 512;  // stack positions in 9 bits
 #ifndef WGPF_DEEP_W
 #define WGPF_DEEP_W 4
@@ -57,22 +79,23 @@ constexpr uint32_t kDeepWarps = WGPF_DEEP_WARPS;
 #define WGPF_DEEP_UNROLL 2  // record pairs per full-step loop iteration (measured: 2 > 1 by 1 %)
 #endif
 constexpr int kDeepUnroll = WGPF_DEEP_UNROLL;
-// stack meta: position | region << 9 | consumable << 15
-constexpr uint32_t kDeepMetaRid = (kDeepRegions - 1u) << 9;
 
 #ifndef WGPF_DEEP_BUFS
 #define WGPF_DEEP_BUFS 3
 #endif
 constexpr uint32_t kDeepBufs = WGPF_DEEP_BUFS;  // record windows: 2 or 3 (1 / 2 ahead)
 
+template <bool kWide>
 struct DeepWarpSmem {
+  using G = DeepGeom<kWide>;
   uint8_t rec[kDeepBufs][32 * kDeepPitch];  // record windows
   uint32_t lo_empty[32];                    // row -1 of each stack array: what
-  uint32_t stk_lo[kDeepDepth][32];          //   an empty stack reads (never
-  uint16_t meta_empty[32];                  //   written; the value is unused)
-  uint16_t stk_meta[kDeepDepth][32];        // START clock (low word);
+  uint32_t stk_lo[G::kDepth][32];           //   an empty stack reads (never
+  typename G::Meta meta_empty[32];          //   written; the value is unused)
+  typename G::Meta stk_meta[G::kDepth][32]; // START clock (low word);
                                             // position | region | consumable
-  uint8_t cnt[kDeepRegions][32];            // iteration counters
+  uint8_t cnt[G::kRegions][32];             // iteration counters
+  uint32_t seen[G::kClasses / 32];          // (kWide) first-key classes met
   unsigned long long bar[kDeepBufs];        // TMA windows: one mbarrier per buffer
 };
 
@@ -86,21 +109,30 @@ struct DeepWarpSmem {
 // keep SMs off each other's L2 lines (one shared table: 40 % slower), and
 // moving the 16-KB histogram out of shared memory buys warps.
 constexpr uint32_t kDeepRep = 2 + WGPF_HIST_BINS;
+template <bool kWide>
 struct DeepCtaSmem {
-  unsigned long long first[kSmemClasses];
-  uint32_t min[kSmemClasses];
-  uint32_t max[kSmemClasses];
-  uint32_t info[kDeepRegions];  // class | marker<<8 | wait class<<16
+  using G = DeepGeom<kWide>;
+  unsigned long long first[G::kClasses];
+  uint32_t min[G::kClasses];
+  uint32_t max[G::kClasses];
+  uint32_t info[G::kRegions];  // class | marker<<8 | wait class<<16
   unsigned long long warn[4];
 };
 
-__host__ __device__ inline size_t deep_smem_bytes(uint32_t warps) {
-  return tps_align(sizeof(DeepCtaSmem)) + warps * tps_align(sizeof(DeepWarpSmem));
+__host__ __device__ inline size_t deep_smem_bytes(uint32_t warps, bool wide = false) {
+  return wide ? tps_align(sizeof(DeepCtaSmem<true>)) +
+                    warps * tps_align(sizeof(DeepWarpSmem<true>))
+              : tps_align(sizeof(DeepCtaSmem<false>)) +
+                    warps * tps_align(sizeof(DeepWarpSmem<false>));
 }
-__host__ inline uint32_t deep_warps(size_t smem_limit) {
+__host__ inline uint32_t deep_warps(size_t smem_limit, bool wide = false) {
   uint32_t w = kDeepWarps;
-  while (w > 1 && deep_smem_bytes(w) > smem_limit) --w;
+  while (w > 1 && deep_smem_bytes(w, wide) > smem_limit) --w;
   return w;
+}
+// per-CTA replica rows of the statistics (k_tpsd / k_deep_reduce)
+__host__ __device__ inline uint32_t deep_classes(bool wide) {
+  return wide ? DeepGeom<true>::kClasses : DeepGeom<false>::kClasses;
 }
 
 __device__ __forceinline__ uint32_t lds8(uint32_t a) {
@@ -126,6 +158,19 @@ __device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
                "r"(a), "r"(v)
                : "memory");
 }
+// stack meta rows: u16 (deep) or u32 (wide)
+template <class M>
+__device__ __forceinline__ uint32_t lds_meta(uint32_t a) {
+  if constexpr (sizeof(M) == 2) return lds16(a); else return lds32(a);
+}
+template <class M>
+__device__ __forceinline__ void sts_meta(uint32_t a, uint32_t v) {
+  if constexpr (sizeof(M) == 2) sts16(a, v); else sts32(a, v);
+}
+template <class M>
+__device__ __forceinline__ void sts_meta_if(bool p, uint32_t a, uint32_t v) {
+  if constexpr (sizeof(M) == 2) sts16_if(p, a, v); else sts32_if(p, a, v);
+}
 __device__ __forceinline__ void red_gadd64(unsigned long long* a, unsigned long long v) {
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
 }
@@ -142,25 +187,30 @@ __device__ __forceinline__ void red_max32(uint32_t a, uint32_t v) {
 // record can be a consumed wait or an orphan marker (replay,
 // trace.hpp:421-485, only pairs a base with a ".wait" class), so that
 // machinery -- about a fifth of an END step -- is compiled out.
-template <bool kEmit, bool kStats, bool kMarkers>
+// kWide: the geometry above (DeepGeom).
+template <bool kEmit, bool kStats, bool kMarkers, bool kWide>
 __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     k_tpsd(FastArgs a, const __grid_constant__ CUtensorMap tm) {
+  using G = DeepGeom<kWide>;
+  using CtaS = DeepCtaSmem<kWide>;
+  using WarpS = DeepWarpSmem<kWide>;
+  constexpr uint32_t kMS = sizeof(typename G::Meta) / 2u;  // meta row scale
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  DeepCtaSmem& cs = *reinterpret_cast<DeepCtaSmem*>(smem_raw);
+  CtaS& cs = *reinterpret_cast<CtaS*>(smem_raw);
   const uint32_t lane = lane_id();
   const uint32_t w = threadIdx.x >> 5;
   const uint32_t nw = blockDim.x >> 5;
   const uint32_t K = a.plan.K;
-  DeepWarpSmem& ws = *reinterpret_cast<DeepWarpSmem*>(
-      smem_raw + tps_align(sizeof(DeepCtaSmem)) + w * tps_align(sizeof(DeepWarpSmem)));
+  WarpS& ws = *reinterpret_cast<WarpS*>(smem_raw + tps_align(sizeof(CtaS)) +
+                                        w * tps_align(sizeof(WarpS)));
   constexpr bool stats = kStats;
   constexpr bool emit = kEmit;
-  for (uint32_t c = threadIdx.x; c < kSmemClasses; c += blockDim.x) {
+  for (uint32_t c = threadIdx.x; c < G::kClasses; c += blockDim.x) {
     cs.first[c] = ~0ull;
     cs.min[c] = 0xFFFFFFFFu;
     cs.max[c] = 0u;
   }
-  for (uint32_t r = threadIdx.x; r < kDeepRegions; r += blockDim.x) {
+  for (uint32_t r = threadIdx.x; r < G::kRegions; r += blockDim.x) {
     uint32_t inf = 0xFFFFFFFFu;
     if (r < a.fast_regions) {
       const uint32_t c = a.plan.class_of[r];
@@ -186,7 +236,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 
   const uint32_t s_info = opaque_u32(smem_addr(cs.info));
   const uint32_t s_lo = smem_addr(&ws.stk_lo[0][lane]);      // + 128 * level
-  const uint32_t s_meta = smem_addr(&ws.stk_meta[0][lane]);  // + 64 * level
+  const uint32_t s_meta = smem_addr(&ws.stk_meta[0][lane]);  // + 64 kMS * level
   const uint32_t s_cnt = smem_addr(&ws.cnt[0][lane]);        // + 32 * region
   const uint32_t s_cnt_all = smem_addr(&ws.cnt[0][0]);
   const uint32_t s_min = opaque_u32(smem_addr(cs.min));
@@ -197,7 +247,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
   const uint64_t n_list = *a.list_len;
 
   // this CTA's replica of the count / sum / histogram table
-  unsigned long long* const rep = a.deep_rep + (size_t)blockIdx.x * kSmemClasses * kDeepRep;
+  unsigned long long* const rep = a.deep_rep + (size_t)blockIdx.x * G::kClasses * kDeepRep;
+  const uint32_t s_seen = smem_addr(ws.seen);  // (kWide)
   // First-event keys.  Keys are (stream, event index): a lane meets its
   // keys in increasing order and the batch's smallest stream (lane `lmin`)
   // beats every other lane.  So once a warp-uniform step of class c has had
@@ -215,7 +266,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     const uint32_t leader = __ffs(pm) - 1u;
     // histogram bin: lanes with the same bin aggregate into one reduction
     const uint32_t bin = hist_bin32(d);
-    if (uni && c0 < kSmemClasses && c0 < K) {
+    if (uni && c0 < G::kClasses && c0 < K) {
       unsigned long long* const rc = rep + c0 * kDeepRep;  // this class's replica row
       const uint32_t dd = p ? d : 0u;
       const uint32_t mn = __reduce_min_sync(FULL, p ? d : 0xFFFFFFFFu);
@@ -231,7 +282,11 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         sum = (unsigned long long)slo + ((unsigned long long)shi << 16);
       }
       const uint32_t same = __match_any_sync(FULL, p ? bin : 0xFFFFFFFFu);
-      const bool seen = (wseen >> c0) & 1ull;
+      bool seen;
+      if constexpr (kWide)  // (lane 0's view of the warp's table, broadcast)
+        seen = (__shfl_sync(FULL, lds32(s_seen + 4u * (c0 >> 5)), 0) >> (c0 & 31u)) & 1u;
+      else
+        seen = (wseen >> c0) & 1ull;
       if (!seen) {
         // smallest 64-bit first-event key of the participating lanes
         const unsigned long long cur_first =
@@ -241,7 +296,14 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         const uint32_t klo = __reduce_min_sync(FULL, cand ? (uint32_t)key : 0xFFFFFFFFu);
         const unsigned long long fk = ((unsigned long long)khi << 32) | klo;
         if (lane == leader && fk < cur_first) atomicMin(&cs.first[c0], fk);
-        if ((pm >> lmin) & 1u) wseen |= 1ull << c0;
+        if ((pm >> lmin) & 1u) {
+          if constexpr (kWide) {
+            if (lane == 0)
+              sts32(s_seen + 4u * (c0 >> 5), lds32(s_seen + 4u * (c0 >> 5)) | (1u << (c0 & 31u)));
+          } else {
+            wseen |= 1ull << c0;
+          }
+        }
       }
       if (lane == leader) {
         // fire-and-forget reductions: nothing comes back to wait for (the
@@ -252,7 +314,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       }
       if (p && lane == __ffs(same) - 1u) red_gadd64(rc + 2u + bin, (unsigned long long)__popc(same));
     } else if (p) {
-      if (cls < kSmemClasses && cls < K) {
+      if (cls < G::kClasses && cls < K) {
         red_gadd64(rep + cls * kDeepRep + 1u, (unsigned long long)d);
         red_gadd64(rep + cls * kDeepRep + 2u + bin, 1ull);
         red_min32(s_min + 4u * cls, d);
@@ -295,11 +357,12 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
           __reduce_min_sync(FULL, act && (uint32_t)(s >> 32) == shi_ ? (uint32_t)s : 0xFFFFFFFFu);
       lmin = __ffs(__ballot_sync(FULL, act && s == (((uint64_t)shi_ << 32) | slo_))) - 1u;
       wseen = 0;
+      if (kWide && lane < G::kClasses / 32u) sts32(s_seen + 4u * lane, 0u);
     }
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
     // iteration counters: the warp clears its 2 KB table with 16-B stores
 #pragma unroll
-    for (uint32_t k = lane; k < kDeepRegions * 32u / 16u; k += 32)
+    for (uint32_t k = lane; k < G::kRegions * 32u / 16u; k += 32)
       sts128_if(true, s_cnt_all + 16u * k, make_uint4(0u, 0u, 0u, 0u));
     __syncwarp();
 
@@ -356,7 +419,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
     uint2 r0 = make_uint2(0u, 0u), r1 = make_uint2(0u, 0u);
     if (n > 0) r0 = slots[start];
     if (n > 1) r1 = slots[start + 1 < cap ? start + 1 : start + 1 - cap];
-    uint32_t inf0 = cs.info[(r0.x >> 12) & (kDeepRegions - 1u)];
+    uint32_t inf0 = cs.info[(r0.x >> 12) & (G::kRegions - 1u)];
     // kDeepBufs - 1 windows in flight ahead of the walk
     issue(0, 2);
     cp_async_commit();
@@ -392,14 +455,14 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       const bool isS = (int32_t)tag < 0;
       const bool st = valid && isS;
       const bool en = valid && !isS;
-      const uint32_t rid = (tag >> 12) & (kDeepRegions - 1u);
+      const uint32_t rid = (tag >> 12) & (G::kRegions - 1u);
       const uint32_t inf = inf0;
-      const uint32_t r1id = (r1.x >> 12) & (kDeepRegions - 1u);
+      const uint32_t r1id = (r1.x >> 12) & (G::kRegions - 1u);
       const uint32_t i1 = lds32(s_info + 4u * r1id);
       const bool wrap = valid && v < vprev;
       const uint32_t meta_new =
-          i | ((tag >> 3) & kDeepMetaRid) |
-          ((kMarkers && pw == (inf & 0xFFu) ? 1u : 0u) << 15);
+          i | ((tag >> 3) & G::kMetaRid) |
+          ((kMarkers && pw == (inf & 0xFFu) ? 1u : 0u) << G::kCons);
       if constexpr (kFull) {
         // every lane at a START (the streams of a trace run the same program
         // from the same wrap position): a push is all that happens
@@ -410,7 +473,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
           vprev = v;
           tp += 64;
           sts32(s_lo + 2 * tp, v);
-          sts16(s_meta + tp, meta_new);
+          sts_meta<typename G::Meta>(s_meta + kMS * tp, meta_new);
           pw = 0xFFu;
           inf0 = i1;
           r0 = r1;
@@ -423,19 +486,19 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       w_last = wrap ? i : w_last;
       vprev = valid ? v : vprev;
       const uint32_t elo = lds32(s_lo + 2 * tp);
-      const uint32_t em = lds16(s_meta + tp);
+      const uint32_t em = lds_meta<typename G::Meta>(s_meta + kMS * tp);
       const bool nonempty = tp >= 0;
       const bool mend = en && nonempty;
       w_drop += (en && !nonempty) ? 1u : 0u;
       sts32_if(st, s_lo + 2 * (tp + 64), v);
-      sts16_if(st, s_meta + tp + 64, meta_new);
+      sts_meta_if<typename G::Meta>(st, s_meta + kMS * (tp + 64), meta_new);
       tp += (st ? 64 : 0) - (mend ? 64 : 0);
       const uint32_t spos = em & 511u;
       const uint32_t meas = v - elo;  // low 32 bits of u - su
       // the pair spans >= 2^32 cycles iff two clock wraps lie after the
       // START, or one and the END's low word is not below the START's
       const bool tl = w_prev > spos || (w_last > spos && v >= elo);
-      const bool mism = mend && ((em ^ (tag >> 3)) & kDeepMetaRid) != 0u;
+      const bool mism = mend && ((em ^ (tag >> 3)) & G::kMetaRid) != 0u;
       const bool tlong = mend && !mism && tl;
       broken |= mism || tlong;
       const bool ok = mend && !mism && !tlong;
@@ -445,12 +508,12 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
       sts8_if(ok, ca, it + 1u);
       const bool is_mk = kMarkers && (inf & 0x100u) != 0u;
       const bool base = ok && !is_mk;
-      const bool orphan = kMarkers && ok && is_mk && !((em >> 15) & 1u);
+      const bool orphan = kMarkers && ok && is_mk && !((em >> G::kCons) & 1u);
       const uint32_t dpos = i - spos;
       const uint32_t ovh = cost * dpos;
       const uint32_t corr = ovh > meas ? 0u : meas - ovh;
       const bool cclose = (kFull || i + 2 < n) && (int32_t)r2.x >= 0 &&
-                          ((r2.x >> 12) & (kDeepRegions - 1u)) == r1id;
+                          ((r2.x >> 12) & (G::kRegions - 1u)) == r1id;
       const bool consumed = kMarkers && base && (kFull || i + 1 < n) && (int32_t)r1.x < 0 &&
                             (i1 & 0x100u) && (inf >> 16) == (i1 & 0xFFu) &&
                             ((int32_t)(i + 1) <= z || cclose);
@@ -531,7 +594,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         put(po, kw, (uint32_t)o.start, (uint32_t)(o.start >> 32), (uint32_t)o.end,
             (uint32_t)(o.end >> 32), o.region, o.iteration);
       if (stats)
-        wstat(po, cs.info[o.region & (kDeepRegions - 1u)] & 0xFFu,
+        wstat(po, cs.info[o.region & (G::kRegions - 1u)] & 0xFFu,
               (uint32_t)(o.end - o.start), gkey | (kw << 1));
       kw += po ? 1u : 0u;
     }
@@ -563,7 +626,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
   if (threadIdx.x < 4 && cs.warn[threadIdx.x])
     atomicAdd(&a.status->warn[threadIdx.x], cs.warn[threadIdx.x]);
   if (stats) {  // the CTA's min / max / first keys into the global table
-    const uint32_t kc = K < kSmemClasses ? K : kSmemClasses;
+    const uint32_t kc = K < G::kClasses ? K : G::kClasses;
     for (uint32_t c = threadIdx.x; c < kc; c += blockDim.x) {
       if (cs.min[c] == 0xFFFFFFFFu && cs.max[c] == 0u && cs.first[c] == ~0ull) continue;
       atomicMin(&a.stats.min[c], (unsigned long long)cs.min[c]);
@@ -574,13 +637,14 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 }
 
 // Sums the per-CTA replicas of the deep kernel into the global table.
+// classes: the replica rows per CTA (deep_classes)
 __global__ void k_deep_reduce(const unsigned long long* rep, uint32_t ctas, uint32_t K,
-                              DevStats st) {
-  const uint32_t kc = K < kSmemClasses ? K : kSmemClasses;
+                              DevStats st, uint32_t classes) {
+  const uint32_t kc = K < classes ? K : classes;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < kc * kDeepRep;
        i += gridDim.x * blockDim.x) {
     unsigned long long t = 0;
-    for (uint32_t b = 0; b < ctas; ++b) t += rep[(size_t)b * kSmemClasses * kDeepRep + i];
+    for (uint32_t b = 0; b < ctas; ++b) t += rep[(size_t)b * classes * kDeepRep + i];
     if (!t) continue;
     const uint32_t c = i / kDeepRep, f = i % kDeepRep;
     if (f == 0)

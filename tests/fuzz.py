@@ -102,7 +102,7 @@ def random_image(seed: int, n_streams: int = 8, cap: int = 64,
 DEEP_LABELS = [f"D{i:02d}" for i in range(56)] + [f"D{i:02d}.wait" for i in range(8)]
 
 
-def _deep_records(rng, writes, depth, big_gaps, violate):
+def _deep_records(rng, writes, depth, big_gaps, violate, level_ids=None, n_base=56):
     """A nesting program `depth` levels deep (labels D00.. by level),
     repeated: START per level going down, at the bottom an async group of an
     eight-label base (S(X) E(X) S(X.wait) E(X.wait)) or a plain scope, then
@@ -121,18 +121,19 @@ def _deep_records(rng, writes, depth, big_gaps, violate):
 
     while len(tags) < writes:
         d = depth if rng.random() < 0.7 else int(rng.integers(1, depth + 1))
+        ids = level_ids if level_ids is not None else list(range(depth))
         for lv in range(d):
-            rec(0x80000000 | (lv << 12))
+            rec(0x80000000 | (ids[lv] << 12))
         x = int(rng.integers(0, 8))
         if rng.random() < 0.5:
             rec(0x80000000 | (x << 12))
             rec(x << 12)
-            rec(0x80000000 | ((56 + x) << 12))
-            rec((56 + x) << 12)
+            rec(0x80000000 | ((n_base + x) << 12))
+            rec((n_base + x) << 12)
         for lv in reversed(range(d)):
-            r = lv
+            r = ids[lv]
             if violate and rng.random() < 0.01:
-                r = (lv + 1) % 56
+                r = ids[(lv + 1) % d] if d > 1 else (r + 1) % n_base
             rec(r << 12)
     return np.array(tags[:writes], np.uint32), np.array(clocks[:writes], np.uint32)
 
@@ -160,3 +161,32 @@ def deep_image(seed: int, n_streams: int = 64, cap: int = 256, depth: int = 40,
             body[s, 5 + 2 * slot] = clocks[w]
     data = S.kpft_v1(body.view(np.uint8).reshape(-1), n_streams)
     return data, cap, 0, list(DEEP_LABELS)
+
+
+def wide_image(seed: int, n_streams: int = 64, cap: int = 256, depth: int = 20,
+               n_labels: int = 200, same_start: bool = True, big_gaps: bool = False,
+               violate: bool = False, per_block: int = 16):
+    """Circular streams of plans with many labels (the wide thread-per-stream
+    kernel's inputs): labels W000.. (n_labels - 8 bases, then ".wait" markers
+    of the first eight), every stream nests `depth` levels whose region ids
+    are drawn from the whole table (ids >= 64 past the deep kernel).
+    Returns (kpft v1 bytes, slots, strategy, labels)."""
+    rng = np.random.default_rng(seed)
+    n_base = n_labels - 8
+    labels = [f"W{i:03d}" for i in range(n_base)] + [f"W{i:03d}.wait" for i in range(8)]
+    level_ids = [int(x) for x in rng.choice(np.arange(8, n_base), depth, replace=False)]
+    body = np.zeros((n_streams, 4 + 2 * cap), np.uint32)
+    base_writes = 3 * cap + 2 * int(rng.integers(0, cap // 2))
+    for s in range(n_streams):
+        writes = base_writes if same_start else int(rng.integers(cap + 1, 4 * cap))
+        tags, clocks = _deep_records(rng, writes, depth, big_gaps, violate, level_ids, n_base)
+        body[s, 0] = s // per_block
+        body[s, 1] = s % per_block
+        body[s, 2] = writes
+        body[s, 3] = cap
+        for w in range(writes):
+            slot = w % cap
+            body[s, 4 + 2 * slot] = tags[w]
+            body[s, 5 + 2 * slot] = clocks[w]
+    data = S.kpft_v1(body.view(np.uint8).reshape(-1), n_streams)
+    return data, cap, 0, labels

@@ -855,6 +855,77 @@ def test_deep_kernel_vs_oracle(ctx, oracle, case):
                                         s.hist), (case, seed, s.label)
 
 
+WIDE_CASES = [
+    dict(n_streams=96, cap=256, depth=20),                          # TMA windows
+    dict(n_streams=96, cap=256, depth=32, same_start=False),        # cp.async, full depth
+    dict(n_streams=64, cap=256, depth=33),                          # past the wide depth
+    dict(n_streams=64, cap=256, depth=12, n_labels=300),            # ids >= 256: general
+    dict(n_streams=64, cap=128, depth=24, big_gaps=True),           # clock wraps
+    dict(n_streams=64, cap=256, depth=16, violate=True),            # broken nesting
+    dict(n_streams=40, cap=512, depth=8, n_labels=120),             # 9-bit positions
+]
+
+
+def _check_vs_oracle(ctx, oracle, data, cap, strategy, labels, tag):
+    t = T()
+    try:
+        o, oerr = oracle.replay_kpft(data, cap, strategy, labels, 33), None
+    except O.OracleError as e:
+        o, oerr = None, (e.category, str(e))
+    try:
+        r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33, flags=0x2)
+        gerr = None
+    except t.Error as e:
+        r, gerr = None, (e.category(), str(e))
+    assert oerr == gerr, (tag, oerr, gerr)
+    if oerr:
+        return None
+    assert len(r.events) == len(o.events) > 0
+    assert np.array_equal(r.events, o.events), tag
+    assert (r.dropped_heads, r.truncated_tails, r.flagged_preconditions,
+            r.malformed_groups) == (o.dropped_heads, o.truncated_tails,
+                                    o.flagged_preconditions, o.malformed_groups)
+    want = oracle.region_stats(o.events, labels)
+    got = ctx.stats()
+    assert list(got) == [s.label for s in want]
+    for s in want:
+        g = got[s.label]
+        assert (g.count, g.min, g.max, g.sum, g.mean, g.first_event, g.warp_group,
+                g.kind, g.hist) == (s.count, s.min, s.max, s.sum, s.mean,
+                                    s.first_event, s.warp_group, s.kind,
+                                    s.hist), (tag, s.label)
+    return r
+
+
+@pytest.mark.parametrize("case", range(len(WIDE_CASES)))
+def test_wide_kernel_vs_oracle(ctx, oracle, case):
+    """Plans with 120-300 labels: nesting up to 32 over region ids < 256 takes
+    the wide thread-per-stream kernel (k_tpsd<kWide>), deeper streams the
+    warp-per-stream kernel, ids >= 256 the general path -- all bit-exact with
+    the oracle (events, warnings, every statistics field)."""
+    for seed in range(3):
+        data, cap, strategy, labels = fuzz.wide_image(41000 + 10 * case + seed,
+                                                      **WIDE_CASES[case])
+        _check_vs_oracle(ctx, oracle, data, cap, strategy, labels, (case, seed))
+
+
+def test_wide_kernel_equals_warp_kernel(ctx, monkeypatch):
+    """The wide thread-per-stream kernel and the warp-per-stream kernel
+    (WGPF_NO_WIDE=1) give the same events and statistics on a larger body
+    with 200 labels, 24-deep nesting."""
+    import torch
+    from paper_2505_21661_b200 import trace as Tm
+    data, cap, strategy, labels = fuzz.wide_image(42000, n_streams=2048, depth=24)
+    r = ctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33, flags=0x2)
+    want_st = ctx.stats()
+    monkeypatch.setenv("WGPF_NO_WIDE", "1")
+    wctx = Tm.Context(0)
+    r2 = wctx.replay_image_bytes(data, plan_of(cap, strategy, labels), 33, flags=0x2)
+    assert np.array_equal(r.events, r2.events)
+    assert wctx.stats() == want_st
+    del torch
+
+
 def test_exact_mean_recurrence_stress(ctx, oracle):
     """region_stats' bit-exact mean (pipeline.hpp:129) over long chains of
     random durations across the whole u32 range (the GPU division by the

@@ -1136,7 +1136,7 @@ static int finalize_stats(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
                    c->d_aux2.as<uint32_t>(), c->d_aux1.as<unsigned long long>(),
                    c->d_aux3.as<unsigned long long>(), (int64_t)n_events, 0, 32,
                    c->stream));
-    k_exact_mean<<<(ns + 127) / 128, 128, 0, c->stream>>>(
+    k_exact_mean<<<ns, kEmThreads, 0, c->stream>>>(
         c->d_aux2.as<uint32_t>(), c->d_aux3.as<unsigned long long>(), n_events,
         dev_stats(c), ns, c->d_mean.as<double>(), nullptr);
     CUDA_OK(c, cudaGetLastError());

@@ -89,85 +89,115 @@ __device__ __forceinline__ double div_rn_by_int(double num, double n, double y) 
 // thread per class: the segment of its class in the class-sorted (stable)
 // durations is found first, so the loop's loads and reciprocals do not wait
 // on the recurrence.
-__global__ void k_exact_mean(const uint32_t* sorted_cls,
-                             const unsigned long long* dur, uint64_t n,
-                             const DevStats st, uint32_t n_slots,
-                             double* mean_out, const int* slot_of_class_dense) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// One CTA per class.  The recurrence is one thread's serial chain, so the
+// rest of the CTA feeds it: warps 1-3 stream the class's durations from HBM
+// and compute the per-step constants -- d as a double and y = RN(1 / (count
+// + 1)) -- into a double-buffered shared-memory ring, one chunk ahead of the
+// consumer (thread 0), which then only runs the chain: 5 dependent FP64
+// operations per event (prod, num, the Markstein quotient q1), with the
+// quotient's exactness check beside it (ILP) rather than on it.  A block of
+// kB steps with a failed check (a tie or a miss, rare) is redone with the
+// checked division (div_rn_by_int) from the block's start.
+constexpr uint32_t kEmChunk = 1024;  // events per ring chunk
+constexpr uint32_t kEmThreads = 128;
+__global__ void __launch_bounds__(kEmThreads) k_exact_mean(
+    const uint32_t* sorted_cls, const unsigned long long* dur, uint64_t n, const DevStats st,
+    uint32_t n_slots, double* mean_out, const int* slot_of_class_dense) {
+  (void)slot_of_class_dense;
+  __shared__ double2 ring[2][kEmChunk];  // {y, d}
+  __shared__ unsigned long long seg[2];
+  const uint32_t i = blockIdx.x;
+  const uint32_t tid = threadIdx.x;
   if (i >= n_slots) return;
-  mean_out[i] = 0.0;
-  if (st.count[i] == 0) return;
-  const uint32_t cls = i < st.K ? i : st.hkey[i - st.K];
-  uint64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (sorted_cls[mid] < cls) lo = mid + 1; else hi = mid;
+  if (st.count[i] == 0) {
+    if (tid == 0) mean_out[i] = 0.0;
+    return;
   }
-  uint64_t end = lo, top = n;
-  while (end < top) {
-    const uint64_t mid = (end + top) >> 1;
-    if (sorted_cls[mid] <= cls) end = mid + 1; else top = mid;
+  if (tid == 0) {
+    const uint32_t cls = i < st.K ? i : st.hkey[i - st.K];
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (sorted_cls[mid] < cls) lo = mid + 1; else hi = mid;
+    }
+    uint64_t end = lo, top = n;
+    while (end < top) {
+      const uint64_t mid = (end + top) >> 1;
+      if (sorted_cls[mid] <= cls) end = mid + 1; else top = mid;
+    }
+    seg[0] = lo;
+    seg[1] = end;
   }
+  __syncthreads();
+  const uint64_t lo = seg[0], len = seg[1] - seg[0];
+  const uint64_t chunks = (len + kEmChunk - 1) / kEmChunk;
+  // producers: warps 1..3 fill chunk q of the ring
+  auto fill = [&](uint64_t q) {
+    const uint64_t base = q * kEmChunk;
+    const uint32_t m = (uint32_t)(len - base < kEmChunk ? len - base : kEmChunk);
+    double2* r = ring[q & 1];
+    for (uint32_t j = tid - 32u; j < m; j += kEmThreads - 32u) {
+      const uint32_t c = (uint32_t)(base + j);  // the u32 count before this event
+      r[j] = make_double2(__drcp_rn((double)(uint32_t)(c + 1u)),
+                          (double)__ldg(dur + lo + base + j));
+    }
+  };
+  if (tid >= 32) fill(0);
+  __syncthreads();
   double mean = 0.0;
   uint32_t count = 0;
-  // blocks of kB durations loaded ahead of the recurrence (the loads and the
-  // reciprocals do not depend on it; one thread per class would otherwise
-  // wait for every load)
-  // Speculation: the quotient's correctness check (div_rn_by_int) is taken
-  // off the recurrence's critical path -- a block runs on the Markstein
-  // quotient q1 alone (5 dependent FP64 operations per event) while the
-  // checks accumulate beside it; a block with any failed check (a tie or a
-  // miss, rare) is redone with the checked division from its start.
-  constexpr uint32_t kB = 16;
-  uint64_t k = lo;
-  for (; k + kB <= end; k += kB) {
-    unsigned long long dv[kB];
+  for (uint64_t q = 0; q < chunks; ++q) {
+    if (tid >= 32) {
+      if (q + 1 < chunks) fill(q + 1);
+    } else if (tid == 0) {
+      const double2* r = ring[q & 1];
+      const uint32_t m = (uint32_t)(len - q * kEmChunk < kEmChunk ? len - q * kEmChunk : kEmChunk);
+      constexpr uint32_t kB = 16;
+      uint32_t j0 = 0;
+      for (; j0 + kB <= m; j0 += kB) {
+        double2 v[kB];
 #pragma unroll
-    for (uint32_t j = 0; j < kB; ++j) dv[j] = __ldg(dur + k + j);
-    double m = mean;
-    bool ok = true;
+        for (uint32_t j = 0; j < kB; ++j) v[j] = r[j0 + j];
+        double mm = mean;
+        bool ok = true;
 #pragma unroll
-    for (uint32_t j = 0; j < kB; ++j) {
-      const uint32_t c = count + j;
-      const double m1 = (double)(uint32_t)(c + 1u);
-      const double y = __drcp_rn(m1);
-      const double prod = __dmul_rn(m, (double)c);
-      const double num = __dadd_rn(prod, (double)dv[j]);
-      const double q0 = __dmul_rn(num, y);
-      const double r0 = __fma_rn(-q0, m1, num);
-      const double q1 = __fma_rn(r0, y, q0);
-      // the check of div_rn_by_int, off the chain
-      const double r1 = __fma_rn(-q1, m1, num);
-      const long long b = __double_as_longlong(q1);
-      const double up = __longlong_as_double(b + 1) - q1;
-      const double down = q1 - __longlong_as_double(b - 1);
-      ok = ok && (num == 0.0 ? q1 == 0.0
-                             : (q1 > 0.0 && r1 < 0.5 * up * m1 && -r1 < 0.5 * down * m1));
-      m = q1;
-    }
-    if (!ok) {
-      m = mean;
-      for (uint32_t j = 0; j < kB; ++j) {
-        const uint32_t c = count + j;
-        const double m1 = (double)(uint32_t)(c + 1u);
-        const double prod = __dmul_rn(m, (double)c);
-        m = div_rn_by_int(__dadd_rn(prod, (double)dv[j]), m1, __drcp_rn(m1));
+        for (uint32_t j = 0; j < kB; ++j) {
+          const uint32_t c = count + j;
+          const double m1 = (double)(uint32_t)(c + 1u), y = v[j].x;
+          const double prod = __dmul_rn(mm, (double)c);
+          const double num = __dadd_rn(prod, v[j].y);
+          const double q0 = __dmul_rn(num, y);
+          const double r0 = __fma_rn(-q0, m1, num);
+          const double q1 = __fma_rn(r0, y, q0);
+          const double r1 = __fma_rn(-q1, m1, num);
+          const long long bb = __double_as_longlong(q1);
+          const double up = __longlong_as_double(bb + 1) - q1;
+          const double down = q1 - __longlong_as_double(bb - 1);
+          ok = ok && (num == 0.0 ? q1 == 0.0
+                                 : (q1 > 0.0 && r1 < 0.5 * up * m1 && -r1 < 0.5 * down * m1));
+          mm = q1;
+        }
+        if (!ok) {
+          mm = mean;
+          for (uint32_t j = 0; j < kB; ++j) {
+            const uint32_t c = count + j;
+            const double m1 = (double)(uint32_t)(c + 1u);
+            mm = div_rn_by_int(__dadd_rn(__dmul_rn(mm, (double)c), v[j].y), m1, v[j].x);
+          }
+        }
+        mean = mm;
+        count += kB;
+      }
+      for (uint32_t j = j0; j < m; ++j) {
+        const double m1 = (double)(uint32_t)(count + 1u);
+        const double prod = __dmul_rn(mean, (double)count);
+        mean = div_rn_by_int(__dadd_rn(prod, r[j].y), m1, r[j].x);
+        ++count;
       }
     }
-    mean = m;
-    count += kB;
+    __syncthreads();
   }
-  for (; k < end; ++k) {
-    const double d = (double)dur[k];
-    const double m1 = (double)(uint32_t)(count + 1u);
-    const double y = __drcp_rn(m1);
-    const double prod = __dmul_rn(mean, (double)count);
-    const double num = __dadd_rn(prod, d);
-    mean = div_rn_by_int(num, m1, y);
-    ++count;
-  }
-  mean_out[i] = mean;
-  (void)slot_of_class_dense;
+  if (tid == 0) mean_out[i] = mean;
 }
 
 __global__ void k_event_class_dur(const wgpf_event* ev, uint64_t n,

@@ -648,6 +648,8 @@ def main():
         p1line["accuracy_scopes"] = [{k: o[k] for k in ("scope", "chain", "true_cycles",
                                                          "record_cycles", "rel_err")}
                                      for o in acc["scopes"]]
+        # FinalizeOp cost: cycles per CTA to copy the profile buffer out
+        p1line["flush_cycles_per_cta"] = bench_p1.measure_flush()
 
     if rank == 0:
         line = {

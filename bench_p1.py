@@ -332,6 +332,31 @@ def measure_attn(B: int = 16, H: int = 16, S: int = 8192, iters: int = 20,
     return line
 
 
+def measure_flush(sizes=(3168, 32768), ctas: int = 148, threads: int = 192) -> dict:
+    """FinalizeOp cost (the P1 flush at kernel exit, vgpu.hpp:136-148): cycles
+    per CTA from the barrier after the last record to the end of the copy-out,
+    every CTA of a one-wave grid flushing at once -- 16-B vector stores by
+    all threads vs one cp.async.bulk (wgpf_dev::flush_bulk, used by the GEMM
+    and attention).  Both must leave the same bytes in HBM."""
+    import torch
+    from paper_2505_21661_b200 import p1
+    out = {}
+    for nb in sizes:
+        row = {}
+        bufs = []
+        for bulk in (False, True):
+            prof = torch.zeros(ctas * nb, dtype=torch.uint8, device="cuda")
+            cyc = torch.zeros(ctas, dtype=torch.int64, device="cuda")
+            for _ in range(3):
+                p1.flush_cost(ctas, threads, nb, bulk, prof.data_ptr(), cyc.data_ptr())
+            torch.cuda.synchronize()
+            row["bulk" if bulk else "vector"] = float(cyc.float().median().item())
+            bufs.append(prof)
+        row["identical"] = bool(torch.equal(bufs[0], bufs[1]))
+        out[str(nb)] = row
+    return out
+
+
 def measure_accuracy(chains=(1000, 10000, 100000), scopes=(8, 40), ctas: int = 148,
                      warps: int = 4, reps: int = 7, record_cost: int | None = None,
                      mem_chains=(100, 1000)) -> dict:

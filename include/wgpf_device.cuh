@@ -466,4 +466,29 @@ __device__ __forceinline__ void flush(const void* smem_buf, void* profile_mem,
   }
 }
 
+// FinalizeOp on the bulk-copy engine: after the CTA's barrier one thread
+// hands the whole buffer (a contiguous KPFT body segment) to cp.async.bulk
+// (shared -> global) and waits for it; the other threads are free at once.
+// Needs a 16-byte aligned segment of a multiple of 16 bytes (even capacities
+// or an even stream count, and a 16-byte aligned profile_mem), else falls
+// back to flush().  The records were written through the generic proxy, so
+// the copy (async proxy) is preceded by a proxy fence.
+__device__ __forceinline__ void flush_bulk(const void* smem_buf, void* profile_mem,
+                                           uint64_t cta_linear, uint32_t bytes, uint32_t tid,
+                                           uint32_t nthreads) {
+  uint8_t* dst = static_cast<uint8_t*>(profile_mem) + cta_linear * (uint64_t)bytes;
+  if ((bytes & 15u) != 0 || (reinterpret_cast<uintptr_t>(dst) & 15u) != 0) {
+    flush(smem_buf, profile_mem, cta_linear, bytes, tid, nthreads);
+    return;
+  }
+  if (tid == 0 && bytes) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_addr(smem_buf)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
 }  // namespace wgpf_dev

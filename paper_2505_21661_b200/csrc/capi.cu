@@ -1006,7 +1006,7 @@ static int replay_overlapped(wgpf_ctx* c, CountArgs ca, const uint8_t* body, uin
 
   const FastArgs f = fast_args(c, body, stride, n_streams, stream_base, record_cost, events,
                                events_cap, no_stats);
-  const void* k_big = (const void*)k_count_tps<kCountWarps, kCountUnroll, 1>;
+  const void* k_big = (const void*)k_count_tps<kCountWarps, kCountUnroll, kCountMinBlocks>;
   const uint32_t g_big = grid_for(c, k_big, kCountWarps * 32, 0);
   for (size_t k = 0; k < C; ++k) {
     const uint64_t s0 = cs[k], n = cs[k + 1] - cs[k];
@@ -1027,7 +1027,7 @@ static int replay_overlapped(wgpf_ctx* c, CountArgs ca, const uint8_t* body, uin
                                                    CU_TENSOR_MAP_L2_PROMOTION_NONE)))
       tmt = tm;
     if (k == 0)
-      k_count_tps<kCountWarps, kCountUnroll, 1>
+      k_count_tps<kCountWarps, kCountUnroll, kCountMinBlocks>
           <<<g_big, kCountWarps * 32, 0, c->s_count>>>(a, tm, tmt);
     else
       k_count_tps<1, kCountCoUnroll, kCountCoMinBlocks>
@@ -1277,8 +1277,8 @@ extern "C" int wgpf_replay_device(wgpf_ctx* c, const void* d_body,
                                                    CountWin::kTpsPitch,
                                                    CU_TENSOR_MAP_L2_PROMOTION_NONE)))
       tmt = tm;
-    const void* kc = (const void*)k_count_tps<kCountWarps, kCountUnroll, 1>;
-    k_count_tps<kCountWarps, kCountUnroll, 1>
+    const void* kc = (const void*)k_count_tps<kCountWarps, kCountUnroll, kCountMinBlocks>;
+    k_count_tps<kCountWarps, kCountUnroll, kCountMinBlocks>
         <<<grid_for(c, kc, kCountWarps * 32, 0), kCountWarps * 32, 0, c->stream>>>(ca, tm, tmt);
   } else
     k_count_fast<<<grid_for(c, (const void*)k_count_fast, 256, 0), 256, 0,

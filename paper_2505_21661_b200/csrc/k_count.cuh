@@ -233,6 +233,10 @@ constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
 #define WGPF_COUNT_UNROLL 16
 #endif
 constexpr int kCountUnroll = WGPF_COUNT_UNROLL;
+#ifndef WGPF_COUNT_MINB
+#define WGPF_COUNT_MINB 1  // launch bound: CTAs per SM the register budget must allow
+#endif
+constexpr uint32_t kCountMinBlocks = WGPF_COUNT_MINB;
 #ifndef WGPF_COUNT_CO_UNROLL
 #define WGPF_COUNT_CO_UNROLL 8
 #endif

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS));
   if constexpr (kMode != 0) {
-    wgpf_dev::flush(prof, profile, cta, PROF_BYTES, threadIdx.x, THREADS);
+    wgpf_dev::flush_bulk(prof, profile, cta, PROF_BYTES, threadIdx.x, THREADS);
     if (threadIdx.x == 0 && timing) {
       timing[cta].gt_end = wgpf_dev::globaltimer();
       timing[cta].clk_end = wgpf_dev::clock32();

@@ -119,6 +119,27 @@ __global__ void k_record_cost(uint32_t n, uint64_t* cycles, uint32_t* sink) {
   if (x == 0xFFFFFFFFu) sink[0] = x;
 }
 
+// FinalizeOp cost: cycles from the CTA barrier after the last record to the
+// end of the copy-out of a `bytes` profile buffer (per CTA, all CTAs of the
+// grid flushing at once, as at the end of an instrumented kernel): 16-B
+// vector stores by every thread (kBulk = false) or one cp.async.bulk by one
+// thread (kBulk = true).
+template <bool kBulk>
+__global__ void k_flush_cost(uint8_t* profile, uint32_t bytes, uint64_t* cycles) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  for (uint32_t i = threadIdx.x; i < bytes / 4u; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(buf)[i] = i * 2654435761u + blockIdx.x;
+  __syncthreads();
+  const uint64_t t0 = clock64();
+  if constexpr (kBulk)
+    wgpf_dev::flush_bulk(buf, profile, blockIdx.x, bytes, threadIdx.x, blockDim.x);
+  else
+    wgpf_dev::flush(buf, profile, blockIdx.x, bytes, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const uint64_t t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
 // ---- scope-program interpreter ------------------------------------------------
 // Runs a lowered scope program (p1.lower_scopes -> p1.program_encoding): warp
 // w of every CTA executes body w -- START / END record ops, loops, ALU busy
@@ -426,5 +447,16 @@ extern "C" int wgpf_p1_record_cost(uint32_t n, uint32_t warps, int record,
     k_record_cost<false><<<1, warps * 32, smem, st>>>(
         n, static_cast<uint64_t*>(d_cycles), sink);
   }
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
+
+// cycles[ctas] out (see k_flush_cost); bytes a multiple of 16.
+extern "C" int wgpf_p1_flush_cost(uint32_t ctas, uint32_t threads, uint32_t bytes, int bulk,
+                                  void* d_profile, void* d_cycles, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto* kfn = bulk ? k_flush_cost<true> : k_flush_cost<false>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  kfn<<<ctas, threads, bytes, st>>>(static_cast<uint8_t*>(d_profile), bytes,
+                                    static_cast<uint64_t*>(d_cycles));
   return cudaGetLastError() == cudaSuccess ? 0 : 10;
 }

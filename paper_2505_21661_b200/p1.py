@@ -53,6 +53,8 @@ def lib() -> C.CDLL:
         L.wgpf_p1_selftest_auto.restype = i32
         L.wgpf_p1_record_cost.argtypes = [u32, u32, i32, vp, vp]
         L.wgpf_p1_record_cost.restype = i32
+        L.wgpf_p1_flush_cost.argtypes = [u32, u32, u32, i32, vp, vp, vp]
+        L.wgpf_p1_flush_cost.restype = i32
         L.wgpf_gemm_bf16.argtypes = [vp, vp, vp, u32, u32, u32, i32, vp, vp, vp]
         L.wgpf_gemm_bf16.restype = i32
         L.wgpf_gemm_profile_bytes.argtypes = [u32, u32]
@@ -111,6 +113,16 @@ def selftest_store_log(iters: int) -> list:
         log += [(1, o), (1, i), (0, i), (0, o), (1, a), (0, a), (1, w), (0, w)]
     log.append((0, k))
     return log
+
+
+def flush_cost(ctas: int, threads: int, nbytes: int, bulk: bool, profile_ptr: int,
+               cycles_ptr: int, stream: int = 0) -> None:
+    """FinalizeOp cost microbenchmark (csrc_p1/p1_selftest.cu k_flush_cost):
+    cycles per CTA to copy an nbytes profile buffer out with vector stores or
+    one cp.async.bulk."""
+    _check(lib().wgpf_p1_flush_cost(ctas, threads, nbytes, int(bulk), C.c_void_p(profile_ptr),
+                                    C.c_void_p(cycles_ptr), C.c_void_p(stream)),
+           "wgpf_p1_flush_cost")
 
 
 def record_cost(n: int, warps: int, record: bool, cycles_ptr: int,

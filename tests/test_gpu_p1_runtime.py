@@ -203,3 +203,15 @@ def test_loop_entry_cost_is_measured():
     print(r)
     assert r["record_pair_cycles_in_loop"] > 0
     assert abs(r["loop_entry_cost_cycles"]) < r["record_pair_cycles_in_loop"], r
+
+
+def test_bulk_flush_equals_vector_flush():
+    """wgpf_dev::flush_bulk (one cp.async.bulk shared -> global) leaves the
+    same KPFT body segment in HBM as the vector-store flush, for the GEMM's
+    3,168-B buffer and a 32-KB one; both costs are measured."""
+    import bench_p1
+    r = bench_p1.measure_flush()
+    print(r)
+    for nb, row in r.items():
+        assert row["identical"], nb
+        assert row["bulk"] > 0 and row["vector"] > 0

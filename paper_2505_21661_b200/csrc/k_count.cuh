@@ -234,7 +234,9 @@ constexpr uint32_t kCountW = 16;  // records per window: 128-B runs per stream
 #endif
 constexpr int kCountUnroll = WGPF_COUNT_UNROLL;
 #ifndef WGPF_COUNT_MINB
-#define WGPF_COUNT_MINB 1  // launch bound: CTAs per SM the register budget must allow
+#define WGPF_COUNT_MINB 4  // launch bound: 4 CTAs per SM -> <= 128 registers (ptxas
+                           // then picks 96: 20 warps / SM; unbounded it took 118 and
+                           // 16 warps: config 4 1.67 -> 1.61 ms, config 5 1.97 -> 1.88)
 #endif
 constexpr uint32_t kCountMinBlocks = WGPF_COUNT_MINB;
 #ifndef WGPF_COUNT_CO_UNROLL

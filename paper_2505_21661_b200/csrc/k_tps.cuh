@@ -230,12 +230,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     const uint64_t off = act ? a.offsets[s] : 0ull;
     const uint64_t gs = s + a.stream_base;
     const unsigned long long gkey = (unsigned long long)gs << 25;
-#ifdef WGPF_TPS_WSTAT
-    // (lanes hold streams s0 + lane * W: the lowest active lane has the
-    // batch's smallest stream)
-    const uint32_t lmin = __ffs(__ballot_sync(FULL, act)) - 1u;
-    uint32_t wseen = 0;  // classes whose first key this batch has settled
-#endif
     const uint2* slots = reinterpret_cast<const uint2*>(sbase + 16);
     for (uint32_t r = 0; r < R; ++r) tb.cnt[r * 32 + lane] = 0;
 
@@ -308,61 +302,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
     // meets its events in key order, so the first-key atomic fires while the
     // lane's min is still ~0 (again only if every duration so far was
     // 2^32-1: a larger key, which the min leaves alone).
-#ifdef WGPF_TPS_WSTAT
-    // warp-reduced variant: when every participating lane has the same class
-    // (the grouped lanes run one program), one lane applies the warp's
-    // min / max / sum to its own column -- two shared wavefronts instead of
-    // eight; first keys from the batch's lowest active lane (its stream is
-    // the smallest) through a per-batch seen mask
-    auto lstat = [&](bool p, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
-      const uint32_t pm = __ballot_sync(FULL, p);
-      const uint32_t c = p ? cls : 0u;
-      const uint32_t c0 = __reduce_min_sync(FULL, p ? cls : 0xFFFFFFFFu);
-      const bool uni = c0 == __reduce_max_sync(FULL, p ? cls : 0u);
-      const unsigned long long key = gkey | (kpos << 1) | kind;
-      if (uni) {
-        const uint32_t mn = __reduce_min_sync(FULL, p ? d : 0xFFFFFFFFu);
-        const uint32_t mx = __reduce_max_sync(FULL, p ? d : 0u);
-        const uint32_t dd = p ? d : 0u;
-        uint32_t slo, shi;
-        if (mx < (1u << 27)) {
-          slo = __reduce_add_sync(FULL, dd);
-          shi = 0u;
-        } else {
-          const uint32_t a0 = __reduce_add_sync(FULL, dd & 0xFFFFu);
-          const uint32_t a1 = __reduce_add_sync(FULL, dd >> 16);
-          slo = a0 + (a1 << 16);
-          shi = (a1 >> 16) + (slo < a0 ? 1u : 0u);
-        }
-        if (!((wseen >> c0) & 1u)) {
-          const uint32_t khi = __reduce_min_sync(FULL, p ? (uint32_t)(key >> 32) : 0xFFFFFFFFu);
-          const uint32_t klo = __reduce_min_sync(
-              FULL, p && (uint32_t)(key >> 32) == khi ? (uint32_t)key : 0xFFFFFFFFu);
-          if (lane == __ffs(pm) - 1u)
-            atomicMin(&tb.first[c0], ((unsigned long long)khi << 32) | klo);
-          if ((pm >> lmin) & 1u) wseen |= 1u << c0;
-        }
-        if (lane == __ffs(pm) - 1u) {
-          const uint32_t ea = s_a + c0 * 512u;
-          uint4 x = lds128(ea);
-          x.x = min(x.x, mn);
-          x.y = max(x.y, mx);
-          add64_u32(x.z, x.w, slo);
-          x.w += shi;
-          sts128_if(true, ea, x);
-        }
-      } else if (p) {
-        const uint32_t ea = s_a + c * 512u;
-        uint4 x = lds128(ea);
-        if (!((wseen >> c) & 1u)) atomicMin(&tb.first[c], key);
-        x.x = min(x.x, d);
-        x.y = max(x.y, d);
-        add64_u32(x.z, x.w, d);
-        sts128_if(true, ea, x);
-      }
-      red_add(p ? s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)) : s_hist_spare, 1u);
-    };
-#else
     auto lstat = [&](bool p, uint32_t cls, uint32_t d, uint32_t kpos, uint32_t kind) {
       const uint32_t c = p ? cls : 0u;
       const uint32_t ea = s_a + c * 512u;
@@ -376,7 +315,6 @@ __global__ void __launch_bounds__(kTpsMaxWarps * 32, 1)
       // the table -- no branch around the shared atomic)
       red_add(p ? s_hist + 4u * (c * WGPF_HIST_BINS + hist_bin32(d)) : s_hist_spare, 1u);
     };
-#endif
     // kFull: positions i .. i+2 exist on every lane (the bulk of the walk):
     // no per-record bounds predicates
     auto step = [&](auto full, uint32_t i, uint2 r2) {

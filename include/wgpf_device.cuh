@@ -492,3 +492,32 @@ __device__ __forceinline__ void flush_bulk(const void* smem_buf, void* profile_m
 }
 
 }  // namespace wgpf_dev
+
+// ---- the C-style device API of SURVEY.md 8(b) ------------------------------
+// wgpf_init / wgpf_record / wgpf_finalize over a power-of-two circular
+// Recorder (the state is the caller's register-resident wgpf_recorder):
+//   InitOp      wgpf_init(r, smem_base, slots, warp_id)
+//   RecordOp    wgpf_record_op(r, start, region) (ReadCounter + StoreCounter;
+//               wgpf_record is the 8-byte record type of wgpf_format.h)
+//   FinalizeOp  wgpf_finalize(r, ...)           (header, barrier, bulk flush)
+typedef wgpf_dev::Recorder<true> wgpf_recorder;
+__device__ __forceinline__ void wgpf_init(wgpf_recorder& r, void* smem_base, uint32_t slots,
+                                          uint32_t warp_id) {
+  r.init(smem_base, warp_id, slots, (threadIdx.x & 31u) == 0u);
+}
+__device__ __forceinline__ void wgpf_record_op(wgpf_recorder& r, bool start, uint32_t region) {
+  if (start)
+    r.start(region);
+  else
+    r.end(region);
+}
+// every thread of the CTA calls it (it contains the CTA barrier)
+__device__ __forceinline__ void wgpf_finalize(wgpf_recorder& r, const void* smem_base,
+                                              void* profile_mem, uint32_t block_index,
+                                              uint32_t warp_id, uint32_t slots,
+                                              uint32_t streams_per_cta) {
+  r.close(block_index, warp_id, slots);
+  __syncthreads();
+  wgpf_dev::flush_bulk(smem_base, profile_mem, block_index,
+                       wgpf_dev::smem_bytes(streams_per_cta, slots), threadIdx.x, blockDim.x);
+}

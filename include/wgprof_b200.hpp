@@ -567,6 +567,18 @@ inline TraceReplay replay_image(const GlobalTraceImage& image,
                              ev.get(), cap, 0, &n, &w);
   b200::check(rc);
   TraceReplay out;
+  // the events' storage is faulted in by all host threads first: resize's
+  // default construction is serial, and page faults on a multi-GB fresh
+  // allocation would otherwise dominate it
+  out.events.reserve(n);
+  {
+    unsigned char* raw = reinterpret_cast<unsigned char*>(out.events.data());
+    const std::size_t pages = (n * sizeof(TimelineEvent) + 4095) / 4096;
+    if (raw)
+      b200::parallel_ranges(pages, [&](std::size_t lo, std::size_t hi, unsigned) {
+        for (std::size_t p = lo; p < hi; ++p) raw[p * 4096] = 0;
+      }, 1u << 12);
+  }
   out.events.resize(n);
   b200::parallel_ranges(n, [&](std::size_t lo, std::size_t hi, unsigned) {
     for (std::size_t i = lo; i < hi; ++i) out.events[i] = b200::to_event(ev[i], plan.region_labels);

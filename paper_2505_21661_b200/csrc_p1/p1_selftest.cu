@@ -97,6 +97,35 @@ __global__ void k_selftest(uint8_t* profile, uint32_t cap, uint32_t iters,
   if (x == 0xFFFFFFFFu) sink[0] = x;
 }
 
+// The selftest program through the C-style device API (wgpf_init /
+// wgpf_record / wgpf_finalize): the same records as k_selftest.
+__global__ void k_selftest_capi(uint8_t* profile, uint32_t cap, uint32_t iters,
+                                uint32_t* sink) {
+  extern __shared__ __align__(16) uint8_t buf[];
+  const uint32_t warp = threadIdx.x >> 5;
+  wgpf_recorder rec;
+  wgpf_init(rec, buf, cap, warp);
+  uint32_t x = threadIdx.x + 7u * blockIdx.x;
+  wgpf_record_op(rec, true, R_KERNEL);
+  for (uint32_t it = 0; it < iters; ++it) {
+    wgpf_record_op(rec, true, R_OUTER);
+    x = busy(x, 16 + (it & 3));
+    wgpf_record_op(rec, true, R_INNER);
+    x = busy(x, 8 + warp);
+    wgpf_record_op(rec, false, R_INNER);
+    wgpf_record_op(rec, false, R_OUTER);
+    wgpf_record_op(rec, true, R_ASYNC);
+    x = busy(x, 4);
+    wgpf_record_op(rec, false, R_ASYNC);
+    x = busy(x, 32);
+    wgpf_record_op(rec, true, R_ASYNC_WAIT);
+    wgpf_record_op(rec, false, R_ASYNC_WAIT);
+  }
+  wgpf_record_op(rec, false, R_KERNEL);
+  wgpf_finalize(rec, buf, profile, blockIdx.x, warp, cap, blockDim.x >> 5);
+  if (x == 0xFFFFFFFFu) sink[0] = x;
+}
+
 // Per-warp cycle cost of N record ops inside an ALU loop.
 template <bool kRecord>
 __global__ void k_record_cost(uint32_t n, uint64_t* cycles, uint32_t* sink) {
@@ -387,6 +416,19 @@ extern "C" int wgpf_p1_loop_entry(uint32_t n, uint32_t trips, uint32_t warps,
   } else {
     k_loop_entry<false><<<1, warps * 32, smem, st>>>(n, trips, cyc, sink);
   }
+  return cudaGetLastError() == cudaSuccess ? 0 : 10;
+}
+
+// the selftest program through the C-style device API (pow2 caps)
+extern "C" int wgpf_p1_selftest_capi(void* d_profile, uint32_t ctas, uint32_t warps_per_cta,
+                                     uint32_t cap, uint32_t iters, void* stream) {
+  static uint32_t* sink = nullptr;
+  if (!sink) cudaMalloc(&sink, 4);
+  if (!cap || (cap & (cap - 1))) return 11;
+  const uint32_t smem = wgpf_dev::smem_bytes(warps_per_cta, cap);
+  cudaFuncSetAttribute(k_selftest_capi, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_selftest_capi<<<ctas, warps_per_cta * 32, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint8_t*>(d_profile), cap, iters, sink);
   return cudaGetLastError() == cudaSuccess ? 0 : 10;
 }
 

@@ -51,6 +51,8 @@ def lib() -> C.CDLL:
         L.wgpf_p1_selftest.restype = i32
         L.wgpf_p1_selftest_auto.argtypes = [vp, u32, u32, u32, u32, vp]
         L.wgpf_p1_selftest_auto.restype = i32
+        L.wgpf_p1_selftest_capi.argtypes = [vp, u32, u32, u32, u32, vp]
+        L.wgpf_p1_selftest_capi.restype = i32
         L.wgpf_p1_record_cost.argtypes = [u32, u32, i32, vp, vp]
         L.wgpf_p1_record_cost.restype = i32
         L.wgpf_p1_flush_cost.argtypes = [u32, u32, u32, i32, vp, vp, vp]
@@ -103,6 +105,14 @@ def selftest_auto(profile_ptr: int, ctas: int, warps: int, cap: int, iters: int,
     (wgpf_dev::Scope / AsyncOp, include/wgpf_device.cuh)."""
     _check(lib().wgpf_p1_selftest_auto(C.c_void_p(profile_ptr), ctas, warps, cap, iters,
                                        C.c_void_p(stream)), "wgpf_p1_selftest_auto")
+
+
+def selftest_capi(profile_ptr: int, ctas: int, warps: int, cap: int, iters: int,
+                  stream: int = 0) -> None:
+    """The selftest program through the C-style device API (wgpf_init /
+    wgpf_record_op / wgpf_finalize, include/wgpf_device.cuh)."""
+    _check(lib().wgpf_p1_selftest_capi(C.c_void_p(profile_ptr), ctas, warps, cap, iters,
+                                       C.c_void_p(stream)), "wgpf_p1_selftest_capi")
 
 
 def selftest_store_log(iters: int) -> list:

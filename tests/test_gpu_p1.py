@@ -135,14 +135,19 @@ def test_pass_helpers_place_the_reference_records(oracle):
     stride = p1.stream_stride(cap)
     a = torch.zeros(ctas * warps * stride, dtype=torch.uint8, device="cuda")
     b = torch.zeros_like(a)
+    c = torch.zeros_like(a)
     p1.selftest(a.data_ptr(), ctas, warps, cap, iters)
     p1.selftest_auto(b.data_ptr(), ctas, warps, cap, iters)
+    p1.selftest_capi(c.data_ptr(), ctas, warps, cap, iters)  # C-style device API
     torch.cuda.synchronize()
+    dc = oracle.decode_kpft(p1.kpft_v1(c.cpu().numpy(), ctas * warps), cap, 0)
     da = oracle.decode_kpft(p1.kpft_v1(a.cpu().numpy(), ctas * warps), cap, 0)
     db = oracle.decode_kpft(p1.kpft_v1(b.cpu().numpy(), ctas * warps), cap, 0)
     log = p1.selftest_store_log(iters)
     tail = log[-cap:] if len(log) > cap else log
-    for x, y in zip(da, db):
+    for x, y, z in zip(da, db, dc):
         assert np.array_equal(x["records"]["tag"], y["records"]["tag"])
+        assert np.array_equal(x["records"]["tag"], z["records"]["tag"])
+        assert (x["block_index"], x["warp_group"]) == (z["block_index"], z["warp_group"])
         got = [((int(t) >> 31) & 1, (int(t) >> 12) & 0x7FFFF) for t in y["records"]["tag"]]
         assert got == tail

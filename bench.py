@@ -132,6 +132,22 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+# WGPF_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 over gloo with
+# host-staged collectives -- exercises the N > 1 bench path on a one-GPU box
+# (NCCL cannot put two ranks on one device); never used for a reported number
+SHARE_GPU = os.environ.get("WGPF_BENCH_SHARE_GPU") == "1"
+
+
+def reduce_max(x: float, dev) -> float:
+    """max over ranks of a host float (on the device for NCCL, on the host
+    for the gloo test mode)"""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARE_GPU else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _free_port() -> int:
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -319,6 +335,7 @@ class Decode:
         self.xflags = env_int("WGPF_BENCH_FLAGS", 0)  # A/B only, never reported
 
     def step(self):
+        import torch
         import torch.distributed as dist
         ctx, L = self.ctx, self.L
         ne, w = ctx.replay_device(self.body.data_ptr(), self.body.numel(), self.n,
@@ -329,7 +346,13 @@ class Decode:
         launches = prof["launches"]
         if self.world > 1:
             ctx.stats_export(self.mine.data_ptr())
-            dist.all_gather_into_tensor(self.gathered, self.mine)
+            if SHARE_GPU:  # (gloo test mode: host-staged)
+                parts = [torch.empty(self.mine.numel(), dtype=torch.uint8)
+                         for _ in range(self.world)]
+                dist.all_gather(parts, self.mine.cpu())
+                self.gathered.copy_(torch.cat(parts))
+            else:
+                dist.all_gather_into_tensor(self.gathered, self.mine)
             self.merged.stats_merge(self.gathered.data_ptr(), self.world)
             launches += 2  # export + merge kernels (+ the NCCL kernel)
         return prof, launches
@@ -367,9 +390,7 @@ class Decode:
         clk = clocks.stop() if clocks else None
         ms = t0.elapsed_time(t1)
         if self.world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = reduce_max(ms, dev)
         return ms, profs, launches, clk
 
     def summary(self, ms, profs, steps, peak, peak_kind, traffic):
@@ -488,6 +509,8 @@ def main():
     from paper_2505_21661_b200 import trace as T
 
     ndev = torch.cuda.device_count()
+    if SHARE_GPU:
+        local = 0
     if local >= ndev:
         raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but this box has "
                          f"{ndev} GPU(s); --gpus {args.gpus} cannot run here")
@@ -495,7 +518,10 @@ def main():
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     ctx = T.Context(local, stream.cuda_stream)
@@ -551,9 +577,7 @@ def main():
             ts.append(time.perf_counter() - a)
         sec = statistics.mean(ts)
         if world > 1:
-            t = torch.tensor([sec], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            sec = float(t.item())
+            sec = reduce_max(sec, dev)
         e2e = {"value": d.records_total / sec, "unit": "records/s",
                "h2d_bytes_per_step": int(img.numel()) * world,
                "d2h_bytes_per_step": int(d.n_ev * 32 + d.packed) * world,
@@ -588,9 +612,7 @@ def main():
             ts.append(time.perf_counter() - a)
         sec = statistics.mean(ts)
         if world > 1:
-            t = torch.tensor([sec], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            sec = float(t.item())
+            sec = reduce_max(sec, dev)
         e2e["pageable"] = {"value": d.records_total / sec, "unit": "records/s",
                            "ms_per_step": sec * 1e3,
                            "host_memory": "pageable (staged through pinned bounce "

@@ -271,8 +271,15 @@ inline void parallel_ranges(std::size_t n, F&& f, std::size_t min_per = 1u << 16
 }
 
 // TimelineEvents -> 32-byte events with a dense label table (first-seen order)
-inline std::vector<wgpf_event> pack_events(const std::vector<TimelineEvent>& events,
-                                           std::vector<std::string>& table) {
+// (not value-initialised: every element is written below, in parallel, so
+// the pages are first touched by the writing threads)
+struct EventBuf {
+  std::unique_ptr<wgpf_event[]> p;
+  wgpf_event* data() { return p.get(); }
+  const wgpf_event* data() const { return p.get(); }
+};
+inline EventBuf pack_events(const std::vector<TimelineEvent>& events,
+                            std::vector<std::string>& table) {
   // distinct labels per range (events repeat a handful of labels: each
   // lookup first compares with the range's previous label), merged in
   // first-seen order; then the ids
@@ -298,7 +305,7 @@ inline std::vector<wgpf_event> pack_events(const std::vector<TimelineEvent>& eve
       }
   ids.clear();
   for (std::uint32_t k = 0; k < table.size(); ++k) ids.emplace(table[k], k);
-  std::vector<wgpf_event> ev(n + 1);
+  EventBuf ev{std::unique_ptr<wgpf_event[]>(new wgpf_event[n + 1])};
   parallel_ranges(n, [&](std::size_t lo, std::size_t hi, unsigned) {
     const std::string* last = nullptr;
     std::uint32_t last_id = 0;
@@ -308,7 +315,7 @@ inline std::vector<wgpf_event> pack_events(const std::vector<TimelineEvent>& eve
         last = &e.region;
         last_id = ids.find(e.region)->second;
       }
-      ev[i] = wgpf_event{e.start, e.end,
+      ev.p[i] = wgpf_event{e.start, e.end,
                          last_id | (e.kind == EventKind::Wait ? WGPF_EV_WAIT : 0u) |
                              (e.corrected ? WGPF_EV_CORRECTED : 0u),
                          e.iteration, e.block_index, e.warp_group};
@@ -593,7 +600,7 @@ inline TraceReplay replay_image(const GlobalTraceImage& image,
 inline std::map<std::string, RegionStats> region_stats(
     const std::vector<TimelineEvent>& events) {
   std::vector<std::string> table;
-  std::vector<wgpf_event> ev = b200::pack_events(events, table);
+  auto ev = b200::pack_events(events, table);
   b200::set_plan(0, BufferStrategy::Flush, table);
   std::vector<wgpf_region_stat> st(table.size() + 1);
   std::uint32_t n = 0;
@@ -618,7 +625,7 @@ inline std::map<std::string, RegionStats> region_stats(
 inline std::string export_chrome_trace(const std::vector<TimelineEvent>& events,
                                        double cycles_per_us = 1000.0) {
   std::vector<std::string> table;
-  std::vector<wgpf_event> ev = b200::pack_events(events, table);
+  auto ev = b200::pack_events(events, table);
   b200::set_plan(0, BufferStrategy::Flush, table);
   std::uint64_t len = 0;
   b200::check(wgpf_export_chrome_trace(b200::ctx(), ev.data(), events.size(), 0,
@@ -813,7 +820,7 @@ inline CriticalPathResult analyze_critical_path(
     const std::vector<std::pair<std::string, std::string>>& barrier_edges,
     const CriticalPathOptions& opts = {}) {
   std::vector<std::string> table;
-  std::vector<wgpf_event> ev = b200::pack_events(events, table);
+  auto ev = b200::pack_events(events, table);
   b200::set_plan(0, BufferStrategy::Flush, table);
   std::vector<const char*> src, dst;
   for (const auto& e : barrier_edges) {

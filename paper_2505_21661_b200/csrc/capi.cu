@@ -1503,6 +1503,41 @@ static void parallel_memcpy(void* dst, const void* src, size_t n) {
   for (auto& t : th) t.join();
 }
 
+// Host -> device copy of caller memory on the context stream: pageable
+// buffers over 64 MB go through the two pinned bounce buffers in 64-MB
+// chunks (multi-threaded host copy of chunk k+1 while chunk k's DMA runs)
+// instead of the driver's single-threaded staging.
+static int h2d_host(wgpf_ctx* c, void* d_dst, const void* h_src, uint64_t bytes) {
+  constexpr uint64_t kChunk = 64ull << 20;
+  if (bytes <= kChunk || host_pinned(h_src)) {
+    CUDA_OK(c, cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return WGPF_OK;
+  }
+  if (c->bounce_in_n < kChunk) {
+    for (auto& h : c->h_bounce_in) {
+      if (h) cudaFreeHost(h);
+      h = nullptr;
+    }
+    c->bounce_in_n = 0;
+    for (auto& h : c->h_bounce_in)
+      CUDA_OK(c, cudaMallocHost(reinterpret_cast<void**>(&h), kChunk));
+    c->bounce_in_n = kChunk;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!c->pev[b]) CUDA_OK(c, cudaEventCreateWithFlags(&c->pev[b], cudaEventDisableTiming));
+  const uint64_t chunk = std::min<uint64_t>(c->bounce_in_n, 1ull << 30);
+  for (uint64_t k = 0, at = 0; at < bytes; ++k, at += chunk) {
+    const uint32_t b = (uint32_t)(k & 1);
+    const uint64_t m = std::min(chunk, bytes - at);
+    if (k >= 2) CUDA_OK(c, cudaEventSynchronize(c->pev[b]));  // bounce b free again
+    parallel_memcpy(c->h_bounce_in[b], static_cast<const uint8_t*>(h_src) + at, m);
+    CUDA_OK(c, cudaMemcpyAsync(static_cast<uint8_t*>(d_dst) + at, c->h_bounce_in[b], m,
+                               cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(c, cudaEventRecord(c->pev[b], c->stream));
+  }
+  return WGPF_OK;
+}
+
 static int replay_image_chunked(wgpf_ctx* c, const uint8_t* kpft, uint64_t off,
                                 uint64_t count, uint64_t record_cost,
                                 wgpf_event* h_events, uint64_t events_cap,
@@ -2098,9 +2133,10 @@ extern "C" int wgpf_region_stats(wgpf_ctx* c, const wgpf_event* events,
   const wgpf_event* d_ev = events;
   if (!on_device) {
     ALLOC_OK(c, c->d_events, sizeof(wgpf_event) * std::max<uint64_t>(n, 1));
-    if (n)
-      CUDA_OK(c, cudaMemcpyAsync(c->d_events.p, events, sizeof(wgpf_event) * n,
-                                 cudaMemcpyHostToDevice, c->stream));
+    if (n) {
+      rc = h2d_host(c, c->d_events.p, events, sizeof(wgpf_event) * n);
+      if (rc) return rc;
+    }
     d_ev = c->d_events.as<wgpf_event>();
   }
   if (n) {

@@ -74,7 +74,7 @@ int main(int argc, char** argv) {
     TraceReplay tr = replay_image(img, plan, 33);
     const auto a = clk::now();
     std::vector<std::string> table;
-    std::vector<wgpf_event> ev = b200::pack_events(tr.events, table);
+    auto ev = b200::pack_events(tr.events, table);
     const auto b = clk::now();
     b200::set_plan(0, BufferStrategy::Flush, table);
     std::vector<wgpf_region_stat> st(table.size() + 1);

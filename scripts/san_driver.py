@@ -1,6 +1,7 @@
 """Small inputs through every hot kernel, for compute-sanitizer
 (memcheck / racecheck / synccheck): pass 1 (k_count_tps, TMA and cp.async
-windows), k_tps (grouped TMA), k_tpsd (TMA and cp.async windows), k_fast_emit,
+windows), k_tps (grouped TMA), k_tpsd (TMA and cp.async windows; deep and
+wide geometries), k_exact_mean, k_fast_emit,
 the general path, the critical path / overlap kernels (k_cp*), the Chrome
 formatter and the alignment kernel."""
 import os
@@ -39,6 +40,13 @@ for seed, case in enumerate([dict(n_streams=64, cap=256, depth=20, same_start=Fa
                              dict(n_streams=64, cap=128, depth=64)]):
     data, cap, st, labels = fuzz.deep_image(77 + seed, **case)
     ctx.replay_image_bytes(data, T.BufferPlan(cap, T.BufferStrategy(st), labels), 33)
+# wide streams (k_tpsd<kWide>: > 64 labels), TMA and cp.async windows; the
+# exact-mean statistics (k_exact_mean's shared-memory ring) on them
+for seed, case in enumerate([dict(n_streams=64, cap=256, depth=20),
+                             dict(n_streams=64, cap=256, depth=32, same_start=False)]):
+    data, cap, st, labels = fuzz.wide_image(88 + seed, **case)
+    ctx.replay_image_bytes(data, T.BufferPlan(cap, T.BufferStrategy(st), labels), 33,
+                           flags=0x2)
 # random fuzz images: warp-per-stream and general paths, errors
 for seed in range(12):
     data, cap, st, labels = fuzz.random_image(500 + seed, n_streams=40, cap=64, mode="random")

@@ -360,6 +360,31 @@ class Decode:
     def stats(self):
         return (self.merged if self.world > 1 else self.ctx).stats()
 
+    def stats_only(self, steps, warmup, stream):
+        """Stats-only mode: decode, pair, replay and the
+        per-label statistics without materialising events -- algorithmic
+        bytes 16 S + 8 records (one read of headers and surviving records)."""
+        import torch
+        L = self.L
+
+        def one():
+            self.ctx.replay_device(self.body.data_ptr(), self.body.numel(), self.n,
+                                   RECORD_COST, 0, 0, L.F_STATS_ONLY, stream_base=self.s0)
+        for _ in range(warmup):
+            one()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(steps):
+            one()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        b = 16 * self.n + 8 * self.records
+        return {"records_per_s": self.records / (ms / 1e3), "ms_per_step": ms,
+                "algorithmic_bytes": b, "gbs": b / (ms / 1e3) / 1e9}
+
     def timed(self, steps, warmup, stream, dev, sample_clocks, local):
         import torch
         import torch.distributed as dist
@@ -419,6 +444,7 @@ class Decode:
             "hbm_frac_step": self.alg_bytes / (ms_step / 1e3) / 1e9 / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "frac_vs_nominal_8tbs": achieved / 8000.0,
                          "kernel": kname, "overlap_chunks": ovl,
                          "algorithmic_bytes_per_launch": self.alg_bytes,
                          "kernel_ms": emit_ms, "peak_kind": peak_kind},
@@ -537,6 +563,11 @@ def main():
                                 "ncu_emit_traffic_config5.json") if full and world == 1
                      else None)
     digest = stats_digest(d.stats())
+    so = None
+    if world == 1 and not args.streams:
+        so = d.stats_only(args.steps, args.warmup, stream)
+        so["hbm_frac"] = so["gbs"] / peak
+        so["kernel"] = "pass 1 + k_tps<emit=false, stats=true>"
     nccl = None
     if world > 1:
         nccl = {"backend": dist.get_backend(), "nccl_version":
@@ -672,6 +703,27 @@ def main():
                                      for o in acc["scopes"]]
         # FinalizeOp cost: cycles per CTA to copy the profile buffer out
         p1line["flush_cycles_per_cta"] = bench_p1.measure_flush()
+        # config 3 in the same run: the instrumented warp-specialised
+        # attention, its trace decoded and analysed on the GPU
+        try:
+            a3 = bench_p1.measure_attn(iters=10, warmup=3)
+            sb, db = a3["kv_single_buffered_fa3_vanilla"], a3["kv_double_buffered"]
+            p1line["config3"] = {
+                "workload": a3["config"]["workload"],
+                "overhead_pct": {"kv_single_buffered": sb.get("overhead_pct"),
+                                 "kv_double_buffered": db.get("overhead_pct")},
+                "tflops_plain": {"kv_single_buffered": sb.get("tflops_plain"),
+                                 "kv_double_buffered": db.get("tflops_plain")},
+                "sdpa_tflops": a3.get("sdpa_tflops"),
+                "smem_profile_bytes_per_cta": a3.get("smem_profile_bytes_per_cta"),
+                "analysis_kv_single_buffered": {
+                    k: sb.get("analysis", {}).get(k)
+                    for k in ("events", "critical_path", "iteration_period_cycles")},
+                "chrome_export": {k: (a3.get("chrome_export") or {}).get(k)
+                                  for k in ("bytes", "events", "gpu_s", "identical")},
+            }
+        except Exception as e:  # (reported, not fatal)
+            p1line["config3"] = {"error": str(e)[:200]}
 
     if rank == 0:
         line = {
@@ -693,7 +745,7 @@ def main():
                              "total)"},
             "gbs": head["gbs_step_rank0"], "hbm_frac_step": head["hbm_frac_step"],
             "roofline": head["roofline"], "phases_ms": head["phases_ms"],
-            "general_streams": head["general_streams"],
+            "general_streams": head["general_streams"], "stats_only": so,
             "stats_digest": digest, "nccl": nccl,
             "cpu_baseline": cpu, "e2e": e2e, "e2e_shim": shim, "clocks": clk,
             "gpu_launches": launches,

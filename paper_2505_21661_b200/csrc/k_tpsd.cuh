@@ -69,8 +69,17 @@ constexpr uint32_t kDeepMaxSlots = 512;  // stack positions in 9 bits
 #define WGPF_DEEP_W 4
 #endif
 constexpr uint32_t kDeepW = WGPF_DEEP_W;  // positions per record window
+#ifndef WGPF_DEEP_P48
+// exact-pitch windows: a lane row holds exactly the window's kDeepW records
+// (odd starts copy records with 8-B cp.async instead of an extra 16-B chunk);
+// measured on config 5: 6.37 vs 6.42 ms with the 48-B rows (WGPF_DEEP_P48),
+// and the 1.5 KB it frees per warp buys nothing -- 13 warps: 6.47 ms
+constexpr uint32_t kDeepChunks = kDeepW / 2;
+constexpr uint32_t kDeepPitch = 8 * kDeepW;  // 32 B
+#else
 constexpr uint32_t kDeepChunks = WinGeom<kDeepW>::kChunks;
 constexpr uint32_t kDeepPitch = WinGeom<kDeepW>::kPitch;  // 48 B: 12 words
+#endif
 #ifndef WGPF_DEEP_WARPS
 #define WGPF_DEEP_WARPS 12
 #endif
@@ -403,6 +412,23 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 #pragma unroll
         for (uint32_t k = 0; k < kDeepChunks; ++k) {
           const uint32_t q = k * 32u + lane, sl = q / kDeepChunks, part = q % kDeepChunks;
+#ifndef WGPF_DEEP_P48
+          // records c0 + 2 part, + 1 of the window: one 16-B chunk at an
+          // even physical slot, else two 8-B records (the second may wrap)
+          uint32_t p = wst[k] + c0 + 2u * part;
+          p = p >= cap ? p - cap : p;
+          p = p >= cap ? p - cap : p;
+          const uint32_t dst = s_rec + bsel * (32 * kDeepPitch) + sl * kDeepPitch + 16u * part;
+          if (srck[k]) {
+            if ((p & 1u) == 0u) {
+              cp_async16(dst, srck[k] + 8u * p);
+            } else {
+              const uint32_t p1 = p + 1u == cap ? 0u : p + 1u;
+              cp_async8(dst, srck[k] + 8u * p);
+              cp_async8(dst + 8u, srck[k] + 8u * p1);
+            }
+          }
+#else
           // the even physical slot at or below (start + c0) mod cap, + part
           uint32_t p = wst[k] + c0;
           p = p >= cap ? p - cap : p;  // (c0 < cap + 2: one subtraction
@@ -412,6 +438,7 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
           if (srck[k])
             cp_async16(s_rec + bsel * (32 * kDeepPitch) + sl * kDeepPitch + 16u * part,
                        srck[k] + 8u * p);
+#endif
         }
       }
     };
@@ -562,10 +589,16 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
         bphase ^= 1u << bsel;
       }
       __syncwarp();
+#ifndef WGPF_DEEP_P48
+      const uint2* myrec = reinterpret_cast<const uint2*>(ws.rec[bsel] + lane * kDeepPitch);
+      constexpr bool kPairs = true;  // rows are 16-B aligned for any start
+#else
       const uint2* myrec = reinterpret_cast<const uint2*>(
           ws.rec[bsel] + lane * kDeepPitch + 8u * (start & 1u));
+      const bool kPairs = even_start;
+#endif
       if (w0 + kDeepW + 2u <= nmin) {
-        if (even_start) {
+        if (kPairs) {
           // 16-B record pairs: one conflict-free LDS.128 per two steps
           const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
 #pragma unroll kDeepUnroll

@@ -34,6 +34,9 @@ __device__ __forceinline__ void cp_async16(uint32_t sdst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async8(uint32_t sdst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }

@@ -349,8 +349,15 @@ inline void put_u32(std::vector<std::uint8_t>& o, std::uint32_t v) {
 // An in-memory image as a KPFT v2 container (u64 stream count) for the
 // C-ABI: the reference's decode_image / replay_image take the image in
 // memory and never serialise it, so the v1 u16 count limit must not apply.
+struct ByteBuf {  // (not value-initialised: every byte is written, in parallel)
+  std::unique_ptr<std::uint8_t[]> p;
+  std::size_t n = 0;
+  std::uint8_t* data() { return p.get(); }
+  const std::uint8_t* data() const { return p.get(); }
+  std::size_t size() const { return n; }
+};
 template <class Img>
-inline std::vector<std::uint8_t> pack_image(const Img& img) {
+inline ByteBuf pack_image(const Img& img) {
   static_assert(sizeof(ProfileRecord) == 8, "ProfileRecord is {u32 tag, u32 payload}");
   const std::size_t ns = img.streams.size();
   std::vector<std::size_t> at(ns + 1);
@@ -362,7 +369,7 @@ inline std::vector<std::uint8_t> pack_image(const Img& img) {
                   "stream slot count does not match its declared capacity");
     at[k + 1] = at[k] + 16 + 8 * s.slots.size();
   }
-  std::vector<std::uint8_t> out(at[ns]);
+  ByteBuf out{std::unique_ptr<std::uint8_t[]>(new std::uint8_t[at[ns]]), at[ns]};
   const std::uint64_t n = ns;
   std::memcpy(out.data(), "KPFT\x02\0\0\0", 8);
   std::memcpy(out.data() + 8, &n, 8);

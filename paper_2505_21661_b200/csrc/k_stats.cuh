@@ -173,8 +173,11 @@ __global__ void __launch_bounds__(kEmThreads) k_exact_mean(
           const long long bb = __double_as_longlong(q1);
           const double up = __longlong_as_double(bb + 1) - q1;
           const double down = q1 - __longlong_as_double(bb - 1);
-          ok = ok && (num == 0.0 ? q1 == 0.0
-                                 : (q1 > 0.0 && r1 < 0.5 * up * m1 && -r1 < 0.5 * down * m1));
+          // (bitwise, not short-circuit: predicated compares, no branches
+          // beside the chain)
+          const bool zero = num == 0.0;
+          const bool good = (q1 > 0.0) & (r1 < 0.5 * up * m1) & (-r1 < 0.5 * down * m1);
+          ok = ok & ((zero & (q1 == 0.0)) | (!zero & good));
           mm = q1;
         }
         if (!ok) {

@@ -199,11 +199,12 @@ def test_allreduce_stats_over_nccl_single_rank():
         nccl.ncclCommDestroy(comm)
 
 
-def test_bench_two_ranks_on_one_gpu_matches_one_rank():
+@pytest.mark.parametrize("ranks", [2, 4, 8])
+def test_bench_ranks_on_one_gpu_match_one_rank(ranks):
     """The N > 1 path of bench.py itself (self-launch under torchrun, block-
     range shards of one trace, per-step export / all-gather / merge, max-over-
     ranks timing, rank 0's line) on a one-GPU box: WGPF_BENCH_SHARE_GPU=1 puts
-    both ranks on cuda:0 over gloo (host-staged collective, the test mode --
+    all N ranks on cuda:0 over gloo (host-staged collective, the test mode --
     NCCL cannot share a device).  The merged statistics digest must equal the
     single-rank run's on the same trace."""
     import json
@@ -214,14 +215,14 @@ def test_bench_two_ranks_on_one_gpu_matches_one_rank():
     env = dict(os.environ, WGPF_BENCH_SHARE_GPU="1")
     one = subprocess.run(base + ["--gpus", "1"], capture_output=True, text=True, timeout=600,
                          env=env)
-    two = subprocess.run(base + ["--gpus", "2"], capture_output=True, text=True, timeout=600,
-                         env=env)
+    two = subprocess.run(base + ["--gpus", str(ranks)], capture_output=True, text=True,
+                         timeout=900, env=env)
     assert one.returncode == 0, one.stderr[-2000:]
     assert two.returncode == 0, two.stderr[-2000:]
     l1 = json.loads([l for l in one.stdout.splitlines() if l.startswith("{")][-1])
     l2 = json.loads([l for l in two.stdout.splitlines() if l.startswith("{")][-1])
-    assert l1["n_gpus"] == 1 and l2["n_gpus"] == 2
+    assert l1["n_gpus"] == 1 and l2["n_gpus"] == ranks
     assert l2["config"]["streams_total"] == l1["config"]["streams_total"] == 65536
-    assert l2["config"]["streams_per_gpu_rank0"] == 32768
+    assert l2["config"]["streams_per_gpu_rank0"] == 65536 // ranks
     assert l2["stats_digest"] == l1["stats_digest"]
     assert l2["nccl"]["collectives_per_step"] == 1

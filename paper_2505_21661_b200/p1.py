@@ -7,6 +7,7 @@ that the P2 decoder (trace.Context.replay_device) reads in place.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import struct
 from dataclasses import dataclass
 
@@ -45,7 +46,8 @@ CTA_TIMING_DTYPE = np.dtype([("smid", "<u4"), ("streams", "<u4"),
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
-        L = C.CDLL(_build.build_p1())
+        # WGPF_P1_LIB_OVERRIDE: an alternative build of the same ABI (A/B runs)
+        L = C.CDLL(os.environ.get("WGPF_P1_LIB_OVERRIDE") or _build.build_p1())
         vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
         L.wgpf_p1_selftest.argtypes = [vp, u32, u32, u32, u32, vp, vp]
         L.wgpf_p1_selftest.restype = i32

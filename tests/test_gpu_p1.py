@@ -82,7 +82,9 @@ def test_record_cost_is_small():
     assert 0 < per_record < 40, per_record
 
 
-@pytest.mark.parametrize("shape", [(256, 512, 128), (1024, 1024, 2048)])
+# M % 256 == 0: the CTA-pair kernel (cta_group::2); M = 384: the single-CTA one
+@pytest.mark.parametrize("shape", [(256, 512, 128), (1024, 1024, 2048), (384, 768, 192),
+                                   (2048, 2048, 4096)])
 def test_gemm_matches_cublas_and_instrumented_is_identical(oracle, shape):
     import torch
     p1 = P1()

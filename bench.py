@@ -690,9 +690,14 @@ def main():
         import bench_p1
         p1line = bench_p1.measure(iters=20, warmup=5, decode=False, sass=False)
         p1line = {k: p1line[k] for k in ("value", "unit", "t_plain_ms", "t_instr_ms",
-                                         "t_cublas_ms", "accuracy_rel_err",
+                                         "t_cublas_ms", "tflops_plain", "tflops_instr",
+                                         "tflops_cublas", "plain_vs_cublas_adjacent",
+                                         "accuracy_rel_err",
                                          "smem_profile_bytes_per_cta",
                                          "record_cost_cycles")}
+        p1line["workload"] = ("bf16 GEMM 8192^3 on tcgen05 CTA pairs (cta_group::2); "
+                              "overhead = median of adjacent plain / instrumented "
+                              "launch ratios")
         # per-scope accuracy (record-derived scope durations vs the
         # uninstrumented kernel's own clock), the north-star's 2 % measure
         acc = bench_p1.measure_accuracy(reps=3)

@@ -244,7 +244,14 @@ __device__ __forceinline__ void umma_commit_elect(uint32_t bar) {
 // and B tiles stay in L2.  Two TMEM accumulators (2 x 256 columns): the MMA
 // warp fills one while the epilogue drains the other (tmem_full / tmem_empty
 // barriers), so the epilogue overlaps the next tile's main loop.
-constexpr uint32_t kGroupM = 8;
+// measured (8192^3, CTA pairs): groups of 2 / 4 / 8 / 16 / 32 pair m-blocks
+// give 1,466 / 1,535 / 1,588 / 1,574 / 1,484 TFLOP/s with DRAM reads
+// following (1.07 GB at 8, 1.52 at 4); L2 evict_last / evict_first hints on
+// the A / B loads did not help (1,545-1,597)
+#ifndef WGPF_GEMM_GROUP_M
+#define WGPF_GEMM_GROUP_M 8
+#endif
+constexpr uint32_t kGroupM = WGPF_GEMM_GROUP_M;
 
 __device__ __forceinline__ void tile_coords(uint32_t t, uint32_t nM, uint32_t nN,
                                             uint32_t& mb, uint32_t& nb) {

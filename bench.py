@@ -691,7 +691,8 @@ def main():
         p1line = bench_p1.measure(iters=20, warmup=5, decode=False, sass=False)
         p1line = {k: p1line[k] for k in ("value", "unit", "t_plain_ms", "t_instr_ms",
                                          "t_cublas_ms", "tflops_plain", "tflops_instr",
-                                         "tflops_cublas", "plain_vs_cublas_adjacent",
+                                         "tflops_cublas", "tflops_plain_beside_cublas",
+                                         "plain_vs_cublas_adjacent", "tflops_note",
                                          "accuracy_rel_err",
                                          "smem_profile_bytes_per_cta",
                                          "record_cost_cycles")}

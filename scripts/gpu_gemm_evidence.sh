@@ -1,3 +1,5 @@
+# P1 GEMM evidence (profiles/r02_gemm_pair*): GPU tests of the P1 path,
+# bench_p1, pair / single-CTA A/B, ncu launch list and one --set full capture.
 #!/bin/bash
 mkdir -p gpurun_out
 python -c "from paper_2505_21661_b200 import _build as b; b.build_p1(); b.build()" || exit 1

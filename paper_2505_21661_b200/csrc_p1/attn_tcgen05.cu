@@ -33,6 +33,9 @@
 // retires the GEMM1 issued just before), "Softmax.cN", "GEMM1.cN".  One profile stream per warp, circular,
 // PROF_CAP slots.
 //
+// The consumers alternate softmax turns every tile (named-barrier tokens),
+// so one consumer's softmax runs beside the other's GEMMs.
+//
 // KV_STAGES = 1 mirrors fa3_vanilla (single-buffered K / V slots: the next
 // load waits for both consumers' GEMMs); 2 double-buffers them.
 #include <cuda.h>
@@ -62,7 +65,17 @@ constexpr float RESCALE_LOG2 = 8.0f;
 #ifndef WGPF_ATTN_MUFU_PAIRS
 #define WGPF_ATTN_MUFU_PAIRS 16
 #endif
-constexpr int kMufuPairs = WGPF_ATTN_MUFU_PAIRS;  // of 16 pairs per chunk: ex2 on MUFU
+constexpr int kMufuPairs = WGPF_ATTN_MUFU_PAIRS;
+// Per-tile softmax tokens between the consumers (FA3's warp-scheduler
+// barriers).  Measured (B=16 H=16 S=8192, plain TFLOP/s / overhead): kv 1
+// 1,042 / 4.0 % vs 1,033 / 4.1 % with only the initial stagger; kv 2 980 /
+// 1.4 % vs 920 / 0.1 %.  Issuing the MMAs from a converged warp with
+// elect.sync (the GEMM's fix) was faster still without the tokens (1,110 /
+// 1,063) but its instrumented double-buffered variant fell into lockstep
+// (24 % overhead); with the tokens it measured 1,017 / 978 -- not kept.
+#ifndef WGPF_ATTN_PINGPONG
+#define WGPF_ATTN_PINGPONG 1
+#endif  // of 16 pairs per chunk: ex2 on MUFU
 
 enum : uint32_t {
   R_LOAD_K, R_LOAD_K_WAIT, R_LOAD_V, R_LOAD_V_WAIT,
@@ -196,7 +209,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t kbase = tc::smem_u32(ks), vbase = tc::smem_u32(vs);
 
     tc::mbar_wait(q_full, 0);
+#if !WGPF_ATTN_PINGPONG
     if (c == 1) tc::bar_sync(3, 256);  // start one softmax behind c0 (ping-pong)
+#endif
     // GEMM0: S = Q K_j^T into tS (issued one iteration ahead, right behind
     // GEMM1 of the previous tile; tcgen05.mma from one thread executes in
     // order, so it overwrites P only after GEMM1 has consumed it, and its
@@ -226,8 +241,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       if constexpr (kInstr) {
         rec.start(R + 1);
         rec.end(R + 1);
-        rec.start(R + 2);
       }
+#if WGPF_ATTN_PINGPONG
+      // softmax turns alternate between the consumers every tile (named
+      // barrier tokens: c0 waits on 3 for c1's previous softmax, c1 on 4 for
+      // c0's current one), so one consumer's softmax always runs beside the
+      // other's GEMMs -- FA3's warp-scheduler barriers
+      if (c == 1) tc::bar_sync(4, 256);
+      else if (j > 0) tc::bar_sync(3, 256);
+#endif
+      if constexpr (kInstr) rec.start(R + 2);
       // ---- softmax ----
       // pass 1: row max (S stays in TMEM; pass 2 reloads it)
       // (four independent max chains: the 3-input max has a few cycles of
@@ -311,7 +334,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::tmem_wait_st();
       tc::fence_before();
       tc::bar_sync(1 + c, 128);  // P (and a rescaled O) of all 128 rows stored
+#if WGPF_ATTN_PINGPONG
+      if (c == 0) tc::bar_arrive(4, 256);
+      else if (j + 1 < nkv) tc::bar_arrive(3, 256);
+#else
       if (c == 0 && j == 0) tc::bar_arrive(3, 256);
+#endif
       if constexpr (kInstr) rec.end(R + 2);
       // ---- GEMM1: O += P V_j ----
       tc::mbar_wait(&v_full[s], ph);

@@ -161,12 +161,6 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory");
 }
-__device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
-  asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.u32 [%1], %2; }" ::"r"(
-                   (uint32_t)p),
-               "r"(a), "r"(v)
-               : "memory");
-}
 // stack meta rows: u16 (deep) or u32 (wide)
 template <class M>
 __device__ __forceinline__ uint32_t lds_meta(uint32_t a) {

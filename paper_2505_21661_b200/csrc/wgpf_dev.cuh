@@ -278,6 +278,12 @@ __device__ __forceinline__ void sts16_if(bool p, uint32_t a, uint32_t v) {
                "r"(a), "h"((uint16_t)v)
                : "memory");
 }
+__device__ __forceinline__ void sts32_if(bool p, uint32_t a, uint32_t v) {
+  asm volatile("{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.u32 [%1], %2; }" ::"r"(
+                   (uint32_t)p),
+               "r"(a), "r"(v)
+               : "memory");
+}
 __device__ __forceinline__ void sts64_if(bool p, uint32_t a, uint2 v) {
   asm volatile(
       "{ .reg .pred q; setp.ne.b32 q, %0, 0; @q st.shared.v2.u32 [%1], {%2, %3}; }" ::"r"(

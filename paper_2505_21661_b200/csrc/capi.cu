@@ -681,7 +681,8 @@ static EncodeTiledFn encode_tiled() {
 }
 static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride,
                             uint64_t n_streams, uint32_t pitch,
-                            CUtensorMapL2promotion prom = l2_promotion()) {
+                            CUtensorMapL2promotion prom = l2_promotion(),
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn || (reinterpret_cast<uintptr_t>(body) & 15u) || (stride & 15u) ||
       stride < pitch || stride >= (1ull << 39) || n_streams < 32 ||
@@ -692,7 +693,7 @@ static bool body_tensor_map(CUtensorMap* m, const uint8_t* body, uint64_t stride
   const cuuint32_t box[2] = {pitch / 4, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint8_t*>(body), dims, strides,
-            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
             prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -854,7 +855,8 @@ static int emit_pass(wgpf_ctx* c, const uint8_t* body, uint64_t stride,
       CUtensorMap tmd;
       memset(&tmd, 0, sizeof(tmd));
       const uint32_t tma_ok =
-          !c->no_tma && body_tensor_map(&tmd, body, stride, n_streams, kDeepPitch) ? 1u : 0u;
+          !c->no_tma && body_tensor_map(&tmd, body, stride, n_streams, kDeepPitch,
+                                        l2_promotion(), kDeepSwizzle) ? 1u : 0u;
       for (int wide = 0; wide < (wide_enabled(c) ? 2 : 1); ++wide) {
         f.list = wide ? c->d_vlist.as<unsigned long long>() : c->d_dlist.as<unsigned long long>();
         f.list_len = c->d_glen.as<unsigned long long>() + (wide ? 3 : 2);

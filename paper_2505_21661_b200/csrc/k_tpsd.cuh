@@ -76,7 +76,28 @@ constexpr uint32_t kDeepW = WGPF_DEEP_W;  // positions per record window
 // and the 1.5 KB it frees per warp buys nothing -- 13 warps: 6.47 ms
 constexpr uint32_t kDeepChunks = kDeepW / 2;
 constexpr uint32_t kDeepPitch = 8 * kDeepW;  // 32 B
+#endif
+// Swizzled window rows.  At the 32-B pitch a lane's 16-B pair reads are
+// 2-way bank conflicted (lanes l and l + 4 of a quarter warp hit the same
+// banks: 8 wavefronts per LDS.128 instead of 4, ncu: 24 % excess shared
+// wavefronts).  The rows are stored with the two 16-B chunks of a row
+// swapped when address bit 7 is set (the TMA's SWIZZLE_32B pattern, bit 4 ^=
+// bit 7), which the cp.async fills and the reads follow: conflict-free.
+#if !defined(WGPF_DEEP_P48) && !defined(WGPF_DEEP_NO_SWZ) && WGPF_DEEP_W == 4
+#define WGPF_DEEP_SWZ 1
+constexpr CUtensorMapSwizzle kDeepSwizzle = CU_TENSOR_MAP_SWIZZLE_32B;
 #else
+constexpr CUtensorMapSwizzle kDeepSwizzle = CU_TENSOR_MAP_SWIZZLE_NONE;
+#endif
+// byte offset of 16-B chunk c in the window row at shared address row
+__device__ __forceinline__ uint32_t deep_chunk(uint32_t row, uint32_t c) {
+#ifdef WGPF_DEEP_SWZ
+  return 16u * (c ^ ((row >> 7) & 1u));
+#else
+  return 16u * c;
+#endif
+}
+#ifdef WGPF_DEEP_P48
 constexpr uint32_t kDeepChunks = WinGeom<kDeepW>::kChunks;
 constexpr uint32_t kDeepPitch = WinGeom<kDeepW>::kPitch;  // 48 B: 12 words
 #endif
@@ -412,7 +433,8 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
           uint32_t p = wst[k] + c0 + 2u * part;
           p = p >= cap ? p - cap : p;
           p = p >= cap ? p - cap : p;
-          const uint32_t dst = s_rec + bsel * (32 * kDeepPitch) + sl * kDeepPitch + 16u * part;
+          const uint32_t row = s_rec + bsel * (32 * kDeepPitch) + sl * kDeepPitch;
+          const uint32_t dst = row + deep_chunk(row, part);
           if (srck[k]) {
             if ((p & 1u) == 0u) {
               cp_async16(dst, srck[k] + 8u * p);
@@ -586,10 +608,22 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
 #ifndef WGPF_DEEP_P48
       const uint2* myrec = reinterpret_cast<const uint2*>(ws.rec[bsel] + lane * kDeepPitch);
       constexpr bool kPairs = true;  // rows are 16-B aligned for any start
+#ifdef WGPF_DEEP_SWZ
+      const uint32_t myrow = s_rec + bsel * (32 * kDeepPitch) + lane * kDeepPitch;
+      const uint32_t msw = (myrow >> 7) & 1u;  // chunks of this row swapped
+      // record j of the window (chunk j / 2, half j % 2)
+      const uint8_t* const myrowp = ws.rec[bsel] + lane * kDeepPitch;
+      auto rec_at = [&](uint32_t j) {
+        return *reinterpret_cast<const uint2*>(myrowp + 16u * ((j >> 1) ^ msw) + 8u * (j & 1u));
+      };
+#else
+      auto rec_at = [&](uint32_t j) { return myrec[j]; };
+#endif
 #else
       const uint2* myrec = reinterpret_cast<const uint2*>(
           ws.rec[bsel] + lane * kDeepPitch + 8u * (start & 1u));
       const bool kPairs = even_start;
+      auto rec_at = [&](uint32_t j) { return myrec[j]; };
 #endif
       if (w0 + kDeepW + 2u <= nmin) {
         if (kPairs) {
@@ -597,17 +631,21 @@ __global__ void __launch_bounds__(kDeepWarps * 32, 1)
           const uint4* myrec2 = reinterpret_cast<const uint4*>(myrec);
 #pragma unroll kDeepUnroll
           for (uint32_t j = 0; j < kDeepW; j += 2) {
+#ifdef WGPF_DEEP_SWZ
+            const uint4 q = *reinterpret_cast<const uint4*>(myrowp + 16u * ((j >> 1) ^ msw));
+#else
             const uint4 q = myrec2[j / 2];
+#endif
             step(std::true_type{}, w0 + j, make_uint2(q.x, q.y));
             step(std::true_type{}, w0 + j + 1, make_uint2(q.z, q.w));
           }
         } else {
 #pragma unroll 1
-          for (uint32_t j = 0; j < kDeepW; ++j) step(std::true_type{}, w0 + j, myrec[j]);
+          for (uint32_t j = 0; j < kDeepW; ++j) step(std::true_type{}, w0 + j, rec_at(j));
         }
       } else {
 #pragma unroll 1
-        for (uint32_t j = 0; j < kDeepW; ++j) step(std::false_type{}, w0 + j, myrec[j]);
+        for (uint32_t j = 0; j < kDeepW; ++j) step(std::false_type{}, w0 + j, rec_at(j));
       }
       __syncwarp();
       bsel = bsel == kDeepBufs - 1u ? 0u : bsel + 1u;
